@@ -1,0 +1,168 @@
+/*
+ * pd_b200.h - C ABI of libpd_b200.so, the B200-native executor behind
+ * paper_1806_03377_b200.run(), the drop-in for pipesim.run().
+ *
+ * The reference (pipesim, pure Python) has no FFI: its hot-path boundary is the
+ * Python call  pipesim.run(cfg, ctx, schedule=None) -> SimResult
+ * (/root/reference/pkg/src/pipesim/simulator.py:401-411).  That call is kept
+ * verbatim in Python (paper_1806_03377_b200/executor.py); this header is the
+ * thin layer under it.  Each entry point below names the reference routine
+ * whose work it takes over.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; device memory is allocated by the caller
+ *     (PyTorch) and never freed here.  Streams are passed as void* (cudaStream_t).
+ *   - Every function returns 0 on success.  PD_ERR_INVALID maps to the
+ *     reference's ValidationError, PD_ERR_TIMEOUT / PD_ERR_DEADLOCK to its
+ *     SimulationError ("deadlock: worker w (stage s, ...)" simulator.py:350-357),
+ *     PD_ERR_CUDA to a RuntimeError.  pd_last_error() holds the message.
+ *   - One host thread per process (one process per GPU), as the reference's
+ *     engine is single-threaded.
+ */
+#ifndef PD_B200_H
+#define PD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PD_ABI_VERSION 1
+
+enum pd_status { PD_OK = 0, PD_ERR_INVALID = 1, PD_ERR_CUDA = 2, PD_ERR_TIMEOUT = 3, PD_ERR_DEADLOCK = 4 };
+enum pd_dtype { PD_F32 = 0, PD_BF16 = 1 };
+enum pd_epi_kind { PD_EPI_STORE = 0, PD_EPI_LOSS = 1, PD_EPI_MASK = 2, PD_EPI_SGD = 3, PD_EPI_GRADF32 = 4 };
+
+/* ------------------------------------------------------------------ library */
+int pd_abi_version(void);
+/* Last error message of the calling thread (empty string if none). */
+const char* pd_last_error(void);
+int pd_device_sm_count(int device, int* out);
+
+/* ------------------------------------------------------------------ kernels
+ * One linear-layer pass as a GEMM with a fused epilogue; replaces the per-stage
+ * numeric step of semantics._step (semantics.py:119-144) generalised to an MLP:
+ *   C[M,N] = sum_k A(m,k) B(n,k);  A(m,k) = A[m*lda+k] (a_mn=0) or A[k*lda+m] (a_mn=1).
+ * dtype PD_BF16 runs the tcgen05/TMEM/TMA kernel, PD_F32 the SIMT FFMA kernel. */
+typedef struct pd_epilogue {
+  int kind;             /* pd_epi_kind */
+  void* out;            /* activation dtype (fp32 for GRADF32) */
+  int64_t ldo;
+  const float* bias;    /* STORE/LOSS: per-column bias or NULL */
+  int relu;             /* STORE */
+  const void* mask;     /* MASK: layer input X; out = acc * (X > 0) */
+  int64_t ldm;
+  const float* target;  /* LOSS: fp32 targets */
+  int64_t ldt;
+  float scale;          /* LOSS: out = (acc+bias-target)*scale, loss += 0.5*scale*sum(d^2) */
+  float* loss;          /* LOSS: fp32 accumulator */
+  float* master;        /* SGD: fp32 latest weights, master -= lr*acc, out = cast(master) */
+  int64_t ldw;
+  float lr;
+} pd_epilogue;
+
+int pd_gemm(int dtype, const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M, int N,
+            int K, const pd_epilogue* ep, void* stream);
+/* Bias gradient + SGD: b_master[j] -= lr * sum_r dz[r*ld+j];  b_out[j] = b_master[j]. */
+int pd_bias_sgd(int dtype, const void* dz, int rows, int cols, int64_t ld, float* b_master, float* b_out, float lr,
+                void* stream);
+/* master[i] -= lr*grad[i]; out[i] = cast(master[i])  (replicated stages, after the allreduce). */
+int pd_sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n, float lr, void* stream);
+
+/* ------------------------------------------------------------------ P2P transport
+ * Replaces _Engine._send (simulator.py:284-292): payloads are stored by the
+ * producing GEMM epilogue straight into the consumer's inbox slot (a peer-mapped
+ * pointer when the consumer is on another GPU); these flags order them.
+ * signal: system-scope release store of `value`; wait: acquire-poll until *flag >= value. */
+int pd_flag_signal(int* flag, int value, void* stream);
+int pd_flag_wait(const int* flag, int value, int* err_word, void* stream);
+/* CUDA IPC so a peer process can map an inbox: handle is 64 opaque bytes. */
+int pd_ipc_get_handle(const void* dev_ptr, void* handle_out64);
+int pd_ipc_open(const void* handle64, void** dev_ptr_out);
+int pd_ipc_close(void* dev_ptr);
+int pd_enable_peer_access(int peer_device);
+
+/* ------------------------------------------------------------------ executor
+ * Replaces _Engine.__init__/run/_try_start/_on_done (simulator.py:150-357) for the
+ * stages hosted by this process: executes a compiled 1F1B-RR program on device. */
+typedef struct pd_stage_desc {
+  int stage;                /* global stage index (0-based, plan order) */
+  int n_layers;
+  const int64_t* dims;      /* n_layers+1 widths: in of layer 0 .. out of layer n-1 */
+  int batch;                /* minibatch size */
+  int dtype;                /* pd_dtype of weights/activations */
+  int is_first, is_last;
+  int relu_last;            /* ReLU after the stage's last layer (all but the model output) */
+  int ring_depth;           /* weight-version ring slots */
+  int act_depth;            /* activation-stash slots (in-flight minibatches) */
+  int in_depth;             /* activation inbox slots (stage > 0) */
+  int grad_depth;           /* gradient inbox slots (stage < n-1) */
+  float lr;
+  /* per layer l: */
+  float* const* w_master;   /* [n_layers]            fp32 [out,in] latest weights */
+  float* const* b_master;   /* [n_layers]            fp32 [out] */
+  void* const* w_ring;      /* [n_layers*ring_depth] dtype [out,in], index l*ring_depth+slot */
+  float* const* b_ring;     /* [n_layers*ring_depth] fp32 [out] */
+  void* const* act;         /* [(n_layers-1)*act_depth] dtype [batch, dims[l+1]], index l*act_depth+slot */
+  void* const* act_in;      /* stage>0: [in_depth] dtype [batch, dims[0]]; stage 0: data blocks */
+  int n_data_blocks;
+  void* const* grad_in;     /* stage<n-1: [grad_depth] dtype [batch, dims[n]] */
+  void* const* dz_last;     /* last stage: [act_depth] dtype [batch, dims[n]] */
+  const float* const* target; /* last stage: [n_data_blocks] fp32 [batch, dims[n]] */
+  float* loss;              /* last stage: fp32 [num_minibatches+1] */
+  void* tmp[2];             /* dtype [batch, max dim] gradient ping-pong */
+  /* neighbours' inboxes (local or peer-mapped) */
+  void* const* next_act_in; /* [next_in_depth] */
+  int next_in_depth;
+  void* const* prev_grad_in;/* [prev_grad_depth] */
+  int prev_grad_depth;
+  /* cross-GPU flags; NULL when the neighbour is in-process */
+  int* act_ready;           /* [in_depth]   local, written by previous stage's GPU */
+  int* act_ack_remote;      /* [in_depth]   on previous stage's GPU, written here when a slot frees */
+  int* next_act_ready;      /* [next in_depth] on next stage's GPU */
+  int* next_act_ack;        /* [next in_depth] local, written by next stage's GPU */
+  int* grad_ready;          /* [grad_depth] local */
+  int* grad_ack_remote;     /* [grad_depth] on next stage's GPU */
+  int* prev_grad_ready;     /* [prev grad_depth] on previous stage's GPU */
+  int* prev_grad_ack;       /* [prev grad_depth] local */
+  int* err_word;            /* device int, set non-zero by a timed-out flag wait */
+} pd_stage_desc;
+
+/* Program item: PD_ITEM_WIDTH int32 fields, see executor.py:compile_program. */
+#define PD_ITEM_WIDTH 16
+enum pd_item_field {
+  PD_IT_OP = 0,        /* 0 forward, 1 backward */
+  PD_IT_STAGE = 1,
+  PD_IT_MB = 2,        /* 1-based minibatch id */
+  PD_IT_WORKER = 3,
+  PD_IT_VERSION = 4,   /* weight version read (ledger value) */
+  PD_IT_WSLOT = 5,     /* ring slot holding that version */
+  PD_IT_WNEW = 6,      /* backward: ring slot receiving version mb (commit) */
+  PD_IT_ACT = 7,       /* activation-stash slot of this minibatch */
+  PD_IT_XSLOT = 8,     /* inbox slot of the stage input (stage 0: data block) */
+  PD_IT_GSLOT = 9,     /* backward: gradient inbox slot (-1 at the last stage) */
+  PD_IT_OUT = 10,      /* forward: next stage's inbox slot; backward: previous stage's grad slot */
+  PD_IT_BLOCK = 11,    /* data / target block */
+  PD_IT_DEP = 12,      /* in-process producer item (index), -1 */
+  PD_IT_WAR = 13,      /* in-process item that must finish before PD_IT_OUT is overwritten, -1 */
+  PD_IT_RWAIT = 14,    /* cross-GPU: inbox flag value to wait for (0 = none) */
+  PD_IT_AWAIT = 15     /* cross-GPU: ack value to wait for before writing PD_IT_OUT (0 = none) */
+};
+
+typedef struct pd_runtime pd_runtime;
+typedef struct pd_record { int32_t item; int32_t pad; double t_start_ms; double t_end_ms; } pd_record;
+
+int pd_rt_create(int device, pd_runtime** out);
+int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc);
+int pd_rt_load_program(pd_runtime* rt, const int32_t* items, int n_items);
+/* Enqueue the whole program behind `stream` (everything joins back onto it).
+ * trace=1 records per-item device timestamps (pd_rt_records). */
+int pd_rt_run(pd_runtime* rt, void* stream, int trace);
+int pd_rt_records(pd_runtime* rt, pd_record* out, int cap, int* n_out);
+int pd_rt_destroy(pd_runtime* rt);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PD_B200_H */

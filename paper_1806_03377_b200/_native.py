@@ -1,0 +1,153 @@
+"""ctypes binding of libpd_b200.so (include/pd_b200.h).
+
+The product path has no CPU fallback: if the library is missing or cannot be
+loaded, every call raises. Return codes map onto the reference's exception
+types (PD_ERR_INVALID -> ValidationError, PD_ERR_TIMEOUT/DEADLOCK ->
+SimulationError, PD_ERR_CUDA -> NativeError).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import POINTER, Structure, c_double, c_float, c_int, c_int32, c_int64, c_void_p
+from pathlib import Path
+
+from .errors import NativeError, SimulationError, ValidationError
+
+LIB_PATH = Path(__file__).resolve().parent / "libpd_b200.so"
+
+PD_F32, PD_BF16 = 0, 1
+EPI_STORE, EPI_LOSS, EPI_MASK, EPI_SGD, EPI_GRADF32 = range(5)
+ITEM_WIDTH = 16
+(IT_OP, IT_STAGE, IT_MB, IT_WORKER, IT_VERSION, IT_WSLOT, IT_WNEW, IT_ACT, IT_XSLOT, IT_GSLOT, IT_OUT,
+ IT_BLOCK, IT_DEP, IT_WAR, IT_RWAIT, IT_AWAIT) = range(16)
+
+# Symbols include/pd_b200.h declares; tests check every one is exported.
+EXPORTED = (
+    "pd_abi_version", "pd_last_error", "pd_device_sm_count", "pd_gemm", "pd_bias_sgd", "pd_sgd_update",
+    "pd_flag_signal", "pd_flag_wait", "pd_ipc_get_handle", "pd_ipc_open", "pd_ipc_close",
+    "pd_enable_peer_access", "pd_rt_create", "pd_rt_add_stage", "pd_rt_load_program", "pd_rt_run",
+    "pd_rt_records", "pd_rt_destroy",
+)
+
+
+class Epilogue(Structure):
+    _fields_ = [
+        ("kind", c_int), ("out", c_void_p), ("ldo", c_int64), ("bias", c_void_p), ("relu", c_int),
+        ("mask", c_void_p), ("ldm", c_int64), ("target", c_void_p), ("ldt", c_int64), ("scale", c_float),
+        ("loss", c_void_p), ("master", c_void_p), ("ldw", c_int64), ("lr", c_float),
+    ]
+
+
+class StageDesc(Structure):
+    _fields_ = [
+        ("stage", c_int), ("n_layers", c_int), ("dims", POINTER(c_int64)), ("batch", c_int), ("dtype", c_int),
+        ("is_first", c_int), ("is_last", c_int), ("relu_last", c_int), ("ring_depth", c_int),
+        ("act_depth", c_int), ("in_depth", c_int), ("grad_depth", c_int), ("lr", c_float),
+        ("w_master", POINTER(c_void_p)), ("b_master", POINTER(c_void_p)), ("w_ring", POINTER(c_void_p)),
+        ("b_ring", POINTER(c_void_p)), ("act", POINTER(c_void_p)), ("act_in", POINTER(c_void_p)),
+        ("n_data_blocks", c_int), ("grad_in", POINTER(c_void_p)), ("dz_last", POINTER(c_void_p)),
+        ("target", POINTER(c_void_p)), ("loss", c_void_p), ("tmp", c_void_p * 2),
+        ("next_act_in", POINTER(c_void_p)), ("next_in_depth", c_int),
+        ("prev_grad_in", POINTER(c_void_p)), ("prev_grad_depth", c_int),
+        ("act_ready", c_void_p), ("act_ack_remote", c_void_p), ("next_act_ready", c_void_p),
+        ("next_act_ack", c_void_p), ("grad_ready", c_void_p), ("grad_ack_remote", c_void_p),
+        ("prev_grad_ready", c_void_p), ("prev_grad_ack", c_void_p), ("err_word", c_void_p),
+    ]
+
+
+class Record(Structure):
+    _fields_ = [("item", c_int32), ("pad", c_int32), ("t_start_ms", c_double), ("t_end_ms", c_double)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libpd_b200.so (built in-tree by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise NativeError(
+                f"{LIB_PATH} is missing: run __graft_entry__.build() (there is no CPU fallback)"
+            )
+        L = ctypes.CDLL(str(LIB_PATH))
+        L.pd_last_error.restype = ctypes.c_char_p
+        L.pd_gemm.argtypes = [c_int, c_void_p, c_int, c_int64, c_void_p, c_int, c_int64, c_int, c_int, c_int,
+                              POINTER(Epilogue), c_void_p]
+        L.pd_bias_sgd.argtypes = [c_int, c_void_p, c_int, c_int, c_int64, c_void_p, c_void_p, c_float, c_void_p]
+        L.pd_sgd_update.argtypes = [c_int, c_void_p, c_void_p, c_void_p, c_int64, c_float, c_void_p]
+        L.pd_flag_signal.argtypes = [c_void_p, c_int, c_void_p]
+        L.pd_flag_wait.argtypes = [c_void_p, c_int, c_void_p, c_void_p]
+        L.pd_ipc_get_handle.argtypes = [c_void_p, c_void_p]
+        L.pd_ipc_open.argtypes = [c_void_p, POINTER(c_void_p)]
+        L.pd_ipc_close.argtypes = [c_void_p]
+        L.pd_rt_create.argtypes = [c_int, POINTER(c_void_p)]
+        L.pd_rt_add_stage.argtypes = [c_void_p, POINTER(StageDesc)]
+        L.pd_rt_load_program.argtypes = [c_void_p, POINTER(c_int32), c_int]
+        L.pd_rt_run.argtypes = [c_void_p, c_void_p, c_int]
+        L.pd_rt_records.argtypes = [c_void_p, POINTER(Record), c_int, POINTER(c_int)]
+        L.pd_rt_destroy.argtypes = [c_void_p]
+        L.pd_device_sm_count.argtypes = [c_int, POINTER(c_int)]
+        _lib = L
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == 0:
+        return
+    msg = lib().pd_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if rc == 1:
+        raise ValidationError(text)
+    if rc in (3, 4):
+        raise SimulationError(text)
+    raise NativeError(text)
+
+
+def ptr(t) -> int:
+    """Raw device address of a torch tensor (or 0 for None)."""
+    return 0 if t is None else int(t.data_ptr())
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def dtype_code(torch_dtype) -> int:
+    import torch
+
+    if torch_dtype == torch.float32:
+        return PD_F32
+    if torch_dtype == torch.bfloat16:
+        return PD_BF16
+    raise ValidationError(f"unsupported dtype {torch_dtype}")
+
+
+def gemm(A, a_mn: bool, B, b_mn: bool, M: int, N: int, K: int, *, kind: int = EPI_STORE, out=None, ldo=None,
+         bias=None, relu=False, mask=None, ldm=None, target=None, ldt=None, scale=1.0, loss=None, master=None,
+         ldw=None, lr=0.0, stream=None) -> None:
+    """C[M,N] = sum_k A(m,k) B(n,k) + fused epilogue, on torch tensors (row-major, contiguous rows)."""
+    lda = A.stride(0)
+    ldb = B.stride(0)
+    ep = Epilogue(kind=kind, out=ptr(out), ldo=ldo if ldo is not None else (out.stride(0) if out is not None else 0),
+                  bias=ptr(bias), relu=int(bool(relu)), mask=ptr(mask),
+                  ldm=ldm if ldm is not None else (mask.stride(0) if mask is not None else 0),
+                  target=ptr(target), ldt=ldt if ldt is not None else (target.stride(0) if target is not None else 0),
+                  scale=scale, loss=ptr(loss), master=ptr(master),
+                  ldw=ldw if ldw is not None else (master.stride(0) if master is not None else 0), lr=lr)
+    check(lib().pd_gemm(dtype_code(A.dtype), ptr(A), int(a_mn), lda, ptr(B), int(b_mn), ldb, M, N, K,
+                        ctypes.byref(ep), stream_ptr(stream)), "pd_gemm")
+
+
+def bias_sgd(dz, rows: int, cols: int, b_master, b_out, lr: float, stream=None) -> None:
+    check(lib().pd_bias_sgd(dtype_code(dz.dtype), ptr(dz), rows, cols, dz.stride(0), ptr(b_master), ptr(b_out),
+                            lr, stream_ptr(stream)), "pd_bias_sgd")
+
+
+def sgd_update(master, grad, out, lr: float, stream=None) -> None:
+    check(lib().pd_sgd_update(dtype_code(out.dtype), ptr(master), ptr(grad), ptr(out), master.numel(), lr,
+                              stream_ptr(stream)), "pd_sgd_update")

@@ -1,0 +1,176 @@
+// GEMM epilogues shared by the tcgen05 and the SIMT GEMM.
+//
+// Every stage GEMM of the pipeline ends in one of these, so no separate
+// elementwise pass touches HBM for bias/ReLU, the ReLU-backward mask, the MSE
+// loss gradient or the SGD weight update:
+//   EPI_STORE : out = act(acc + bias)                          (forward, K1)
+//   EPI_LOSS  : d = acc + bias - target; out = d*scale;
+//               loss += 0.5*scale*sum(d^2)                     (last layer fwd + MSE bwd)
+//   EPI_MASK  : out = acc * (mask > 0)                         (dgrad + ReLU bwd, K2)
+//   EPI_SGD   : master -= lr*acc; out = cast(master)           (wgrad + SGD, K3; writes the
+//                                                               new weight version's ring slot)
+//   EPI_GRADF32: out(fp32) = acc                                (wgrad for replicated stages,
+//                                                               allreduced before the update)
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+
+namespace pd {
+
+enum EpiKind : int { EPI_STORE = 0, EPI_LOSS = 1, EPI_MASK = 2, EPI_SGD = 3, EPI_GRADF32 = 4 };
+
+struct EpiArgs {
+  void* out;            // activation dtype (fp32 for EPI_GRADF32)
+  int64_t ldo;
+  const float* bias;    // STORE / LOSS, per output column, nullable
+  int relu;             // STORE
+  const void* mask;     // MASK: the layer input X, activation dtype
+  int64_t ldm;
+  const float* target;  // LOSS
+  int64_t ldt;
+  float scale;          // LOSS: dL/dZ scale (1/B)
+  float* loss;          // LOSS: accumulates 0.5*scale*sum(d^2)
+  float* master;        // SGD: fp32 latest weights [M, N]
+  int64_t ldw;
+  float lr;             // SGD
+};
+
+template <typename T> __device__ __forceinline__ float to_f(T x);
+template <> __device__ __forceinline__ float to_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) {
+  return __bfloat162float(x);
+}
+template <typename T> __device__ __forceinline__ T from_f(float x);
+template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+
+// Per-element epilogue: returns the loss contribution (EPI_LOSS) or 0.
+template <int KIND, typename T>
+__device__ __forceinline__ float epi_elem(const EpiArgs& ep, int64_t r, int64_t c, float v) {
+  if constexpr (KIND == EPI_STORE) {
+    float x = v + (ep.bias ? ep.bias[c] : 0.f);
+    if (ep.relu) x = fmaxf(x, 0.f);
+    static_cast<T*>(ep.out)[r * ep.ldo + c] = from_f<T>(x);
+    return 0.f;
+  } else if constexpr (KIND == EPI_LOSS) {
+    float d = v + (ep.bias ? ep.bias[c] : 0.f) - ep.target[r * ep.ldt + c];
+    static_cast<T*>(ep.out)[r * ep.ldo + c] = from_f<T>(d * ep.scale);
+    return d * d;
+  } else if constexpr (KIND == EPI_MASK) {
+    float m = to_f<T>(static_cast<const T*>(ep.mask)[r * ep.ldm + c]);
+    static_cast<T*>(ep.out)[r * ep.ldo + c] = from_f<T>(m > 0.f ? v : 0.f);
+    return 0.f;
+  } else if constexpr (KIND == EPI_SGD) {
+    float w = ep.master[r * ep.ldw + c] - ep.lr * v;
+    ep.master[r * ep.ldw + c] = w;
+    static_cast<T*>(ep.out)[r * ep.ldo + c] = from_f<T>(w);
+    return 0.f;
+  } else {
+    static_cast<float*>(ep.out)[r * ep.ldo + c] = v;
+    return 0.f;
+  }
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void unpack_bf16x2(uint32_t u, float& a, float& b) {
+  __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&u);
+  a = __low2float(h);
+  b = __high2float(h);
+}
+
+// 32 consecutive columns [c0, c0+32) of row r, bf16 activations, vectorised.
+// Requires c0 + 32 <= N, 16-byte aligned rows (ld % 8 == 0) and c0 % 32 == 0.
+template <int KIND>
+__device__ __forceinline__ float epi_row32_bf16(const EpiArgs& ep, int64_t r, int64_t c0,
+                                                float (&v)[32]) {
+  float lsum = 0.f;
+  if constexpr (KIND == EPI_STORE) {
+    if (ep.bias) {
+      const float4* b4 = reinterpret_cast<const float4*>(ep.bias + c0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 b = __ldg(b4 + i);
+        v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
+      }
+    }
+    if (ep.relu) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+    }
+    uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + r * ep.ldo + c0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      o[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                        pack_bf16x2(v[8 * i + 4], v[8 * i + 5]),
+                        pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+  } else if constexpr (KIND == EPI_LOSS) {
+    const float4* t4 = reinterpret_cast<const float4*>(ep.target + r * ep.ldt + c0);
+    const float4* b4 = reinterpret_cast<const float4*>(ep.bias + c0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 t = t4[i];
+      float4 b = ep.bias ? __ldg(b4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[4 * i] += b.x - t.x; v[4 * i + 1] += b.y - t.y;
+      v[4 * i + 2] += b.z - t.z; v[4 * i + 3] += b.w - t.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) { lsum += v[i] * v[i]; v[i] *= ep.scale; }
+    uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + r * ep.ldo + c0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      o[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                        pack_bf16x2(v[8 * i + 4], v[8 * i + 5]),
+                        pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+  } else if constexpr (KIND == EPI_MASK) {
+    const uint4* m4 =
+        reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.mask) + r * ep.ldm + c0);
+    uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + r * ep.ldo + c0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint4 m = m4[i];
+      uint32_t mw[4] = {m.x, m.y, m.z, m.w};
+      uint32_t ow[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float a, b;
+        unpack_bf16x2(mw[j], a, b);
+        ow[j] = pack_bf16x2(a > 0.f ? v[8 * i + 2 * j] : 0.f, b > 0.f ? v[8 * i + 2 * j + 1] : 0.f);
+      }
+      o[i] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    }
+  } else if constexpr (KIND == EPI_SGD) {
+    float4* w4 = reinterpret_cast<float4*>(ep.master + r * ep.ldw + c0);
+    uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + r * ep.ldo + c0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 w = w4[i];
+      w.x -= ep.lr * v[4 * i]; w.y -= ep.lr * v[4 * i + 1];
+      w.z -= ep.lr * v[4 * i + 2]; w.w -= ep.lr * v[4 * i + 3];
+      w4[i] = w;
+      v[4 * i] = w.x; v[4 * i + 1] = w.y; v[4 * i + 2] = w.z; v[4 * i + 3] = w.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      o[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                        pack_bf16x2(v[8 * i + 4], v[8 * i + 5]),
+                        pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+  } else {
+    float4* o = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + r * ep.ldo + c0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  }
+  return lsum;
+}
+
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+}  // namespace pd

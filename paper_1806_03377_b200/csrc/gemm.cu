@@ -1,0 +1,367 @@
+// Stage GEMMs for the pipeline runtime.
+//
+//   C[M,N] = sum_k A(m,k) * B(n,k)   followed by one fused epilogue (epilogue.cuh)
+//
+// A operand "K-major": A(m,k) = A[m*lda + k]; "MN-major": A(m,k) = A[k*lda + m] (same for B).
+// With X=[batch,in], W=[out,in], dZ=[batch,out] (all row-major) the three passes of a
+// linear layer are:
+//   forward  Y  = X W^T : A=X  (K-major), B=W (K-major),  M=batch, N=out, K=in
+//   dgrad    dX = dZ W  : A=dZ (K-major), B=W (MN-major), M=batch, N=in,  K=out
+//   wgrad    dW = dZ^T X: A=dZ (MN-major),B=X (MN-major), M=out,   N=in,  K=batch
+// so no operand is ever transposed in HBM: the tcgen05 smem descriptors take both majors.
+//
+// bf16 path: persistent, warp-specialised tcgen05 kernel. TMA (128B swizzle) fills a
+// STAGES-deep smem ring; one elected thread issues tcgen05.mma (M=128, N=BN, K=16)
+// into a double-buffered TMEM accumulator; four epilogue warps drain TMEM with
+// tcgen05.ld while the next tile's MMAs run.
+// fp32 path (the 4-stage MLP-1024 fp32 config): SIMT FFMA GEMM with the same epilogues
+// (tcgen05 has no IEEE-fp32 kind; tf32 would not meet the fp32 tolerance).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cstdio>
+#include <mutex>
+
+#include "epilogue.cuh"
+#include "ptx.cuh"
+#include "pd_internal.h"
+
+namespace pd {
+
+// ============================================================== tcgen05 bf16 GEMM
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 64;        // 64 bf16 = 128 B = one swizzle row
+constexpr int TC_THREADS = 192;  // warp0 TMA, warp1 MMA (+TMEM alloc), warps2-5 epilogue
+
+template <int BN>
+struct TcCfg {
+  static constexpr int A_BYTES = TC_BM * TC_BK * 2;
+  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulator
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, bool A_MN, bool B_MN, int KIND>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              int M, int N, int K, EpiArgs ep) {
+  using C = TcCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tmem_full = empty + C::STAGES;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = warp_id();
+  const int num_m = (M + TC_BM - 1) / TC_BM;
+  const int num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n;
+  const int num_kb = (K + TC_BK - 1) / TC_BK;
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tmem_full[a], 1); mbar_init(&tmem_empty[a], 128); }
+    fence_barrier_init();
+    fence_proxy_async_smem();
+  }
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t % num_m) * TC_BM;
+        const int n0 = (t / num_m) * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          uint8_t* a_dst = sA + stage * C::A_BYTES;
+          uint8_t* b_dst = sB + stage * C::B_BYTES;
+          const int k0 = kb * TC_BK;
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int i = 0; i < TC_BM / 64; ++i) tma_load_2d(a_dst + i * 8192, &tmA, &full[stage], m0 + 64 * i, k0);
+          } else {
+            tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i) tma_load_2d(b_dst + i * 8192, &tmB, &full[stage], n0 + 64 * i, k0);
+          } else {
+            tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (single thread)
+    if (elect_one()) {
+      constexpr uint32_t idesc = make_idesc_bf16(TC_BM, BN, A_MN, B_MN);
+      // K-major SW128: 8-row core groups 1024 B apart (SBO); +32 B per K=16 step.
+      // MN-major SW128: 64-element MN atoms of 64 K-rows are 8 KB apart (LBO), 8-K-row
+      // groups 1024 B apart (SBO); +2048 B per K=16 step.
+      constexpr uint32_t A_LBO = A_MN ? 8192 : 16, A_SBO = 1024, A_KSTEP = A_MN ? 2048 : 32;
+      constexpr uint32_t B_LBO = B_MN ? 8192 : 16, B_SBO = 1024, B_KSTEP = B_MN ? 2048 : 32;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            uint64_t ad = make_sw128_desc(a_addr + k * A_KSTEP, A_LBO, A_SBO);
+            uint64_t bd = make_sw128_desc(b_addr + k * B_KSTEP, B_LBO, B_SBO);
+            umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tmem_full[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ---------------- epilogue warps: TMEM -> registers -> fused epilogue -> HBM
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    float lsum = 0.f;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int m0 = (t % num_m) * TC_BM;
+      const int n0 = (t / num_m) * BN;
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const int64_t r = m0 + 32 * q + lane_id();
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN + c * 32, v);
+        const int64_t c0 = n0 + c * 32;
+        if (r < M) {
+          if (c0 + 32 <= N) {
+            lsum += epi_row32_bf16<KIND>(ep, r, c0, v);
+          } else {
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < N) lsum += epi_elem<KIND, __nv_bfloat16>(ep, r, c0 + j, v[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tmem_empty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if constexpr (KIND == EPI_LOSS) {
+      lsum = warp_sum(lsum);
+      if (lane_id() == 0 && lsum != 0.f) atomicAdd(ep.loss, 0.5f * ep.scale * lsum);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ============================================================== SIMT GEMM (fp32 / bf16)
+constexpr int SM_BM = 32, SM_BN = 32, SM_BK = 32;
+
+template <typename T, int KIND>
+__global__ void __launch_bounds__(256)
+    k_gemm_simt(const T* __restrict__ A, int a_mn, int64_t lda, const T* __restrict__ B, int b_mn,
+                int64_t ldb, int M, int N, int K, EpiArgs ep) {
+  __shared__ float sA[SM_BK][SM_BM + 1];
+  __shared__ float sB[SM_BK][SM_BN + 1];
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.y * SM_BM, n0 = blockIdx.x * SM_BN;
+  const int tr = tid / 16, tc = tid % 16;  // 16x16 threads, 2x2 outputs each
+  float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+  for (int k0 = 0; k0 < K; k0 += SM_BK) {
+    for (int i = tid; i < SM_BM * SM_BK; i += 256) {
+      int mm, kk;
+      if (a_mn) { kk = i / SM_BM; mm = i % SM_BM; } else { mm = i / SM_BK; kk = i % SM_BK; }
+      const int m = m0 + mm, k = k0 + kk;
+      float x = 0.f;
+      if (m < M && k < K) x = to_f<T>(a_mn ? A[(int64_t)k * lda + m] : A[(int64_t)m * lda + k]);
+      sA[kk][mm] = x;
+    }
+    for (int i = tid; i < SM_BN * SM_BK; i += 256) {
+      int nn, kk;
+      if (b_mn) { kk = i / SM_BN; nn = i % SM_BN; } else { nn = i / SM_BK; kk = i % SM_BK; }
+      const int n = n0 + nn, k = k0 + kk;
+      float x = 0.f;
+      if (n < N && k < K) x = to_f<T>(b_mn ? B[(int64_t)k * ldb + n] : B[(int64_t)n * ldb + k]);
+      sB[kk][nn] = x;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < SM_BK; ++kk) {
+      const float a0 = sA[kk][tr], a1 = sA[kk][tr + 16];
+      const float b0 = sB[kk][tc], b1 = sB[kk][tc + 16];
+      acc[0][0] = fmaf(a0, b0, acc[0][0]);
+      acc[0][1] = fmaf(a0, b1, acc[0][1]);
+      acc[1][0] = fmaf(a1, b0, acc[1][0]);
+      acc[1][1] = fmaf(a1, b1, acc[1][1]);
+    }
+    __syncthreads();
+  }
+  float lsum = 0.f;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int m = m0 + tr + 16 * i, n = n0 + tc + 16 * j;
+      if (m < M && n < N) lsum += epi_elem<KIND, T>(ep, m, n, acc[i][j]);
+    }
+  if constexpr (KIND == EPI_LOSS) {
+    lsum = warp_sum(lsum);
+    if ((tid & 31) == 0 && lsum != 0.f) atomicAdd(ep.loss, 0.5f * ep.scale * lsum);
+  }
+}
+
+// ============================================================== host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map: `inner` contiguous elements per row, `outer` rows, row pitch ld elements.
+static int make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                    uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return set_error(PD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(PD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return 0;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int BN, bool A_MN, bool B_MN, int KIND>
+static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiArgs& ep,
+                     cudaStream_t st) {
+  using C = TcCfg<BN>;
+  auto kern = k_gemm_tc<BN, A_MN, B_MN, KIND>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
+      return set_error(PD_ERR_CUDA, "cudaFuncSetAttribute(smem=%d) failed", C::SMEM_BYTES);
+    attr_set = true;
+  }
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, TC_THREADS, C::SMEM_BYTES, st>>>(ta, tb, M, N, K, ep);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(PD_ERR_CUDA, "tcgen05 gemm launch: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+template <bool A_MN, bool B_MN>
+static int dispatch_kind(int kind, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+                         const EpiArgs& ep, cudaStream_t st) {
+  switch (kind) {
+    case EPI_STORE: return launch_tc<256, A_MN, B_MN, EPI_STORE>(ta, tb, M, N, K, ep, st);
+    case EPI_LOSS: return launch_tc<256, A_MN, B_MN, EPI_LOSS>(ta, tb, M, N, K, ep, st);
+    case EPI_MASK: return launch_tc<256, A_MN, B_MN, EPI_MASK>(ta, tb, M, N, K, ep, st);
+    case EPI_SGD: return launch_tc<256, A_MN, B_MN, EPI_SGD>(ta, tb, M, N, K, ep, st);
+    case EPI_GRADF32: return launch_tc<256, A_MN, B_MN, EPI_GRADF32>(ta, tb, M, N, K, ep, st);
+  }
+  return set_error(PD_ERR_INVALID, "unknown epilogue kind %d", kind);
+}
+
+int gemm_bf16_tc(const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M, int N,
+                 int K, int kind, const EpiArgs& ep, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return set_error(PD_ERR_INVALID, "gemm: empty shape %dx%dx%d", M, N, K);
+  if ((lda % 8) || (ldb % 8) || (reinterpret_cast<uintptr_t>(A) % 16) || (reinterpret_cast<uintptr_t>(B) % 16))
+    return set_error(PD_ERR_INVALID, "gemm: operands must be 16-byte aligned with ld %% 8 == 0");
+  if ((kind != EPI_GRADF32 && (ep.ldo % 8)) || (reinterpret_cast<uintptr_t>(ep.out) % 16))
+    return set_error(PD_ERR_INVALID, "gemm: output must be 16-byte aligned with ld %% 8 == 0");
+  CUtensorMap ta, tb;
+  int rc;
+  if (a_mn) rc = make_map(&ta, A, (uint64_t)M, (uint64_t)K, lda, 64, 64);
+  else rc = make_map(&ta, A, (uint64_t)K, (uint64_t)M, lda, 64, TC_BM);
+  if (rc) return rc;
+  if (b_mn) rc = make_map(&tb, B, (uint64_t)N, (uint64_t)K, ldb, 64, 64);
+  else rc = make_map(&tb, B, (uint64_t)K, (uint64_t)N, ldb, 64, 256);
+  if (rc) return rc;
+  if (!a_mn && !b_mn) return dispatch_kind<false, false>(kind, ta, tb, M, N, K, ep, st);
+  if (!a_mn && b_mn) return dispatch_kind<false, true>(kind, ta, tb, M, N, K, ep, st);
+  if (a_mn && !b_mn) return dispatch_kind<true, false>(kind, ta, tb, M, N, K, ep, st);
+  return dispatch_kind<true, true>(kind, ta, tb, M, N, K, ep, st);
+}
+
+template <typename T>
+static int simt(const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M, int N, int K,
+                int kind, const EpiArgs& ep, cudaStream_t st) {
+  dim3 grid((N + SM_BN - 1) / SM_BN, (M + SM_BM - 1) / SM_BM);
+  const T* a = static_cast<const T*>(A);
+  const T* b = static_cast<const T*>(B);
+  switch (kind) {
+    case EPI_STORE: k_gemm_simt<T, EPI_STORE><<<grid, 256, 0, st>>>(a, a_mn, lda, b, b_mn, ldb, M, N, K, ep); break;
+    case EPI_LOSS: k_gemm_simt<T, EPI_LOSS><<<grid, 256, 0, st>>>(a, a_mn, lda, b, b_mn, ldb, M, N, K, ep); break;
+    case EPI_MASK: k_gemm_simt<T, EPI_MASK><<<grid, 256, 0, st>>>(a, a_mn, lda, b, b_mn, ldb, M, N, K, ep); break;
+    case EPI_SGD: k_gemm_simt<T, EPI_SGD><<<grid, 256, 0, st>>>(a, a_mn, lda, b, b_mn, ldb, M, N, K, ep); break;
+    case EPI_GRADF32: k_gemm_simt<T, EPI_GRADF32><<<grid, 256, 0, st>>>(a, a_mn, lda, b, b_mn, ldb, M, N, K, ep); break;
+    default: return set_error(PD_ERR_INVALID, "unknown epilogue kind %d", kind);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(PD_ERR_CUDA, "simt gemm launch: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+int gemm_simt(int dtype, const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M, int N,
+              int K, int kind, const EpiArgs& ep, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return set_error(PD_ERR_INVALID, "gemm: empty shape %dx%dx%d", M, N, K);
+  if (dtype == PD_F32) return simt<float>(A, a_mn, lda, B, b_mn, ldb, M, N, K, kind, ep, st);
+  if (dtype == PD_BF16) return simt<__nv_bfloat16>(A, a_mn, lda, B, b_mn, ldb, M, N, K, kind, ep, st);
+  return set_error(PD_ERR_INVALID, "unknown dtype %d", dtype);
+}
+
+}  // namespace pd

@@ -1,0 +1,183 @@
+// Elementwise / reduction kernels, cross-GPU flags, error state and the C ABI wrappers
+// for single kernels (include/pd_b200.h).
+#include <cuda_runtime.h>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "pd_internal.h"
+#include "ptx.cuh"
+
+namespace pd {
+
+static thread_local char g_err[1024] = {0};
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int gemm(int dtype, const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M, int N, int K,
+         int kind, const EpiArgs& ep, cudaStream_t st) {
+  if (dtype == PD_BF16) return gemm_bf16_tc(A, a_mn, lda, B, b_mn, ldb, M, N, K, kind, ep, st);
+  if (dtype == PD_F32) return gemm_simt(PD_F32, A, a_mn, lda, B, b_mn, ldb, M, N, K, kind, ep, st);
+  return set_error(PD_ERR_INVALID, "unknown dtype %d", dtype);
+}
+
+// ---------------------------------------------------------------- bias gradient + SGD
+// Block = 32 columns x 16 row groups; coalesced across the 32 lanes of each row.
+template <typename T>
+__global__ void __launch_bounds__(512)
+    k_bias_sgd(const T* __restrict__ dz, int rows, int cols, int64_t ld, float* __restrict__ bm,
+               float* __restrict__ bo, float lr) {
+  __shared__ float part[16][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (c < cols)
+    for (int r = grp; r < rows; r += 16) s += to_f<T>(dz[(int64_t)r * ld + c]);
+  part[grp][lane] = s;
+  __syncthreads();
+  if (grp == 0 && c < cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int g = 0; g < 16; ++g) t += part[g][lane];
+    const float b = bm[c] - lr * t;
+    bm[c] = b;
+    bo[c] = b;
+  }
+}
+
+int bias_sgd(int dtype, const void* dz, int rows, int cols, int64_t ld, float* b_master, float* b_out, float lr,
+             cudaStream_t st) {
+  dim3 grid((cols + 31) / 32);
+  if (dtype == PD_BF16)
+    k_bias_sgd<__nv_bfloat16><<<grid, 512, 0, st>>>(static_cast<const __nv_bfloat16*>(dz), rows, cols, ld,
+                                                     b_master, b_out, lr);
+  else
+    k_bias_sgd<float><<<grid, 512, 0, st>>>(static_cast<const float*>(dz), rows, cols, ld, b_master, b_out, lr);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "bias_sgd: %s", cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- SGD on a flat buffer
+template <typename T>
+__global__ void k_sgd(float* __restrict__ m, const float* __restrict__ g, T* __restrict__ o, int64_t n, float lr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float w = m[i] - lr * g[i];
+    m[i] = w;
+    o[i] = from_f<T>(w);
+  }
+}
+
+int sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n, float lr, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = sms * 8;
+  if (dtype == PD_BF16)
+    k_sgd<__nv_bfloat16><<<grid, 256, 0, st>>>(master, grad, static_cast<__nv_bfloat16*>(out), n, lr);
+  else
+    k_sgd<float><<<grid, 256, 0, st>>>(master, grad, static_cast<float*>(out), n, lr);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "sgd_update: %s", cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- flags
+__global__ void k_flag_signal(int* flag, int v) {
+  __threadfence_system();
+  st_release_sys(flag, v);
+}
+
+// Bounded spin: ~10 s at %globaltimer resolution, then report through err_word so the host
+// raises SimulationError instead of hanging the GPU.
+__global__ void k_flag_wait(const int* flag, int v, int* err) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (ld_acquire_sys(const_cast<volatile int*>(flag)) < v) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 10ull * 1000 * 1000 * 1000) {
+      if (err) atomicExch(err, v);
+      break;
+    }
+    __nanosleep(200);
+  }
+}
+
+int flag_signal(int* flag, int value, cudaStream_t st) {
+  k_flag_signal<<<1, 1, 0, st>>>(flag, value);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "flag_signal: %s", cudaGetErrorString(e));
+}
+int flag_wait(const int* flag, int value, int* err_word, cudaStream_t st) {
+  k_flag_wait<<<1, 1, 0, st>>>(flag, value, err_word);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "flag_wait: %s", cudaGetErrorString(e));
+}
+
+}  // namespace pd
+
+// ==================================================================== C ABI
+using namespace pd;
+
+extern "C" {
+
+int pd_abi_version(void) { return PD_ABI_VERSION; }
+const char* pd_last_error(void) { return g_err; }
+
+int pd_device_sm_count(int device, int* out) {
+  cudaError_t e = cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, device);
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "sm count: %s", cudaGetErrorString(e));
+}
+
+int pd_gemm(int dtype, const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M, int N,
+            int K, const pd_epilogue* ep, void* stream) {
+  if (!ep) return set_error(PD_ERR_INVALID, "pd_gemm: null epilogue");
+  return gemm(dtype, A, a_mn, lda, B, b_mn, ldb, M, N, K, ep->kind, to_epi(*ep), static_cast<cudaStream_t>(stream));
+}
+
+int pd_bias_sgd(int dtype, const void* dz, int rows, int cols, int64_t ld, float* b_master, float* b_out, float lr,
+                void* stream) {
+  return bias_sgd(dtype, dz, rows, cols, ld, b_master, b_out, lr, static_cast<cudaStream_t>(stream));
+}
+
+int pd_sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n, float lr, void* stream) {
+  return sgd_update(dtype, master, grad, out, n, lr, static_cast<cudaStream_t>(stream));
+}
+
+int pd_flag_signal(int* flag, int value, void* stream) {
+  return flag_signal(flag, value, static_cast<cudaStream_t>(stream));
+}
+int pd_flag_wait(const int* flag, int value, int* err_word, void* stream) {
+  return flag_wait(flag, value, err_word, static_cast<cudaStream_t>(stream));
+}
+
+int pd_ipc_get_handle(const void* dev_ptr, void* handle_out64) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+  if (e != cudaSuccess) return set_error(PD_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  memcpy(handle_out64, &h, sizeof(h));
+  return 0;
+}
+int pd_ipc_open(const void* handle64, void** dev_ptr_out) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+}
+int pd_ipc_close(void* dev_ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+}
+int pd_enable_peer_access(int peer_device) {
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) { cudaGetLastError(); return 0; }
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "enable peer access: %s", cudaGetErrorString(e));
+}
+
+}  // extern "C"

@@ -1,0 +1,37 @@
+// Internal declarations shared by the CUDA translation units of libpd_b200.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/pd_b200.h"
+#include "epilogue.cuh"
+
+namespace pd {
+
+// Records the message for pd_last_error() and returns `code`.
+int set_error(int code, const char* fmt, ...);
+
+int gemm_bf16_tc(const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M, int N,
+                 int K, int kind, const EpiArgs& ep, cudaStream_t st);
+int gemm_simt(int dtype, const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M, int N,
+              int K, int kind, const EpiArgs& ep, cudaStream_t st);
+
+// Dispatch: bf16 -> tcgen05, fp32 -> SIMT.
+int gemm(int dtype, const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M, int N, int K,
+         int kind, const EpiArgs& ep, cudaStream_t st);
+
+int bias_sgd(int dtype, const void* dz, int rows, int cols, int64_t ld, float* b_master, float* b_out, float lr,
+             cudaStream_t st);
+int sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n, float lr, cudaStream_t st);
+int flag_signal(int* flag, int value, cudaStream_t st);
+int flag_wait(const int* flag, int value, int* err_word, cudaStream_t st);
+
+inline EpiArgs to_epi(const pd_epilogue& e) {
+  EpiArgs a{};
+  a.out = e.out; a.ldo = e.ldo; a.bias = e.bias; a.relu = e.relu; a.mask = e.mask; a.ldm = e.ldm;
+  a.target = e.target; a.ldt = e.ldt; a.scale = e.scale; a.loss = e.loss; a.master = e.master;
+  a.ldw = e.ldw; a.lr = e.lr;
+  return a;
+}
+
+}  // namespace pd

@@ -1,0 +1,312 @@
+// Device executor for a compiled 1F1B-RR program (include/pd_b200.h, "executor").
+//
+// Takes over the reference's discrete-event engine (simulator.py:150-357): instead of
+// advancing simulated clocks, each hosted stage owns a CUDA stream and every program
+// item (one forward or backward pass of one minibatch at one stage) becomes the
+// stage's GEMM chain on that stream.  Readiness (_try_start's ready[] gate,
+// simulator.py:255-260) becomes a cudaStreamWaitEvent on the producing item when the
+// neighbour stage lives in this process, or a device-side acquire-poll on an inbox
+// flag written by the neighbour GPU.  Version selection and commits are resolved
+// ahead of time into ring slots (PD_IT_WSLOT / PD_IT_WNEW): the wgrad epilogue writes
+// version mb into its slot (commit, simulator.py:315).
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "pd_internal.h"
+
+namespace {
+
+using namespace pd;
+
+struct Stage {
+  pd_stage_desc d{};
+  std::vector<int64_t> dims;
+  std::vector<float*> w_master, b_master, b_ring;
+  std::vector<void*> w_ring, act, act_in, grad_in, dz_last, next_act_in, prev_grad_in;
+  std::vector<const float*> target;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_done = nullptr;
+};
+
+template <typename T>
+std::vector<T> copy_arr(const T* p, int64_t n) {
+  return p && n > 0 ? std::vector<T>(p, p + n) : std::vector<T>();
+}
+
+}  // namespace
+
+struct pd_runtime {
+  int device = 0;
+  int epoch = 0;
+  std::map<int, Stage> stages;
+  std::vector<int32_t> items;
+  std::vector<cudaEvent_t> ev_start, ev_end;
+  cudaEvent_t ev0 = nullptr;
+  bool traced = false;
+};
+
+namespace {
+
+#define PD_CHECK(x)                                                                               \
+  do {                                                                                            \
+    cudaError_t e_ = (x);                                                                         \
+    if (e_ != cudaSuccess) return set_error(PD_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+  } while (0)
+#define PD_TRY(x)          \
+  do {                     \
+    int rc_ = (x);         \
+    if (rc_) return rc_;   \
+  } while (0)
+
+inline int flag_val(int epoch, int mb) { return epoch * 65536 + mb; }
+
+int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
+  const pd_stage_desc& d = S.d;
+  const int L = d.n_layers, B = d.batch;
+  const int wslot = it[PD_IT_WSLOT], act = it[PD_IT_ACT], mb = it[PD_IT_MB];
+  const void* x = d.is_first ? S.act_in[it[PD_IT_BLOCK]] : S.act_in[it[PD_IT_XSLOT]];
+  for (int l = 0; l < L; ++l) {
+    const int K = (int)S.dims[l], N = (int)S.dims[l + 1];
+    EpiArgs ep{};
+    ep.bias = S.b_ring[(size_t)l * d.ring_depth + wslot];
+    ep.ldo = N;
+    int kind = EPI_STORE;
+    if (l < L - 1) {
+      ep.out = S.act[(size_t)l * d.act_depth + act];
+      ep.relu = 1;
+    } else if (d.is_last) {
+      kind = EPI_LOSS;
+      ep.out = S.dz_last[act];
+      ep.target = S.target[it[PD_IT_BLOCK]];
+      ep.ldt = N;
+      ep.scale = 1.0f / (float)B;
+      ep.loss = d.loss + mb;
+    } else {
+      ep.out = S.next_act_in[it[PD_IT_OUT]];
+      ep.relu = d.relu_last;
+    }
+    const void* W = S.w_ring[(size_t)l * d.ring_depth + wslot];
+    PD_TRY(gemm(d.dtype, x, 0, K, W, 0, K, B, N, K, kind, ep, S.stream));
+    x = ep.out;
+  }
+  (void)rt;
+  return 0;
+}
+
+int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
+  const pd_stage_desc& d = S.d;
+  const int L = d.n_layers, B = d.batch;
+  const int wslot = it[PD_IT_WSLOT], wnew = it[PD_IT_WNEW], act = it[PD_IT_ACT];
+  const void* dz = d.is_last ? S.dz_last[act] : S.grad_in[it[PD_IT_GSLOT]];
+  for (int l = L - 1; l >= 0; --l) {
+    const int Kin = (int)S.dims[l], Nout = (int)S.dims[l + 1];
+    const void* X = (l == 0) ? (d.is_first ? S.act_in[it[PD_IT_BLOCK]] : S.act_in[it[PD_IT_XSLOT]])
+                             : S.act[(size_t)(l - 1) * d.act_depth + act];
+    const void* Wst = S.w_ring[(size_t)l * d.ring_depth + wslot];
+    void* out = nullptr;
+    if (!(d.is_first && l == 0)) {
+      // dgrad + ReLU-backward: dZ_{l-1} = (dZ_l W_l^{stashed}) * (X_l > 0)
+      out = (l == 0) ? S.prev_grad_in[it[PD_IT_OUT]] : d.tmp[l & 1];
+      EpiArgs ep{};
+      ep.out = out;
+      ep.ldo = Kin;
+      ep.mask = X;
+      ep.ldm = Kin;
+      PD_TRY(gemm(d.dtype, dz, 0, Nout, Wst, 1, Kin, B, Kin, Nout, EPI_MASK, ep, S.stream));
+    }
+    if (wnew >= 0) {
+      // wgrad + SGD onto the latest weights, written as version mb into ring slot wnew
+      EpiArgs ep{};
+      ep.master = S.w_master[l];
+      ep.ldw = Kin;
+      ep.out = S.w_ring[(size_t)l * d.ring_depth + wnew];
+      ep.ldo = Kin;
+      ep.lr = d.lr;
+      PD_TRY(gemm(d.dtype, dz, 1, Nout, X, 1, Kin, Nout, Kin, B, EPI_SGD, ep, S.stream));
+      PD_TRY(bias_sgd(d.dtype, dz, B, Nout, Nout, S.b_master[l], S.b_ring[(size_t)l * d.ring_depth + wnew], d.lr,
+                      S.stream));
+    }
+    dz = out;
+  }
+  (void)rt;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pd_rt_create(int device, pd_runtime** out) {
+  if (!out) return set_error(PD_ERR_INVALID, "pd_rt_create: null out");
+  PD_CHECK(cudaSetDevice(device));
+  auto* rt = new pd_runtime();
+  rt->device = device;
+  if (cudaEventCreate(&rt->ev0) != cudaSuccess) {
+    delete rt;
+    return set_error(PD_ERR_CUDA, "cudaEventCreate failed");
+  }
+  *out = rt;
+  return 0;
+}
+
+int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc) {
+  if (!rt || !desc) return set_error(PD_ERR_INVALID, "pd_rt_add_stage: null argument");
+  const pd_stage_desc& d = *desc;
+  if (d.n_layers < 1 || d.batch < 1 || d.ring_depth < 1 || d.act_depth < 1)
+    return set_error(PD_ERR_INVALID, "stage %d: bad descriptor (layers=%d batch=%d ring=%d act=%d)", d.stage,
+                     d.n_layers, d.batch, d.ring_depth, d.act_depth);
+  if (d.dtype != PD_F32 && d.dtype != PD_BF16) return set_error(PD_ERR_INVALID, "stage %d: bad dtype", d.stage);
+  if (rt->stages.count(d.stage)) return set_error(PD_ERR_INVALID, "stage %d added twice", d.stage);
+  Stage S;
+  S.d = d;
+  const int L = d.n_layers;
+  S.dims = copy_arr(d.dims, L + 1);
+  S.w_master = copy_arr(d.w_master, L);
+  S.b_master = copy_arr(d.b_master, L);
+  S.w_ring = copy_arr(d.w_ring, (int64_t)L * d.ring_depth);
+  S.b_ring = copy_arr(d.b_ring, (int64_t)L * d.ring_depth);
+  S.act = copy_arr(d.act, (int64_t)(L - 1) * d.act_depth);
+  S.act_in = copy_arr(d.act_in, d.is_first ? d.n_data_blocks : d.in_depth);
+  if (!d.is_last) S.grad_in = copy_arr(d.grad_in, d.grad_depth);
+  if (d.is_last) {
+    S.dz_last = copy_arr(d.dz_last, d.act_depth);
+    S.target = copy_arr(d.target, d.n_data_blocks);
+  }
+  // neighbour inbox views: sizes are implied by the program's slot indices
+  if (!d.is_last) S.next_act_in = copy_arr(d.next_act_in, d.next_in_depth);
+  if (!d.is_first) S.prev_grad_in = copy_arr(d.prev_grad_in, d.prev_grad_depth);
+  S.d.dims = nullptr;
+  PD_CHECK(cudaSetDevice(rt->device));
+  PD_CHECK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
+  PD_CHECK(cudaEventCreateWithFlags(&S.ev_done, cudaEventDisableTiming));
+  rt->stages.emplace(d.stage, std::move(S));
+  return 0;
+}
+
+int pd_rt_load_program(pd_runtime* rt, const int32_t* items, int n_items) {
+  if (!rt || (!items && n_items)) return set_error(PD_ERR_INVALID, "pd_rt_load_program: null argument");
+  for (int i = 0; i < n_items; ++i) {
+    const int32_t* it = items + (size_t)i * PD_ITEM_WIDTH;
+    auto f = rt->stages.find(it[PD_IT_STAGE]);
+    if (f == rt->stages.end())
+      return set_error(PD_ERR_INVALID, "item %d: stage %d is not hosted here", i, it[PD_IT_STAGE]);
+    const Stage& S = f->second;
+    if (it[PD_IT_DEP] >= i || it[PD_IT_WAR] >= i)
+      return set_error(PD_ERR_INVALID, "item %d: dependency %d/%d not issued earlier (program not topological)", i,
+                       it[PD_IT_DEP], it[PD_IT_WAR]);
+    if (it[PD_IT_WSLOT] < 0 || it[PD_IT_WSLOT] >= S.d.ring_depth || it[PD_IT_WNEW] >= S.d.ring_depth ||
+        it[PD_IT_ACT] < 0 || it[PD_IT_ACT] >= S.d.act_depth)
+      return set_error(PD_ERR_INVALID, "item %d: slot out of range", i);
+    const bool fwd = it[PD_IT_OP] == 0;
+    if (fwd && !S.d.is_last && (it[PD_IT_OUT] < 0 || it[PD_IT_OUT] >= (int)S.next_act_in.size()))
+      return set_error(PD_ERR_INVALID, "item %d: forward outbox slot %d out of range", i, it[PD_IT_OUT]);
+    if (!fwd && !S.d.is_first && (it[PD_IT_OUT] < 0 || it[PD_IT_OUT] >= (int)S.prev_grad_in.size()))
+      return set_error(PD_ERR_INVALID, "item %d: backward outbox slot %d out of range", i, it[PD_IT_OUT]);
+  }
+  rt->items.assign(items, items + (size_t)n_items * PD_ITEM_WIDTH);
+  for (auto e : rt->ev_start) cudaEventDestroy(e);
+  for (auto e : rt->ev_end) cudaEventDestroy(e);
+  rt->ev_start.assign(n_items, nullptr);
+  rt->ev_end.assign(n_items, nullptr);
+  PD_CHECK(cudaSetDevice(rt->device));
+  for (int i = 0; i < n_items; ++i) {
+    PD_CHECK(cudaEventCreate(&rt->ev_start[i]));
+    PD_CHECK(cudaEventCreate(&rt->ev_end[i]));
+  }
+  return 0;
+}
+
+int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
+  if (!rt) return set_error(PD_ERR_INVALID, "pd_rt_run: null runtime");
+  cudaStream_t main = static_cast<cudaStream_t>(stream);
+  PD_CHECK(cudaSetDevice(rt->device));
+  rt->epoch += 1;
+  rt->traced = trace != 0;
+  PD_CHECK(cudaEventRecord(rt->ev0, main));
+  for (auto& kv : rt->stages) {
+    Stage& S = kv.second;
+    PD_CHECK(cudaStreamWaitEvent(S.stream, rt->ev0, 0));
+    if (S.d.is_last && S.d.loss) {
+      // losses are indexed by minibatch id; the program's largest id bounds the buffer
+      int max_mb = 0;
+      for (size_t i = 0; i < rt->items.size(); i += PD_ITEM_WIDTH) max_mb = std::max(max_mb, rt->items[i + PD_IT_MB]);
+      PD_CHECK(cudaMemsetAsync(S.d.loss, 0, sizeof(float) * (size_t)(max_mb + 1), S.stream));
+    }
+  }
+  const int n = (int)(rt->items.size() / PD_ITEM_WIDTH);
+  for (int i = 0; i < n; ++i) {
+    const int32_t* it = rt->items.data() + (size_t)i * PD_ITEM_WIDTH;
+    Stage& S = rt->stages[it[PD_IT_STAGE]];
+    const bool fwd = it[PD_IT_OP] == 0;
+    const int dep = it[PD_IT_DEP], war = it[PD_IT_WAR];
+    if (dep >= 0) PD_CHECK(cudaStreamWaitEvent(S.stream, rt->ev_end[dep], 0));
+    if (war >= 0) PD_CHECK(cudaStreamWaitEvent(S.stream, rt->ev_end[war], 0));
+    if (it[PD_IT_RWAIT] > 0) {
+      int* flag = fwd ? S.d.act_ready + it[PD_IT_XSLOT] : S.d.grad_ready + it[PD_IT_GSLOT];
+      PD_TRY(flag_wait(flag, flag_val(rt->epoch, it[PD_IT_RWAIT]), S.d.err_word, S.stream));
+    }
+    if (it[PD_IT_AWAIT] > 0) {
+      int* flag = fwd ? S.d.next_act_ack + it[PD_IT_OUT] : S.d.prev_grad_ack + it[PD_IT_OUT];
+      PD_TRY(flag_wait(flag, flag_val(rt->epoch, it[PD_IT_AWAIT]), S.d.err_word, S.stream));
+    }
+    if (rt->traced) PD_CHECK(cudaEventRecord(rt->ev_start[i], S.stream));
+    PD_TRY(fwd ? run_forward(rt, S, it) : run_backward(rt, S, it));
+    // cross-GPU hand-off: publish the payload the epilogue stored into the peer inbox
+    const int mb = it[PD_IT_MB];
+    if (fwd && !S.d.is_last && S.d.next_act_ready)
+      PD_TRY(flag_signal(S.d.next_act_ready + it[PD_IT_OUT], flag_val(rt->epoch, mb), S.stream));
+    if (!fwd && !S.d.is_first && S.d.prev_grad_ready)
+      PD_TRY(flag_signal(S.d.prev_grad_ready + it[PD_IT_OUT], flag_val(rt->epoch, mb), S.stream));
+    if (!fwd && !S.d.is_first && S.d.act_ack_remote)
+      PD_TRY(flag_signal(S.d.act_ack_remote + it[PD_IT_XSLOT], flag_val(rt->epoch, mb), S.stream));
+    if (!fwd && !S.d.is_last && S.d.grad_ack_remote)
+      PD_TRY(flag_signal(S.d.grad_ack_remote + it[PD_IT_GSLOT], flag_val(rt->epoch, mb), S.stream));
+    PD_CHECK(cudaEventRecord(rt->ev_end[i], S.stream));
+  }
+  for (auto& kv : rt->stages) {
+    Stage& S = kv.second;
+    PD_CHECK(cudaEventRecord(S.ev_done, S.stream));
+    PD_CHECK(cudaStreamWaitEvent(main, S.ev_done, 0));
+  }
+  return 0;
+}
+
+int pd_rt_records(pd_runtime* rt, pd_record* out, int cap, int* n_out) {
+  if (!rt || !n_out) return set_error(PD_ERR_INVALID, "pd_rt_records: null argument");
+  if (!rt->traced) return set_error(PD_ERR_INVALID, "pd_rt_records: last run was not traced");
+  const int n = (int)(rt->items.size() / PD_ITEM_WIDTH);
+  PD_CHECK(cudaSetDevice(rt->device));
+  int k = 0;
+  for (int i = 0; i < n && k < cap; ++i, ++k) {
+    float a = 0.f, b = 0.f;
+    PD_CHECK(cudaEventSynchronize(rt->ev_end[i]));
+    PD_CHECK(cudaEventElapsedTime(&a, rt->ev0, rt->ev_start[i]));
+    PD_CHECK(cudaEventElapsedTime(&b, rt->ev0, rt->ev_end[i]));
+    out[k].item = i;
+    out[k].pad = 0;
+    out[k].t_start_ms = a;
+    out[k].t_end_ms = b;
+  }
+  *n_out = k;
+  return 0;
+}
+
+int pd_rt_destroy(pd_runtime* rt) {
+  if (!rt) return 0;
+  cudaSetDevice(rt->device);
+  for (auto& kv : rt->stages) {
+    cudaStreamSynchronize(kv.second.stream);
+    cudaStreamDestroy(kv.second.stream);
+    cudaEventDestroy(kv.second.ev_done);
+  }
+  for (auto e : rt->ev_start) cudaEventDestroy(e);
+  for (auto e : rt->ev_end) cudaEventDestroy(e);
+  if (rt->ev0) cudaEventDestroy(rt->ev0);
+  delete rt;
+  return 0;
+}
+
+}  // extern "C"

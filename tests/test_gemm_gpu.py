@@ -1,0 +1,111 @@
+"""Stage-GEMM kernels (tcgen05 bf16, SIMT fp32) vs a plain PyTorch fp32 reference."""
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_1806_03377_b200 import _native as nat  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(256, 512, 192), (128, 256, 64), (100, 300, 72), (32, 1024, 1024), (384, 768, 1000), (2048, 2048, 512)]
+
+
+def operands(M, N, K, a_mn, b_mn, dtype, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    a = torch.randn((K, M) if a_mn else (M, K), device="cuda", generator=g).to(dtype)
+    b = torch.randn((K, N) if b_mn else (N, K), device="cuda", generator=g).to(dtype)
+    A = (a.t() if a_mn else a).float()  # logical [M, K]
+    Bm = (b.t() if b_mn else b).float()  # logical [N, K]
+    return a, b, A @ Bm.t()
+
+
+def tol(dtype, K):
+    # fp32 accumulate in both; inputs identical, so only summation order differs (+ bf16 output rounding)
+    return (2e-2, 2e-2) if dtype == torch.bfloat16 else (1e-4 * max(1, K) ** 0.5, 1e-4)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_gemm_store_bias_relu(dtype, a_mn, b_mn, M, N, K):
+    a, b, ref = operands(M, N, K, a_mn, b_mn, dtype)
+    bias = torch.randn(N, device="cuda")
+    out = torch.empty(M, N, device="cuda", dtype=dtype)
+    nat.gemm(a, a_mn, b, b_mn, M, N, K, kind=nat.EPI_STORE, out=out, bias=bias, relu=True)
+    torch.cuda.synchronize()
+    expect = torch.relu(ref + bias)
+    atol, rtol = tol(dtype, K)
+    scale = max(1.0, K ** 0.5)
+    torch.testing.assert_close(out.float(), expect, atol=atol * scale, rtol=rtol)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_gemm_mask_dgrad(dtype):
+    M, N, K = 256, 512, 384
+    a, b, ref = operands(M, N, K, False, True, dtype, seed=1)
+    mask = torch.randn(M, N, device="cuda").to(dtype)
+    out = torch.empty(M, N, device="cuda", dtype=dtype)
+    nat.gemm(a, False, b, True, M, N, K, kind=nat.EPI_MASK, out=out, mask=mask)
+    torch.cuda.synchronize()
+    expect = ref * (mask.float() > 0)
+    atol, rtol = tol(dtype, K)
+    torch.testing.assert_close(out.float(), expect, atol=atol * K ** 0.5, rtol=rtol)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_gemm_sgd_wgrad(dtype):
+    M, N, K = 512, 256, 96  # out, in, batch
+    a, b, ref = operands(M, N, K, True, True, dtype, seed=2)
+    master = torch.randn(M, N, device="cuda")
+    m0 = master.clone()
+    ring = torch.empty(M, N, device="cuda", dtype=dtype)
+    lr = 0.01
+    nat.gemm(a, True, b, True, M, N, K, kind=nat.EPI_SGD, out=ring, master=master, lr=lr)
+    torch.cuda.synchronize()
+    expect = m0 - lr * ref
+    torch.testing.assert_close(master, expect, atol=1e-3, rtol=1e-4)
+    torch.testing.assert_close(ring.float(), master.to(dtype).float(), atol=0, rtol=0)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_gemm_loss(dtype):
+    M, N, K = 64, 512, 256
+    a, b, ref = operands(M, N, K, False, False, dtype, seed=3)
+    bias = torch.randn(N, device="cuda")
+    target = torch.randn(M, N, device="cuda")
+    out = torch.empty(M, N, device="cuda", dtype=dtype)
+    loss = torch.zeros(1, device="cuda")
+    scale = 1.0 / M
+    nat.gemm(a, False, b, False, M, N, K, kind=nat.EPI_LOSS, out=out, bias=bias, target=target, scale=scale, loss=loss)
+    torch.cuda.synchronize()
+    d = ref + bias - target
+    torch.testing.assert_close(out.float(), d * scale, atol=2e-2 * scale * K ** 0.5, rtol=2e-2)
+    expect_loss = 0.5 * scale * float((d * d).sum())
+    assert abs(float(loss) - expect_loss) / expect_loss < 1e-3
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_bias_sgd(dtype):
+    rows, cols = 300, 1000
+    dz = torch.randn(rows, cols, device="cuda").to(dtype)
+    bm = torch.randn(cols, device="cuda")
+    b0 = bm.clone()
+    bo = torch.empty(cols, device="cuda")
+    nat.bias_sgd(dz, rows, cols, bm, bo, 0.1)
+    torch.cuda.synchronize()
+    expect = b0 - 0.1 * dz.float().sum(0)
+    torch.testing.assert_close(bm, expect, atol=1e-3, rtol=1e-4)
+    torch.testing.assert_close(bo, bm, atol=0, rtol=0)
+
+
+def test_gemm_large_bf16_all_layouts():
+    # the cfg2 layer shape at a reduced batch: one tile wave plus tails on every axis
+    M, N, K = 1024, 8192, 8192
+    for a_mn, b_mn in [(False, False), (False, True), (True, True)]:
+        a, b, ref = operands(M, N, K, a_mn, b_mn, torch.bfloat16, seed=7)
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        nat.gemm(a, a_mn, b, b_mn, M, N, K, kind=nat.EPI_STORE, out=out)
+        torch.cuda.synchronize()
+        err = (out.float() - ref).abs().max().item()
+        assert err < 0.02 * ref.abs().max().item(), (a_mn, b_mn, err)
