@@ -8,7 +8,7 @@ from paper_1806_03377_b200 import _native as nat  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [(256, 512, 192), (128, 256, 64), (100, 300, 72), (32, 1024, 1024), (384, 768, 1000), (2048, 2048, 512)]
+SHAPES = [(256, 512, 192), (128, 256, 64), (100, 296, 72), (32, 1024, 1024), (384, 768, 1000), (2048, 2048, 512)]
 
 
 def operands(M, N, K, a_mn, b_mn, dtype, seed=0):
@@ -109,3 +109,13 @@ def test_gemm_large_bf16_all_layouts():
         torch.cuda.synchronize()
         err = (out.float() - ref).abs().max().item()
         assert err < 0.02 * ref.abs().max().item(), (a_mn, b_mn, err)
+
+
+def test_gemm_rejects_unaligned_leading_dim():
+    from paper_1806_03377_b200.errors import ValidationError
+
+    a = torch.randn(64, 100, device="cuda").to(torch.bfloat16)  # ld 100 is fine (multiple of 8? no: 100 % 8 = 4)
+    b = torch.randn(64, 100, device="cuda").to(torch.bfloat16)
+    out = torch.empty(64, 64, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(ValidationError):
+        nat.gemm(a, False, b, False, 64, 64, 100, kind=nat.EPI_STORE, out=out)
