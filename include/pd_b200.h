@@ -69,6 +69,8 @@ int pd_bias_sgd(int dtype, const void* dz, int rows, int cols, int64_t ld, float
                 void* stream);
 /* master[i] -= lr*grad[i]; out[i] = cast(master[i])  (replicated stages, after the allreduce). */
 int pd_sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n, float lr, void* stream);
+/* out[i] = cast(src[i]) (fp32 -> dtype). */
+int pd_cast(int dtype, const float* src, void* out, int64_t n, void* stream);
 
 /* ------------------------------------------------------------------ P2P transport
  * Replaces _Engine._send (simulator.py:284-292): payloads are stored by the
@@ -95,6 +97,7 @@ typedef struct pd_stage_desc {
   int is_first, is_last;
   int relu_last;            /* ReLU after the stage's last layer (all but the model output) */
   int ring_depth;           /* weight-version ring slots */
+  int init_slot;            /* slot of version 0: refreshed from the masters at every run start */
   int act_depth;            /* activation-stash slots (in-flight minibatches) */
   int in_depth;             /* activation inbox slots (stage > 0) */
   int grad_depth;           /* gradient inbox slots (stage < n-1) */

@@ -1,0 +1,164 @@
+"""CPU oracle for the pipeline-training hot path (TEST INFRASTRUCTURE ONLY).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+arm may import this module, and only as the checker or the timed CPU
+baseline; the product path (paper_1806_03377_b200) never calls it.
+
+It restates, in numpy, the reference's numeric semantics of delayed SGD under
+pipelining (pipesim/semantics.py):
+
+* ``closed_form_version`` - the version each pass reads at a straight pipeline:
+  stash max(0, mb - cap_s) for both passes (cap_s = n - s at NOAM; the
+  simulator's staleness equation simulator.py:457-460 / semantics.py:211-217),
+  vertical sync max(0, mb - cap_0) everywhere, naive forward like stash and
+  naive backward mb - 1 (the latest commit at its start, simulator.py:243).
+* ``toy_pipeline`` - the linear least-squares toy of semantics.py:39-116 run
+  *as a pipeline*: stage s adds X_b[:, slice_s] @ w_s^(fwd version) to a running
+  sum, the last stage forms the residual, the gradient flows back unchanged and
+  dw_s = X_s^T r, applied to the latest weights (semantics.py:119-144, commit
+  order of replay :169-191).  With fwd == bwd versions this equals
+  ``equation_oracle`` (semantics.py:194-221) bit-for-bit up to summation order;
+  tests pin it against the reference's own trajectories (tests/golden/toy_n*.npz).
+* ``mlp_train`` - the same delayed-SGD rule for the MLP the device trains:
+  forward with every stage's forward version, backward with each stage's
+  backward version, update applied to the latest weights, minibatches committed
+  in order 1..K.  ``emulate="bf16"`` rounds exactly where the device stores bf16
+  (activations, dZ, weight-ring copies) while keeping fp32 master weights.
+
+Parity status: schedule/ledger and the toy trajectories are pinned to the
+reference's golden vectors; the MLP rule has no reference golden vector (the
+reference has no MLP) and is pinned through ``toy_pipeline`` sharing its
+version/commit logic.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+# ---------------------------------------------------------------- versions (straight pipelines)
+def caps_straight(n: int, max_inflight: int | None = None) -> list[int]:
+    """cap_s = n - s, clipped by max_inflight (schedule.py:51-70 with replication 1)."""
+    return [max(1, min(n - s, max_inflight) if max_inflight else n - s) for s in range(n)]
+
+
+def closed_form_version(mode: str, n: int, s: int, mb: int, direction: str, max_inflight: int | None = None) -> int:
+    caps = caps_straight(n, max_inflight)
+    if mode == "vertical_sync":
+        return max(0, mb - caps[0])
+    if mode == "naive_pipeline" and direction == "backward":
+        return mb - 1
+    return max(0, mb - caps[s])
+
+
+def closed_form_ledger(mode: str, n: int, K: int, max_inflight: int | None = None) -> dict:
+    return {(s, mb, d): closed_form_version(mode, n, s, mb, d, max_inflight)
+            for s in range(n) for mb in range(1, K + 1) for d in ("forward", "backward")}
+
+
+# ---------------------------------------------------------------- linear toy pipeline
+def toy_pipeline(design, targets, params, lr, block_size, versions, steps):
+    """Trajectory (steps+1, n*p) of the toy model executed stage by stage.
+
+    versions(s, mb, direction) -> int.  params: (n, p) initial blocks.
+    """
+    n, p = params.shape
+    n_blocks = design.shape[0] // block_size
+    archives = [[params[s].copy()] for s in range(n)]
+    for mb in range(1, steps + 1):
+        b = (mb - 1) % n_blocks
+        xb = design[b * block_size:(b + 1) * block_size]
+        yb = targets[b * block_size:(b + 1) * block_size]
+        fv = [versions(s, mb, "forward") for s in range(n)]
+        bv = [versions(s, mb, "backward") for s in range(n)]
+        # forward: running sum of per-stage contributions
+        run = np.zeros(block_size)
+        for s in range(n):
+            run = run + xb[:, s * p:(s + 1) * p] @ archives[s][fv[s]]
+        resid = run - yb
+        new = []
+        for s in range(n):
+            r = resid
+            if bv[s] != fv[s]:  # own block re-read at the backward version (semantics.py:138-142)
+                xs = xb[:, s * p:(s + 1) * p]
+                r = resid + xs @ (archives[s][bv[s]] - archives[s][fv[s]])
+            grad = xb[:, s * p:(s + 1) * p].T @ r
+            new.append(archives[s][-1] - lr * grad)
+        for s in range(n):
+            archives[s].append(new[s])
+    return np.stack([np.concatenate([archives[s][t] for s in range(n)]) for t in range(steps + 1)])
+
+
+# ---------------------------------------------------------------- MLP
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """Round to bfloat16 (nearest-even) and return as float64."""
+    f = np.asarray(x, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def _fp32(x):
+    return np.asarray(x, dtype=np.float32).astype(np.float64)
+
+
+def mlp_train(params, X, T, lr, stage_bounds, versions, K, emulate: str | None = None):
+    """Delayed-SGD training of a ReLU MLP split into stages.
+
+    params: list of (W [out,in], b [out]) fp64 per global layer; X: [n_blocks,B,d0]; T: [n_blocks,B,dL]
+    stage_bounds: [(first, last)] 1-based layer ranges; versions(s, mb, dir) -> int.
+    Returns (losses[K], final params list).  Loss per minibatch = 1/(2B) sum (Z - T)^2.
+    """
+    q = bf16_round if emulate == "bf16" else (lambda a: a)
+    master = _fp32 if emulate == "bf16" else (lambda a: a)
+    n = len(stage_bounds)
+    L = len(params)
+    layer_stage = {}
+    for s, (a, b) in enumerate(stage_bounds):
+        for l in range(a, b + 1):
+            layer_stage[l - 1] = s
+    # archives[s][v] = list of (W, b) for the stage's layers at version v (master precision)
+    archives = [[[(master(params[l - 1][0]), master(params[l - 1][1])) for l in range(a, b + 1)]]
+                for (a, b) in stage_bounds]
+    first = [a - 1 for a, _ in stage_bounds]
+    n_blocks = X.shape[0]
+    losses = []
+    for mb in range(1, K + 1):
+        blk = (mb - 1) % n_blocks
+        x, t = X[blk], T[blk]
+        B = x.shape[0]
+        fv = [versions(s, mb, "forward") for s in range(n)]
+        bv = [versions(s, mb, "backward") for s in range(n)]
+        h = q(x)
+        inputs = []
+        z = None
+        for l in range(L):
+            s = layer_stage[l]
+            W, b = archives[s][fv[s]][l - first[s]]
+            inputs.append(h)
+            z = h @ q(W).T + b
+            if l < L - 1:
+                h = q(np.maximum(z, 0.0))
+        d = z - t
+        losses.append(0.5 / B * float(np.sum(d * d)))
+        dz = q(d / B)
+        grads = [None] * L
+        for l in range(L - 1, -1, -1):
+            s = layer_stage[l]
+            Xl = inputs[l]
+            grads[l] = (dz.T @ Xl, dz.sum(axis=0))
+            if l > 0:
+                Wb, _ = archives[s][bv[s]][l - first[s]]
+                dz = q((dz @ q(Wb)) * (Xl > 0))
+        for s, (a, b) in enumerate(stage_bounds):
+            latest = archives[s][-1]
+            new = []
+            for i, l in enumerate(range(a - 1, b)):
+                W, bias = latest[i]
+                gW, gb = grads[l]
+                new.append((master(W - lr * gW), master(bias - lr * gb)))
+            archives[s].append(new)
+    final = []
+    for s, (a, b) in enumerate(stage_bounds):
+        final.extend(archives[s][-1])
+    return np.array(losses), final

@@ -1,1 +1,72 @@
-"""B200-native PipeDream (arXiv 1806.03377) pipeline-parallel training runtime."""
+"""B200-native PipeDream (arXiv 1806.03377) pipeline-parallel training runtime.
+
+Drop-in for the reference package ``pipesim``'s hot path: the same plan,
+schedule, config, ledger and result types, and ``run(cfg, ctx, schedule)``
+executes the 1F1B-RR schedule on B200s (tcgen05 GEMM kernels, on-device
+weight-version ring, peer-store inboxes) instead of simulating it.
+"""
+
+__version__ = "0.1.0"
+
+from .errors import (  # noqa: F401
+    ConsistencyError,
+    NativeError,
+    PipesimError,
+    ProfileFormatError,
+    SimulationError,
+    ValidationError,
+)
+from .executor import Executor, run  # noqa: F401
+from .ledger import (  # noqa: F401
+    Mode,
+    SimConfig,
+    SimReport,
+    SimResult,
+    StalenessViolation,
+    TraceEvent,
+    VersionLedger,
+    analytic_throughput,
+    build_report,
+    compare_analytic,
+    staleness_check,
+    write_trace_csv,
+)
+from .models import MLPSpec, init_params, make_data, mlp, mlp_context, mlp_profile  # noqa: F401
+from .orders import (  # noqa: F401
+    Direction,
+    Schedule,
+    WorkItem,
+    assigned_minibatches,
+    build_schedule,
+    replica_for,
+    stage_inflight_caps,
+    worker_order,
+    write_schedule_csv,
+)
+from .plans import (  # noqa: F401
+    Plan,
+    Stage,
+    load_plan,
+    noam,
+    noam_for,
+    parse_config,
+    plan_from_dict,
+    replicated_plan,
+    straight_plan,
+)
+from .profiles import (  # noqa: F401
+    CostContext,
+    HardwareSpec,
+    LayerProfile,
+    ModelProfile,
+    build_context,
+    comm_time_activations,
+    comm_volume_bsp,
+    comm_volume_pp,
+    compute_time,
+    load_profile,
+    save_profile,
+    stage_time,
+    weight_sync_time,
+)
+from .program import Program, compile_program, resolve_versions  # noqa: F401

@@ -24,7 +24,7 @@ ITEM_WIDTH = 16
 
 # Symbols include/pd_b200.h declares; tests check every one is exported.
 EXPORTED = (
-    "pd_abi_version", "pd_last_error", "pd_device_sm_count", "pd_gemm", "pd_bias_sgd", "pd_sgd_update",
+    "pd_abi_version", "pd_last_error", "pd_device_sm_count", "pd_gemm", "pd_bias_sgd", "pd_sgd_update", "pd_cast",
     "pd_flag_signal", "pd_flag_wait", "pd_ipc_get_handle", "pd_ipc_open", "pd_ipc_close",
     "pd_enable_peer_access", "pd_rt_create", "pd_rt_add_stage", "pd_rt_load_program", "pd_rt_run",
     "pd_rt_records", "pd_rt_destroy",
@@ -42,7 +42,7 @@ class Epilogue(Structure):
 class StageDesc(Structure):
     _fields_ = [
         ("stage", c_int), ("n_layers", c_int), ("dims", POINTER(c_int64)), ("batch", c_int), ("dtype", c_int),
-        ("is_first", c_int), ("is_last", c_int), ("relu_last", c_int), ("ring_depth", c_int),
+        ("is_first", c_int), ("is_last", c_int), ("relu_last", c_int), ("ring_depth", c_int), ("init_slot", c_int),
         ("act_depth", c_int), ("in_depth", c_int), ("grad_depth", c_int), ("lr", c_float),
         ("w_master", POINTER(c_void_p)), ("b_master", POINTER(c_void_p)), ("w_ring", POINTER(c_void_p)),
         ("b_ring", POINTER(c_void_p)), ("act", POINTER(c_void_p)), ("act_in", POINTER(c_void_p)),
@@ -77,6 +77,7 @@ def lib() -> ctypes.CDLL:
                               POINTER(Epilogue), c_void_p]
         L.pd_bias_sgd.argtypes = [c_int, c_void_p, c_int, c_int, c_int64, c_void_p, c_void_p, c_float, c_void_p]
         L.pd_sgd_update.argtypes = [c_int, c_void_p, c_void_p, c_void_p, c_int64, c_float, c_void_p]
+        L.pd_cast.argtypes = [c_int, c_void_p, c_void_p, c_int64, c_void_p]
         L.pd_flag_signal.argtypes = [c_void_p, c_int, c_void_p]
         L.pd_flag_wait.argtypes = [c_void_p, c_int, c_void_p, c_void_p]
         L.pd_ipc_get_handle.argtypes = [c_void_p, c_void_p]

@@ -86,6 +86,24 @@ int sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n
   return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "sgd_update: %s", cudaGetErrorString(e));
 }
 
+template <typename T>
+__global__ void k_cast(const float* __restrict__ src, T* __restrict__ o, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = from_f<T>(src[i]);
+}
+
+int cast_f32(int dtype, const float* src, void* out, int64_t n, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dtype == PD_BF16)
+    k_cast<__nv_bfloat16><<<sms * 8, 256, 0, st>>>(src, static_cast<__nv_bfloat16*>(out), n);
+  else
+    k_cast<float><<<sms * 8, 256, 0, st>>>(src, static_cast<float*>(out), n);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "cast: %s", cudaGetErrorString(e));
+}
+
 // ---------------------------------------------------------------- flags
 __global__ void k_flag_signal(int* flag, int v) {
   __threadfence_system();
@@ -147,6 +165,10 @@ int pd_bias_sgd(int dtype, const void* dz, int rows, int cols, int64_t ld, float
 
 int pd_sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n, float lr, void* stream) {
   return sgd_update(dtype, master, grad, out, n, lr, static_cast<cudaStream_t>(stream));
+}
+
+int pd_cast(int dtype, const float* src, void* out, int64_t n, void* stream) {
+  return cast_f32(dtype, src, out, n, static_cast<cudaStream_t>(stream));
 }
 
 int pd_flag_signal(int* flag, int value, void* stream) {

@@ -159,6 +159,7 @@ int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc) {
     return set_error(PD_ERR_INVALID, "stage %d: bad descriptor (layers=%d batch=%d ring=%d act=%d)", d.stage,
                      d.n_layers, d.batch, d.ring_depth, d.act_depth);
   if (d.dtype != PD_F32 && d.dtype != PD_BF16) return set_error(PD_ERR_INVALID, "stage %d: bad dtype", d.stage);
+  if (d.init_slot < 0 || d.init_slot >= d.ring_depth) return set_error(PD_ERR_INVALID, "stage %d: bad init_slot", d.stage);
   if (rt->stages.count(d.stage)) return set_error(PD_ERR_INVALID, "stage %d added twice", d.stage);
   Stage S;
   S.d = d;
@@ -229,6 +230,13 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
   for (auto& kv : rt->stages) {
     Stage& S = kv.second;
     PD_CHECK(cudaStreamWaitEvent(S.stream, rt->ev0, 0));
+    // version 0 of this run = the current (latest) weights
+    for (int l = 0; l < S.d.n_layers; ++l) {
+      const int64_t n = S.dims[l] * S.dims[l + 1];
+      PD_TRY(cast_f32(S.d.dtype, S.w_master[l], S.w_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], n, S.stream));
+      PD_CHECK(cudaMemcpyAsync(S.b_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], S.b_master[l],
+                               sizeof(float) * S.dims[l + 1], cudaMemcpyDeviceToDevice, S.stream));
+    }
     if (S.d.is_last && S.d.loss) {
       // losses are indexed by minibatch id; the program's largest id bounds the buffer
       int max_mb = 0;

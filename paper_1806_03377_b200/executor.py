@@ -1,0 +1,325 @@
+"""``run(cfg, ctx, schedule=None, *, model=...) -> SimResult`` on B200s.
+
+This is the drop-in for ``pipesim.run`` (simulator.py:401-411).  Same inputs
+(``SimConfig`` with a plan and a mode, a ``CostContext``, an optional explicit
+``Schedule``), same output types; the difference is that the schedule is
+*executed*: every stage of the plan trains a real MLP slice on a B200 with the
+tcgen05 GEMM kernels of libpd_b200.so, and the trace holds measured device
+times.  ``model=`` (an ``MLPSpec``) is the one required addition: the reference
+has no tensors to run.
+
+Layout in HBM (per hosted stage):
+  w_master[l]  fp32 [out,in]            latest weights (SGD target)
+  w_ring[l]    dtype [depth,out,in]     weight versions; slot from program.py
+  b_master/b_ring                       same for biases (fp32)
+  act[l]       dtype [act_depth,B,d]    stashed layer inputs of in-flight minibatches
+  act_in       dtype [in_depth,B,d_0]   activation inbox (stage 0: resident data blocks)
+  grad_in      dtype [grad_depth,B,d_L] gradient inbox
+  dz_last      dtype [act_depth,B,d_L]  loss gradient (last stage)
+PyTorch only allocates these; all math runs in the library.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .errors import SimulationError, ValidationError
+from .ledger import Mode, SimConfig, SimResult, TraceEvent, build_report
+from .models import MLPSpec, init_params, make_data
+from .orders import Direction, Schedule, build_schedule, stage_inflight_caps
+from .program import Program, compile_program
+
+HOST_INIT_LIMIT = 64 * 1024 * 1024  # parameters; above this, weights/data are drawn on the device
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+@dataclass
+class _StageBuf:
+    wid: int
+    stage: int
+    dims: list[int]
+    ring_depth: int
+    init_slot: int
+    act_depth: int
+    in_depth: int
+    grad_depth: int
+    tensors: dict = field(default_factory=dict)
+    desc: object = None
+    keep: list = field(default_factory=list)  # ctypes arrays referenced by desc
+
+
+def _validate(cfg: SimConfig, ctx, model: MLPSpec) -> None:
+    plan = cfg.plan
+    if ctx is not None and plan.num_layers != ctx.num_layers:
+        raise ValidationError(f"plan covers {plan.num_layers} layers, profile has {ctx.num_layers}")
+    if plan.num_layers != model.num_layers:
+        raise ValidationError(f"plan covers {plan.num_layers} layers, model has {model.num_layers}")
+    for s, st in enumerate(plan.stages):
+        if st.replication > 1:
+            raise ValidationError(
+                f"stage {s} is replicated {st.replication}x: replicated stages need the multi-GPU "
+                "allreduce path (paper_1806_03377_b200.replicated), not yet wired into run()"
+            )
+
+
+class Executor:
+    """Allocates one pipeline's device state and runs its compiled program repeatedly."""
+
+    def __init__(self, cfg: SimConfig, ctx=None, schedule: Schedule | None = None, *, model: MLPSpec,
+                 device: int | None = None, init: str | None = None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise nat.NativeError("no CUDA device: the B200 executor has no CPU fallback")
+        _validate(cfg, ctx, model)
+        self.cfg, self.ctx, self.model = cfg, ctx, model
+        self.schedule = schedule or build_schedule(cfg.plan, cfg.num_minibatches, cfg.max_inflight)
+        dist = torch.distributed
+        self.world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+        self.rank = dist.get_rank() if self.world > 1 else 0
+        if self.world > 1:
+            raise ValidationError("multi-process execution goes through paper_1806_03377_b200.distributed")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        torch.cuda.set_device(self.device)
+        self.program: Program = compile_program(self.schedule, cfg.mode, n_blocks=model.n_blocks, world_size=1)
+        self.dtype = torch.float32 if model.dtype == "fp32" else torch.bfloat16
+        self.pd_dtype = nat.PD_F32 if model.dtype == "fp32" else nat.PD_BF16
+        n_params = sum(a * b for a, b in zip(model.widths[:-1], model.widths[1:]))
+        self.init = init or ("host" if n_params <= HOST_INIT_LIMIT else "device")
+        self._alloc()
+        self._build_runtime()
+        self.runs = 0
+
+    # ------------------------------------------------------------------ setup
+    def _alloc(self) -> None:
+        torch = _torch()
+        dev, dt, m = self.device, self.dtype, self.model
+        plan = self.cfg.plan
+        if self.init == "host":
+            params = init_params(m)
+            X, T = make_data(m)
+        else:
+            params = None
+            g = torch.Generator(device=dev).manual_seed(m.seed)
+        self.bufs: dict[int, _StageBuf] = {}
+        for wp in self.program.workers:
+            st = plan.stages[wp.stage]
+            dims = list(m.widths[st.first_layer - 1: st.last_layer + 1])
+            b = _StageBuf(wid=wp.wid, stage=wp.stage, dims=dims, ring_depth=wp.ring_depth,
+                          init_slot=wp.ring_slot[0], act_depth=wp.act_depth, in_depth=wp.in_depth,
+                          grad_depth=wp.grad_depth)
+            L = len(dims) - 1
+            t = b.tensors
+            t["w_master"], t["b_master"], t["w_ring"], t["b_ring"] = [], [], [], []
+            for l in range(L):
+                din, dout = dims[l], dims[l + 1]
+                gl = st.first_layer - 1 + l
+                if params is not None:
+                    W = torch.from_numpy(params[gl][0]).float().to(dev)
+                    bias = torch.from_numpy(params[gl][1]).float().to(dev)
+                else:
+                    W = torch.randn(dout, din, device=dev, generator=g) * math.sqrt(2.0 / din)
+                    bias = torch.randn(dout, device=dev, generator=g) * 0.01
+                t["w_master"].append(W.contiguous())
+                t["b_master"].append(bias.contiguous())
+                t["w_ring"].append(torch.empty(b.ring_depth, dout, din, device=dev, dtype=dt))
+                t["b_ring"].append(torch.empty(b.ring_depth, dout, device=dev, dtype=torch.float32))
+            t["act"] = [torch.empty(b.act_depth, m.batch, dims[l + 1], device=dev, dtype=dt) for l in range(L - 1)]
+            if wp.stage == 0:
+                if params is not None:
+                    t["act_in"] = torch.from_numpy(X).to(dev).to(dt).contiguous()
+                else:
+                    t["act_in"] = torch.randn(m.n_blocks, m.batch, dims[0], device=dev, generator=g).to(dt)
+            else:
+                t["act_in"] = torch.zeros(b.in_depth, m.batch, dims[0], device=dev, dtype=dt)
+            if wp.stage < plan.num_stages - 1:
+                t["grad_in"] = torch.zeros(b.grad_depth, m.batch, dims[-1], device=dev, dtype=dt)
+            else:
+                t["dz_last"] = torch.empty(b.act_depth, m.batch, dims[-1], device=dev, dtype=dt)
+                if params is not None:
+                    t["target"] = torch.from_numpy(T).float().to(dev).contiguous()
+                else:
+                    t["target"] = torch.randn(m.n_blocks, m.batch, dims[-1], device=dev, generator=g)
+                t["loss"] = torch.zeros(self.cfg.num_minibatches + 1, device=dev, dtype=torch.float32)
+            t["tmp"] = [torch.empty(m.batch, max(dims), device=dev, dtype=dt) for _ in range(2)]
+            t["err"] = torch.zeros(1, device=dev, dtype=torch.int32)
+            self.bufs[wp.wid] = b
+
+    @staticmethod
+    def _parr(ptrs) -> ctypes.Array:
+        return (ctypes.c_void_p * max(1, len(ptrs)))(*[int(p) for p in ptrs])
+
+    def _build_runtime(self) -> None:
+        L = nat.lib()
+        plan = self.cfg.plan
+        n = plan.num_stages
+        rt = ctypes.c_void_p()
+        nat.check(L.pd_rt_create(self.device.index, ctypes.byref(rt)), "pd_rt_create")
+        self._rt = rt
+        by_stage = {b.stage: b for b in self.bufs.values()}
+        for b in self.bufs.values():
+            t = b.tensors
+            nl = len(b.dims) - 1
+            keep = []
+
+            def arr(ptrs):
+                a = self._parr(ptrs)
+                keep.append(a)
+                return ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p))
+
+            dims = (ctypes.c_int64 * len(b.dims))(*b.dims)
+            keep.append(dims)
+            is_first, is_last = b.stage == 0, b.stage == n - 1
+            d = nat.StageDesc()
+            d.stage, d.n_layers, d.dims, d.batch, d.dtype = b.stage, nl, dims, self.model.batch, self.pd_dtype
+            d.is_first, d.is_last, d.relu_last = int(is_first), int(is_last), int(not is_last)
+            d.ring_depth, d.init_slot, d.act_depth = b.ring_depth, b.init_slot, b.act_depth
+            d.in_depth, d.grad_depth, d.lr = b.in_depth, b.grad_depth, self.model.lr
+            d.w_master = arr([w.data_ptr() for w in t["w_master"]])
+            d.b_master = arr([x.data_ptr() for x in t["b_master"]])
+            d.w_ring = arr([t["w_ring"][l][k].data_ptr() for l in range(nl) for k in range(b.ring_depth)])
+            d.b_ring = arr([t["b_ring"][l][k].data_ptr() for l in range(nl) for k in range(b.ring_depth)])
+            d.act = arr([t["act"][l][k].data_ptr() for l in range(nl - 1) for k in range(b.act_depth)])
+            d.act_in = arr([x.data_ptr() for x in t["act_in"]])
+            d.n_data_blocks = self.model.n_blocks
+            if not is_last:
+                d.grad_in = arr([x.data_ptr() for x in t["grad_in"]])
+                nxt = by_stage[b.stage + 1]
+                d.next_act_in = arr([x.data_ptr() for x in nxt.tensors["act_in"]])
+                d.next_in_depth = nxt.in_depth
+            else:
+                d.dz_last = arr([x.data_ptr() for x in t["dz_last"]])
+                d.target = arr([x.data_ptr() for x in t["target"]])
+                d.loss = t["loss"].data_ptr()
+            if not is_first:
+                prv = by_stage[b.stage - 1]
+                d.prev_grad_in = arr([x.data_ptr() for x in prv.tensors["grad_in"]])
+                d.prev_grad_depth = prv.grad_depth
+            d.tmp[0], d.tmp[1] = t["tmp"][0].data_ptr(), t["tmp"][1].data_ptr()
+            d.err_word = t["err"].data_ptr()
+            b.desc, b.keep = d, keep
+            nat.check(L.pd_rt_add_stage(rt, ctypes.byref(d)), "pd_rt_add_stage")
+        prog = np.ascontiguousarray(self.program.items_for_rank(0))
+        self._prog = prog
+        nat.check(L.pd_rt_load_program(rt, prog.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), prog.shape[0]),
+                  "pd_rt_load_program")
+
+    # ------------------------------------------------------------------ execution
+    def step(self, stream=None, trace: bool = False) -> None:
+        """Enqueue one execution of the whole schedule behind ``stream`` (async)."""
+        torch = _torch()
+        s = stream or torch.cuda.current_stream(self.device)
+        nat.check(nat.lib().pd_rt_run(self._rt, int(s.cuda_stream), int(trace)), "pd_rt_run")
+        self.runs += 1
+        self._traced = trace
+
+    def load_inputs(self, X_host, T_host, stream=None) -> None:
+        """Copy host (pinned) input / target blocks into the resident data buffers (e2e path)."""
+        torch = _torch()
+        s = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(s):
+            for b in self.bufs.values():
+                if b.stage == 0:
+                    b.tensors["act_in"].copy_(X_host, non_blocking=True)
+                if b.stage == self.cfg.plan.num_stages - 1:
+                    b.tensors["target"].copy_(T_host, non_blocking=True)
+
+    def losses(self) -> list[float]:
+        last = [b for b in self.bufs.values() if b.stage == self.cfg.plan.num_stages - 1][0]
+        return last.tensors["loss"][1:].float().cpu().tolist()
+
+    def loss_tensor(self):
+        last = [b for b in self.bufs.values() if b.stage == self.cfg.plan.num_stages - 1][0]
+        return last.tensors["loss"]
+
+    def weights(self) -> dict[int, tuple[np.ndarray, np.ndarray]]:
+        """Final fp32 (W, b) per global 1-based layer id."""
+        out = {}
+        plan = self.cfg.plan
+        for b in self.bufs.values():
+            st = plan.stages[b.stage]
+            for l, (W, bias) in enumerate(zip(b.tensors["w_master"], b.tensors["b_master"])):
+                out[st.first_layer + l] = (W.cpu().numpy().astype(np.float64), bias.cpu().numpy().astype(np.float64))
+        return out
+
+    def records(self) -> list[tuple[int, float, float]]:
+        L = nat.lib()
+        n = self._prog.shape[0]
+        recs = (nat.Record * n)()
+        got = ctypes.c_int(0)
+        nat.check(L.pd_rt_records(self._rt, recs, n, ctypes.byref(got)), "pd_rt_records")
+        err = [int(b.tensors["err"].item()) for b in self.bufs.values()]
+        if any(err):
+            raise SimulationError(f"flag wait timed out (values {err}): a neighbour never delivered")
+        return [(r.item, r.t_start_ms, r.t_end_ms) for r in recs[: got.value]]
+
+    def trace(self) -> list[TraceEvent]:
+        evs = []
+        for idx, t0, t1 in self.records():
+            row = self._prog[idx]
+            evs.append(TraceEvent(
+                time_start=t0 * 1e-3, time_end=t1 * 1e-3, worker=int(row[nat.IT_WORKER]),
+                minibatch=int(row[nat.IT_MB]), stage=int(row[nat.IT_STAGE]),
+                direction=Direction.FORWARD if row[nat.IT_OP] == 0 else Direction.BACKWARD,
+                version_used=int(row[nat.IT_VERSION]),
+            ))
+        return evs
+
+    def comm_bytes(self) -> float:
+        """Boundary crossings x message size, counted from the executed program (simulator.py:288)."""
+        m = self.model
+        plan = self.cfg.plan
+        total = 0.0
+        for row in self._prog:
+            s = int(row[nat.IT_STAGE])
+            if row[nat.IT_OP] == 0 and s < plan.num_stages - 1:
+                total += m.batch * m.widths[plan.stages[s].last_layer] * m.bytes_per_elem
+            if row[nat.IT_OP] == 1 and s > 0:
+                total += m.batch * m.widths[plan.stages[s].first_layer - 1] * m.bytes_per_elem
+        return total
+
+    def result(self) -> SimResult:
+        torch = _torch()
+        torch.cuda.synchronize(self.device)
+        trace = self.trace() if getattr(self, "_traced", False) else []
+        report = build_report(self.cfg, trace, len(self.schedule.workers), self.comm_bytes()) if trace else None
+        losses = self.losses()
+        bubble = None
+        if report is not None:
+            bubble = 1.0 - sum(report.per_worker_utilization) / len(report.per_worker_utilization)
+        return SimResult(report=report, ledger=self.program.ledger, trace=trace, losses=losses,
+                         weights=self.weights(),
+                         extras={"bubble_fraction": bubble, "ring_depths": {b.stage: b.ring_depth for b in self.bufs.values()},
+                                 "device": str(self.device), "runs": self.runs})
+
+    def close(self) -> None:
+        if getattr(self, "_rt", None) is not None:
+            nat.lib().pd_rt_destroy(self._rt)
+            self._rt = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run(cfg: SimConfig, ctx=None, schedule: Schedule | None = None, *, model: MLPSpec, trace: bool = True,
+        device: int | None = None, init: str | None = None) -> SimResult:
+    """Execute ``cfg`` on the GPU and return the reference's ``SimResult`` shape (simulator.py:401-411)."""
+    ex = Executor(cfg, ctx, schedule, model=model, device=device, init=init)
+    try:
+        ex.step(trace=trace)
+        return ex.result()
+    finally:
+        ex.close()

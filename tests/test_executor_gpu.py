@@ -1,0 +1,117 @@
+"""End-to-end parity of the B200 executor against the CPU oracle (the -m gpu suite proper).
+
+Tolerances (stated per BASELINE.json north_star):
+  fp32 (SIMT FFMA, fp32 accumulate) vs fp64 oracle: per-minibatch loss rel <= 1e-4;
+    final weights: |dW_dev - dW_oracle| <= 1e-3 * max|dW_oracle| on the training delta.
+  bf16 (tcgen05, fp32 accumulate, bf16 storage) vs the bf16-emulating oracle: loss rel <= 2e-2,
+    weight delta within 5e-2 * max|delta|.
+Integer results (ledger versions) are exact.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_1806_03377_b200 as pd  # noqa: E402
+from oracle.pipeline_oracle import mlp_train  # noqa: E402
+from helpers_golden import load_json  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def straight_cfg(n_stages, layers_per_stage, K, mode, max_inflight=None):
+    bounds = [(s * layers_per_stage + 1, (s + 1) * layers_per_stage) for s in range(n_stages)]
+    stages = tuple(pd.Stage(a, b, 1) for a, b in bounds)
+    plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=n_stages, machines_used=n_stages)
+    return pd.SimConfig(plan=plan, mode=mode, num_minibatches=K, max_inflight=max_inflight), bounds
+
+
+def oracle_for(spec, cfg, bounds, ledger, params=None):
+    P = params if params is not None else pd.init_params(spec)
+    X, T = pd.make_data(spec)
+    versions = lambda s, mb, d: ledger.version_used(s, mb, pd.Direction(d))  # noqa: E731
+    return mlp_train(P, X, T, spec.lr, bounds, versions, cfg.num_minibatches,
+                     emulate="bf16" if spec.dtype == "bf16" else None)
+
+
+def weight_delta_err(spec, res_weights, oracle_final, params0=None):
+    P0 = params0 if params0 is not None else pd.init_params(spec)
+    worst = 0.0
+    for l, (W_o, b_o) in enumerate(oracle_final, start=1):
+        W_d, b_d = res_weights[l]
+        for dev, orc, init in ((W_d, W_o, P0[l - 1][0]), (b_d, b_o, P0[l - 1][1])):
+            init32 = init.astype(np.float32).astype(np.float64)
+            delta = orc - init32
+            scale = max(np.max(np.abs(delta)), 1e-30)
+            worst = max(worst, np.max(np.abs((dev - init32) - delta)) / scale)
+    return worst
+
+
+@pytest.mark.parametrize("mode", ["weight_stashing", "vertical_sync", "naive_pipeline"])
+def test_cfg1_mlp1024_fp32_parity(mode):
+    """BASELINE configs[0]: 4-stage 8-layer MLP-1024 fp32, minibatch 32, 20 steps."""
+    cfg, bounds = straight_cfg(4, 2, 20, mode)
+    spec = pd.mlp(1024, 8, batch=32, dtype="fp32", lr=1e-2, n_blocks=8, seed=0)
+    res = pd.run(cfg, pd.mlp_context(spec, 4), model=spec)
+    # ledger: exactly the reference simulator's (golden straight4_k20)
+    g = load_json("ledgers.json")["straight4_k20"][mode]
+    assert sorted([s, mb, d.value, v] for (s, mb, d), v in res.ledger.entries.items()) == g
+    if mode != "naive_pipeline":
+        assert pd.staleness_check(res.ledger, mode, 4) == []
+    losses, final = oracle_for(spec, cfg, bounds, res.ledger)
+    got = np.array(res.losses[:20])
+    rel = np.max(np.abs(got - losses) / np.abs(losses))
+    assert rel <= 1e-4, (rel, got[:5], losses[:5])
+    assert weight_delta_err(spec, res.weights, final) <= 1e-3
+    # trace: the executed per-worker order is the schedule's order, and the report is well formed
+    by_worker = {}
+    for ev in sorted(res.trace, key=lambda e: (e.worker, e.time_start)):
+        by_worker.setdefault(ev.worker, []).append((ev.direction, ev.minibatch))
+    sch = pd.build_schedule(cfg.plan, 20)
+    for wid, order in enumerate(sch.orders):
+        assert by_worker[wid] == [(i.direction, i.minibatch_id) for i in order]
+    assert res.report.steady_throughput > 0
+    assert all(0.0 <= u <= 1.0 + 1e-6 for u in res.report.per_worker_utilization)
+    assert res.report.comm_bytes_total == 2 * 3 * 20 * 32 * 1024 * 4  # Appendix A.3 accounting
+
+
+@pytest.mark.parametrize("mode", ["weight_stashing", "vertical_sync"])
+def test_bf16_pipeline_parity(mode):
+    cfg, bounds = straight_cfg(4, 2, 20, mode)
+    spec = pd.mlp(256, 8, batch=128, dtype="bf16", lr=2e-2, n_blocks=4, seed=1)
+    res = pd.run(cfg, model=spec)
+    losses, final = oracle_for(spec, cfg, bounds, res.ledger)
+    got = np.array(res.losses[:20])
+    rel = np.max(np.abs(got - losses) / np.abs(losses))
+    assert rel <= 2e-2, (rel, got[:5], losses[:5])
+    assert weight_delta_err(spec, res.weights, final) <= 5e-2
+
+
+def test_bf16_eight_stage_max_inflight_and_repeat():
+    """8 stages x 2 layers (cfg2 shape, reduced width), max_inflight=3, two back-to-back runs."""
+    cfg, bounds = straight_cfg(8, 2, 25, "weight_stashing", max_inflight=3)
+    spec = pd.mlp(512, 16, batch=256, dtype="bf16", lr=1e-2, n_blocks=4, seed=2)
+    ex = pd.Executor(cfg, model=spec)
+    try:
+        ex.step(trace=True)
+        r1 = ex.result()
+        l1, f1 = oracle_for(spec, cfg, bounds, r1.ledger)
+        assert np.max(np.abs(np.array(r1.losses[:25]) - l1) / np.abs(l1)) <= 2e-2
+        # second run continues from the trained weights with a fresh pipeline fill
+        ex.step(trace=False)
+        r2 = ex.result()
+        l2, _ = oracle_for(spec, cfg, bounds, r1.ledger, params=f1)
+        assert np.max(np.abs(np.array(r2.losses[:25]) - l2) / np.abs(l2)) <= 3e-2
+    finally:
+        ex.close()
+
+
+def test_executor_rejects_bad_inputs():
+    cfg, _ = straight_cfg(2, 1, 12, "weight_stashing")
+    with pytest.raises(pd.ValidationError):
+        pd.run(cfg, model=pd.mlp(64, 3, dtype="fp32"))  # plan has 2 layers, model 3
+    spec = pd.mlp(64, 2, dtype="fp32")
+    ctx = pd.mlp_context(pd.mlp(64, 3, dtype="fp32"))
+    with pytest.raises(pd.ValidationError):
+        pd.run(cfg, ctx, model=spec)  # profile mismatch (simulator.py:153-156)
