@@ -1,0 +1,338 @@
+"""Benchmark: pipeline-training samples/s of the 1F1B weight-stashing executor on B200.
+
+Contract (see task): `python bench.py --gpus N --steps K --warmup W [--impl reference]`
+prints ONE JSON line on rank 0.
+
+Workload (BASELINE.json configs[1]): 8-stage, 16-layer MLP, width 8192, bf16 storage /
+fp32 accumulate, straight pipeline (one stage per GPU at N=8; 8/N stages per GPU below),
+1F1B with weight stashing, minibatch 2048, synthetic data.
+A bench "step" = one execution of the whole 1F1B schedule over K=32 minibatches
+(pipeline fill + steady state + drain), i.e. 32*2048 = 65,536 samples.
+The working set (~15 GB of weight versions + activations) is >100x the 126 MB L2, so no
+explicit L2 flush is needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "pipeline training samples/s at 1/2/4/8 B200; stage TC util %; bubble %"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--batch", type=int, default=2048)
+    p.add_argument("--minibatches", type=int, default=32)
+    p.add_argument("--width", type=int, default=8192)
+    p.add_argument("--layers", type=int, default=16)
+    p.add_argument("--stages", type=int, default=8)
+    p.add_argument("--mode", default="weight_stashing")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    return p.parse_args()
+
+
+def workload(args):
+    return {
+        "workload": f"cfg2: {args.stages}-stage {args.layers}-layer MLP-{args.width} bf16 straight pipeline, "
+                    f"1F1B {args.mode}",
+        "minibatch": args.batch,
+        "minibatches_per_step": args.minibatches,
+        "stages": args.stages,
+        "stages_per_gpu": args.stages // max(1, args.gpus),
+        "lr": 1e-5,
+        "l2": "working set > 100x L2 (126 MB); no flush needed",
+        "loss": "1/(2B) sum (Z-T)^2",
+    }
+
+
+def load_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            with open(self.path) as fh:
+                for line in fh:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[5:9]) if v.lower() == "active"})
+        loaded = [x for x in sm if x > 0.5 * (max(sm) if sm else 1)]
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+_CPU_CACHE: dict = {}
+
+
+def cpu_sample(args, seconds=12.0, batch=128, max_minibatches=3):
+    """Time the CPU oracle (numpy fp32, all host threads) on a bounded sample of the workload."""
+    import numpy as np
+
+    import paper_1806_03377_b200 as pd
+    from oracle.pipeline_oracle import closed_form_version, mlp_train
+
+    per = args.layers // args.stages
+    bounds = [(s * per + 1, (s + 1) * per) for s in range(args.stages)]
+    w = args.width
+    key = (w, args.layers, batch)
+    if key not in _CPU_CACHE:
+        rng = np.random.default_rng(0)
+        params = [(rng.standard_normal((w, w), dtype=np.float32) * np.float32((2.0 / w) ** 0.5),
+                   np.zeros(w, dtype=np.float32)) for _ in range(args.layers)]
+        X = rng.standard_normal((1, batch, w), dtype=np.float32)
+        T = rng.standard_normal((1, batch, w), dtype=np.float32)
+        _CPU_CACHE[key] = (params, X, T)
+    params, X, T = _CPU_CACHE[key]
+    n = args.stages
+    versions = lambda s, mb, d: closed_form_version(args.mode, n, s, mb, d)  # noqa: E731
+    done, t0 = 0, time.perf_counter()
+    while True:
+        k = done + 1
+        mlp_train(params, X, T, 1e-5, bounds, versions, 1, dtype=np.float32, prune=True)
+        done = k
+        el = time.perf_counter() - t0
+        if el >= seconds or done >= max_minibatches:
+            break
+    try:
+        from threadpoolctl import threadpool_info
+
+        cores = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
+    except Exception:
+        cores = os.cpu_count()
+    return {"value": done * batch / el, "unit": "samples/s", "cores": cores, "kind": "port",
+            "sample": f"{done} minibatch(es) of {batch} samples through all {args.layers} layers "
+                      f"(fwd+bwd+SGD, numpy fp32, weight-stashing versions) in {el:.1f} s"}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+
+    cfg = workload(args)
+    for _ in range(args.warmup):
+        cpu_sample(args, seconds=0.0, max_minibatches=1)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_sample(args, seconds=0.0, max_minibatches=1))
+    el = time.perf_counter() - t0
+    samples = 128 * len(vals)
+    value = samples / el
+    cb = dict(vals[-1])
+    cb["value"] = value
+    cb["sample"] = f"{args.steps} steps x 1 minibatch of 128 samples, all {args.layers} layers, numpy fp32"
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+           "config": cfg, "cpu_baseline": cb,
+           "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def run_ours(args, rank, world):
+    import torch
+
+    import paper_1806_03377_b200 as pd
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.cuda.current_device()
+    per = args.layers // args.stages
+    stages = tuple(pd.Stage(s * per + 1, (s + 1) * per, 1) for s in range(args.stages))
+    plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=args.stages, machines_used=args.stages)
+    cfg = pd.SimConfig(plan=plan, mode=args.mode, num_minibatches=args.minibatches)
+    spec = pd.mlp(args.width, args.layers, batch=args.batch, dtype="bf16", lr=1e-5, n_blocks=4, seed=0)
+    if world > 1:
+        from paper_1806_03377_b200.distributed import DistributedExecutor
+
+        ex = DistributedExecutor(cfg, model=spec)
+    else:
+        ex = pd.Executor(cfg, model=spec)
+    dist = torch.distributed if world > 1 else None
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        ex.step(stream=stream)
+    torch.cuda.synchronize()
+    # ---------------- timed region (device events, max over ranks)
+    launches0 = ex.launch_count()
+    ex.kernel_timing(True)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        start.record(stream)
+        for _ in range(args.steps):
+            ex.step(stream=stream)
+        end.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = start.elapsed_time(end)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    launches = ex.launch_count() - launches0
+    kstats = ex.kernel_stats()
+    ex.kernel_timing(False)
+    samples = args.steps * args.minibatches * args.batch
+    value = samples / (ms * 1e-3)
+    # ---------------- traced step: bubble / utilisation with the reference's window rule
+    ex.step(stream=stream, trace=True)
+    res = ex.result()
+    # ---------------- e2e through the public API with host buffers
+    X_host = torch.randn(spec.n_blocks, spec.batch, spec.widths[0]).to(torch.bfloat16).pin_memory()
+    T_host = torch.randn(spec.n_blocks, spec.batch, spec.widths[-1]).pin_memory()
+    loss_host = torch.empty(args.minibatches + 1, dtype=torch.float32).pin_memory()
+    h2d = 0
+    hosts_first = any(b.stage == 0 for b in ex.bufs.values())
+    hosts_last = any(b.stage == args.stages - 1 for b in ex.bufs.values())
+    h2d = (X_host.numel() * X_host.element_size() if hosts_first else 0) + \
+          (T_host.numel() * T_host.element_size() if hosts_last else 0)
+    d2h = loss_host.numel() * 4 if hosts_last else 0
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        ex.load_inputs(X_host if hosts_first else None, T_host if hosts_last else None, stream=stream)
+        ex.step(stream=stream)
+        if hosts_last:
+            loss_host.copy_(ex.loss_tensor(), non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = args.e2e_steps * args.minibatches * args.batch / (e2e_ms * 1e-3)
+    if rank != 0:
+        ex.close()
+        return
+    # ---------------- roofline for the dominant kernel class (largest total GEMM time)
+    peaks, peak_kind = load_peaks()
+    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    dom_name, dom = max(kstats.items(), key=lambda kv: kv[1]["total_ms"])
+    achieved = dom["flops_per_launch"] / (dom["avg_ms"] * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get(dom_name)
+    per_class = {k: {"launches": v["launches"], "avg_ms": round(v["avg_ms"], 4),
+                     "tflops": round(v["flops_per_launch"] / (v["avg_ms"] * 1e-3) / 1e12, 1),
+                     "frac_of_sustained_peak": round(v["flops_per_launch"] / (v["avg_ms"] * 1e-3) / 1e12 / peak, 3)}
+                 for k, v in kstats.items()}
+    flops_per_sample = spec.flops_per_sample()
+    rep = res.report
+    out = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": workload(args),
+        "roofline": {"bound": "tensor", "kernel": f"k_gemm_tc ({dom_name})", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": f"{peak_kind} bf16_tflops_sustained (MEASURED_PEAKS.json)"},
+        "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "gemm_classes": per_class,
+        "model_tflops": value * flops_per_sample / 1e12,
+        "model_frac_of_sustained_peak": value * flops_per_sample / 1e12 / peak / world,
+        "bubble_fraction": res.extras.get("bubble_fraction"),
+        "per_worker_utilization": [round(u, 4) for u in rep.per_worker_utilization] if rep else None,
+        "steady_minibatches_per_s": rep.steady_throughput if rep else None,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        out["cpu_baseline"] = cpu_sample(args)
+    ex.close()
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        torch.distributed.init_process_group("nccl")
+    args.gpus = world
+    run_ours(args, rank, world)
+    if world > 1:
+        import torch
+
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

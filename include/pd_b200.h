@@ -163,6 +163,12 @@ int pd_rt_load_program(pd_runtime* rt, const int32_t* items, int n_items);
  * trace=1 records per-item device timestamps (pd_rt_records). */
 int pd_rt_run(pd_runtime* rt, void* stream, int trace);
 int pd_rt_records(pd_runtime* rt, pd_record* out, int cap, int* n_out);
+/* Per-GEMM CUDA-event timing on the launching stage stream (resets the counters).
+ * stats: 3 classes (forward, dgrad, wgrad+SGD) x {launches, total ms, algorithmic flops}. */
+int pd_rt_kernel_timing(pd_runtime* rt, int on);
+int pd_rt_kernel_stats(pd_runtime* rt, double* out9);
+/* Kernels of this library launched by the runtime since creation. */
+int pd_rt_launch_count(pd_runtime* rt, int64_t* out);
 int pd_rt_destroy(pd_runtime* rt);
 
 #ifdef __cplusplus

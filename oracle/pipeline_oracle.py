@@ -102,11 +102,14 @@ def _fp32(x):
     return np.asarray(x, dtype=np.float32).astype(np.float64)
 
 
-def mlp_train(params, X, T, lr, stage_bounds, versions, K, emulate: str | None = None):
+def mlp_train(params, X, T, lr, stage_bounds, versions, K, emulate: str | None = None, dtype=np.float64,
+              prune: bool = False):
     """Delayed-SGD training of a ReLU MLP split into stages.
 
-    params: list of (W [out,in], b [out]) fp64 per global layer; X: [n_blocks,B,d0]; T: [n_blocks,B,dL]
+    params: list of (W [out,in], b [out]) per global layer; X: [n_blocks,B,d0]; T: [n_blocks,B,dL]
     stage_bounds: [(first, last)] 1-based layer ranges; versions(s, mb, dir) -> int.
+    dtype: arithmetic type (float64 for parity, float32 for the timed CPU baseline).
+    prune: drop weight versions no later minibatch reads (bounded memory for big models).
     Returns (losses[K], final params list).  Loss per minibatch = 1/(2B) sum (Z - T)^2.
     """
     q = bf16_round if emulate == "bf16" else (lambda a: a)
@@ -118,14 +121,23 @@ def mlp_train(params, X, T, lr, stage_bounds, versions, K, emulate: str | None =
         for l in range(a, b + 1):
             layer_stage[l - 1] = s
     # archives[s][v] = list of (W, b) for the stage's layers at version v (master precision)
-    archives = [[[(master(params[l - 1][0]), master(params[l - 1][1])) for l in range(a, b + 1)]]
+    archives = [{0: [(master(np.asarray(params[l - 1][0], dtype=dtype)), master(np.asarray(params[l - 1][1], dtype=dtype)))
+                     for l in range(a, b + 1)]}
                 for (a, b) in stage_bounds]
+    latest_v = [0] * n
+    last_reader = [dict() for _ in range(n)]
+    if prune:
+        for mb in range(1, K + 1):
+            for s in range(n):
+                for d in ("forward", "backward"):
+                    v = versions(s, mb, d)
+                    last_reader[s][v] = max(last_reader[s].get(v, 0), mb)
     first = [a - 1 for a, _ in stage_bounds]
     n_blocks = X.shape[0]
     losses = []
     for mb in range(1, K + 1):
         blk = (mb - 1) % n_blocks
-        x, t = X[blk], T[blk]
+        x, t = np.asarray(X[blk], dtype=dtype), np.asarray(T[blk], dtype=dtype)
         B = x.shape[0]
         fv = [versions(s, mb, "forward") for s in range(n)]
         bv = [versions(s, mb, "backward") for s in range(n)]
@@ -151,14 +163,18 @@ def mlp_train(params, X, T, lr, stage_bounds, versions, K, emulate: str | None =
                 Wb, _ = archives[s][bv[s]][l - first[s]]
                 dz = q((dz @ q(Wb)) * (Xl > 0))
         for s, (a, b) in enumerate(stage_bounds):
-            latest = archives[s][-1]
+            latest = archives[s][latest_v[s]]
             new = []
             for i, l in enumerate(range(a - 1, b)):
                 W, bias = latest[i]
                 gW, gb = grads[l]
                 new.append((master(W - lr * gW), master(bias - lr * gb)))
-            archives[s].append(new)
+            archives[s][mb] = new
+            latest_v[s] = mb
+            if prune:
+                for v in [v for v in archives[s] if v != mb and last_reader[s].get(v, 0) <= mb]:
+                    del archives[s][v]
     final = []
-    for s, (a, b) in enumerate(stage_bounds):
-        final.extend(archives[s][-1])
+    for s in range(n):
+        final.extend(archives[s][latest_v[s]])
     return np.array(losses), final

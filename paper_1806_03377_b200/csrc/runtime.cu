@@ -46,6 +46,12 @@ struct pd_runtime {
   std::vector<cudaEvent_t> ev_start, ev_end;
   cudaEvent_t ev0 = nullptr;
   bool traced = false;
+  // kernel accounting: launches of our kernels, and optional per-GEMM event timing by class
+  int64_t launches = 0;
+  bool ktiming = false;
+  struct KT { int cls; double flops; cudaEvent_t a, b; };
+  std::vector<KT> kt;
+  size_t kt_used = 0;
 };
 
 namespace {
@@ -62,6 +68,29 @@ namespace {
   } while (0)
 
 inline int flag_val(int epoch, int mb) { return epoch * 65536 + mb; }
+
+enum { KC_FWD = 0, KC_DGRAD = 1, KC_WGRAD = 2, KC_N = 3 };
+
+int timed_gemm(pd_runtime* rt, int cls, int dtype, const void* A, int a_mn, int64_t lda, const void* B, int b_mn,
+               int64_t ldb, int M, int N, int K, int kind, const EpiArgs& ep, cudaStream_t st) {
+  pd_runtime::KT* slot = nullptr;
+  if (rt->ktiming) {
+    if (rt->kt_used == rt->kt.size()) {
+      pd_runtime::KT k{};
+      PD_CHECK(cudaEventCreate(&k.a));
+      PD_CHECK(cudaEventCreate(&k.b));
+      rt->kt.push_back(k);
+    }
+    slot = &rt->kt[rt->kt_used++];
+    slot->cls = cls;
+    slot->flops = 2.0 * (double)M * (double)N * (double)K;
+    PD_CHECK(cudaEventRecord(slot->a, st));
+  }
+  PD_TRY(gemm(dtype, A, a_mn, lda, B, b_mn, ldb, M, N, K, kind, ep, st));
+  rt->launches += 1;
+  if (slot) PD_CHECK(cudaEventRecord(slot->b, st));
+  return 0;
+}
 
 int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
   const pd_stage_desc& d = S.d;
@@ -89,10 +118,9 @@ int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.relu = d.relu_last;
     }
     const void* W = S.w_ring[(size_t)l * d.ring_depth + wslot];
-    PD_TRY(gemm(d.dtype, x, 0, K, W, 0, K, B, N, K, kind, ep, S.stream));
+    PD_TRY(timed_gemm(rt, KC_FWD, d.dtype, x, 0, K, W, 0, K, B, N, K, kind, ep, S.stream));
     x = ep.out;
   }
-  (void)rt;
   return 0;
 }
 
@@ -115,7 +143,7 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.ldo = Kin;
       ep.mask = X;
       ep.ldm = Kin;
-      PD_TRY(gemm(d.dtype, dz, 0, Nout, Wst, 1, Kin, B, Kin, Nout, EPI_MASK, ep, S.stream));
+      PD_TRY(timed_gemm(rt, KC_DGRAD, d.dtype, dz, 0, Nout, Wst, 1, Kin, B, Kin, Nout, EPI_MASK, ep, S.stream));
     }
     if (wnew >= 0) {
       // wgrad + SGD onto the latest weights, written as version mb into ring slot wnew
@@ -125,13 +153,13 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.out = S.w_ring[(size_t)l * d.ring_depth + wnew];
       ep.ldo = Kin;
       ep.lr = d.lr;
-      PD_TRY(gemm(d.dtype, dz, 1, Nout, X, 1, Kin, Nout, Kin, B, EPI_SGD, ep, S.stream));
+      PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, Nout, X, 1, Kin, Nout, Kin, B, EPI_SGD, ep, S.stream));
       PD_TRY(bias_sgd(d.dtype, dz, B, Nout, Nout, S.b_master[l], S.b_ring[(size_t)l * d.ring_depth + wnew], d.lr,
                       S.stream));
+      rt->launches += 1;
     }
     dz = out;
   }
-  (void)rt;
   return 0;
 }
 
@@ -234,6 +262,7 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
     for (int l = 0; l < S.d.n_layers; ++l) {
       const int64_t n = S.dims[l] * S.dims[l + 1];
       PD_TRY(cast_f32(S.d.dtype, S.w_master[l], S.w_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], n, S.stream));
+      rt->launches += 1;
       PD_CHECK(cudaMemcpyAsync(S.b_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], S.b_master[l],
                                sizeof(float) * S.dims[l + 1], cudaMemcpyDeviceToDevice, S.stream));
     }
@@ -255,10 +284,12 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
     if (it[PD_IT_RWAIT] > 0) {
       int* flag = fwd ? S.d.act_ready + it[PD_IT_XSLOT] : S.d.grad_ready + it[PD_IT_GSLOT];
       PD_TRY(flag_wait(flag, flag_val(rt->epoch, it[PD_IT_RWAIT]), S.d.err_word, S.stream));
+      rt->launches += 1;
     }
     if (it[PD_IT_AWAIT] > 0) {
       int* flag = fwd ? S.d.next_act_ack + it[PD_IT_OUT] : S.d.prev_grad_ack + it[PD_IT_OUT];
       PD_TRY(flag_wait(flag, flag_val(rt->epoch, it[PD_IT_AWAIT]), S.d.err_word, S.stream));
+      rt->launches += 1;
     }
     if (rt->traced) PD_CHECK(cudaEventRecord(rt->ev_start[i], S.stream));
     PD_TRY(fwd ? run_forward(rt, S, it) : run_backward(rt, S, it));
@@ -272,6 +303,8 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
       PD_TRY(flag_signal(S.d.act_ack_remote + it[PD_IT_XSLOT], flag_val(rt->epoch, mb), S.stream));
     if (!fwd && !S.d.is_last && S.d.grad_ack_remote)
       PD_TRY(flag_signal(S.d.grad_ack_remote + it[PD_IT_GSLOT], flag_val(rt->epoch, mb), S.stream));
+    rt->launches += (fwd && !S.d.is_last && S.d.next_act_ready) + (!fwd && !S.d.is_first && S.d.prev_grad_ready) +
+                    (!fwd && !S.d.is_first && S.d.act_ack_remote) + (!fwd && !S.d.is_last && S.d.grad_ack_remote);
     PD_CHECK(cudaEventRecord(rt->ev_end[i], S.stream));
   }
   for (auto& kv : rt->stages) {
@@ -302,6 +335,35 @@ int pd_rt_records(pd_runtime* rt, pd_record* out, int cap, int* n_out) {
   return 0;
 }
 
+int pd_rt_kernel_timing(pd_runtime* rt, int on) {
+  if (!rt) return set_error(PD_ERR_INVALID, "pd_rt_kernel_timing: null runtime");
+  rt->ktiming = on != 0;
+  rt->kt_used = 0;
+  return 0;
+}
+
+int pd_rt_kernel_stats(pd_runtime* rt, double* out9) {
+  if (!rt || !out9) return set_error(PD_ERR_INVALID, "pd_rt_kernel_stats: null argument");
+  for (int i = 0; i < 3 * KC_N; ++i) out9[i] = 0.0;
+  PD_CHECK(cudaSetDevice(rt->device));
+  for (size_t i = 0; i < rt->kt_used; ++i) {
+    auto& k = rt->kt[i];
+    float ms = 0.f;
+    PD_CHECK(cudaEventSynchronize(k.b));
+    PD_CHECK(cudaEventElapsedTime(&ms, k.a, k.b));
+    out9[3 * k.cls + 0] += 1.0;
+    out9[3 * k.cls + 1] += ms;
+    out9[3 * k.cls + 2] += k.flops;
+  }
+  return 0;
+}
+
+int pd_rt_launch_count(pd_runtime* rt, int64_t* out) {
+  if (!rt || !out) return set_error(PD_ERR_INVALID, "pd_rt_launch_count: null argument");
+  *out = rt->launches;
+  return 0;
+}
+
 int pd_rt_destroy(pd_runtime* rt) {
   if (!rt) return 0;
   cudaSetDevice(rt->device);
@@ -312,6 +374,7 @@ int pd_rt_destroy(pd_runtime* rt) {
   }
   for (auto e : rt->ev_start) cudaEventDestroy(e);
   for (auto e : rt->ev_end) cudaEventDestroy(e);
+  for (auto& k : rt->kt) { cudaEventDestroy(k.a); cudaEventDestroy(k.b); }
   if (rt->ev0) cudaEventDestroy(rt->ev0);
   delete rt;
   return 0;

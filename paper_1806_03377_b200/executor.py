@@ -252,6 +252,26 @@ class Executor:
                 out[st.first_layer + l] = (W.cpu().numpy().astype(np.float64), bias.cpu().numpy().astype(np.float64))
         return out
 
+    def kernel_timing(self, on: bool) -> None:
+        """Per-GEMM CUDA events on the launching stage streams (resets the counters)."""
+        nat.check(nat.lib().pd_rt_kernel_timing(self._rt, int(on)), "pd_rt_kernel_timing")
+
+    def kernel_stats(self) -> dict:
+        """{class: (launches, avg ms, algorithmic flops per launch)} for forward / dgrad / wgrad+SGD GEMMs."""
+        buf = (ctypes.c_double * 9)()
+        nat.check(nat.lib().pd_rt_kernel_stats(self._rt, buf), "pd_rt_kernel_stats")
+        out = {}
+        for i, name in enumerate(("fwd", "dgrad", "wgrad_sgd")):
+            n, ms, fl = buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]
+            if n:
+                out[name] = {"launches": int(n), "avg_ms": ms / n, "flops_per_launch": fl / n, "total_ms": ms}
+        return out
+
+    def launch_count(self) -> int:
+        v = ctypes.c_int64(0)
+        nat.check(nat.lib().pd_rt_launch_count(self._rt, ctypes.byref(v)), "pd_rt_launch_count")
+        return int(v.value)
+
     def records(self) -> list[tuple[int, float, float]]:
         L = nat.lib()
         n = self._prog.shape[0]
