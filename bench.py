@@ -43,6 +43,8 @@ def parse():
     p.add_argument("--mode", default="weight_stashing")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--serial", choices=["on", "off"], default="on",
+                   help="single-GPU: issue all hosted stages on one stream (on) or one stream per stage (off)")
     return p.parse_args()
 
 
@@ -57,6 +59,7 @@ def workload(args):
         "lr": 1e-5,
         "l2": "working set > 100x L2 (126 MB); no flush needed",
         "loss": "1/(2B) sum (Z-T)^2",
+        "streams": "one per GPU (stages in program order)" if args.serial == "on" else "one per stage",
     }
 
 
@@ -209,6 +212,7 @@ def run_ours(args, rank, world):
         ex = DistributedExecutor(cfg, model=spec)
     else:
         ex = pd.Executor(cfg, model=spec)
+        ex.set_serial(args.serial == "on")
     dist = torch.distributed if world > 1 else None
 
     def barrier():

@@ -163,6 +163,9 @@ int pd_rt_load_program(pd_runtime* rt, const int32_t* items, int n_items);
  * trace=1 records per-item device timestamps (pd_rt_records). */
 int pd_rt_run(pd_runtime* rt, void* stream, int trace);
 int pd_rt_records(pd_runtime* rt, pd_record* out, int cap, int* n_out);
+/* serial=1: every hosted stage issues on one stream in program order (single-GPU mode;
+ * the per-item dependencies are then satisfied by stream order). */
+int pd_rt_set_serial(pd_runtime* rt, int on);
 /* Per-GEMM CUDA-event timing on the launching stage stream (resets the counters).
  * stats: 3 classes (forward, dgrad, wgrad+SGD) x {launches, total ms, algorithmic flops}. */
 int pd_rt_kernel_timing(pd_runtime* rt, int on);

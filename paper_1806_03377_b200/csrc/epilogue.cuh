@@ -83,11 +83,45 @@ __device__ __forceinline__ void unpack_bf16x2(uint32_t u, float& a, float& b) {
   b = __high2float(h);
 }
 
-// 32 consecutive columns [c0, c0+32) of row r, bf16 activations, vectorised.
-// Requires c0 + 32 <= N, 16-byte aligned rows (ld % 8 == 0) and c0 % 32 == 0.
+// ---------------------------------------------------------------------------------------
+// Chunked tcgen05 epilogue with one-chunk-ahead prefetch of the per-element global input
+// (fp32 master for SGD, bf16 mask for dgrad, fp32 target for the loss), so the HBM latency
+// of chunk c+1 overlaps the math/stores of chunk c.
+template <int KIND> struct Aux { };
+template <> struct Aux<EPI_SGD> { float4 m[8]; };
+template <> struct Aux<EPI_MASK> { uint4 m[4]; };
+template <> struct Aux<EPI_LOSS> { float4 t[8]; };
+
 template <int KIND>
-__device__ __forceinline__ float epi_row32_bf16(const EpiArgs& ep, int64_t r, int64_t c0,
-                                                float (&v)[32]) {
+__device__ __forceinline__ void aux_load(const EpiArgs& ep, int64_t r, int64_t c0, Aux<KIND>& a) {
+  if constexpr (KIND == EPI_SGD) {
+    const float4* w4 = reinterpret_cast<const float4*>(ep.master + r * ep.ldw + c0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a.m[i] = w4[i];
+  } else if constexpr (KIND == EPI_MASK) {
+    const uint4* m4 =
+        reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.mask) + r * ep.ldm + c0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a.m[i] = m4[i];
+  } else if constexpr (KIND == EPI_LOSS) {
+    const float4* t4 = reinterpret_cast<const float4*>(ep.target + r * ep.ldt + c0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a.t[i] = t4[i];
+  }
+}
+
+__device__ __forceinline__ void store32_bf16(void* out, int64_t ld, int64_t r, int64_t c0, const float (&v)[32]) {
+  uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + r * ld + c0);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    o[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                      pack_bf16x2(v[8 * i + 4], v[8 * i + 5]), pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+}
+
+// Full 32-column chunk (c0 + 32 <= N); returns the loss contribution.
+template <int KIND>
+__device__ __forceinline__ float apply_chunk(const EpiArgs& ep, int64_t r, int64_t c0, float (&v)[32],
+                                             const Aux<KIND>& a) {
   float lsum = 0.f;
   if constexpr (KIND == EPI_STORE) {
     if (ep.bias) {
@@ -102,63 +136,41 @@ __device__ __forceinline__ float epi_row32_bf16(const EpiArgs& ep, int64_t r, in
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
     }
-    uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + r * ep.ldo + c0);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      o[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
-                        pack_bf16x2(v[8 * i + 4], v[8 * i + 5]),
-                        pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+    store32_bf16(ep.out, ep.ldo, r, c0, v);
   } else if constexpr (KIND == EPI_LOSS) {
-    const float4* t4 = reinterpret_cast<const float4*>(ep.target + r * ep.ldt + c0);
-    const float4* b4 = reinterpret_cast<const float4*>(ep.bias + c0);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      float4 t = t4[i];
-      float4 b = ep.bias ? __ldg(b4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-      v[4 * i] += b.x - t.x; v[4 * i + 1] += b.y - t.y;
-      v[4 * i + 2] += b.z - t.z; v[4 * i + 3] += b.w - t.w;
+      float4 b = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + c0) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[4 * i] += b.x - a.t[i].x; v[4 * i + 1] += b.y - a.t[i].y;
+      v[4 * i + 2] += b.z - a.t[i].z; v[4 * i + 3] += b.w - a.t[i].w;
     }
 #pragma unroll
     for (int i = 0; i < 32; ++i) { lsum += v[i] * v[i]; v[i] *= ep.scale; }
-    uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + r * ep.ldo + c0);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      o[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
-                        pack_bf16x2(v[8 * i + 4], v[8 * i + 5]),
-                        pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+    store32_bf16(ep.out, ep.ldo, r, c0, v);
   } else if constexpr (KIND == EPI_MASK) {
-    const uint4* m4 =
-        reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.mask) + r * ep.ldm + c0);
-    uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + r * ep.ldo + c0);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      uint4 m = m4[i];
-      uint32_t mw[4] = {m.x, m.y, m.z, m.w};
-      uint32_t ow[4];
+      const uint32_t mw[4] = {a.m[i].x, a.m[i].y, a.m[i].z, a.m[i].w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        float a, b;
-        unpack_bf16x2(mw[j], a, b);
-        ow[j] = pack_bf16x2(a > 0.f ? v[8 * i + 2 * j] : 0.f, b > 0.f ? v[8 * i + 2 * j + 1] : 0.f);
+        float x0, x1;
+        unpack_bf16x2(mw[j], x0, x1);
+        if (!(x0 > 0.f)) v[8 * i + 2 * j] = 0.f;
+        if (!(x1 > 0.f)) v[8 * i + 2 * j + 1] = 0.f;
       }
-      o[i] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
     }
+    store32_bf16(ep.out, ep.ldo, r, c0, v);
   } else if constexpr (KIND == EPI_SGD) {
     float4* w4 = reinterpret_cast<float4*>(ep.master + r * ep.ldw + c0);
-    uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + r * ep.ldo + c0);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      float4 w = w4[i];
+      float4 w = a.m[i];
       w.x -= ep.lr * v[4 * i]; w.y -= ep.lr * v[4 * i + 1];
       w.z -= ep.lr * v[4 * i + 2]; w.w -= ep.lr * v[4 * i + 3];
       w4[i] = w;
       v[4 * i] = w.x; v[4 * i + 1] = w.y; v[4 * i + 2] = w.z; v[4 * i + 3] = w.w;
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      o[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]), pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
-                        pack_bf16x2(v[8 * i + 4], v[8 * i + 5]),
-                        pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+    store32_bf16(ep.out, ep.ldo, r, c0, v);
   } else {
     float4* o = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + r * ep.ldo + c0);
 #pragma unroll

@@ -12,8 +12,10 @@
 //
 // bf16 path: persistent, warp-specialised tcgen05 kernel. TMA (128B swizzle) fills a
 // STAGES-deep smem ring; one elected thread issues tcgen05.mma (M=128, N=BN, K=16)
-// into a double-buffered TMEM accumulator; four epilogue warps drain TMEM with
-// tcgen05.ld while the next tile's MMAs run.
+// into a double-buffered TMEM accumulator; eight epilogue warps (two per TMEM lane
+// quadrant) drain TMEM with tcgen05.ld while the next tile's MMAs run, prefetching the
+// next 32-column chunk's global operand (master weights / mask / targets) one chunk ahead.
+// The tile width is picked per problem (256 or 224) to avoid a partial last wave.
 // fp32 path (the 4-stage MLP-1024 fp32 config): SIMT FFMA GEMM with the same epilogues
 // (tcgen05 has no IEEE-fp32 kind; tf32 would not meet the fp32 tolerance).
 #include <cuda.h>
@@ -30,24 +32,29 @@ namespace pd {
 
 // ============================================================== tcgen05 bf16 GEMM
 constexpr int TC_BM = 128;
-constexpr int TC_BK = 64;        // 64 bf16 = 128 B = one swizzle row
-constexpr int TC_THREADS = 192;  // warp0 TMA, warp1 MMA (+TMEM alloc), warps2-5 epilogue
+constexpr int TC_BK = 64;           // 64 bf16 = 128 B = one swizzle row
+constexpr int TC_EPI_WARPS = 8;     // two warps per TMEM lane quadrant, each owning half the columns
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;  // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2.. epilogue
+constexpr int TC_ACC_STRIDE = 256;  // TMEM columns between the two accumulator buffers
 
-template <int BN>
+template <int BN, bool B_MN>
 struct TcCfg {
+  // MN-major B tiles are loaded as whole 64-wide swizzle atoms; the MMA uses the first BN columns
+  static constexpr int BNL = B_MN ? ((BN + 63) / 64) * 64 : BN;
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
-  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int B_BYTES = BNL * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : 6;
-  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulator
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = 512;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(BN % 32 == 0 && BN % 16 == 0 && BN <= 256, "BN");
 };
 
 template <int BN, bool A_MN, bool B_MN, int KIND>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               int M, int N, int K, EpiArgs ep) {
-  using C = TcCfg<BN>;
+  using C = TcCfg<BN, B_MN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -68,7 +75,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tmem_full[a], 1); mbar_init(&tmem_empty[a], 128); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tmem_full[a], 1); mbar_init(&tmem_empty[a], 32 * TC_EPI_WARPS); }
     fence_barrier_init();
     fence_proxy_async_smem();
   }
@@ -100,7 +107,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
           if constexpr (B_MN) {
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i) tma_load_2d(b_dst + i * 8192, &tmB, &full[stage], n0 + 64 * i, k0);
+            for (int i = 0; i < C::BNL / 64; ++i) tma_load_2d(b_dst + i * 8192, &tmB, &full[stage], n0 + 64 * i, k0);
           } else {
             tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
           }
@@ -124,7 +131,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * BN;
+        const uint32_t d = tmem_base + acc * TC_ACC_STRIDE;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -146,29 +153,38 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else {
     // ---------------- epilogue warps: TMEM -> registers -> fused epilogue -> HBM
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int q = warp & 3;                 // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) / 4;        // which half of the tile's 32-column chunks
+    constexpr int NC = BN / 32;
+    const int c_begin = half ? (NC + 1) / 2 : 0;
+    const int c_end = half ? NC : (NC + 1) / 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     float lsum = 0.f;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       const int m0 = (t % num_m) * TC_BM;
       const int n0 = (t / num_m) * BN;
+      const int64_t r = m0 + 32 * q + lane_id();
+      const bool row_ok = r < M;
+      Aux<KIND> cur, nxt;
+      if (row_ok && c_begin < c_end && n0 + c_begin * 32 + 32 <= N) aux_load<KIND>(ep, r, n0 + c_begin * 32, cur);
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
-      const int64_t r = m0 + 32 * q + lane_id();
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        float v[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN + c * 32, v);
+      for (int c = c_begin; c < c_end; ++c) {
         const int64_t c0 = n0 + c * 32;
-        if (r < M) {
+        if (row_ok && c + 1 < c_end && c0 + 64 <= N) aux_load<KIND>(ep, r, c0 + 32, nxt);
+        float v[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * TC_ACC_STRIDE + c * 32, v);
+        if (row_ok) {
           if (c0 + 32 <= N) {
-            lsum += epi_row32_bf16<KIND>(ep, r, c0, v);
+            lsum += apply_chunk<KIND>(ep, r, c0, v, cur);
           } else {
             for (int j = 0; j < 32; ++j)
               if (c0 + j < N) lsum += epi_elem<KIND, __nv_bfloat16>(ep, r, c0 + j, v[j]);
           }
         }
+        cur = nxt;
       }
       tc_fence_before();
       mbar_arrive(&tmem_empty[acc]);
@@ -285,9 +301,17 @@ static int num_sms() {
 }
 
 template <int BN, bool A_MN, bool B_MN, int KIND>
-static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiArgs& ep,
+static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
                      cudaStream_t st) {
-  using C = TcCfg<BN>;
+  using C = TcCfg<BN, B_MN>;
+  CUtensorMap ta, tb;
+  int rc;
+  if (A_MN) rc = make_map(&ta, A, (uint64_t)M, (uint64_t)K, lda, 64, 64);
+  else rc = make_map(&ta, A, (uint64_t)K, (uint64_t)M, lda, 64, TC_BM);
+  if (rc) return rc;
+  if (B_MN) rc = make_map(&tb, B, (uint64_t)N, (uint64_t)K, ldb, 64, 64);
+  else rc = make_map(&tb, B, (uint64_t)K, (uint64_t)N, ldb, 64, BN);
+  if (rc) return rc;
   auto kern = k_gemm_tc<BN, A_MN, B_MN, KIND>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
@@ -303,15 +327,37 @@ static int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N,
   return 0;
 }
 
+// Tile width minimising (waves x tile width): e.g. 2048x8192 -> BN=224 gives 592 tiles = 4.00
+// waves on 148 SMs instead of 512 tiles = 3.46 waves (a 46 %-full tail wave) at BN=256.
+static int pick_bn(int M, int N) {
+  const int sms = num_sms();
+  const int cands[2] = {256, 224};
+  int best = 256;
+  long best_cost = -1;
+  for (int bn : cands) {
+    const long tiles = (long)((M + TC_BM - 1) / TC_BM) * ((N + bn - 1) / bn);
+    const long cost = ((tiles + sms - 1) / sms) * bn;
+    if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = bn; }
+  }
+  return best;
+}
+
+template <bool A_MN, bool B_MN, int KIND>
+static int launch_bn(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
+                     cudaStream_t st) {
+  if (pick_bn(M, N) == 224) return launch_tc<224, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
+  return launch_tc<256, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
+}
+
 template <bool A_MN, bool B_MN>
-static int dispatch_kind(int kind, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+static int dispatch_kind(int kind, const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K,
                          const EpiArgs& ep, cudaStream_t st) {
   switch (kind) {
-    case EPI_STORE: return launch_tc<256, A_MN, B_MN, EPI_STORE>(ta, tb, M, N, K, ep, st);
-    case EPI_LOSS: return launch_tc<256, A_MN, B_MN, EPI_LOSS>(ta, tb, M, N, K, ep, st);
-    case EPI_MASK: return launch_tc<256, A_MN, B_MN, EPI_MASK>(ta, tb, M, N, K, ep, st);
-    case EPI_SGD: return launch_tc<256, A_MN, B_MN, EPI_SGD>(ta, tb, M, N, K, ep, st);
-    case EPI_GRADF32: return launch_tc<256, A_MN, B_MN, EPI_GRADF32>(ta, tb, M, N, K, ep, st);
+    case EPI_STORE: return launch_bn<A_MN, B_MN, EPI_STORE>(A, lda, B, ldb, M, N, K, ep, st);
+    case EPI_LOSS: return launch_bn<A_MN, B_MN, EPI_LOSS>(A, lda, B, ldb, M, N, K, ep, st);
+    case EPI_MASK: return launch_bn<A_MN, B_MN, EPI_MASK>(A, lda, B, ldb, M, N, K, ep, st);
+    case EPI_SGD: return launch_bn<A_MN, B_MN, EPI_SGD>(A, lda, B, ldb, M, N, K, ep, st);
+    case EPI_GRADF32: return launch_bn<A_MN, B_MN, EPI_GRADF32>(A, lda, B, ldb, M, N, K, ep, st);
   }
   return set_error(PD_ERR_INVALID, "unknown epilogue kind %d", kind);
 }
@@ -323,18 +369,10 @@ int gemm_bf16_tc(const void* A, int a_mn, int64_t lda, const void* B, int b_mn, 
     return set_error(PD_ERR_INVALID, "gemm: operands must be 16-byte aligned with ld %% 8 == 0");
   if ((kind != EPI_GRADF32 && (ep.ldo % 8)) || (reinterpret_cast<uintptr_t>(ep.out) % 16))
     return set_error(PD_ERR_INVALID, "gemm: output must be 16-byte aligned with ld %% 8 == 0");
-  CUtensorMap ta, tb;
-  int rc;
-  if (a_mn) rc = make_map(&ta, A, (uint64_t)M, (uint64_t)K, lda, 64, 64);
-  else rc = make_map(&ta, A, (uint64_t)K, (uint64_t)M, lda, 64, TC_BM);
-  if (rc) return rc;
-  if (b_mn) rc = make_map(&tb, B, (uint64_t)N, (uint64_t)K, ldb, 64, 64);
-  else rc = make_map(&tb, B, (uint64_t)K, (uint64_t)N, ldb, 64, 256);
-  if (rc) return rc;
-  if (!a_mn && !b_mn) return dispatch_kind<false, false>(kind, ta, tb, M, N, K, ep, st);
-  if (!a_mn && b_mn) return dispatch_kind<false, true>(kind, ta, tb, M, N, K, ep, st);
-  if (a_mn && !b_mn) return dispatch_kind<true, false>(kind, ta, tb, M, N, K, ep, st);
-  return dispatch_kind<true, true>(kind, ta, tb, M, N, K, ep, st);
+  if (!a_mn && !b_mn) return dispatch_kind<false, false>(kind, A, lda, B, ldb, M, N, K, ep, st);
+  if (!a_mn && b_mn) return dispatch_kind<false, true>(kind, A, lda, B, ldb, M, N, K, ep, st);
+  if (a_mn && !b_mn) return dispatch_kind<true, false>(kind, A, lda, B, ldb, M, N, K, ep, st);
+  return dispatch_kind<true, true>(kind, A, lda, B, ldb, M, N, K, ep, st);
 }
 
 template <typename T>

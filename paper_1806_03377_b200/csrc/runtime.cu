@@ -48,6 +48,8 @@ struct pd_runtime {
   bool traced = false;
   // kernel accounting: launches of our kernels, and optional per-GEMM event timing by class
   int64_t launches = 0;
+  bool serial = false;             // all hosted stages on one stream (single-GPU timing mode)
+  cudaStream_t shared = nullptr;
   bool ktiming = false;
   struct KT { int cls; double flops; cudaEvent_t a, b; };
   std::vector<KT> kt;
@@ -93,6 +95,7 @@ int timed_gemm(pd_runtime* rt, int cls, int dtype, const void* A, int a_mn, int6
 }
 
 int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
+  cudaStream_t ST = rt->serial ? rt->shared : S.stream;
   const pd_stage_desc& d = S.d;
   const int L = d.n_layers, B = d.batch;
   const int wslot = it[PD_IT_WSLOT], act = it[PD_IT_ACT], mb = it[PD_IT_MB];
@@ -118,13 +121,14 @@ int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.relu = d.relu_last;
     }
     const void* W = S.w_ring[(size_t)l * d.ring_depth + wslot];
-    PD_TRY(timed_gemm(rt, KC_FWD, d.dtype, x, 0, K, W, 0, K, B, N, K, kind, ep, S.stream));
+    PD_TRY(timed_gemm(rt, KC_FWD, d.dtype, x, 0, K, W, 0, K, B, N, K, kind, ep, ST));
     x = ep.out;
   }
   return 0;
 }
 
 int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
+  cudaStream_t ST = rt->serial ? rt->shared : S.stream;
   const pd_stage_desc& d = S.d;
   const int L = d.n_layers, B = d.batch;
   const int wslot = it[PD_IT_WSLOT], wnew = it[PD_IT_WNEW], act = it[PD_IT_ACT];
@@ -143,7 +147,7 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.ldo = Kin;
       ep.mask = X;
       ep.ldm = Kin;
-      PD_TRY(timed_gemm(rt, KC_DGRAD, d.dtype, dz, 0, Nout, Wst, 1, Kin, B, Kin, Nout, EPI_MASK, ep, S.stream));
+      PD_TRY(timed_gemm(rt, KC_DGRAD, d.dtype, dz, 0, Nout, Wst, 1, Kin, B, Kin, Nout, EPI_MASK, ep, ST));
     }
     if (wnew >= 0) {
       // wgrad + SGD onto the latest weights, written as version mb into ring slot wnew
@@ -153,9 +157,9 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.out = S.w_ring[(size_t)l * d.ring_depth + wnew];
       ep.ldo = Kin;
       ep.lr = d.lr;
-      PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, Nout, X, 1, Kin, Nout, Kin, B, EPI_SGD, ep, S.stream));
+      PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, Nout, X, 1, Kin, Nout, Kin, B, EPI_SGD, ep, ST));
       PD_TRY(bias_sgd(d.dtype, dz, B, Nout, Nout, S.b_master[l], S.b_ring[(size_t)l * d.ring_depth + wnew], d.lr,
-                      S.stream));
+                      ST));
       rt->launches += 1;
     }
     dz = out;
@@ -257,59 +261,61 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
   PD_CHECK(cudaEventRecord(rt->ev0, main));
   for (auto& kv : rt->stages) {
     Stage& S = kv.second;
-    PD_CHECK(cudaStreamWaitEvent(S.stream, rt->ev0, 0));
+    cudaStream_t ST = rt->serial ? rt->shared : S.stream;
+    PD_CHECK(cudaStreamWaitEvent(ST, rt->ev0, 0));
     // version 0 of this run = the current (latest) weights
     for (int l = 0; l < S.d.n_layers; ++l) {
       const int64_t n = S.dims[l] * S.dims[l + 1];
-      PD_TRY(cast_f32(S.d.dtype, S.w_master[l], S.w_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], n, S.stream));
+      PD_TRY(cast_f32(S.d.dtype, S.w_master[l], S.w_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], n, ST));
       rt->launches += 1;
       PD_CHECK(cudaMemcpyAsync(S.b_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], S.b_master[l],
-                               sizeof(float) * S.dims[l + 1], cudaMemcpyDeviceToDevice, S.stream));
+                               sizeof(float) * S.dims[l + 1], cudaMemcpyDeviceToDevice, ST));
     }
     if (S.d.is_last && S.d.loss) {
       // losses are indexed by minibatch id; the program's largest id bounds the buffer
       int max_mb = 0;
       for (size_t i = 0; i < rt->items.size(); i += PD_ITEM_WIDTH) max_mb = std::max(max_mb, rt->items[i + PD_IT_MB]);
-      PD_CHECK(cudaMemsetAsync(S.d.loss, 0, sizeof(float) * (size_t)(max_mb + 1), S.stream));
+      PD_CHECK(cudaMemsetAsync(S.d.loss, 0, sizeof(float) * (size_t)(max_mb + 1), ST));
     }
   }
   const int n = (int)(rt->items.size() / PD_ITEM_WIDTH);
   for (int i = 0; i < n; ++i) {
     const int32_t* it = rt->items.data() + (size_t)i * PD_ITEM_WIDTH;
     Stage& S = rt->stages[it[PD_IT_STAGE]];
+    cudaStream_t ST = rt->serial ? rt->shared : S.stream;
     const bool fwd = it[PD_IT_OP] == 0;
     const int dep = it[PD_IT_DEP], war = it[PD_IT_WAR];
-    if (dep >= 0) PD_CHECK(cudaStreamWaitEvent(S.stream, rt->ev_end[dep], 0));
-    if (war >= 0) PD_CHECK(cudaStreamWaitEvent(S.stream, rt->ev_end[war], 0));
+    if (dep >= 0) PD_CHECK(cudaStreamWaitEvent(ST, rt->ev_end[dep], 0));
+    if (war >= 0) PD_CHECK(cudaStreamWaitEvent(ST, rt->ev_end[war], 0));
     if (it[PD_IT_RWAIT] > 0) {
       int* flag = fwd ? S.d.act_ready + it[PD_IT_XSLOT] : S.d.grad_ready + it[PD_IT_GSLOT];
-      PD_TRY(flag_wait(flag, flag_val(rt->epoch, it[PD_IT_RWAIT]), S.d.err_word, S.stream));
+      PD_TRY(flag_wait(flag, flag_val(rt->epoch, it[PD_IT_RWAIT]), S.d.err_word, ST));
       rt->launches += 1;
     }
     if (it[PD_IT_AWAIT] > 0) {
       int* flag = fwd ? S.d.next_act_ack + it[PD_IT_OUT] : S.d.prev_grad_ack + it[PD_IT_OUT];
-      PD_TRY(flag_wait(flag, flag_val(rt->epoch, it[PD_IT_AWAIT]), S.d.err_word, S.stream));
+      PD_TRY(flag_wait(flag, flag_val(rt->epoch, it[PD_IT_AWAIT]), S.d.err_word, ST));
       rt->launches += 1;
     }
-    if (rt->traced) PD_CHECK(cudaEventRecord(rt->ev_start[i], S.stream));
+    if (rt->traced) PD_CHECK(cudaEventRecord(rt->ev_start[i], ST));
     PD_TRY(fwd ? run_forward(rt, S, it) : run_backward(rt, S, it));
     // cross-GPU hand-off: publish the payload the epilogue stored into the peer inbox
     const int mb = it[PD_IT_MB];
     if (fwd && !S.d.is_last && S.d.next_act_ready)
-      PD_TRY(flag_signal(S.d.next_act_ready + it[PD_IT_OUT], flag_val(rt->epoch, mb), S.stream));
+      PD_TRY(flag_signal(S.d.next_act_ready + it[PD_IT_OUT], flag_val(rt->epoch, mb), ST));
     if (!fwd && !S.d.is_first && S.d.prev_grad_ready)
-      PD_TRY(flag_signal(S.d.prev_grad_ready + it[PD_IT_OUT], flag_val(rt->epoch, mb), S.stream));
+      PD_TRY(flag_signal(S.d.prev_grad_ready + it[PD_IT_OUT], flag_val(rt->epoch, mb), ST));
     if (!fwd && !S.d.is_first && S.d.act_ack_remote)
-      PD_TRY(flag_signal(S.d.act_ack_remote + it[PD_IT_XSLOT], flag_val(rt->epoch, mb), S.stream));
+      PD_TRY(flag_signal(S.d.act_ack_remote + it[PD_IT_XSLOT], flag_val(rt->epoch, mb), ST));
     if (!fwd && !S.d.is_last && S.d.grad_ack_remote)
-      PD_TRY(flag_signal(S.d.grad_ack_remote + it[PD_IT_GSLOT], flag_val(rt->epoch, mb), S.stream));
+      PD_TRY(flag_signal(S.d.grad_ack_remote + it[PD_IT_GSLOT], flag_val(rt->epoch, mb), ST));
     rt->launches += (fwd && !S.d.is_last && S.d.next_act_ready) + (!fwd && !S.d.is_first && S.d.prev_grad_ready) +
                     (!fwd && !S.d.is_first && S.d.act_ack_remote) + (!fwd && !S.d.is_last && S.d.grad_ack_remote);
-    PD_CHECK(cudaEventRecord(rt->ev_end[i], S.stream));
+    PD_CHECK(cudaEventRecord(rt->ev_end[i], ST));
   }
   for (auto& kv : rt->stages) {
     Stage& S = kv.second;
-    PD_CHECK(cudaEventRecord(S.ev_done, S.stream));
+    PD_CHECK(cudaEventRecord(S.ev_done, rt->serial ? rt->shared : S.stream));
     PD_CHECK(cudaStreamWaitEvent(main, S.ev_done, 0));
   }
   return 0;
@@ -332,6 +338,14 @@ int pd_rt_records(pd_runtime* rt, pd_record* out, int cap, int* n_out) {
     out[k].t_end_ms = b;
   }
   *n_out = k;
+  return 0;
+}
+
+int pd_rt_set_serial(pd_runtime* rt, int on) {
+  if (!rt) return set_error(PD_ERR_INVALID, "pd_rt_set_serial: null runtime");
+  PD_CHECK(cudaSetDevice(rt->device));
+  if (on && !rt->shared) PD_CHECK(cudaStreamCreateWithFlags(&rt->shared, cudaStreamNonBlocking));
+  rt->serial = on != 0;
   return 0;
 }
 
@@ -376,6 +390,7 @@ int pd_rt_destroy(pd_runtime* rt) {
   for (auto e : rt->ev_end) cudaEventDestroy(e);
   for (auto& k : rt->kt) { cudaEventDestroy(k.a); cudaEventDestroy(k.b); }
   if (rt->ev0) cudaEventDestroy(rt->ev0);
+  if (rt->shared) { cudaStreamSynchronize(rt->shared); cudaStreamDestroy(rt->shared); }
   delete rt;
   return 0;
 }

@@ -252,6 +252,10 @@ class Executor:
                 out[st.first_layer + l] = (W.cpu().numpy().astype(np.float64), bias.cpu().numpy().astype(np.float64))
         return out
 
+    def set_serial(self, on: bool) -> None:
+        """Issue every hosted stage on one stream in program order (single-GPU timing mode)."""
+        nat.check(nat.lib().pd_rt_set_serial(self._rt, int(on)), "pd_rt_set_serial")
+
     def kernel_timing(self, on: bool) -> None:
         """Per-GEMM CUDA events on the launching stage streams (resets the counters)."""
         nat.check(nat.lib().pd_rt_kernel_timing(self._rt, int(on)), "pd_rt_kernel_timing")

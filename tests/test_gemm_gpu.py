@@ -119,3 +119,21 @@ def test_gemm_rejects_unaligned_leading_dim():
     out = torch.empty(64, 64, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(ValidationError):
         nat.gemm(a, False, b, False, 64, 64, 100, kind=nat.EPI_STORE, out=out)
+
+
+def test_gemm_bn224_partial_tiles_mask_and_sgd():
+    # 2048x1024: pick_bn chooses 224 (80 tiles in one wave), so the last tile is 128 wide and the
+    # MN-major B operand uses a partial 64-wide swizzle atom
+    M, N, K = 2048, 1024, 512
+    a, b, ref = operands(M, N, K, False, True, torch.bfloat16, seed=11)
+    mask = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    nat.gemm(a, False, b, True, M, N, K, kind=nat.EPI_MASK, out=out, mask=mask)
+    a2, b2, ref2 = operands(M, N, K, True, True, torch.bfloat16, seed=12)
+    master = torch.randn(M, N, device="cuda")
+    m0 = master.clone()
+    ring = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    nat.gemm(a2, True, b2, True, M, N, K, kind=nat.EPI_SGD, out=ring, master=master, lr=0.01)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(out.float(), ref * (mask.float() > 0), atol=2e-2 * K ** 0.5, rtol=2e-2)
+    torch.testing.assert_close(master, m0 - 0.01 * ref2, atol=1e-3, rtol=1e-4)

@@ -11,6 +11,8 @@ if [[ $what == tests || $what == all ]]; then
 fi
 if [[ $what == bench || $what == all ]]; then
   timeout -s KILL 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -5 gpurun_out/bench.err; cat gpurun_out/bench.json
+  timeout -s KILL 600 python bench.py --serial off --no-cpu-baseline > gpurun_out/bench_multistream.json 2>&1; cat gpurun_out/bench_multistream.json
+  timeout -s KILL 200 python tools/gemm_bench.py 2048 8192 > gpurun_out/gemm_bench.log 2>&1; cat gpurun_out/gemm_bench.log
   timeout -s KILL 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1; cat gpurun_out/bench_ref.json
 fi
 if [[ $what == ncu || $what == all ]]; then
