@@ -309,6 +309,8 @@ def run_ours(args, rank, world):
         "model_tflops": value * flops_per_sample / 1e12,
         "model_frac_of_sustained_peak": value * flops_per_sample / 1e12 / peak / world,
         "bubble_fraction": res.extras.get("bubble_fraction"),
+        "bubble_definition": "1 - fraction of the reference's steady window (simulator.py:361-385) in which the GPU "
+                             "runs a pass (union over its hosted stages)",
         "per_worker_utilization": [round(u, 4) for u in rep.per_worker_utilization] if rep else None,
         "steady_minibatches_per_s": rep.steady_throughput if rep else None,
     }

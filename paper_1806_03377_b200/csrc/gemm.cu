@@ -329,7 +329,9 @@ static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int
 
 // Tile width minimising (waves x tile width): e.g. 2048x8192 -> BN=224 gives 592 tiles = 4.00
 // waves on 148 SMs instead of 512 tiles = 3.46 waves (a 46 %-full tail wave) at BN=256.
-static int pick_bn(int M, int N) {
+static int pick_bn(int M, int N, bool b_mn) {
+  // an MN-major B tile is loaded in whole 64-wide atoms, so BN=224 would still move 256 columns
+  if (b_mn) return 256;
   const int sms = num_sms();
   const int cands[2] = {256, 224};
   int best = 256;
@@ -345,7 +347,7 @@ static int pick_bn(int M, int N) {
 template <bool A_MN, bool B_MN, int KIND>
 static int launch_bn(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
                      cudaStream_t st) {
-  if (pick_bn(M, N) == 224) return launch_tc<224, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
+  if (pick_bn(M, N, B_MN) == 224) return launch_tc<224, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
   return launch_tc<256, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
 }
 

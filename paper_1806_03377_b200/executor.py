@@ -312,18 +312,43 @@ class Executor:
                 total += m.batch * m.widths[plan.stages[s].first_layer - 1] * m.bytes_per_elem
         return total
 
+    def gpu_utilization(self, trace) -> float:
+        """Fraction of the steady window during which this GPU runs at least one pass.
+
+        The reference's per-worker utilisation (simulator.py:379-385) is kept in the report;
+        with several stages per GPU the device-level bubble is 1 - (union of their busy time).
+        """
+        from .ledger import steady_window
+
+        k1, k2 = steady_window(self.cfg, self.cfg.plan.num_stages, self.cfg.plan.stages[0].replication)
+        done = {ev.minibatch: ev.time_end for ev in trace if ev.stage == 0 and ev.direction is Direction.BACKWARD}
+        t1, t2 = done[k1], done[k2]
+        iv = sorted((max(ev.time_start, t1), min(ev.time_end, t2)) for ev in trace if ev.time_end > t1 and ev.time_start < t2)
+        busy, cur_lo, cur_hi = 0.0, None, None
+        for lo, hi in iv:
+            if cur_hi is None or lo > cur_hi:
+                if cur_hi is not None:
+                    busy += cur_hi - cur_lo
+                cur_lo, cur_hi = lo, hi
+            else:
+                cur_hi = max(cur_hi, hi)
+        if cur_hi is not None:
+            busy += cur_hi - cur_lo
+        return busy / (t2 - t1)
+
     def result(self) -> SimResult:
         torch = _torch()
         torch.cuda.synchronize(self.device)
         trace = self.trace() if getattr(self, "_traced", False) else []
         report = build_report(self.cfg, trace, len(self.schedule.workers), self.comm_bytes()) if trace else None
         losses = self.losses()
-        bubble = None
+        bubble, gpu_util = None, None
         if report is not None:
-            bubble = 1.0 - sum(report.per_worker_utilization) / len(report.per_worker_utilization)
+            gpu_util = self.gpu_utilization(trace)
+            bubble = 1.0 - gpu_util
         return SimResult(report=report, ledger=self.program.ledger, trace=trace, losses=losses,
                          weights=self.weights(),
-                         extras={"bubble_fraction": bubble, "ring_depths": {b.stage: b.ring_depth for b in self.bufs.values()},
+                         extras={"bubble_fraction": bubble, "gpu_utilization": gpu_util, "ring_depths": {b.stage: b.ring_depth for b in self.bufs.values()},
                                  "device": str(self.device), "runs": self.runs})
 
     def close(self) -> None:

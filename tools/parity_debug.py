@@ -21,12 +21,16 @@ def main(width=1024, layers=8, stages=4, batch=32, dtype="fp32", lr=2e-4, K=20, 
     vers = lambda s, mb, d: res.ledger.version_used(s, mb, pd.Direction(d))  # noqa: E731
     losses, final = mlp_train(P, X, T, lr, bounds, vers, K, emulate="bf16" if dtype == "bf16" else None)
     print("loss rel", np.max(np.abs(np.array(res.losses[:K]) - losses) / losses))
+    print("per-step loss rel", np.array2string(np.abs(np.array(res.losses[:K]) - losses) / losses, precision=2))
     for l in range(1, layers + 1):
         Wd, bd = res.weights[l]
         Wo, bo = final[l - 1]
         W0, b0 = P[l - 1]
         dW, dWo = Wd - W0, Wo - W0
         db, dbo = bd - b0, bo - b0
+        if not np.any(dWo):
+            print(l, "W max|dev-init|", np.abs(dW).max(), "b", np.abs(db).max())
+            continue
         print(l, "W delta relerr %.3e" % (np.abs(dW - dWo).max() / np.abs(dWo).max()),
               "b delta relerr %.3e" % (np.abs(db - dbo).max() / np.abs(dbo).max()),
               "ratio |dW|/|dWo| %.4f" % (np.linalg.norm(dW) / np.linalg.norm(dWo)),
