@@ -206,13 +206,8 @@ def run_ours(args, rank, world):
     plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=args.stages, machines_used=args.stages)
     cfg = pd.SimConfig(plan=plan, mode=args.mode, num_minibatches=args.minibatches)
     spec = pd.mlp(args.width, args.layers, batch=args.batch, dtype="bf16", lr=1e-5, n_blocks=4, seed=0)
-    if world > 1:
-        from paper_1806_03377_b200.distributed import DistributedExecutor
-
-        ex = DistributedExecutor(cfg, model=spec)
-    else:
-        ex = pd.Executor(cfg, model=spec)
-        ex.set_serial(args.serial == "on")
+    ex = pd.Executor(cfg, model=spec)
+    ex.set_serial(args.serial == "on")
     dist = torch.distributed if world > 1 else None
 
     def barrier():
@@ -247,15 +242,16 @@ def run_ours(args, rank, world):
     samples = args.steps * args.minibatches * args.batch
     value = samples / (ms * 1e-3)
     # ---------------- traced step: bubble / utilisation with the reference's window rule
+    barrier()
+    torch.cuda.synchronize()
     ex.step(stream=stream, trace=True)
     res = ex.result()
     # ---------------- e2e through the public API with host buffers
     X_host = torch.randn(spec.n_blocks, spec.batch, spec.widths[0]).to(torch.bfloat16).pin_memory()
     T_host = torch.randn(spec.n_blocks, spec.batch, spec.widths[-1]).pin_memory()
     loss_host = torch.empty(args.minibatches + 1, dtype=torch.float32).pin_memory()
-    h2d = 0
-    hosts_first = any(b.stage == 0 for b in ex.bufs.values())
-    hosts_last = any(b.stage == args.stages - 1 for b in ex.bufs.values())
+    hosts_first = ex.hosts_stage(0)
+    hosts_last = ex.hosts_stage(args.stages - 1)
     h2d = (X_host.numel() * X_host.element_size() if hosts_first else 0) + \
           (T_host.numel() * T_host.element_size() if hosts_last else 0)
     d2h = loss_host.numel() * 4 if hosts_last else 0
@@ -276,6 +272,10 @@ def run_ours(args, rank, world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_value = args.e2e_steps * args.minibatches * args.batch / (e2e_ms * 1e-3)
+    if dist is not None:  # whole-job counts
+        t = torch.tensor([float(h2d), float(d2h), float(launches)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        h2d, d2h, launches = int(t[0]), int(t[1]), int(t[2])
     if rank != 0:
         ex.close()
         return

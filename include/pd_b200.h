@@ -79,8 +79,9 @@ int pd_cast(int dtype, const float* src, void* out, int64_t n, void* stream);
  * signal: system-scope release store of `value`; wait: acquire-poll until *flag >= value. */
 int pd_flag_signal(int* flag, int value, void* stream);
 int pd_flag_wait(const int* flag, int value, int* err_word, void* stream);
-/* CUDA IPC so a peer process can map an inbox: handle is 64 opaque bytes. */
-int pd_ipc_get_handle(const void* dev_ptr, void* handle_out64);
+/* CUDA IPC so a peer process can map an inbox: handle is 64 opaque bytes naming the whole
+ * allocation that contains dev_ptr; *offset_out is dev_ptr's byte offset inside it. */
+int pd_ipc_get_handle(const void* dev_ptr, void* handle_out64, int64_t* offset_out);
 int pd_ipc_open(const void* handle64, void** dev_ptr_out);
 int pd_ipc_close(void* dev_ptr);
 int pd_enable_peer_access(int peer_device);

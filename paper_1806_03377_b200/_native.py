@@ -80,7 +80,7 @@ def lib() -> ctypes.CDLL:
         L.pd_cast.argtypes = [c_int, c_void_p, c_void_p, c_int64, c_void_p]
         L.pd_flag_signal.argtypes = [c_void_p, c_int, c_void_p]
         L.pd_flag_wait.argtypes = [c_void_p, c_int, c_void_p, c_void_p]
-        L.pd_ipc_get_handle.argtypes = [c_void_p, c_void_p]
+        L.pd_ipc_get_handle.argtypes = [c_void_p, c_void_p, POINTER(c_int64)]
         L.pd_ipc_open.argtypes = [c_void_p, POINTER(c_void_p)]
         L.pd_ipc_close.argtypes = [c_void_p]
         L.pd_rt_create.argtypes = [c_int, POINTER(c_void_p)]
@@ -156,3 +156,25 @@ def bias_sgd(dz, rows: int, cols: int, b_master, b_out, lr: float, stream=None) 
 def sgd_update(master, grad, out, lr: float, stream=None) -> None:
     check(lib().pd_sgd_update(dtype_code(out.dtype), ptr(master), ptr(grad), ptr(out), master.numel(), lr,
                               stream_ptr(stream)), "pd_sgd_update")
+
+
+def ipc_export(t) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of t's allocation, byte offset of t inside it)."""
+    h = (ctypes.c_char * 64)()
+    off = ctypes.c_int64(0)
+    check(lib().pd_ipc_get_handle(ptr(t), h, ctypes.byref(off)), "pd_ipc_get_handle")
+    return bytes(h), int(off.value)
+
+
+_ipc_bases: dict = {}
+
+
+def ipc_import(handle: bytes, offset: int) -> int:
+    """Device address in this process of an exported (handle, offset); allocations opened once."""
+    base = _ipc_bases.get(handle)
+    if base is None:
+        out = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(handle, 64)
+        check(lib().pd_ipc_open(buf, ctypes.byref(out)), "pd_ipc_open")
+        base = _ipc_bases[handle] = int(out.value)
+    return base + offset

@@ -1,5 +1,6 @@
 // Elementwise / reduction kernels, cross-GPU flags, error state and the C ABI wrappers
 // for single kernels (include/pd_b200.h).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdarg>
 #include <cstdio>
@@ -178,12 +179,30 @@ int pd_flag_wait(const int* flag, int value, int* err_word, void* stream) {
   return flag_wait(flag, value, err_word, static_cast<cudaStream_t>(stream));
 }
 
-int pd_ipc_get_handle(const void* dev_ptr, void* handle_out64) {
+int pd_ipc_get_handle(const void* dev_ptr, void* handle_out64, int64_t* offset_out) {
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
   cudaIpcMemHandle_t h;
   cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
   if (e != cudaSuccess) return set_error(PD_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
   memcpy(handle_out64, &h, sizeof(h));
+  if (offset_out) {
+    // the handle names the allocation, not the pointer: report where dev_ptr sits inside it
+    using range_fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static range_fn fn = nullptr;
+    if (!fn) {
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        return set_error(PD_ERR_CUDA, "cuMemGetAddressRange unavailable");
+      fn = reinterpret_cast<range_fn>(p);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+      return set_error(PD_ERR_CUDA, "cuMemGetAddressRange failed");
+    *offset_out = (int64_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  }
   return 0;
 }
 int pd_ipc_open(const void* handle64, void** dev_ptr_out) {

@@ -49,6 +49,10 @@ struct pd_runtime {
   // kernel accounting: launches of our kernels, and optional per-GEMM event timing by class
   int64_t launches = 0;
   bool serial = false;             // all hosted stages on one stream (single-GPU timing mode)
+  // end-of-run drain: (stage, local ack flag, final occupant mb) of every outbox slot that
+  // lives on another GPU, so the next run cannot overwrite a slot the peer still reads
+  struct Drain { int stage; int* flag; int mb; };
+  std::vector<Drain> drain;
   cudaStream_t shared = nullptr;
   bool ktiming = false;
   struct KT { int cls; double flops; cudaEvent_t a, b; };
@@ -240,6 +244,34 @@ int pd_rt_load_program(pd_runtime* rt, const int32_t* items, int n_items) {
       return set_error(PD_ERR_INVALID, "item %d: backward outbox slot %d out of range", i, it[PD_IT_OUT]);
   }
   rt->items.assign(items, items + (size_t)n_items * PD_ITEM_WIDTH);
+  rt->drain.clear();
+  {
+    std::map<std::pair<int*, int>, int> last;  // (ack array, slot) -> final occupant
+    for (int i = 0; i < n_items; ++i) {
+      const int32_t* it = items + (size_t)i * PD_ITEM_WIDTH;
+      const Stage& S = rt->stages.at(it[PD_IT_STAGE]);
+      const bool fwd = it[PD_IT_OP] == 0;
+      int* ack = nullptr;
+      if (fwd && !S.d.is_last && S.d.next_act_ready) ack = S.d.next_act_ack;
+      if (!fwd && !S.d.is_first && S.d.prev_grad_ready) ack = S.d.prev_grad_ack;
+      if (ack) {
+        int& m = last[{ack, it[PD_IT_OUT]}];
+        m = std::max(m, it[PD_IT_MB]);
+      }
+    }
+    for (int i = 0; i < n_items; ++i) {  // attach each drain wait to the stage that owns the ack array
+      const int32_t* it = items + (size_t)i * PD_ITEM_WIDTH;
+      const Stage& S = rt->stages.at(it[PD_IT_STAGE]);
+      for (auto kv = last.begin(); kv != last.end();) {
+        if (kv->first.first == S.d.next_act_ack || kv->first.first == S.d.prev_grad_ack) {
+          rt->drain.push_back({it[PD_IT_STAGE], kv->first.first + kv->first.second, kv->second});
+          kv = last.erase(kv);
+        } else {
+          ++kv;
+        }
+      }
+    }
+  }
   for (auto e : rt->ev_start) cudaEventDestroy(e);
   for (auto e : rt->ev_end) cudaEventDestroy(e);
   rt->ev_start.assign(n_items, nullptr);
@@ -312,6 +344,12 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
     rt->launches += (fwd && !S.d.is_last && S.d.next_act_ready) + (!fwd && !S.d.is_first && S.d.prev_grad_ready) +
                     (!fwd && !S.d.is_first && S.d.act_ack_remote) + (!fwd && !S.d.is_last && S.d.grad_ack_remote);
     PD_CHECK(cudaEventRecord(rt->ev_end[i], ST));
+  }
+  for (const auto& dr : rt->drain) {
+    Stage& S = rt->stages[dr.stage];
+    cudaStream_t ST = rt->serial ? rt->shared : S.stream;
+    PD_TRY(flag_wait(dr.flag, flag_val(rt->epoch, dr.mb), S.d.err_word, ST));
+    rt->launches += 1;
   }
   for (auto& kv : rt->stages) {
     Stage& S = kv.second;

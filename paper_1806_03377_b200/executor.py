@@ -77,7 +77,7 @@ class Executor:
     """Allocates one pipeline's device state and runs its compiled program repeatedly."""
 
     def __init__(self, cfg: SimConfig, ctx=None, schedule: Schedule | None = None, *, model: MLPSpec,
-                 device: int | None = None, init: str | None = None):
+                 device: int | None = None, init: str | None = None, group=None):
         torch = _torch()
         if not torch.cuda.is_available():
             raise nat.NativeError("no CUDA device: the B200 executor has no CPU fallback")
@@ -85,18 +85,23 @@ class Executor:
         self.cfg, self.ctx, self.model = cfg, ctx, model
         self.schedule = schedule or build_schedule(cfg.plan, cfg.num_minibatches, cfg.max_inflight)
         dist = torch.distributed
-        self.world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
-        self.rank = dist.get_rank() if self.world > 1 else 0
-        if self.world > 1:
-            raise ValidationError("multi-process execution goes through paper_1806_03377_b200.distributed")
-        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        if device is None:
+            device = (int(os.environ.get("LOCAL_RANK", self.rank)) % torch.cuda.device_count()
+                      if self.world > 1 else torch.cuda.current_device())
+        self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
-        self.program: Program = compile_program(self.schedule, cfg.mode, n_blocks=model.n_blocks, world_size=1)
+        self.program: Program = compile_program(self.schedule, cfg.mode, n_blocks=model.n_blocks,
+                                                world_size=self.world)
+        self.hosted = [wp for wp in self.program.workers if self.program.device_of[wp.wid] == self.rank]
         self.dtype = torch.float32 if model.dtype == "fp32" else torch.bfloat16
         self.pd_dtype = nat.PD_F32 if model.dtype == "fp32" else nat.PD_BF16
         n_params = sum(a * b for a, b in zip(model.widths[:-1], model.widths[1:]))
         self.init = init or ("host" if n_params <= HOST_INIT_LIMIT else "device")
         self._alloc()
+        self._exchange()
         self._build_runtime()
         self.runs = 0
 
@@ -112,7 +117,8 @@ class Executor:
             params = None
             g = torch.Generator(device=dev).manual_seed(m.seed)
         self.bufs: dict[int, _StageBuf] = {}
-        for wp in self.program.workers:
+        workers = self.program.workers
+        for wp in self.hosted:
             st = plan.stages[wp.stage]
             dims = list(m.widths[st.first_layer - 1: st.last_layer + 1])
             b = _StageBuf(wid=wp.wid, stage=wp.stage, dims=dims, ring_depth=wp.ring_depth,
@@ -153,7 +159,58 @@ class Executor:
                 t["loss"] = torch.zeros(self.cfg.num_minibatches + 1, device=dev, dtype=torch.float32)
             t["tmp"] = [torch.empty(m.batch, max(dims), device=dev, dtype=dt) for _ in range(2)]
             t["err"] = torch.zeros(1, device=dev, dtype=torch.int32)
+            # cross-GPU flags (zero = nothing delivered yet); used only when a neighbour is remote
+            i32 = dict(device=dev, dtype=torch.int32)
+            n = plan.num_stages
+            if wp.stage > 0:
+                t["act_ready"] = torch.zeros(b.in_depth, **i32)
+                t["prev_grad_ack"] = torch.zeros(workers[self._neighbour(wp.wid, -1)].grad_depth, **i32)
+            if wp.stage < n - 1:
+                t["grad_ready"] = torch.zeros(b.grad_depth, **i32)
+                t["next_act_ack"] = torch.zeros(workers[self._neighbour(wp.wid, +1)].in_depth, **i32)
             self.bufs[wp.wid] = b
+
+    def _neighbour(self, wid: int, step: int) -> int:
+        """Worker id of the (unique, straight-pipeline) neighbour stage."""
+        s, _ = self.schedule.workers[wid]
+        return self.schedule.worker_id(s + step, 0)
+
+    EXPORTS = ("act_in", "act_ready", "grad_in", "grad_ready", "next_act_ack", "prev_grad_ack")
+
+    def _exchange(self) -> None:
+        """Publish CUDA IPC handles of this rank's inboxes and flags; map the neighbours' ones."""
+        self._remote: dict[int, dict] = {}
+        if self.world == 1:
+            return
+        torch = _torch()
+        mine = {}
+        for b in self.bufs.values():
+            ent = {}
+            for name in self.EXPORTS:
+                if name == "act_in" and b.stage == 0:
+                    continue
+                t = b.tensors.get(name)
+                if t is None:
+                    continue
+                h, off = nat.ipc_export(t)
+                slot = t[0].numel() * t.element_size() if t.dim() > 1 else t.element_size()
+                ent[name] = (h, off, slot, t.shape[0])
+            mine[b.wid] = ent
+        gathered = [None] * self.world
+        torch.distributed.all_gather_object(gathered, mine, group=self.group)
+        for part in gathered:
+            for wid, ent in part.items():
+                if self.program.device_of[wid] != self.rank:
+                    self._remote[wid] = ent
+
+    def _view(self, wid: int, name: str) -> list[int]:
+        """Per-slot device addresses of worker wid's buffer `name` (local or peer-mapped)."""
+        if self.program.device_of[wid] == self.rank:
+            t = self.bufs[wid].tensors[name]
+            return [x.data_ptr() for x in t] if t.dim() > 1 else [t.data_ptr() + 4 * k for k in range(t.shape[0])]
+        h, off, slot, count = self._remote[wid][name]
+        base = nat.ipc_import(h, off)
+        return [base + k * slot for k in range(count)]
 
     @staticmethod
     def _parr(ptrs) -> ctypes.Array:
@@ -166,7 +223,6 @@ class Executor:
         rt = ctypes.c_void_p()
         nat.check(L.pd_rt_create(self.device.index, ctypes.byref(rt)), "pd_rt_create")
         self._rt = rt
-        by_stage = {b.stage: b for b in self.bufs.values()}
         for b in self.bufs.values():
             t = b.tensors
             nl = len(b.dims) - 1
@@ -194,22 +250,32 @@ class Executor:
             d.n_data_blocks = self.model.n_blocks
             if not is_last:
                 d.grad_in = arr([x.data_ptr() for x in t["grad_in"]])
-                nxt = by_stage[b.stage + 1]
-                d.next_act_in = arr([x.data_ptr() for x in nxt.tensors["act_in"]])
-                d.next_in_depth = nxt.in_depth
+                nw = self._neighbour(b.wid, +1)
+                d.next_act_in = arr(self._view(nw, "act_in"))
+                d.next_in_depth = self.program.workers[nw].in_depth
+                if self.program.device_of[nw] != self.rank:  # peer GPU: flag-ordered hand-off
+                    d.next_act_ready = self._view(nw, "act_ready")[0]
+                    d.next_act_ack = t["next_act_ack"].data_ptr()
+                    d.grad_ready = t["grad_ready"].data_ptr()
+                    d.grad_ack_remote = self._view(nw, "prev_grad_ack")[0]
             else:
                 d.dz_last = arr([x.data_ptr() for x in t["dz_last"]])
                 d.target = arr([x.data_ptr() for x in t["target"]])
                 d.loss = t["loss"].data_ptr()
             if not is_first:
-                prv = by_stage[b.stage - 1]
-                d.prev_grad_in = arr([x.data_ptr() for x in prv.tensors["grad_in"]])
-                d.prev_grad_depth = prv.grad_depth
+                pw = self._neighbour(b.wid, -1)
+                d.prev_grad_in = arr(self._view(pw, "grad_in"))
+                d.prev_grad_depth = self.program.workers[pw].grad_depth
+                if self.program.device_of[pw] != self.rank:
+                    d.prev_grad_ready = self._view(pw, "grad_ready")[0]
+                    d.prev_grad_ack = t["prev_grad_ack"].data_ptr()
+                    d.act_ready = t["act_ready"].data_ptr()
+                    d.act_ack_remote = self._view(pw, "next_act_ack")[0]
             d.tmp[0], d.tmp[1] = t["tmp"][0].data_ptr(), t["tmp"][1].data_ptr()
             d.err_word = t["err"].data_ptr()
             b.desc, b.keep = d, keep
             nat.check(L.pd_rt_add_stage(rt, ctypes.byref(d)), "pd_rt_add_stage")
-        prog = np.ascontiguousarray(self.program.items_for_rank(0))
+        prog = np.ascontiguousarray(self.program.items_for_rank(self.rank))
         self._prog = prog
         nat.check(L.pd_rt_load_program(rt, prog.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), prog.shape[0]),
                   "pd_rt_load_program")
@@ -229,18 +295,21 @@ class Executor:
         s = stream or torch.cuda.current_stream(self.device)
         with torch.cuda.stream(s):
             for b in self.bufs.values():
-                if b.stage == 0:
+                if b.stage == 0 and X_host is not None:
                     b.tensors["act_in"].copy_(X_host, non_blocking=True)
-                if b.stage == self.cfg.plan.num_stages - 1:
+                if b.stage == self.cfg.plan.num_stages - 1 and T_host is not None:
                     b.tensors["target"].copy_(T_host, non_blocking=True)
 
-    def losses(self) -> list[float]:
-        last = [b for b in self.bufs.values() if b.stage == self.cfg.plan.num_stages - 1][0]
-        return last.tensors["loss"][1:].float().cpu().tolist()
+    def hosts_stage(self, s: int) -> bool:
+        return any(b.stage == s for b in self.bufs.values())
+
+    def losses(self) -> list[float] | None:
+        last = [b for b in self.bufs.values() if b.stage == self.cfg.plan.num_stages - 1]
+        return last[0].tensors["loss"][1:].float().cpu().tolist() if last else None
 
     def loss_tensor(self):
-        last = [b for b in self.bufs.values() if b.stage == self.cfg.plan.num_stages - 1][0]
-        return last.tensors["loss"]
+        last = [b for b in self.bufs.values() if b.stage == self.cfg.plan.num_stages - 1]
+        return last[0].tensors["loss"] if last else None
 
     def weights(self) -> dict[int, tuple[np.ndarray, np.ndarray]]:
         """Final fp32 (W, b) per global 1-based layer id."""
@@ -312,18 +381,20 @@ class Executor:
                 total += m.batch * m.widths[plan.stages[s].first_layer - 1] * m.bytes_per_elem
         return total
 
-    def gpu_utilization(self, trace) -> float:
-        """Fraction of the steady window during which this GPU runs at least one pass.
+    def gpu_utilization(self, trace, rank: int | None = None) -> float:
+        """Fraction of the steady window during which GPU `rank` runs at least one pass.
 
         The reference's per-worker utilisation (simulator.py:379-385) is kept in the report;
         with several stages per GPU the device-level bubble is 1 - (union of their busy time).
         """
         from .ledger import steady_window
 
+        rank = self.rank if rank is None else rank
         k1, k2 = steady_window(self.cfg, self.cfg.plan.num_stages, self.cfg.plan.stages[0].replication)
         done = {ev.minibatch: ev.time_end for ev in trace if ev.stage == 0 and ev.direction is Direction.BACKWARD}
         t1, t2 = done[k1], done[k2]
-        iv = sorted((max(ev.time_start, t1), min(ev.time_end, t2)) for ev in trace if ev.time_end > t1 and ev.time_start < t2)
+        iv = sorted((max(ev.time_start, t1), min(ev.time_end, t2)) for ev in trace
+                    if self.program.device_of[ev.worker] == rank and ev.time_end > t1 and ev.time_start < t2)
         busy, cur_lo, cur_hi = 0.0, None, None
         for lo, hi in iv:
             if cur_hi is None or lo > cur_hi:
@@ -337,18 +408,28 @@ class Executor:
         return busy / (t2 - t1)
 
     def result(self) -> SimResult:
+        """SimResult of the last run; with several ranks every rank returns the merged result."""
         torch = _torch()
         torch.cuda.synchronize(self.device)
-        trace = self.trace() if getattr(self, "_traced", False) else []
-        report = build_report(self.cfg, trace, len(self.schedule.workers), self.comm_bytes()) if trace else None
-        losses = self.losses()
+        traced = getattr(self, "_traced", False)
+        trace = self.trace() if traced else []
+        losses, weights, comm = self.losses(), self.weights(), self.comm_bytes()
+        if self.world > 1:
+            parts = [None] * self.world
+            torch.distributed.all_gather_object(parts, (trace, losses, weights, comm), group=self.group)
+            trace = sorted((ev for p in parts for ev in p[0]), key=lambda e: (e.time_start, e.worker))
+            losses = next((p[1] for p in parts if p[1] is not None), None)
+            weights = {k: v for p in parts for k, v in p[2].items()}
+            comm = sum(p[3] for p in parts)
+        report = build_report(self.cfg, trace, len(self.schedule.workers), comm) if trace else None
         bubble, gpu_util = None, None
         if report is not None:
-            gpu_util = self.gpu_utilization(trace)
+            gpu_util = sum(self.gpu_utilization(trace, r) for r in range(self.world)) / self.world
             bubble = 1.0 - gpu_util
-        return SimResult(report=report, ledger=self.program.ledger, trace=trace, losses=losses,
-                         weights=self.weights(),
-                         extras={"bubble_fraction": bubble, "gpu_utilization": gpu_util, "ring_depths": {b.stage: b.ring_depth for b in self.bufs.values()},
+        return SimResult(report=report, ledger=self.program.ledger, trace=trace, losses=losses, weights=weights,
+                         extras={"bubble_fraction": bubble, "gpu_utilization": gpu_util,
+                                 "ring_depths": {b.stage: b.ring_depth for b in self.bufs.values()},
+                                 "device_of_worker": list(self.program.device_of),
                                  "device": str(self.device), "runs": self.runs})
 
     def close(self) -> None:
