@@ -1,0 +1,194 @@
+"""N>1 hand-off protocol, checked on CPU.
+
+A discrete model of what runtime.cu enqueues for each rank (per-stage streams, event waits for
+in-process producers, acquire-polls on inbox/ack flags for peer GPUs, release-signals after each
+pass, the end-of-run ack drain) executes the per-rank programs that program.py emits.  It asserts
+that no inbox slot is overwritten before its consumer's backward finished, that every read sees
+the minibatch it expects, that nothing deadlocks, and that back-to-back runs (epoch-tagged flag
+values) stay correct.  The world_size-2 variant exchanges the per-rank programs over a gloo
+process group, the same host path the GPU executor uses.
+"""
+import os
+
+import pytest
+
+import paper_1806_03377_b200 as pd
+from helpers_golden import plan_from_stages
+
+FIELDS = dict(op=0, stage=1, mb=2, worker=3, wslot=5, wnew=6, act=7, x=8, g=9, out=10, dep=12, war=13, rwait=14,
+              await_=15)
+
+
+def f(row, name):
+    return int(row[FIELDS[name]])
+
+
+def enqueue(rank, prog, n_stages, epoch):
+    """Per-stage op queues for one rank, mirroring pd_rt_run."""
+    queues = {}
+    val = lambda mb: epoch * 65536 + mb  # noqa: E731
+    last_ack = {}
+    for i, row in enumerate(prog):
+        s, mb, fwd = f(row, "stage"), f(row, "mb"), f(row, "op") == 0
+        q = queues.setdefault(s, [])
+        if f(row, "dep") >= 0:
+            q.append(("event", (rank, f(row, "dep"))))
+        if f(row, "war") >= 0:
+            q.append(("event", (rank, f(row, "war"))))
+        if f(row, "rwait") > 0:
+            key = ("act_ready", s, f(row, "x")) if fwd else ("grad_ready", s, f(row, "g"))
+            q.append(("wait", key, val(f(row, "rwait"))))
+        if f(row, "await_") > 0:
+            key = ("act_ack", s + 1, f(row, "out")) if fwd else ("grad_ack", s - 1, f(row, "out"))
+            q.append(("wait", key, val(f(row, "await_"))))
+        q.append(("exec", row))
+        q.append(("record", (rank, i)))
+        q.append(("signals", row, epoch))
+        if f(row, "out") >= 0:
+            k = ("act" if fwd else "grad", s, f(row, "out"))
+            last_ack[k] = max(last_ack.get(k, 0), mb)
+    return queues, last_ack
+
+
+class World:
+    def __init__(self, plan, K, world, mode="weight_stashing"):
+        self.plan = plan
+        self.n = plan.num_stages
+        self.prog = pd.compile_program(pd.build_schedule(plan, K), mode, world_size=world)
+        self.world = world
+        self.rank_of_stage = {wp.stage: self.prog.device_of[wp.wid] for wp in self.prog.workers}
+        self.flags = {}
+        self.slots = {}  # (kind, receiver stage, slot) -> [occupant mb, consumed?]
+        self.events = set()
+
+    def remote(self, a, b):
+        return self.rank_of_stage[a] != self.rank_of_stage[b]
+
+    def run_epoch(self, epoch):
+        queues = {}
+        drains = {}
+        for r in range(self.world):
+            q, last = enqueue(r, self.prog.items_for_rank(r), self.n, epoch)
+            for s, ops in q.items():
+                # end-of-run drain for peer-GPU outboxes (runtime.cu pd_rt_run)
+                for (kind, st, slot), mb in last.items():
+                    if st != s:
+                        continue
+                    if kind == "act" and s < self.n - 1 and self.remote(s, s + 1):
+                        ops.append(("wait", ("act_ack", s + 1, slot), epoch * 65536 + mb))
+                    if kind == "grad" and s > 0 and self.remote(s, s - 1):
+                        ops.append(("wait", ("grad_ack", s - 1, slot), epoch * 65536 + mb))
+                queues[(r, s)] = ops
+        self.events = set()
+        while any(queues.values()):
+            progressed = False
+            for key, ops in queues.items():
+                while ops and self.ready(ops[0]):
+                    self.apply(ops.pop(0))
+                    progressed = True
+            assert progressed, {k: v[0] for k, v in queues.items() if v}
+
+    def ready(self, op):
+        if op[0] == "event":
+            return op[1] in self.events
+        if op[0] == "wait":
+            return self.flags.get(op[1], 0) >= op[2]
+        return True
+
+    def apply(self, op):
+        kind = op[0]
+        if kind == "record":
+            self.events.add(op[1])
+        elif kind == "exec":
+            row = op[1]
+            s, mb, fwd = f(row, "stage"), f(row, "mb"), f(row, "op") == 0
+            if fwd:
+                if s > 0:
+                    occ = self.slots[("act", s, f(row, "x"))]
+                    assert occ[0] == mb, ("forward read wrong activation", s, mb, occ)
+                if s < self.n - 1:
+                    k = ("act", s + 1, f(row, "out"))
+                    assert k not in self.slots or self.slots[k][1], ("activation inbox overwritten", k, mb)
+                    self.slots[k] = [mb, False]
+            else:
+                if s > 0:
+                    occ = self.slots[("act", s, f(row, "x"))]
+                    assert occ[0] == mb
+                    occ[1] = True  # stage input no longer needed after the backward (wgrad consumed it)
+                if s < self.n - 1:
+                    occ = self.slots[("grad", s, f(row, "g"))]
+                    assert occ[0] == mb, ("backward read wrong gradient", s, mb, occ)
+                    occ[1] = True
+                if s > 0:
+                    k = ("grad", s - 1, f(row, "out"))
+                    assert k not in self.slots or self.slots[k][1], ("gradient inbox overwritten", k, mb)
+                    self.slots[k] = [mb, False]
+        elif kind == "signals":
+            row, epoch = op[1], op[2]
+            s, mb, fwd = f(row, "stage"), f(row, "mb"), f(row, "op") == 0
+            v = epoch * 65536 + mb
+            if fwd and s < self.n - 1 and self.remote(s, s + 1):
+                self.flags[("act_ready", s + 1, f(row, "out"))] = v
+            if not fwd and s > 0 and self.remote(s, s - 1):
+                self.flags[("grad_ready", s - 1, f(row, "out"))] = v
+            if not fwd and s > 0 and self.remote(s, s - 1):
+                self.flags[("act_ack", s, f(row, "x"))] = v
+            if not fwd and s < self.n - 1 and self.remote(s, s + 1):
+                self.flags[("grad_ack", s, f(row, "g"))] = v
+
+
+@pytest.mark.parametrize("n,world,K", [(4, 2, 20), (8, 2, 25), (8, 4, 25), (8, 8, 25), (3, 2, 16), (4, 4, 14)])
+@pytest.mark.parametrize("mode", ["weight_stashing", "vertical_sync", "naive_pipeline"])
+def test_protocol_runs_clean_for_three_epochs(n, world, K, mode):
+    plan = plan_from_stages([[i, i, 1] for i in range(1, n + 1)])
+    w = World(plan, K, world, mode)
+    for epoch in (1, 2, 3):
+        w.run_epoch(epoch)
+
+
+def test_protocol_with_max_inflight():
+    plan = plan_from_stages([[i, i, 1] for i in range(1, 9)])
+    sched = pd.build_schedule(plan, 25, max_inflight=3)
+    w = World(plan, 25, 4)
+    w.prog = pd.compile_program(sched, "weight_stashing", world_size=4)
+    for epoch in (1, 2):
+        w.run_epoch(epoch)
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    plan = plan_from_stages([[i, i, 1] for i in range(1, 5)])
+    prog = pd.compile_program(pd.build_schedule(plan, 20), "weight_stashing", world_size=world)
+    mine = prog.items_for_rank(rank).tolist()
+    parts = [None] * world
+    dist.all_gather_object(parts, mine)
+    dist.destroy_process_group()
+    q.put((rank, parts))
+
+
+def test_world2_gloo_exchange_of_programs():
+    """Two gloo ranks exchange their compiled programs; every cross-rank flag wait has a producer."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29400 + os.getpid() % 500
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    parts = got[0]
+    assert parts == got[1]
+    produced = {(r[1], r[2], r[0]) for part in parts for r in part}
+    for rank, part in enumerate(parts):
+        for r in part:
+            if r[14] > 0:  # waits on a remote producer: forward of stage-1 or backward of stage+1
+                src = (r[1] - 1, r[2], 0) if r[0] == 0 else (r[1] + 1, r[2], 1)
+                assert src in produced
+    assert sum(len(p) for p in parts) == 2 * 4 * 20
