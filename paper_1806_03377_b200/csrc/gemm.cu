@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "epilogue.cuh"
@@ -37,24 +38,38 @@ constexpr int TC_EPI_WARPS = 8;     // two warps per TMEM lane quadrant, each ow
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;  // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2.. epilogue
 constexpr int TC_ACC_STRIDE = 256;  // TMEM columns between the two accumulator buffers
 
-template <int BN, bool B_MN>
+// fp32-output epilogues (SGD update of the fp32 master, raw fp32 gradient) stage each warp's
+// 32x32 accumulator block through shared memory so global traffic is row-contiguous per warp.
+__host__ __device__ constexpr bool transposed_epilogue(int kind) { return kind == EPI_SGD || kind == EPI_GRADF32; }
+constexpr int TC_STG_FLOATS = 32 * 33;  // per epilogue warp, padded against bank conflicts
+
+// CG = CTA group: 1 -> one SM computes a 128 x BN tile; 2 -> a CTA pair (cluster of 2) computes
+// 256 x BN with tcgen05 cta_group::2: each CTA stages its 128 rows of A and BN/2 rows of B, the
+// leader issues the M=256 MMA, and each CTA's TMEM receives its own 128 accumulator rows.  The
+// pair halves the per-SM operand traffic from L2 and lets each CTA keep more pipeline stages.
+template <int CG, int BN, bool B_MN, int KIND = EPI_STORE>
 struct TcCfg {
-  // MN-major B tiles are loaded as whole 64-wide swizzle atoms; the MMA uses the first BN columns
-  static constexpr int BNL = B_MN ? ((BN + 63) / 64) * 64 : BN;
+  static constexpr int B_ROWS = BN / CG;  // B rows (N extent) staged by each CTA
+  // MN-major B tiles are loaded as whole 64-wide swizzle atoms
+  static constexpr int BNL = B_MN ? ((B_ROWS + 63) / 64) * 64 : B_ROWS;
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
   static constexpr int B_BYTES = BNL * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int STG_BYTES = transposed_epilogue(KIND) ? TC_EPI_WARPS * TC_STG_FLOATS * 4 : 0;
+  static constexpr int PIPE_BUDGET = 200 * 1024 - STG_BYTES;
+  static constexpr int STAGES = PIPE_BUDGET / STAGE_BYTES > 8 ? 8 : PIPE_BUDGET / STAGE_BYTES;
   static constexpr int TMEM_COLS = 512;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static_assert(BN % 32 == 0 && BN % 16 == 0 && BN <= 256, "BN");
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + STG_BYTES;
+  static_assert(BN % 32 == 0 && BN % (16 * CG) == 0 && BN <= 256, "BN");
+  static_assert(!B_MN || B_ROWS % 64 == 0, "MN-major B needs whole 64-wide atoms per CTA");
 };
 
-template <int BN, bool A_MN, bool B_MN, int KIND>
+template <int CG, int BN, bool A_MN, bool B_MN, int KIND>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               int M, int N, int K, EpiArgs ep) {
-  using C = TcCfg<BN, B_MN>;
+  using C = TcCfg<CG, BN, B_MN, KIND>;
+  constexpr int UM = TC_BM * CG;  // tile rows per unit (CTA or CTA pair)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -66,7 +81,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = warp_id();
-  const int num_m = (M + TC_BM - 1) / TC_BM;
+  const uint32_t cta = CG == 2 ? cluster_ctarank() : 0;  // rank inside the pair
+  const bool leader = cta == 0;
+  const int unit = blockIdx.x / CG, units = gridDim.x / CG;
+  const int num_m = (M + UM - 1) / UM;
   const int num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int num_kb = (K + TC_BK - 1) / TC_BK;
@@ -74,51 +92,58 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tmem_full[a], 1); mbar_init(&tmem_empty[a], 32 * TC_EPI_WARPS); }
+    // full: leader's arrive.expect_tx (+ the peer's remote arrive for a pair); empty: one MMA commit;
+    // tmem_empty: one arrival per epilogue warp of every CTA of the unit
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], CG); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tmem_full[a], 1); mbar_init(&tmem_empty[a], CG * TC_EPI_WARPS); }
     fence_barrier_init();
     fence_proxy_async_smem();
   }
-  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp == 1) tmem_alloc<C::TMEM_COLS, CG>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- TMA producer
+    // ---------------- TMA producer (every CTA loads its own halves)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m0 = (t % num_m) * TC_BM;
-        const int n0 = (t / num_m) * BN;
+      for (int t = unit; t < tiles; t += units) {
+        const int m0 = (t % num_m) * UM + TC_BM * cta;
+        const int n0 = (t / num_m) * BN + C::B_ROWS * cta;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
+          else mbar_arrive_cluster(&full[stage], 0);
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
           const int k0 = kb * TC_BK;
+          auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
+            if constexpr (CG == 2) tma_load_2d_2sm(dst, map, &full[stage], c0, c1);
+            else tma_load_2d(dst, map, &full[stage], c0, c1);
+          };
           if constexpr (A_MN) {
 #pragma unroll
-            for (int i = 0; i < TC_BM / 64; ++i) tma_load_2d(a_dst + i * 8192, &tmA, &full[stage], m0 + 64 * i, k0);
+            for (int i = 0; i < TC_BM / 64; ++i) load(a_dst + i * 8192, &tmA, m0 + 64 * i, k0);
           } else {
-            tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
+            load(a_dst, &tmA, k0, m0);
           }
           if constexpr (B_MN) {
 #pragma unroll
-            for (int i = 0; i < C::BNL / 64; ++i) tma_load_2d(b_dst + i * 8192, &tmB, &full[stage], n0 + 64 * i, k0);
+            for (int i = 0; i < C::BNL / 64; ++i) load(b_dst + i * 8192, &tmB, n0 + 64 * i, k0);
           } else {
-            tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
+            load(b_dst, &tmB, k0, n0);
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (single thread)
-    if (elect_one()) {
-      constexpr uint32_t idesc = make_idesc_bf16(TC_BM, BN, A_MN, B_MN);
+    // ---------------- MMA issuer (single thread of the leader CTA)
+    if (leader && elect_one()) {
+      constexpr uint32_t idesc = make_idesc_bf16(UM, BN, A_MN, B_MN);
       // K-major SW128: 8-row core groups 1024 B apart (SBO); +32 B per K=16 step.
       // MN-major SW128: 64-element MN atoms of 64 K-rows are 8 KB apart (LBO), 8-K-row
       // groups 1024 B apart (SBO); +2048 B per K=16 step.
@@ -128,7 +153,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = unit; t < tiles; t += units) {
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * TC_ACC_STRIDE;
@@ -141,15 +166,69 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int k = 0; k < TC_BK / 16; ++k) {
             uint64_t ad = make_sw128_desc(a_addr + k * A_KSTEP, A_LBO, A_SBO);
             uint64_t bd = make_sw128_desc(b_addr + k * B_KSTEP, B_LBO, B_SBO);
-            umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+            if constexpr (CG == 2) umma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0);
+            else umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
           }
-          umma_commit(&empty[stage]);
+          if constexpr (CG == 2) umma_commit_2sm_mc(&empty[stage]); else umma_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tmem_full[acc]);
+        if constexpr (CG == 2) umma_commit_2sm_mc(&tmem_full[acc]); else umma_commit(&tmem_full[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
+    }
+  } else if constexpr (transposed_epilogue(KIND)) {
+    // ---------------- fp32 epilogue: TMEM -> regs -> smem (transpose within the warp) -> lanes
+    // along columns, so each warp reads/writes whole 128-byte rows of the fp32 master.
+    const int q = warp & 3;
+    const int half = (warp - 2) / 4;
+    constexpr int NC = BN / 32;
+    const int c_begin = half ? (NC + 1) / 2 : 0;
+    const int c_end = half ? NC : (NC + 1) / 2;
+    float* stg = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 256) + (warp - 2) * TC_STG_FLOATS;
+    const int lane = lane_id();
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = unit; t < tiles; t += units) {
+      const int m0 = (t % num_m) * UM + TC_BM * cta;
+      const int n0 = (t / num_m) * BN;
+      const int64_t row0 = m0 + 32 * q;
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = c_begin; c < c_end; ++c) {
+        float v[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * TC_ACC_STRIDE + c * 32, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = v[j];
+        __syncwarp();
+        const int64_t col = n0 + c * 32 + lane;
+        const bool col_ok = col < N;
+        if constexpr (KIND == EPI_SGD) {
+          float m[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            m[i] = (col_ok && row0 + i < M) ? ep.master[(row0 + i) * ep.ldw + col] : 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (col_ok && row0 + i < M) {
+              const float w = m[i] - ep.lr * stg[i * 33 + lane];
+              ep.master[(row0 + i) * ep.ldw + col] = w;
+              static_cast<__nv_bfloat16*>(ep.out)[(row0 + i) * ep.ldo + col] = __float2bfloat16_rn(w);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (col_ok && row0 + i < M) static_cast<float*>(ep.out)[(row0 + i) * ep.ldo + col] = stg[i * 33 + lane];
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tmem_empty[acc], 0);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
     }
   } else {
     // ---------------- epilogue warps: TMEM -> registers -> fused epilogue -> HBM
@@ -161,8 +240,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     float lsum = 0.f;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int m0 = (t % num_m) * TC_BM;
+    for (int t = unit; t < tiles; t += units) {
+      const int m0 = (t % num_m) * UM + TC_BM * cta;
       const int n0 = (t / num_m) * BN;
       const int64_t r = m0 + 32 * q + lane_id();
       const bool row_ok = r < M;
@@ -187,7 +266,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         cur = nxt;
       }
       tc_fence_before();
-      mbar_arrive(&tmem_empty[acc]);
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive_cluster(&tmem_empty[acc], 0);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -197,10 +277,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    tmem_dealloc<C::TMEM_COLS, CG>(tmem_base);
   }
 }
 
@@ -300,55 +380,86 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, bool A_MN, bool B_MN, int KIND>
+template <int CG, int BN, bool A_MN, bool B_MN, int KIND>
 static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
                      cudaStream_t st) {
-  using C = TcCfg<BN, B_MN>;
+  using C = TcCfg<CG, BN, B_MN, KIND>;
   CUtensorMap ta, tb;
   int rc;
   if (A_MN) rc = make_map(&ta, A, (uint64_t)M, (uint64_t)K, lda, 64, 64);
   else rc = make_map(&ta, A, (uint64_t)K, (uint64_t)M, lda, 64, TC_BM);
   if (rc) return rc;
   if (B_MN) rc = make_map(&tb, B, (uint64_t)N, (uint64_t)K, ldb, 64, 64);
-  else rc = make_map(&tb, B, (uint64_t)K, (uint64_t)N, ldb, 64, BN);
+  else rc = make_map(&tb, B, (uint64_t)K, (uint64_t)N, ldb, 64, C::B_ROWS);
   if (rc) return rc;
-  auto kern = k_gemm_tc<BN, A_MN, B_MN, KIND>;
+  auto kern = k_gemm_tc<CG, BN, A_MN, B_MN, KIND>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
       return set_error(PD_ERR_CUDA, "cudaFuncSetAttribute(smem=%d) failed", C::SMEM_BYTES);
     attr_set = true;
   }
-  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, TC_THREADS, C::SMEM_BYTES, st>>>(ta, tb, M, N, K, ep);
-  cudaError_t e = cudaGetLastError();
+  const int units = ((M + TC_BM * CG - 1) / (TC_BM * CG)) * ((N + BN - 1) / BN);
+  const int max_units = num_sms() / CG;
+  const int grid = CG * (units < max_units ? units : max_units);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, ep);
   if (e != cudaSuccess) return set_error(PD_ERR_CUDA, "tcgen05 gemm launch: %s", cudaGetErrorString(e));
   return 0;
 }
 
-// Tile width minimising (waves x tile width): e.g. 2048x8192 -> BN=224 gives 592 tiles = 4.00
-// waves on 148 SMs instead of 512 tiles = 3.46 waves (a 46 %-full tail wave) at BN=256.
-static int pick_bn(int M, int N, bool b_mn) {
-  // an MN-major B tile is loaded in whole 64-wide atoms, so BN=224 would still move 256 columns
-  if (b_mn) return 256;
-  const int sms = num_sms();
-  const int cands[2] = {256, 224};
-  int best = 256;
-  long best_cost = -1;
-  for (int bn : cands) {
-    const long tiles = (long)((M + TC_BM - 1) / TC_BM) * ((N + bn - 1) / bn);
-    const long cost = ((tiles + sms - 1) / sms) * bn;
-    if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = bn; }
+// CTA group and tile width: minimise (waves x tile time).  E.g. 2048x8192 with a K-major B:
+// CTA pairs with BN=224 give 296 pair-tiles = 4.00 waves over 74 pairs, where BN=256 leaves a
+// 46 %-full last wave.  PD_GEMM_CG=1|2 forces the CTA group (benchmarks / A-B tests).
+static int g_force_cg = -1;
+static void pick_cfg(int M, int N, bool b_mn, int* cg, int* bn) {
+  if (g_force_cg < 0) {
+    const char* e = getenv("PD_GEMM_CG");
+    g_force_cg = e ? atoi(e) : 0;
   }
-  return best;
+  const int sms = num_sms();
+  long best = -1;
+  *cg = 1;
+  *bn = 256;
+  for (int c = 1; c <= 2; ++c) {
+    if (g_force_cg && c != g_force_cg) continue;
+    if (c == 2 && M <= TC_BM) continue;  // a single 128-row tile gains nothing from a pair
+    for (int b : {256, 224}) {
+      if (b_mn && b != 256) continue;  // MN-major B is staged in whole 64-wide atoms
+      const long units = (long)((M + TC_BM * c - 1) / (TC_BM * c)) * ((N + b - 1) / b);
+      const long slots = sms / c;
+      const long cost = ((units + slots - 1) / slots) * b * (c == 2 ? 2 : 1) * 100 / (c == 2 ? 205 : 100);
+      if (best < 0 || cost < best) { best = cost; *cg = c; *bn = b; }
+    }
+  }
 }
 
 template <bool A_MN, bool B_MN, int KIND>
 static int launch_bn(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
                      cudaStream_t st) {
-  if (pick_bn(M, N, B_MN) == 224) return launch_tc<224, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
-  return launch_tc<256, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
+  int cg, bn;
+  pick_cfg(M, N, B_MN, &cg, &bn);
+  if (cg == 2) {
+    if (bn == 224) {
+      if constexpr (!B_MN) return launch_tc<2, 224, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
+    }
+    return launch_tc<2, 256, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
+  }
+  if (bn == 224) {
+    if constexpr (!B_MN) return launch_tc<1, 224, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
+  }
+  return launch_tc<1, 256, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
 }
 
 template <bool A_MN, bool B_MN>
