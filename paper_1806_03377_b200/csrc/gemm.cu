@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
-          else mbar_arrive_cluster(&full[stage], 0);
+          else mbar_arrive_cluster_relaxed(&full[stage], 0);
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
           const int k0 = kb * TC_BK;
@@ -226,7 +226,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(&tmem_empty[acc], 0);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(&tmem_empty[acc], 0); else mbar_arrive(&tmem_empty[acc]);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -267,7 +269,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane_id() == 0) mbar_arrive_cluster(&tmem_empty[acc], 0);
+      if (lane_id() == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(&tmem_empty[acc], 0); else mbar_arrive(&tmem_empty[acc]);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }

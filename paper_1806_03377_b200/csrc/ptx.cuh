@@ -87,6 +87,16 @@ PD_DEVICE void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
       "r"(cta)
       : "memory");
 }
+// Relaxed variant for the producer's per-k-block handshake: no data of this thread is published
+// (the payload arrives through TMA complete_tx), so no release fence (MEMBAR) is needed.
+PD_DEVICE void mbar_arrive_cluster_relaxed(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
 // 2-CTA TMA load: data lands in this CTA's smem, the byte count goes to the leader CTA's barrier.
 PD_DEVICE void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
