@@ -88,6 +88,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int num_kb = (K + TC_BK - 1) / TC_BK;
+  // Rasterisation.  Forward/dgrad stream a large B (the weights) through L2, so co-resident
+  // tiles share B (m fastest).  The wgrad+SGD operands (dZ, X) are L2-resident and its cost is
+  // the fp32 master read-modify-write, so co-resident tiles walk along the rows (n fastest) and
+  // HBM sees long contiguous row runs instead of 1 KB pieces 32 KB apart.
+  constexpr bool kNFast = transposed_epilogue(KIND);
+  auto tile_m = [&](int t) { return kNFast ? t / num_n : t % num_m; };
+  auto tile_n = [&](int t) { return kNFast ? t % num_n : t / num_m; };
 
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch_desc(&tmA);
@@ -108,11 +115,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0) {
     // ---------------- TMA producer (every CTA loads its own halves)
     if (elect_one()) {
+      const uint64_t keep = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int t = unit; t < tiles; t += units) {
-        const int m0 = (t % num_m) * UM + TC_BM * cta;
-        const int n0 = (t / num_m) * BN + C::B_ROWS * cta;
+        const int m0 = tile_m(t) * UM + TC_BM * cta;
+        const int n0 = tile_n(t) * BN + C::B_ROWS * cta;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
@@ -121,8 +129,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           uint8_t* b_dst = sB + stage * C::B_BYTES;
           const int k0 = kb * TC_BK;
           auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
-            if constexpr (CG == 2) tma_load_2d_2sm(dst, map, &full[stage], c0, c1);
-            else tma_load_2d(dst, map, &full[stage], c0, c1);
+            // operands are re-read by many tiles: keep them in L2 ahead of streamed epilogue data
+            if constexpr (CG == 2) tma_load_2d_2sm(dst, map, &full[stage], c0, c1, keep);
+            else tma_load_2d_hint(dst, map, &full[stage], c0, c1, keep);
           };
           if constexpr (A_MN) {
 #pragma unroll
@@ -187,42 +196,66 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int c_end = half ? NC : (NC + 1) / 2;
     float* stg = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 256) + (warp - 2) * TC_STG_FLOATS;
     const int lane = lane_id();
+    const uint64_t stream = l2_policy_evict_first();  // master / ring are touched once per GEMM
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = unit; t < tiles; t += units) {
-      const int m0 = (t % num_m) * UM + TC_BM * cta;
-      const int n0 = (t / num_m) * BN;
+      const int m0 = tile_m(t) * UM + TC_BM * cta;
+      const int n0 = tile_n(t) * BN;
       const int64_t row0 = m0 + 32 * q;
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
+      // Two 32-column chunks per step: 64 independent 128-byte master loads in flight per warp
+      // (the epilogue is HBM-latency bound, it has to keep up with the next tile's MMAs).
 #pragma unroll 1
-      for (int c = c_begin; c < c_end; ++c) {
-        float v[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * TC_ACC_STRIDE + c * 32, v);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = v[j];
-        __syncwarp();
-        const int64_t col = n0 + c * 32 + lane;
-        const bool col_ok = col < N;
+      for (int c = c_begin; c < c_end; c += 2) {
+        const bool two = c + 1 < c_end;
+        const int64_t colA = n0 + c * 32 + lane, colB = colA + 32;
+        const bool okA = colA < N, okB = two && colB < N;
+        const int rows = M - row0 < 32 ? (int)(M - row0) : 32;
+        float mA[32], mB[32];
         if constexpr (KIND == EPI_SGD) {
-          float m[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            m[i] = (col_ok && row0 + i < M) ? ep.master[(row0 + i) * ep.ldw + col] : 0.f;
+          const float* pa = ep.master + row0 * ep.ldw + colA;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            if (col_ok && row0 + i < M) {
-              const float w = m[i] - ep.lr * stg[i * 33 + lane];
-              ep.master[(row0 + i) * ep.ldw + col] = w;
-              static_cast<__nv_bfloat16*>(ep.out)[(row0 + i) * ep.ldo + col] = __float2bfloat16_rn(w);
+            mA[i] = (okA && i < rows) ? ld_stream_f32(pa, stream) : 0.f;
+            mB[i] = (okB && i < rows) ? ld_stream_f32(pa + 32, stream) : 0.f;
+            pa += ep.ldw;
+          }
+        }
+        auto process = [&](int cc, int64_t col, bool col_ok, const float (&m)[32]) {
+          float v[32];
+          tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * TC_ACC_STRIDE + cc * 32, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = v[j];
+          __syncwarp();
+          if (col_ok) {
+            if constexpr (KIND == EPI_SGD) {
+              float* pm = ep.master + row0 * ep.ldw + col;
+              __nv_bfloat16* po = static_cast<__nv_bfloat16*>(ep.out) + row0 * ep.ldo + col;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                if (i < rows) {
+                  const float w = m[i] - ep.lr * stg[i * 33 + lane];
+                  st_stream_f32(pm, w, stream);
+                  st_stream_b16(po, __bfloat16_as_ushort(__float2bfloat16_rn(w)), stream);
+                }
+                pm += ep.ldw;
+                po += ep.ldo;
+              }
+            } else {
+              float* po = static_cast<float*>(ep.out) + row0 * ep.ldo + col;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                if (i < rows) *po = stg[i * 33 + lane];
+                po += ep.ldo;
+              }
             }
           }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (col_ok && row0 + i < M) static_cast<float*>(ep.out)[(row0 + i) * ep.ldo + col] = stg[i * 33 + lane];
-        }
-        __syncwarp();
+          __syncwarp();
+        };
+        process(c, colA, okA, mA);
+        if (two) process(c + 1, colB, okB, mB);
       }
       tc_fence_before();
       __syncwarp();
@@ -243,8 +276,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t acc_phase = 0;
     float lsum = 0.f;
     for (int t = unit; t < tiles; t += units) {
-      const int m0 = (t % num_m) * UM + TC_BM * cta;
-      const int n0 = (t / num_m) * BN;
+      const int m0 = tile_m(t) * UM + TC_BM * cta;
+      const int n0 = tile_n(t) * BN;
       const int64_t r = m0 + 32 * q + lane_id();
       const bool row_ok = r < M;
       Aux<KIND> cur, nxt;
