@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "epilogue.cuh"
@@ -55,11 +56,15 @@ struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
   static constexpr int B_BYTES = BNL * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STG_BYTES = transposed_epilogue(KIND) ? TC_EPI_WARPS * TC_STG_FLOATS * 4 : 0;
+  // SGD: per epilogue warp two TMA-fed 32x32 fp32 master blocks (4 KB each, 128B-swizzled);
+  // GRADF32: per warp a padded 32x33 transpose block.
+  static constexpr int STG_BYTES = KIND == EPI_SGD ? TC_EPI_WARPS * 2 * 4096
+                                 : (KIND == EPI_GRADF32 ? TC_EPI_WARPS * TC_STG_FLOATS * 4 : 0);
   static constexpr int PIPE_BUDGET = 200 * 1024 - STG_BYTES;
   static constexpr int STAGES = PIPE_BUDGET / STAGE_BYTES > 8 ? 8 : PIPE_BUDGET / STAGE_BYTES;
   static constexpr int TMEM_COLS = 512;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + STG_BYTES;
+  static constexpr int BAR_BYTES = 1024;  // mbarriers + TMEM slot, keeps the epilogue region 1 KB aligned
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + BAR_BYTES + STG_BYTES;
   static_assert(BN % 32 == 0 && BN % (16 * CG) == 0 && BN <= 256, "BN");
   static_assert(!B_MN || B_ROWS % 64 == 0, "MN-major B needs whole 64-wide atoms per CTA");
 };
@@ -67,7 +72,7 @@ struct TcCfg {
 template <int CG, int BN, bool A_MN, bool B_MN, int KIND>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              int M, int N, int K, EpiArgs ep) {
+              const __grid_constant__ CUtensorMap tmW, int M, int N, int K, EpiArgs ep) {
   using C = TcCfg<CG, BN, B_MN, KIND>;
   constexpr int UM = TC_BM * CG;  // tile rows per unit (CTA or CTA pair)
   extern __shared__ uint8_t smem_raw[];
@@ -79,6 +84,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tmem_full = empty + C::STAGES;
   uint64_t* tmem_empty = tmem_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* epi_bar = tmem_empty + 4;  // SGD: two per epilogue warp (master block loaded)
+  uint8_t* epi_smem = smem + C::STAGES * C::STAGE_BYTES + C::BAR_BYTES;
 
   const int warp = warp_id();
   const uint32_t cta = CG == 2 ? cluster_ctarank() : 0;  // rank inside the pair
@@ -99,10 +106,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if constexpr (KIND == EPI_SGD) tma_prefetch_desc(&tmW);
     // full: leader's arrive.expect_tx (+ the peer's remote arrive for a pair); empty: one MMA commit;
     // tmem_empty: one arrival per epilogue warp of every CTA of the unit
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], CG); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tmem_full[a], 1); mbar_init(&tmem_empty[a], CG * TC_EPI_WARPS); }
+    if constexpr (KIND == EPI_SGD)
+      for (int i = 0; i < 2 * TC_EPI_WARPS; ++i) mbar_init(&epi_bar[i], 1);
     fence_barrier_init();
     fence_proxy_async_smem();
   }
@@ -186,6 +196,98 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (acc == 0) acc_phase ^= 1;
       }
     }
+  } else if constexpr (KIND == EPI_SGD) {
+    // ---------------- wgrad + SGD epilogue.  Each warp owns 32 accumulator rows (its TMEM lane
+    // quadrant) and half of the tile's 32-column chunks.  The fp32 master block of a chunk
+    // (32x32, 4 KB) is TMA-loaded into a 128B-swizzled smem buffer ahead of use (double
+    // buffered, issued before the tile's accumulator is ready), updated in place
+    // (w = m - lr*acc), TMA-stored back, and the bf16 version copy is written from registers.
+    // HBM sees only bulk, fully coalesced master traffic.
+    const int q = warp & 3;
+    const int half = (warp - 2) / 4;
+    constexpr int NC = BN / 32;
+    const int c_begin = half ? (NC + 1) / 2 : 0;
+    const int c_end = half ? NC : (NC + 1) / 2;
+    const int e = warp - 2;
+    uint8_t* buf0 = epi_smem + e * 2 * 4096;
+    uint64_t* bars = epi_bar + 2 * e;
+    const int lane = lane_id();
+    uint32_t bar_phase[2] = {0, 0};
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = unit; t < tiles; t += units) {
+      const int m0 = tile_m(t) * UM + TC_BM * cta;
+      const int n0 = tile_n(t) * BN;
+      const int row0 = m0 + 32 * q;
+      const int nck = c_end - c_begin;
+      // prefetch the first two master blocks of this tile while its MMAs are still running
+      if (lane == 0) {
+        bulk_wait_read0();  // previous tile's stores have finished reading both buffers
+        for (int i = 0; i < 2 && i < nck; ++i) {
+          mbar_arrive_expect_tx(&bars[i], 4096);
+          tma_load_2d(buf0 + i * 4096, &tmW, &bars[i], n0 + (c_begin + i) * 32, row0);
+        }
+      }
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int i = 0; i < nck; ++i) {
+        const int c = c_begin + i, b = i & 1;
+        float v[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * TC_ACC_STRIDE + c * 32, v);
+        mbar_wait(&bars[b], bar_phase[b]);
+        bar_phase[b] ^= 1;
+        // row `lane` of the block: 16-byte chunk j sits at position j ^ (lane & 7) (SWIZZLE_128B)
+        float4* row = reinterpret_cast<float4*>(buf0 + b * 4096 + lane * 128);
+        uint32_t packed[16];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 m = row[j ^ (lane & 7)];
+          m.x -= ep.lr * v[4 * j];
+          m.y -= ep.lr * v[4 * j + 1];
+          m.z -= ep.lr * v[4 * j + 2];
+          m.w -= ep.lr * v[4 * j + 3];
+          row[j ^ (lane & 7)] = m;
+          packed[2 * j] = pack_bf16x2(m.x, m.y);
+          packed[2 * j + 1] = pack_bf16x2(m.z, m.w);
+        }
+        const int64_t r = row0 + lane, col0 = n0 + c * 32;
+        if (r < M) {
+          if (col0 + 32 <= N) {
+            uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + r * ep.ldo + col0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              o[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+          } else {
+            for (int j = 0; j < 32 && col0 + j < N; ++j) {
+              float a, bb;
+              unpack_bf16x2(packed[j / 2], a, bb);
+              static_cast<__nv_bfloat16*>(ep.out)[r * ep.ldo + col0 + j] = __float2bfloat16_rn(j & 1 ? bb : a);
+            }
+          }
+        }
+        fence_proxy_async_shared();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmW, buf0 + b * 4096, col0, row0);  // TMA clips rows/cols outside [M, N)
+          bulk_commit();
+          if (i + 2 < nck) {
+            bulk_wait_read0();  // this buffer's store has read the smem block
+            mbar_arrive_expect_tx(&bars[b], 4096);
+            tma_load_2d(buf0 + b * 4096, &tmW, &bars[b], n0 + (c + 2) * 32, row0);
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(&tmem_empty[acc], 0); else mbar_arrive(&tmem_empty[acc]);
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (lane == 0) bulk_wait_all0();
   } else if constexpr (transposed_epilogue(KIND)) {
     // ---------------- fp32 epilogue: TMEM -> regs -> smem (transpose within the warp) -> lanes
     // along columns, so each warp reads/writes whole 128-byte rows of the fp32 master.
@@ -194,7 +296,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr int NC = BN / 32;
     const int c_begin = half ? (NC + 1) / 2 : 0;
     const int c_end = half ? NC : (NC + 1) / 2;
-    float* stg = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 256) + (warp - 2) * TC_STG_FLOATS;
+    float* stg = reinterpret_cast<float*>(epi_smem) + (warp - 2) * TC_STG_FLOATS;
     const int lane = lane_id();
     const uint64_t stream = l2_policy_evict_first();  // master / ring are touched once per GEMM
     int acc = 0;
@@ -393,14 +495,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D bf16 tensor map: `inner` contiguous elements per row, `outer` rows, row pitch ld elements.
 static int make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
-                    uint32_t box_inner, uint32_t box_outer) {
+                    uint32_t box_inner, uint32_t box_outer, bool fp32 = false) {
   auto fn = encode_fn();
   if (!fn) return set_error(PD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
+  cuuint64_t strides[1] = {ld * (fp32 ? 4 : 2)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+  CUresult r = fn(map, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(PD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -429,6 +531,14 @@ static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int
   if (B_MN) rc = make_map(&tb, B, (uint64_t)N, (uint64_t)K, ldb, 64, 64);
   else rc = make_map(&tb, B, (uint64_t)K, (uint64_t)N, ldb, 64, C::B_ROWS);
   if (rc) return rc;
+  CUtensorMap tw;
+  memset(&tw, 0, sizeof(tw));
+  if (KIND == EPI_SGD) {
+    if ((ep.ldw % 4) || (reinterpret_cast<uintptr_t>(ep.master) % 16))
+      return set_error(PD_ERR_INVALID, "gemm: SGD master must be 16-byte aligned with ld %% 4 == 0");
+    rc = make_map(&tw, ep.master, (uint64_t)N, (uint64_t)M, ep.ldw, 32, 32, true);
+    if (rc) return rc;
+  }
   auto kern = k_gemm_tc<CG, BN, A_MN, B_MN, KIND>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
@@ -451,7 +561,7 @@ static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, ep);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tw, M, N, K, ep);
   if (e != cudaSuccess) return set_error(PD_ERR_CUDA, "tcgen05 gemm launch: %s", cudaGetErrorString(e));
   return 0;
 }
