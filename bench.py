@@ -6,8 +6,9 @@ prints ONE JSON line on rank 0.
 Workload (BASELINE.json configs[1]): 8-stage, 16-layer MLP, width 8192, bf16 storage /
 fp32 accumulate, straight pipeline (one stage per GPU at N=8; 8/N stages per GPU below),
 1F1B with weight stashing, minibatch 2048, synthetic data.
-A bench "step" = one execution of the whole 1F1B schedule over K=32 minibatches
-(pipeline fill + steady state + drain), i.e. 32*2048 = 65,536 samples.
+A bench "step" = one execution of the whole 1F1B schedule over K=64 minibatches
+(pipeline fill + steady state + drain), i.e. 64*2048 = 131,072 samples; at 8 GPUs the
+fill/drain bubble of a 64-minibatch schedule is 7/71.
 The working set (~15 GB of weight versions + activations) is >100x the 126 MB L2, so no
 explicit L2 flush is needed between steps.
 """
@@ -36,7 +37,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--batch", type=int, default=2048)
-    p.add_argument("--minibatches", type=int, default=32)
+    p.add_argument("--minibatches", type=int, default=64)
     p.add_argument("--width", type=int, default=8192)
     p.add_argument("--layers", type=int, default=16)
     p.add_argument("--stages", type=int, default=8)
