@@ -67,8 +67,15 @@ int pd_gemm(int dtype, const void* A, int a_mn, int64_t lda, const void* B, int 
 /* Bias gradient + SGD: b_master[j] -= lr * sum_r dz[r*ld+j];  b_out[j] = b_master[j]. */
 int pd_bias_sgd(int dtype, const void* dz, int rows, int cols, int64_t ld, float* b_master, float* b_out, float lr,
                 void* stream);
-/* master[i] -= lr*grad[i]; out[i] = cast(master[i])  (replicated stages, after the allreduce). */
+/* master[i] -= lr*grad[i]; out[i] = cast(master[i]). */
 int pd_sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n, float lr, void* stream);
+/* Replicated-stage allreduce fused with SGD, over peer memory: every replica reads all n_rep
+ * gradient buffers (its own and the peers' mapped ones, summed in replica order so all
+ * replicas compute bit-identical weights), then master -= lr*sum; out = cast(master). */
+int pd_allreduce_sgd(int dtype, const float* const* grads, int n_rep, float* master, void* out, int64_t n, float lr,
+                     void* stream);
+/* out[j] = sum_r dz[r*ld+j] (bias gradient of a replicated stage). */
+int pd_bias_grad(int dtype, const void* dz, int rows, int cols, int64_t ld, float* out, void* stream);
 /* out[i] = cast(src[i]) (fp32 -> dtype). */
 int pd_cast(int dtype, const float* src, void* out, int64_t n, void* stream);
 
@@ -88,9 +95,19 @@ int pd_enable_peer_access(int peer_device);
 
 /* ------------------------------------------------------------------ executor
  * Replaces _Engine.__init__/run/_try_start/_on_done (simulator.py:150-357) for the
- * stages hosted by this process: executes a compiled 1F1B-RR program on device. */
+ * workers (stage replicas) hosted by this process: executes a compiled 1F1B-RR program.
+ *
+ * Every inbox is owned by its receiving worker, together with its flags:
+ *   ready[slot]  written by the producer after its epilogue stored the payload (peer store)
+ *   ack[slot]    written by the receiver once the slot's backward no longer needs it
+ * Producers in another process poll the receiver's ack before overwriting a slot, and
+ * release-signal its ready after writing; in-process neighbours use CUDA events instead. */
 typedef struct pd_stage_desc {
+  int worker;               /* Schedule.worker_id(stage, replica) */
   int stage;                /* global stage index (0-based, plan order) */
+  int replica;
+  int rep;                  /* replication of this stage */
+  int first_worker;         /* worker id of replica 0 of this stage */
   int n_layers;
   const int64_t* dims;      /* n_layers+1 widths: in of layer 0 .. out of layer n-1 */
   int batch;                /* minibatch size */
@@ -102,6 +119,9 @@ typedef struct pd_stage_desc {
   int act_depth;            /* activation-stash slots (in-flight minibatches) */
   int in_depth;             /* activation inbox slots (stage > 0) */
   int grad_depth;           /* gradient inbox slots (stage < n-1) */
+  int n_data_blocks;
+  int remote_prev;          /* some producer of my activation inbox lives in another process */
+  int remote_next;          /* some producer of my gradient inbox lives in another process */
   float lr;
   /* per layer l: */
   float* const* w_master;   /* [n_layers]            fp32 [out,in] latest weights */
@@ -110,48 +130,58 @@ typedef struct pd_stage_desc {
   float* const* b_ring;     /* [n_layers*ring_depth] fp32 [out] */
   void* const* act;         /* [(n_layers-1)*act_depth] dtype [batch, dims[l+1]], index l*act_depth+slot */
   void* const* act_in;      /* stage>0: [in_depth] dtype [batch, dims[0]]; stage 0: data blocks */
-  int n_data_blocks;
   void* const* grad_in;     /* stage<n-1: [grad_depth] dtype [batch, dims[n]] */
   void* const* dz_last;     /* last stage: [act_depth] dtype [batch, dims[n]] */
   const float* const* target; /* last stage: [n_data_blocks] fp32 [batch, dims[n]] */
   float* loss;              /* last stage: fp32 [num_minibatches+1] */
   void* tmp[2];             /* dtype [batch, max dim] gradient ping-pong */
-  /* neighbours' inboxes (local or peer-mapped) */
-  void* const* next_act_in; /* [next_in_depth] */
-  int next_in_depth;
-  void* const* prev_grad_in;/* [prev_grad_depth] */
-  int prev_grad_depth;
-  /* cross-GPU flags; NULL when the neighbour is in-process */
-  int* act_ready;           /* [in_depth]   local, written by previous stage's GPU */
-  int* act_ack_remote;      /* [in_depth]   on previous stage's GPU, written here when a slot frees */
-  int* next_act_ready;      /* [next in_depth] on next stage's GPU */
-  int* next_act_ack;        /* [next in_depth] local, written by next stage's GPU */
-  int* grad_ready;          /* [grad_depth] local */
-  int* grad_ack_remote;     /* [grad_depth] on next stage's GPU */
-  int* prev_grad_ready;     /* [prev grad_depth] on previous stage's GPU */
-  int* prev_grad_ack;       /* [prev grad_depth] local */
+  int* act_ready;           /* [in_depth]   my inbox flags */
+  int* act_ack;             /* [in_depth] */
+  int* grad_ready;          /* [grad_depth] */
+  int* grad_ack;            /* [grad_depth] */
+  /* replicated stages (rep > 1): this replica's round-parity gradient buffers and flags */
+  float* const* red_grad;   /* [n_layers*2] fp32 [out,in] */
+  float* const* red_bgrad;  /* [n_layers*2] fp32 [out] */
+  int* red_ready;           /* last round whose gradients are complete here */
+  int* red_done;            /* last round whose reduction has finished reading every replica */
   int* err_word;            /* device int, set non-zero by a timed-out flag wait */
 } pd_stage_desc;
 
-/* Program item: PD_ITEM_WIDTH int32 fields, see executor.py:compile_program. */
-#define PD_ITEM_WIDTH 16
+/* What any worker (in this process or a peer-mapped one in another) exposes to the others. */
+typedef struct pd_worker_view {
+  int worker;
+  int remote;               /* 1: pointers below are peer mappings of another process's memory */
+  int in_depth, grad_depth, n_layers;
+  void* const* act_in;      /* [in_depth] */
+  void* const* grad_in;     /* [grad_depth] */
+  int* act_ready; int* act_ack; int* grad_ready; int* grad_ack;
+  float* const* red_grad;   /* [n_layers*2] */
+  float* const* red_bgrad;  /* [n_layers*2] */
+  int* red_ready; int* red_done;
+} pd_worker_view;
+
+/* Program item: PD_ITEM_WIDTH int32 fields, see program.py:compile_program. */
+#define PD_ITEM_WIDTH 20
 enum pd_item_field {
-  PD_IT_OP = 0,        /* 0 forward, 1 backward */
+  PD_IT_OP = 0,        /* 0 forward, 1 backward, 2 reduce (replicated stage: sum replicas, SGD, commit) */
   PD_IT_STAGE = 1,
   PD_IT_MB = 2,        /* 1-based minibatch id */
   PD_IT_WORKER = 3,
   PD_IT_VERSION = 4,   /* weight version read (ledger value) */
   PD_IT_WSLOT = 5,     /* ring slot holding that version */
-  PD_IT_WNEW = 6,      /* backward: ring slot receiving version mb (commit) */
+  PD_IT_WNEW = 6,      /* ring slot receiving the committed version (-1: none) */
   PD_IT_ACT = 7,       /* activation-stash slot of this minibatch */
   PD_IT_XSLOT = 8,     /* inbox slot of the stage input (stage 0: data block) */
   PD_IT_GSLOT = 9,     /* backward: gradient inbox slot (-1 at the last stage) */
-  PD_IT_OUT = 10,      /* forward: next stage's inbox slot; backward: previous stage's grad slot */
+  PD_IT_OUT = 10,      /* forward: slot in dst's activation inbox; backward: slot in dst's gradient inbox */
   PD_IT_BLOCK = 11,    /* data / target block */
   PD_IT_DEP = 12,      /* in-process producer item (index), -1 */
   PD_IT_WAR = 13,      /* in-process item that must finish before PD_IT_OUT is overwritten, -1 */
-  PD_IT_RWAIT = 14,    /* cross-GPU: inbox flag value to wait for (0 = none) */
-  PD_IT_AWAIT = 15     /* cross-GPU: ack value to wait for before writing PD_IT_OUT (0 = none) */
+  PD_IT_RWAIT = 14,    /* cross-process: my inbox ready value to wait for (0 = none) */
+  PD_IT_AWAIT = 15,    /* cross-process: dst's ack value to wait for before writing PD_IT_OUT (0 = none) */
+  PD_IT_DST = 16,      /* worker receiving PD_IT_OUT (-1) */
+  PD_IT_SRC = 17,      /* worker that produced this item's input (-1) */
+  PD_IT_ROUND = 18     /* replicated stage: allreduce round of this backward / reduce (0 otherwise) */
 };
 
 typedef struct pd_runtime pd_runtime;
@@ -159,6 +189,8 @@ typedef struct pd_record { int32_t item; int32_t pad; double t_start_ms; double 
 
 int pd_rt_create(int device, pd_runtime** out);
 int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc);
+/* Register the view of every worker of the plan (hosted here or peer-mapped). */
+int pd_rt_add_view(pd_runtime* rt, const pd_worker_view* view);
 int pd_rt_load_program(pd_runtime* rt, const int32_t* items, int n_items);
 /* Enqueue the whole program behind `stream` (everything joins back onto it).
  * trace=1 records per-item device timestamps (pd_rt_records). */

@@ -103,15 +103,19 @@ def _fp32(x):
 
 
 def mlp_train(params, X, T, lr, stage_bounds, versions, K, emulate: str | None = None, dtype=np.float64,
-              prune: bool = False):
+              prune: bool = False, reps=None):
     """Delayed-SGD training of a ReLU MLP split into stages.
 
     params: list of (W [out,in], b [out]) per global layer; X: [n_blocks,B,d0]; T: [n_blocks,B,dL]
     stage_bounds: [(first, last)] 1-based layer ranges; versions(s, mb, dir) -> int.
     dtype: arithmetic type (float64 for parity, float32 for the timed CPU baseline).
     prune: drop weight versions no later minibatch reads (bounded memory for big models).
+    reps: per-stage replication.  A stage replicated R ways follows the round rule of DESIGN.md §5:
+      minibatches (k-1)R+1..kR form round k; their gradients (each at its own ledger versions) are
+      summed and applied once to the latest weights, committing version kR.
     Returns (losses[K], final params list).  Loss per minibatch = 1/(2B) sum (Z - T)^2.
     """
+    reps = list(reps) if reps is not None else [1] * len(stage_bounds)
     q = bf16_round if emulate == "bf16" else (lambda a: a)
     master = _fp32 if emulate == "bf16" else (lambda a: a)
     n = len(stage_bounds)
@@ -135,6 +139,7 @@ def mlp_train(params, X, T, lr, stage_bounds, versions, K, emulate: str | None =
     first = [a - 1 for a, _ in stage_bounds]
     n_blocks = X.shape[0]
     losses = []
+    round_acc: dict = {}
     for mb in range(1, K + 1):
         blk = (mb - 1) % n_blocks
         x, t = np.asarray(X[blk], dtype=dtype), np.asarray(T[blk], dtype=dtype)
@@ -163,11 +168,22 @@ def mlp_train(params, X, T, lr, stage_bounds, versions, K, emulate: str | None =
                 Wb, _ = archives[s][bv[s]][l - first[s]]
                 dz = q((dz @ q(Wb)) * (Xl > 0))
         for s, (a, b) in enumerate(stage_bounds):
+            R = reps[s]
+            if R > 1:  # accumulate this minibatch's gradient into its round
+                acc = round_acc.setdefault(s, [None] * (b - a + 1))
+                for i, l in enumerate(range(a - 1, b)):
+                    gW, gb = grads[l]
+                    acc[i] = (gW, gb) if acc[i] is None else (acc[i][0] + gW, acc[i][1] + gb)
+                if mb % R:
+                    continue
+                step = round_acc.pop(s)
+            else:
+                step = [grads[l] for l in range(a - 1, b)]
             latest = archives[s][latest_v[s]]
             new = []
-            for i, l in enumerate(range(a - 1, b)):
+            for i in range(b - a + 1):
                 W, bias = latest[i]
-                gW, gb = grads[l]
+                gW, gb = step[i]
                 new.append((master(W - lr * gW), master(bias - lr * gb)))
             archives[s][mb] = new
             latest_v[s] = mb

@@ -18,15 +18,15 @@ LIB_PATH = Path(__file__).resolve().parent / "libpd_b200.so"
 
 PD_F32, PD_BF16 = 0, 1
 EPI_STORE, EPI_LOSS, EPI_MASK, EPI_SGD, EPI_GRADF32 = range(5)
-ITEM_WIDTH = 16
+ITEM_WIDTH = 20
 (IT_OP, IT_STAGE, IT_MB, IT_WORKER, IT_VERSION, IT_WSLOT, IT_WNEW, IT_ACT, IT_XSLOT, IT_GSLOT, IT_OUT,
- IT_BLOCK, IT_DEP, IT_WAR, IT_RWAIT, IT_AWAIT) = range(16)
+ IT_BLOCK, IT_DEP, IT_WAR, IT_RWAIT, IT_AWAIT, IT_DST, IT_SRC, IT_ROUND) = range(19)
 
 # Symbols include/pd_b200.h declares; tests check every one is exported.
 EXPORTED = (
-    "pd_abi_version", "pd_last_error", "pd_device_sm_count", "pd_gemm", "pd_bias_sgd", "pd_sgd_update", "pd_cast",
+    "pd_abi_version", "pd_last_error", "pd_device_sm_count", "pd_gemm", "pd_bias_sgd", "pd_sgd_update", "pd_cast", "pd_allreduce_sgd", "pd_bias_grad",
     "pd_flag_signal", "pd_flag_wait", "pd_ipc_get_handle", "pd_ipc_open", "pd_ipc_close",
-    "pd_enable_peer_access", "pd_rt_create", "pd_rt_add_stage", "pd_rt_load_program", "pd_rt_run",
+    "pd_enable_peer_access", "pd_rt_create", "pd_rt_add_stage", "pd_rt_add_view", "pd_rt_load_program", "pd_rt_run",
     "pd_rt_records", "pd_rt_set_serial", "pd_rt_kernel_timing", "pd_rt_kernel_stats", "pd_rt_launch_count", "pd_rt_destroy",
 )
 
@@ -41,18 +41,28 @@ class Epilogue(Structure):
 
 class StageDesc(Structure):
     _fields_ = [
-        ("stage", c_int), ("n_layers", c_int), ("dims", POINTER(c_int64)), ("batch", c_int), ("dtype", c_int),
+        ("worker", c_int), ("stage", c_int), ("replica", c_int), ("rep", c_int), ("first_worker", c_int),
+        ("n_layers", c_int), ("dims", POINTER(c_int64)), ("batch", c_int), ("dtype", c_int),
         ("is_first", c_int), ("is_last", c_int), ("relu_last", c_int), ("ring_depth", c_int), ("init_slot", c_int),
-        ("act_depth", c_int), ("in_depth", c_int), ("grad_depth", c_int), ("lr", c_float),
+        ("act_depth", c_int), ("in_depth", c_int), ("grad_depth", c_int), ("n_data_blocks", c_int),
+        ("remote_prev", c_int), ("remote_next", c_int), ("lr", c_float),
         ("w_master", POINTER(c_void_p)), ("b_master", POINTER(c_void_p)), ("w_ring", POINTER(c_void_p)),
         ("b_ring", POINTER(c_void_p)), ("act", POINTER(c_void_p)), ("act_in", POINTER(c_void_p)),
-        ("n_data_blocks", c_int), ("grad_in", POINTER(c_void_p)), ("dz_last", POINTER(c_void_p)),
+        ("grad_in", POINTER(c_void_p)), ("dz_last", POINTER(c_void_p)),
         ("target", POINTER(c_void_p)), ("loss", c_void_p), ("tmp", c_void_p * 2),
-        ("next_act_in", POINTER(c_void_p)), ("next_in_depth", c_int),
-        ("prev_grad_in", POINTER(c_void_p)), ("prev_grad_depth", c_int),
-        ("act_ready", c_void_p), ("act_ack_remote", c_void_p), ("next_act_ready", c_void_p),
-        ("next_act_ack", c_void_p), ("grad_ready", c_void_p), ("grad_ack_remote", c_void_p),
-        ("prev_grad_ready", c_void_p), ("prev_grad_ack", c_void_p), ("err_word", c_void_p),
+        ("act_ready", c_void_p), ("act_ack", c_void_p), ("grad_ready", c_void_p), ("grad_ack", c_void_p),
+        ("red_grad", POINTER(c_void_p)), ("red_bgrad", POINTER(c_void_p)), ("red_ready", c_void_p),
+        ("red_done", c_void_p), ("err_word", c_void_p),
+    ]
+
+
+class WorkerView(Structure):
+    _fields_ = [
+        ("worker", c_int), ("remote", c_int), ("in_depth", c_int), ("grad_depth", c_int), ("n_layers", c_int),
+        ("act_in", POINTER(c_void_p)), ("grad_in", POINTER(c_void_p)),
+        ("act_ready", c_void_p), ("act_ack", c_void_p), ("grad_ready", c_void_p), ("grad_ack", c_void_p),
+        ("red_grad", POINTER(c_void_p)), ("red_bgrad", POINTER(c_void_p)), ("red_ready", c_void_p),
+        ("red_done", c_void_p),
     ]
 
 
@@ -85,6 +95,9 @@ def lib() -> ctypes.CDLL:
         L.pd_ipc_close.argtypes = [c_void_p]
         L.pd_rt_create.argtypes = [c_int, POINTER(c_void_p)]
         L.pd_rt_add_stage.argtypes = [c_void_p, POINTER(StageDesc)]
+        L.pd_rt_add_view.argtypes = [c_void_p, POINTER(WorkerView)]
+        L.pd_allreduce_sgd.argtypes = [c_int, POINTER(c_void_p), c_int, c_void_p, c_void_p, c_int64, c_float, c_void_p]
+        L.pd_bias_grad.argtypes = [c_int, c_void_p, c_int, c_int, c_int64, c_void_p, c_void_p]
         L.pd_rt_load_program.argtypes = [c_void_p, POINTER(c_int32), c_int]
         L.pd_rt_run.argtypes = [c_void_p, c_void_p, c_int]
         L.pd_rt_records.argtypes = [c_void_p, POINTER(Record), c_int, POINTER(c_int)]

@@ -87,6 +87,82 @@ int sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n
   return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "sgd_update: %s", cudaGetErrorString(e));
 }
 
+// ---------------------------------------------------------------- replicated stages
+constexpr int PD_MAX_REP = 16;
+struct GradPtrs { const float* p[PD_MAX_REP]; };
+
+// Sum of every replica's gradient (peer-mapped loads over NVLink for the remote ones), fused
+// with the SGD step.  Fixed summation order r = 0..R-1 -> every replica gets identical weights.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_allreduce_sgd(GradPtrs g, int R, float* __restrict__ m, T* __restrict__ o, int64_t n, float lr) {
+  const int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 s = reinterpret_cast<const float4*>(g.p[0])[i];
+    for (int r = 1; r < R; ++r) {
+      const float4 t = reinterpret_cast<const float4*>(g.p[r])[i];
+      s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
+    }
+    float4 w = reinterpret_cast<float4*>(m)[i];
+    w.x -= lr * s.x; w.y -= lr * s.y; w.z -= lr * s.z; w.w -= lr * s.w;
+    reinterpret_cast<float4*>(m)[i] = w;
+    o[4 * i] = from_f<T>(w.x); o[4 * i + 1] = from_f<T>(w.y);
+    o[4 * i + 2] = from_f<T>(w.z); o[4 * i + 3] = from_f<T>(w.w);
+  }
+  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int r = 0; r < R; ++r) s += g.p[r][i];
+    const float w = m[i] - lr * s;
+    m[i] = w;
+    o[i] = from_f<T>(w);
+  }
+}
+
+int allreduce_sgd(int dtype, const float* const* grads, int n_rep, float* master, void* out, int64_t n, float lr,
+                  cudaStream_t st) {
+  if (n_rep < 1 || n_rep > PD_MAX_REP) return set_error(PD_ERR_INVALID, "allreduce_sgd: %d replicas", n_rep);
+  GradPtrs g{};
+  for (int r = 0; r < n_rep; ++r) g.p[r] = grads[r];
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dtype == PD_BF16)
+    k_allreduce_sgd<__nv_bfloat16><<<sms * 8, 256, 0, st>>>(g, n_rep, master, static_cast<__nv_bfloat16*>(out), n, lr);
+  else
+    k_allreduce_sgd<float><<<sms * 8, 256, 0, st>>>(g, n_rep, master, static_cast<float*>(out), n, lr);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "allreduce_sgd: %s", cudaGetErrorString(e));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512)
+    k_bias_grad(const T* __restrict__ dz, int rows, int cols, int64_t ld, float* __restrict__ out) {
+  __shared__ float part[16][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (c < cols)
+    for (int r = grp; r < rows; r += 16) s += to_f<T>(dz[(int64_t)r * ld + c]);
+  part[grp][lane] = s;
+  __syncthreads();
+  if (grp == 0 && c < cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) t += part[q][lane];
+    out[c] = t;
+  }
+}
+
+int bias_grad(int dtype, const void* dz, int rows, int cols, int64_t ld, float* out, cudaStream_t st) {
+  dim3 grid((cols + 31) / 32);
+  if (dtype == PD_BF16)
+    k_bias_grad<__nv_bfloat16><<<grid, 512, 0, st>>>(static_cast<const __nv_bfloat16*>(dz), rows, cols, ld, out);
+  else
+    k_bias_grad<float><<<grid, 512, 0, st>>>(static_cast<const float*>(dz), rows, cols, ld, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "bias_grad: %s", cudaGetErrorString(e));
+}
+
 template <typename T>
 __global__ void k_cast(const float* __restrict__ src, T* __restrict__ o, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -166,6 +242,14 @@ int pd_bias_sgd(int dtype, const void* dz, int rows, int cols, int64_t ld, float
 
 int pd_sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n, float lr, void* stream) {
   return sgd_update(dtype, master, grad, out, n, lr, static_cast<cudaStream_t>(stream));
+}
+
+int pd_allreduce_sgd(int dtype, const float* const* grads, int n_rep, float* master, void* out, int64_t n, float lr,
+                     void* stream) {
+  return allreduce_sgd(dtype, grads, n_rep, master, out, n, lr, static_cast<cudaStream_t>(stream));
+}
+int pd_bias_grad(int dtype, const void* dz, int rows, int cols, int64_t ld, float* out, void* stream) {
+  return bias_grad(dtype, dz, rows, cols, ld, out, static_cast<cudaStream_t>(stream));
 }
 
 int pd_cast(int dtype, const float* src, void* out, int64_t n, void* stream) {

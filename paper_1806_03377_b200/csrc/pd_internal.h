@@ -23,6 +23,9 @@ int gemm(int dtype, const void* A, int a_mn, int64_t lda, const void* B, int b_m
 int bias_sgd(int dtype, const void* dz, int rows, int cols, int64_t ld, float* b_master, float* b_out, float lr,
              cudaStream_t st);
 int sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n, float lr, cudaStream_t st);
+int allreduce_sgd(int dtype, const float* const* grads, int n_rep, float* master, void* out, int64_t n, float lr,
+                  cudaStream_t st);
+int bias_grad(int dtype, const void* dz, int rows, int cols, int64_t ld, float* out, cudaStream_t st);
 int cast_f32(int dtype, const float* src, void* out, int64_t n, cudaStream_t st);
 int flag_signal(int* flag, int value, cudaStream_t st);
 int flag_wait(const int* flag, int value, int* err_word, cudaStream_t st);

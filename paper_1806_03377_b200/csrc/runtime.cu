@@ -1,14 +1,14 @@
 // Device executor for a compiled 1F1B-RR program (include/pd_b200.h, "executor").
 //
 // Takes over the reference's discrete-event engine (simulator.py:150-357): instead of
-// advancing simulated clocks, each hosted stage owns a CUDA stream and every program
-// item (one forward or backward pass of one minibatch at one stage) becomes the
-// stage's GEMM chain on that stream.  Readiness (_try_start's ready[] gate,
+// advancing simulated clocks, each hosted worker (stage replica) owns a CUDA stream and every
+// program item (one forward / backward / replica-reduce of one minibatch) becomes that
+// worker's kernel chain on the stream.  Readiness (_try_start's ready[] gate,
 // simulator.py:255-260) becomes a cudaStreamWaitEvent on the producing item when the
-// neighbour stage lives in this process, or a device-side acquire-poll on an inbox
-// flag written by the neighbour GPU.  Version selection and commits are resolved
-// ahead of time into ring slots (PD_IT_WSLOT / PD_IT_WNEW): the wgrad epilogue writes
-// version mb into its slot (commit, simulator.py:315).
+// neighbour lives in this process, or a device-side acquire-poll on the receiver-owned inbox
+// flag when it lives in another.  Version selection and commits are resolved ahead of time
+// into ring slots (PD_IT_WSLOT / PD_IT_WNEW): the wgrad epilogue (or, for a replicated stage,
+// the fused allreduce+SGD kernel) writes the committed version into its slot (simulator.py:315).
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstring>
@@ -24,11 +24,17 @@ using namespace pd;
 struct Stage {
   pd_stage_desc d{};
   std::vector<int64_t> dims;
-  std::vector<float*> w_master, b_master, b_ring;
-  std::vector<void*> w_ring, act, act_in, grad_in, dz_last, next_act_in, prev_grad_in;
+  std::vector<float*> w_master, b_master, b_ring, red_grad, red_bgrad;
+  std::vector<void*> w_ring, act, act_in, grad_in, dz_last;
   std::vector<const float*> target;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_done = nullptr;
+};
+
+struct View {
+  pd_worker_view v{};
+  std::vector<void*> act_in, grad_in;
+  std::vector<float*> red_grad, red_bgrad;
 };
 
 template <typename T>
@@ -41,19 +47,20 @@ std::vector<T> copy_arr(const T* p, int64_t n) {
 struct pd_runtime {
   int device = 0;
   int epoch = 0;
-  std::map<int, Stage> stages;
+  std::map<int, Stage> stages;  // hosted workers
+  std::map<int, View> views;    // every worker of the plan
   std::vector<int32_t> items;
   std::vector<cudaEvent_t> ev_start, ev_end;
   cudaEvent_t ev0 = nullptr;
   bool traced = false;
   // kernel accounting: launches of our kernels, and optional per-GEMM event timing by class
   int64_t launches = 0;
-  bool serial = false;             // all hosted stages on one stream (single-GPU timing mode)
-  // end-of-run drain: (stage, local ack flag, final occupant mb) of every outbox slot that
-  // lives on another GPU, so the next run cannot overwrite a slot the peer still reads
-  struct Drain { int stage; int* flag; int mb; };
-  std::vector<Drain> drain;
+  bool serial = false;             // all hosted workers on one stream (single-GPU timing mode)
   cudaStream_t shared = nullptr;
+  // end-of-run drain: (worker, peer ack flag, final occupant) of every outbox slot in another
+  // process, so the next run cannot overwrite a slot the peer still reads
+  struct Drain { int worker; int* flag; int mb; };
+  std::vector<Drain> drain;
   bool ktiming = false;
   struct KT { int cls; double flops; cudaEvent_t a, b; };
   std::vector<KT> kt;
@@ -73,9 +80,11 @@ namespace {
     if (rc_) return rc_;   \
   } while (0)
 
-inline int flag_val(int epoch, int mb) { return epoch * 65536 + mb; }
+inline int flag_val(int epoch, int v) { return epoch * 65536 + v; }
 
 enum { KC_FWD = 0, KC_DGRAD = 1, KC_WGRAD = 2, KC_N = 3 };
+
+inline cudaStream_t stream_of(pd_runtime* rt, Stage& S) { return rt->serial ? rt->shared : S.stream; }
 
 int timed_gemm(pd_runtime* rt, int cls, int dtype, const void* A, int a_mn, int64_t lda, const void* B, int b_mn,
                int64_t ldb, int M, int N, int K, int kind, const EpiArgs& ep, cudaStream_t st) {
@@ -98,8 +107,19 @@ int timed_gemm(pd_runtime* rt, int cls, int dtype, const void* A, int a_mn, int6
   return 0;
 }
 
+int wait_flag(pd_runtime* rt, Stage& S, const int* flag, int value) {
+  PD_TRY(flag_wait(flag, flag_val(rt->epoch, value), S.d.err_word, stream_of(rt, S)));
+  rt->launches += 1;
+  return 0;
+}
+int signal_flag(pd_runtime* rt, Stage& S, int* flag, int value) {
+  PD_TRY(flag_signal(flag, flag_val(rt->epoch, value), stream_of(rt, S)));
+  rt->launches += 1;
+  return 0;
+}
+
 int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
-  cudaStream_t ST = rt->serial ? rt->shared : S.stream;
+  cudaStream_t ST = stream_of(rt, S);
   const pd_stage_desc& d = S.d;
   const int L = d.n_layers, B = d.batch;
   const int wslot = it[PD_IT_WSLOT], act = it[PD_IT_ACT], mb = it[PD_IT_MB];
@@ -121,7 +141,8 @@ int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.scale = 1.0f / (float)B;
       ep.loss = d.loss + mb;
     } else {
-      ep.out = S.next_act_in[it[PD_IT_OUT]];
+      // the epilogue stores straight into the next stage's inbox slot (peer-mapped if remote)
+      ep.out = rt->views.at(it[PD_IT_DST]).act_in[it[PD_IT_OUT]];
       ep.relu = d.relu_last;
     }
     const void* W = S.w_ring[(size_t)l * d.ring_depth + wslot];
@@ -132,10 +153,16 @@ int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
 }
 
 int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
-  cudaStream_t ST = rt->serial ? rt->shared : S.stream;
+  cudaStream_t ST = stream_of(rt, S);
   const pd_stage_desc& d = S.d;
   const int L = d.n_layers, B = d.batch;
-  const int wslot = it[PD_IT_WSLOT], wnew = it[PD_IT_WNEW], act = it[PD_IT_ACT];
+  const int wslot = it[PD_IT_WSLOT], wnew = it[PD_IT_WNEW], act = it[PD_IT_ACT], round = it[PD_IT_ROUND];
+  const bool replicated = d.rep > 1;
+  const int par = round & 1;
+  if (replicated && round >= 3) {
+    // this round's gradient buffers (parity round % 2) were last read by round-2's reductions
+    for (int r = 0; r < d.rep; ++r) PD_TRY(wait_flag(rt, S, rt->views.at(d.first_worker + r).v.red_done, round - 2));
+  }
   const void* dz = d.is_last ? S.dz_last[act] : S.grad_in[it[PD_IT_GSLOT]];
   for (int l = L - 1; l >= 0; --l) {
     const int Kin = (int)S.dims[l], Nout = (int)S.dims[l + 1];
@@ -144,8 +171,9 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
     const void* Wst = S.w_ring[(size_t)l * d.ring_depth + wslot];
     void* out = nullptr;
     if (!(d.is_first && l == 0)) {
-      // dgrad + ReLU-backward: dZ_{l-1} = (dZ_l W_l^{stashed}) * (X_l > 0)
-      out = (l == 0) ? S.prev_grad_in[it[PD_IT_OUT]] : d.tmp[l & 1];
+      // dgrad + ReLU-backward: dZ_{l-1} = (dZ_l W_l^{stashed}) * (X_l > 0); the first layer's
+      // result goes straight into the previous stage's gradient inbox
+      out = (l == 0) ? rt->views.at(it[PD_IT_DST]).grad_in[it[PD_IT_OUT]] : d.tmp[l & 1];
       EpiArgs ep{};
       ep.out = out;
       ep.ldo = Kin;
@@ -153,7 +181,15 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.ldm = Kin;
       PD_TRY(timed_gemm(rt, KC_DGRAD, d.dtype, dz, 0, Nout, Wst, 1, Kin, B, Kin, Nout, EPI_MASK, ep, ST));
     }
-    if (wnew >= 0) {
+    if (replicated) {
+      // this replica's fp32 gradient; the REDUCE item sums all replicas and commits
+      EpiArgs ep{};
+      ep.out = S.red_grad[(size_t)l * 2 + par];
+      ep.ldo = Kin;
+      PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, Nout, X, 1, Kin, Nout, Kin, B, EPI_GRADF32, ep, ST));
+      PD_TRY(bias_grad(d.dtype, dz, B, Nout, Nout, S.red_bgrad[(size_t)l * 2 + par], ST));
+      rt->launches += 1;
+    } else if (wnew >= 0) {
       // wgrad + SGD onto the latest weights, written as version mb into ring slot wnew
       EpiArgs ep{};
       ep.master = S.w_master[l];
@@ -168,6 +204,32 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
     }
     dz = out;
   }
+  if (replicated) PD_TRY(signal_flag(rt, S, d.red_ready, round));
+  return 0;
+}
+
+// Replicated stage, round k: wait until every replica's round-k gradients exist, then the fused
+// allreduce (peer loads) + SGD kernel commits version k*rep into ring slot wnew on each replica.
+int run_reduce(pd_runtime* rt, Stage& S, const int32_t* it) {
+  cudaStream_t ST = stream_of(rt, S);
+  const pd_stage_desc& d = S.d;
+  const int round = it[PD_IT_ROUND], wnew = it[PD_IT_WNEW], par = round & 1;
+  for (int r = 0; r < d.rep; ++r) PD_TRY(wait_flag(rt, S, rt->views.at(d.first_worker + r).v.red_ready, round));
+  std::vector<const float*> g(d.rep), gb(d.rep);
+  for (int l = 0; l < d.n_layers; ++l) {
+    for (int r = 0; r < d.rep; ++r) {
+      const View& V = rt->views.at(d.first_worker + r);
+      g[r] = V.red_grad[(size_t)l * 2 + par];
+      gb[r] = V.red_bgrad[(size_t)l * 2 + par];
+    }
+    const int64_t n = S.dims[l] * S.dims[l + 1];
+    PD_TRY(allreduce_sgd(d.dtype, g.data(), d.rep, S.w_master[l], S.w_ring[(size_t)l * d.ring_depth + wnew], n,
+                         d.lr, ST));
+    PD_TRY(allreduce_sgd(PD_F32, gb.data(), d.rep, S.b_master[l], S.b_ring[(size_t)l * d.ring_depth + wnew],
+                         S.dims[l + 1], d.lr, ST));
+    rt->launches += 2;
+  }
+  PD_TRY(signal_flag(rt, S, d.red_done, round));
   return 0;
 }
 
@@ -191,12 +253,15 @@ int pd_rt_create(int device, pd_runtime** out) {
 int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc) {
   if (!rt || !desc) return set_error(PD_ERR_INVALID, "pd_rt_add_stage: null argument");
   const pd_stage_desc& d = *desc;
-  if (d.n_layers < 1 || d.batch < 1 || d.ring_depth < 1 || d.act_depth < 1)
-    return set_error(PD_ERR_INVALID, "stage %d: bad descriptor (layers=%d batch=%d ring=%d act=%d)", d.stage,
-                     d.n_layers, d.batch, d.ring_depth, d.act_depth);
-  if (d.dtype != PD_F32 && d.dtype != PD_BF16) return set_error(PD_ERR_INVALID, "stage %d: bad dtype", d.stage);
-  if (d.init_slot < 0 || d.init_slot >= d.ring_depth) return set_error(PD_ERR_INVALID, "stage %d: bad init_slot", d.stage);
-  if (rt->stages.count(d.stage)) return set_error(PD_ERR_INVALID, "stage %d added twice", d.stage);
+  if (d.n_layers < 1 || d.batch < 1 || d.ring_depth < 1 || d.act_depth < 1 || d.rep < 1)
+    return set_error(PD_ERR_INVALID, "worker %d: bad descriptor (layers=%d batch=%d ring=%d act=%d rep=%d)",
+                     d.worker, d.n_layers, d.batch, d.ring_depth, d.act_depth, d.rep);
+  if (d.dtype != PD_F32 && d.dtype != PD_BF16) return set_error(PD_ERR_INVALID, "worker %d: bad dtype", d.worker);
+  if (d.init_slot < 0 || d.init_slot >= d.ring_depth)
+    return set_error(PD_ERR_INVALID, "worker %d: bad init_slot", d.worker);
+  if (d.rep > 1 && (!d.red_grad || !d.red_bgrad || !d.red_ready || !d.red_done))
+    return set_error(PD_ERR_INVALID, "worker %d: replicated stage without reduction buffers", d.worker);
+  if (rt->stages.count(d.worker)) return set_error(PD_ERR_INVALID, "worker %d added twice", d.worker);
   Stage S;
   S.d = d;
   const int L = d.n_layers;
@@ -212,14 +277,27 @@ int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc) {
     S.dz_last = copy_arr(d.dz_last, d.act_depth);
     S.target = copy_arr(d.target, d.n_data_blocks);
   }
-  // neighbour inbox views: sizes are implied by the program's slot indices
-  if (!d.is_last) S.next_act_in = copy_arr(d.next_act_in, d.next_in_depth);
-  if (!d.is_first) S.prev_grad_in = copy_arr(d.prev_grad_in, d.prev_grad_depth);
+  if (d.rep > 1) {
+    S.red_grad = copy_arr(d.red_grad, (int64_t)L * 2);
+    S.red_bgrad = copy_arr(d.red_bgrad, (int64_t)L * 2);
+  }
   S.d.dims = nullptr;
   PD_CHECK(cudaSetDevice(rt->device));
   PD_CHECK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
   PD_CHECK(cudaEventCreateWithFlags(&S.ev_done, cudaEventDisableTiming));
-  rt->stages.emplace(d.stage, std::move(S));
+  rt->stages.emplace(d.worker, std::move(S));
+  return 0;
+}
+
+int pd_rt_add_view(pd_runtime* rt, const pd_worker_view* view) {
+  if (!rt || !view) return set_error(PD_ERR_INVALID, "pd_rt_add_view: null argument");
+  View V;
+  V.v = *view;
+  V.act_in = copy_arr(view->act_in, view->in_depth);
+  V.grad_in = copy_arr(view->grad_in, view->grad_depth);
+  V.red_grad = copy_arr(view->red_grad, (int64_t)view->n_layers * 2);
+  V.red_bgrad = copy_arr(view->red_bgrad, (int64_t)view->n_layers * 2);
+  rt->views[view->worker] = std::move(V);
   return 0;
 }
 
@@ -227,51 +305,47 @@ int pd_rt_load_program(pd_runtime* rt, const int32_t* items, int n_items) {
   if (!rt || (!items && n_items)) return set_error(PD_ERR_INVALID, "pd_rt_load_program: null argument");
   for (int i = 0; i < n_items; ++i) {
     const int32_t* it = items + (size_t)i * PD_ITEM_WIDTH;
-    auto f = rt->stages.find(it[PD_IT_STAGE]);
+    auto f = rt->stages.find(it[PD_IT_WORKER]);
     if (f == rt->stages.end())
-      return set_error(PD_ERR_INVALID, "item %d: stage %d is not hosted here", i, it[PD_IT_STAGE]);
+      return set_error(PD_ERR_INVALID, "item %d: worker %d is not hosted here", i, it[PD_IT_WORKER]);
     const Stage& S = f->second;
+    const int op = it[PD_IT_OP];
+    if (op < 0 || op > 2) return set_error(PD_ERR_INVALID, "item %d: bad op %d", i, op);
     if (it[PD_IT_DEP] >= i || it[PD_IT_WAR] >= i)
       return set_error(PD_ERR_INVALID, "item %d: dependency %d/%d not issued earlier (program not topological)", i,
                        it[PD_IT_DEP], it[PD_IT_WAR]);
-    if (it[PD_IT_WSLOT] < 0 || it[PD_IT_WSLOT] >= S.d.ring_depth || it[PD_IT_WNEW] >= S.d.ring_depth ||
-        it[PD_IT_ACT] < 0 || it[PD_IT_ACT] >= S.d.act_depth)
+    if (it[PD_IT_WSLOT] >= S.d.ring_depth || it[PD_IT_WNEW] >= S.d.ring_depth || it[PD_IT_ACT] >= S.d.act_depth)
       return set_error(PD_ERR_INVALID, "item %d: slot out of range", i);
-    const bool fwd = it[PD_IT_OP] == 0;
-    if (fwd && !S.d.is_last && (it[PD_IT_OUT] < 0 || it[PD_IT_OUT] >= (int)S.next_act_in.size()))
-      return set_error(PD_ERR_INVALID, "item %d: forward outbox slot %d out of range", i, it[PD_IT_OUT]);
-    if (!fwd && !S.d.is_first && (it[PD_IT_OUT] < 0 || it[PD_IT_OUT] >= (int)S.prev_grad_in.size()))
-      return set_error(PD_ERR_INVALID, "item %d: backward outbox slot %d out of range", i, it[PD_IT_OUT]);
+    if (op == 2 && S.d.rep < 2) return set_error(PD_ERR_INVALID, "item %d: reduce on an unreplicated stage", i);
+    const bool sends = (op == 0 && !S.d.is_last) || (op == 1 && !S.d.is_first);
+    if (sends) {
+      auto v = rt->views.find(it[PD_IT_DST]);
+      if (v == rt->views.end()) return set_error(PD_ERR_INVALID, "item %d: no view of worker %d", i, it[PD_IT_DST]);
+      const int depth = op == 0 ? v->second.v.in_depth : v->second.v.grad_depth;
+      if (it[PD_IT_OUT] < 0 || it[PD_IT_OUT] >= depth)
+        return set_error(PD_ERR_INVALID, "item %d: outbox slot %d out of range", i, it[PD_IT_OUT]);
+    }
+    if (S.d.rep > 1)
+      for (int r = 0; r < S.d.rep; ++r)
+        if (!rt->views.count(S.d.first_worker + r))
+          return set_error(PD_ERR_INVALID, "item %d: no view of replica worker %d", i, S.d.first_worker + r);
   }
   rt->items.assign(items, items + (size_t)n_items * PD_ITEM_WIDTH);
+  // drain list: final occupant of every remote outbox slot
   rt->drain.clear();
-  {
-    std::map<std::pair<int*, int>, int> last;  // (ack array, slot) -> final occupant
-    for (int i = 0; i < n_items; ++i) {
-      const int32_t* it = items + (size_t)i * PD_ITEM_WIDTH;
-      const Stage& S = rt->stages.at(it[PD_IT_STAGE]);
-      const bool fwd = it[PD_IT_OP] == 0;
-      int* ack = nullptr;
-      if (fwd && !S.d.is_last && S.d.next_act_ready) ack = S.d.next_act_ack;
-      if (!fwd && !S.d.is_first && S.d.prev_grad_ready) ack = S.d.prev_grad_ack;
-      if (ack) {
-        int& m = last[{ack, it[PD_IT_OUT]}];
-        m = std::max(m, it[PD_IT_MB]);
-      }
-    }
-    for (int i = 0; i < n_items; ++i) {  // attach each drain wait to the stage that owns the ack array
-      const int32_t* it = items + (size_t)i * PD_ITEM_WIDTH;
-      const Stage& S = rt->stages.at(it[PD_IT_STAGE]);
-      for (auto kv = last.begin(); kv != last.end();) {
-        if (kv->first.first == S.d.next_act_ack || kv->first.first == S.d.prev_grad_ack) {
-          rt->drain.push_back({it[PD_IT_STAGE], kv->first.first + kv->first.second, kv->second});
-          kv = last.erase(kv);
-        } else {
-          ++kv;
-        }
-      }
-    }
+  std::map<std::pair<int*, int>, std::pair<int, int>> last;  // (ack array, slot) -> (worker, mb)
+  for (int i = 0; i < n_items; ++i) {
+    const int32_t* it = items + (size_t)i * PD_ITEM_WIDTH;
+    const Stage& S = rt->stages.at(it[PD_IT_WORKER]);
+    const int op = it[PD_IT_OP];
+    if (!((op == 0 && !S.d.is_last) || (op == 1 && !S.d.is_first))) continue;
+    const View& V = rt->views.at(it[PD_IT_DST]);
+    if (!V.v.remote) continue;
+    int* ack = op == 0 ? V.v.act_ack : V.v.grad_ack;
+    auto& e = last[{ack, it[PD_IT_OUT]}];
+    if (it[PD_IT_MB] > e.second) e = {it[PD_IT_WORKER], it[PD_IT_MB]};
   }
+  for (const auto& kv : last) rt->drain.push_back({kv.second.first, kv.first.first + kv.first.second, kv.second.second});
   for (auto e : rt->ev_start) cudaEventDestroy(e);
   for (auto e : rt->ev_end) cudaEventDestroy(e);
   rt->ev_start.assign(n_items, nullptr);
@@ -291,9 +365,11 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
   rt->epoch += 1;
   rt->traced = trace != 0;
   PD_CHECK(cudaEventRecord(rt->ev0, main));
+  int max_mb = 0;
+  for (size_t i = 0; i < rt->items.size(); i += PD_ITEM_WIDTH) max_mb = std::max(max_mb, rt->items[i + PD_IT_MB]);
   for (auto& kv : rt->stages) {
     Stage& S = kv.second;
-    cudaStream_t ST = rt->serial ? rt->shared : S.stream;
+    cudaStream_t ST = stream_of(rt, S);
     PD_CHECK(cudaStreamWaitEvent(ST, rt->ev0, 0));
     // version 0 of this run = the current (latest) weights
     for (int l = 0; l < S.d.n_layers; ++l) {
@@ -303,57 +379,45 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
       PD_CHECK(cudaMemcpyAsync(S.b_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], S.b_master[l],
                                sizeof(float) * S.dims[l + 1], cudaMemcpyDeviceToDevice, ST));
     }
-    if (S.d.is_last && S.d.loss) {
-      // losses are indexed by minibatch id; the program's largest id bounds the buffer
-      int max_mb = 0;
-      for (size_t i = 0; i < rt->items.size(); i += PD_ITEM_WIDTH) max_mb = std::max(max_mb, rt->items[i + PD_IT_MB]);
+    if (S.d.is_last && S.d.loss)  // losses are indexed by minibatch id
       PD_CHECK(cudaMemsetAsync(S.d.loss, 0, sizeof(float) * (size_t)(max_mb + 1), ST));
-    }
   }
   const int n = (int)(rt->items.size() / PD_ITEM_WIDTH);
   for (int i = 0; i < n; ++i) {
     const int32_t* it = rt->items.data() + (size_t)i * PD_ITEM_WIDTH;
-    Stage& S = rt->stages[it[PD_IT_STAGE]];
-    cudaStream_t ST = rt->serial ? rt->shared : S.stream;
-    const bool fwd = it[PD_IT_OP] == 0;
+    Stage& S = rt->stages[it[PD_IT_WORKER]];
+    cudaStream_t ST = stream_of(rt, S);
+    const int op = it[PD_IT_OP], mb = it[PD_IT_MB];
+    const bool fwd = op == 0;
     const int dep = it[PD_IT_DEP], war = it[PD_IT_WAR];
     if (dep >= 0) PD_CHECK(cudaStreamWaitEvent(ST, rt->ev_end[dep], 0));
     if (war >= 0) PD_CHECK(cudaStreamWaitEvent(ST, rt->ev_end[war], 0));
-    if (it[PD_IT_RWAIT] > 0) {
-      int* flag = fwd ? S.d.act_ready + it[PD_IT_XSLOT] : S.d.grad_ready + it[PD_IT_GSLOT];
-      PD_TRY(flag_wait(flag, flag_val(rt->epoch, it[PD_IT_RWAIT]), S.d.err_word, ST));
-      rt->launches += 1;
-    }
-    if (it[PD_IT_AWAIT] > 0) {
-      int* flag = fwd ? S.d.next_act_ack + it[PD_IT_OUT] : S.d.prev_grad_ack + it[PD_IT_OUT];
-      PD_TRY(flag_wait(flag, flag_val(rt->epoch, it[PD_IT_AWAIT]), S.d.err_word, ST));
-      rt->launches += 1;
+    if (it[PD_IT_RWAIT] > 0)  // payload produced in another process: acquire my inbox flag
+      PD_TRY(wait_flag(rt, S, fwd ? S.d.act_ready + it[PD_IT_XSLOT] : S.d.grad_ready + it[PD_IT_GSLOT],
+                       it[PD_IT_RWAIT]));
+    if (it[PD_IT_AWAIT] > 0) {  // receiver in another process: its previous occupant must be done
+      const View& V = rt->views.at(it[PD_IT_DST]);
+      PD_TRY(wait_flag(rt, S, (fwd ? V.v.act_ack : V.v.grad_ack) + it[PD_IT_OUT], it[PD_IT_AWAIT]));
     }
     if (rt->traced) PD_CHECK(cudaEventRecord(rt->ev_start[i], ST));
-    PD_TRY(fwd ? run_forward(rt, S, it) : run_backward(rt, S, it));
-    // cross-GPU hand-off: publish the payload the epilogue stored into the peer inbox
-    const int mb = it[PD_IT_MB];
-    if (fwd && !S.d.is_last && S.d.next_act_ready)
-      PD_TRY(flag_signal(S.d.next_act_ready + it[PD_IT_OUT], flag_val(rt->epoch, mb), ST));
-    if (!fwd && !S.d.is_first && S.d.prev_grad_ready)
-      PD_TRY(flag_signal(S.d.prev_grad_ready + it[PD_IT_OUT], flag_val(rt->epoch, mb), ST));
-    if (!fwd && !S.d.is_first && S.d.act_ack_remote)
-      PD_TRY(flag_signal(S.d.act_ack_remote + it[PD_IT_XSLOT], flag_val(rt->epoch, mb), ST));
-    if (!fwd && !S.d.is_last && S.d.grad_ack_remote)
-      PD_TRY(flag_signal(S.d.grad_ack_remote + it[PD_IT_GSLOT], flag_val(rt->epoch, mb), ST));
-    rt->launches += (fwd && !S.d.is_last && S.d.next_act_ready) + (!fwd && !S.d.is_first && S.d.prev_grad_ready) +
-                    (!fwd && !S.d.is_first && S.d.act_ack_remote) + (!fwd && !S.d.is_last && S.d.grad_ack_remote);
+    if (op == 0) PD_TRY(run_forward(rt, S, it));
+    else if (op == 1) PD_TRY(run_backward(rt, S, it));
+    else PD_TRY(run_reduce(rt, S, it));
+    // cross-process hand-off: publish the payload the epilogue stored into the peer inbox
+    if ((op == 0 && !S.d.is_last) || (op == 1 && !S.d.is_first)) {
+      const View& V = rt->views.at(it[PD_IT_DST]);
+      if (V.v.remote) PD_TRY(signal_flag(rt, S, (fwd ? V.v.act_ready : V.v.grad_ready) + it[PD_IT_OUT], mb));
+    }
+    if (op == 1) {  // my inbox slots are free again: tell producers in other processes
+      if (!S.d.is_first && S.d.remote_prev) PD_TRY(signal_flag(rt, S, S.d.act_ack + it[PD_IT_XSLOT], mb));
+      if (!S.d.is_last && S.d.remote_next) PD_TRY(signal_flag(rt, S, S.d.grad_ack + it[PD_IT_GSLOT], mb));
+    }
     PD_CHECK(cudaEventRecord(rt->ev_end[i], ST));
   }
-  for (const auto& dr : rt->drain) {
-    Stage& S = rt->stages[dr.stage];
-    cudaStream_t ST = rt->serial ? rt->shared : S.stream;
-    PD_TRY(flag_wait(dr.flag, flag_val(rt->epoch, dr.mb), S.d.err_word, ST));
-    rt->launches += 1;
-  }
+  for (const auto& dr : rt->drain) PD_TRY(wait_flag(rt, rt->stages[dr.worker], dr.flag, dr.mb));
   for (auto& kv : rt->stages) {
     Stage& S = kv.second;
-    PD_CHECK(cudaEventRecord(S.ev_done, rt->serial ? rt->shared : S.stream));
+    PD_CHECK(cudaEventRecord(S.ev_done, stream_of(rt, S)));
     PD_CHECK(cudaStreamWaitEvent(main, S.ev_done, 0));
   }
   return 0;
@@ -426,9 +490,15 @@ int pd_rt_destroy(pd_runtime* rt) {
   }
   for (auto e : rt->ev_start) cudaEventDestroy(e);
   for (auto e : rt->ev_end) cudaEventDestroy(e);
-  for (auto& k : rt->kt) { cudaEventDestroy(k.a); cudaEventDestroy(k.b); }
+  for (auto& k : rt->kt) {
+    cudaEventDestroy(k.a);
+    cudaEventDestroy(k.b);
+  }
   if (rt->ev0) cudaEventDestroy(rt->ev0);
-  if (rt->shared) { cudaStreamSynchronize(rt->shared); cudaStreamDestroy(rt->shared); }
+  if (rt->shared) {
+    cudaStreamSynchronize(rt->shared);
+    cudaStreamDestroy(rt->shared);
+  }
   delete rt;
   return 0;
 }

@@ -65,11 +65,13 @@ def _validate(cfg: SimConfig, ctx, model: MLPSpec) -> None:
         raise ValidationError(f"plan covers {plan.num_layers} layers, profile has {ctx.num_layers}")
     if plan.num_layers != model.num_layers:
         raise ValidationError(f"plan covers {plan.num_layers} layers, model has {model.num_layers}")
+    if any(st.replication > 16 for st in plan.stages):
+        raise ValidationError("at most 16 replicas per stage")
     for s, st in enumerate(plan.stages):
-        if st.replication > 1:
+        if st.replication > 1 and cfg.num_minibatches % st.replication:
             raise ValidationError(
-                f"stage {s} is replicated {st.replication}x: replicated stages need the multi-GPU "
-                "allreduce path (paper_1806_03377_b200.replicated), not yet wired into run()"
+                f"stage {s} is replicated {st.replication}x: num_minibatches ({cfg.num_minibatches}) must be a "
+                "multiple of the replication so every allreduce round is complete (DESIGN.md §5)"
             )
 
 
@@ -159,42 +161,45 @@ class Executor:
                 t["loss"] = torch.zeros(self.cfg.num_minibatches + 1, device=dev, dtype=torch.float32)
             t["tmp"] = [torch.empty(m.batch, max(dims), device=dev, dtype=dt) for _ in range(2)]
             t["err"] = torch.zeros(1, device=dev, dtype=torch.int32)
-            # cross-GPU flags (zero = nothing delivered yet); used only when a neighbour is remote
+            # receiver-owned inbox flags (zero = nothing delivered yet); used when a producer is remote
             i32 = dict(device=dev, dtype=torch.int32)
-            n = plan.num_stages
             if wp.stage > 0:
                 t["act_ready"] = torch.zeros(b.in_depth, **i32)
-                t["prev_grad_ack"] = torch.zeros(workers[self._neighbour(wp.wid, -1)].grad_depth, **i32)
-            if wp.stage < n - 1:
+                t["act_ack"] = torch.zeros(b.in_depth, **i32)
+            if wp.stage < plan.num_stages - 1:
                 t["grad_ready"] = torch.zeros(b.grad_depth, **i32)
-                t["next_act_ack"] = torch.zeros(workers[self._neighbour(wp.wid, +1)].in_depth, **i32)
+                t["grad_ack"] = torch.zeros(b.grad_depth, **i32)
+            if st.replication > 1:  # round-parity gradient buffers + reduction flags
+                t["red_grad"] = [[torch.zeros(dims[l + 1], dims[l], device=dev) for _ in range(2)] for l in range(L)]
+                t["red_bgrad"] = [[torch.zeros(dims[l + 1], device=dev) for _ in range(2)] for l in range(L)]
+                t["red_flags"] = torch.zeros(2, **i32)
             self.bufs[wp.wid] = b
 
-    def _neighbour(self, wid: int, step: int) -> int:
-        """Worker id of the (unique, straight-pipeline) neighbour stage."""
-        s, _ = self.schedule.workers[wid]
-        return self.schedule.worker_id(s + step, 0)
-
-    EXPORTS = ("act_in", "act_ready", "grad_in", "grad_ready", "next_act_ack", "prev_grad_ack")
+    EXPORTS = ("act_in", "grad_in", "act_ready", "act_ack", "grad_ready", "grad_ack", "red_flags")
 
     def _exchange(self) -> None:
-        """Publish CUDA IPC handles of this rank's inboxes and flags; map the neighbours' ones."""
+        """Publish CUDA IPC handles of this rank's inboxes, flags and reduction buffers."""
         self._remote: dict[int, dict] = {}
         if self.world == 1:
             return
         torch = _torch()
+
+        def export(t):
+            h, off = nat.ipc_export(t)
+            slot = t[0].numel() * t.element_size() if t.dim() > 1 else t.element_size()
+            return (h, off, slot, t.shape[0])
+
         mine = {}
         for b in self.bufs.values():
             ent = {}
             for name in self.EXPORTS:
                 if name == "act_in" and b.stage == 0:
                     continue
-                t = b.tensors.get(name)
-                if t is None:
-                    continue
-                h, off = nat.ipc_export(t)
-                slot = t[0].numel() * t.element_size() if t.dim() > 1 else t.element_size()
-                ent[name] = (h, off, slot, t.shape[0])
+                if name in b.tensors:
+                    ent[name] = export(b.tensors[name])
+            if "red_grad" in b.tensors:
+                ent["red_grad"] = [[export(g) for g in pair] for pair in b.tensors["red_grad"]]
+                ent["red_bgrad"] = [[export(g) for g in pair] for pair in b.tensors["red_bgrad"]]
             mine[b.wid] = ent
         gathered = [None] * self.world
         torch.distributed.all_gather_object(gathered, mine, group=self.group)
@@ -203,14 +208,24 @@ class Executor:
                 if self.program.device_of[wid] != self.rank:
                     self._remote[wid] = ent
 
-    def _view(self, wid: int, name: str) -> list[int]:
+    def _addr(self, wid: int, name: str) -> list[int]:
         """Per-slot device addresses of worker wid's buffer `name` (local or peer-mapped)."""
         if self.program.device_of[wid] == self.rank:
-            t = self.bufs[wid].tensors[name]
+            t = self.bufs[wid].tensors.get(name)
+            if t is None:
+                return []
             return [x.data_ptr() for x in t] if t.dim() > 1 else [t.data_ptr() + 4 * k for k in range(t.shape[0])]
-        h, off, slot, count = self._remote[wid][name]
+        ent = self._remote[wid].get(name)
+        if ent is None:
+            return []
+        h, off, slot, count = ent
         base = nat.ipc_import(h, off)
         return [base + k * slot for k in range(count)]
+
+    def _red_addrs(self, wid: int, name: str) -> list[int]:
+        if self.program.device_of[wid] == self.rank:
+            return [g.data_ptr() for pair in self.bufs[wid].tensors[name] for g in pair]
+        return [nat.ipc_import(h, off) for pair in self._remote[wid][name] for (h, off, _s, _c) in pair]
 
     @staticmethod
     def _parr(ptrs) -> ctypes.Array:
@@ -223,57 +238,84 @@ class Executor:
         rt = ctypes.c_void_p()
         nat.check(L.pd_rt_create(self.device.index, ctypes.byref(rt)), "pd_rt_create")
         self._rt = rt
+        self._keep = []
+
+        def arr(ptrs):
+            a = self._parr(ptrs)
+            self._keep.append(a)
+            return ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p))
+
+        def iptr(addrs):
+            return addrs[0] if addrs else None
+
+        # views of every worker the hosted ones talk to (all workers: cheap, and replicas need them)
+        for wp in self.program.workers:
+            wid = wp.wid
+            v = nat.WorkerView()
+            v.worker = wid
+            v.remote = int(self.program.device_of[wid] != self.rank)
+            v.in_depth, v.grad_depth = wp.in_depth, wp.grad_depth
+            st = plan.stages[wp.stage]
+            v.n_layers = st.last_layer - st.first_layer + 1
+            if wp.stage > 0:
+                v.act_in = arr(self._addr(wid, "act_in"))
+                v.act_ready, v.act_ack = iptr(self._addr(wid, "act_ready")), iptr(self._addr(wid, "act_ack"))
+            if wp.stage < n - 1:
+                v.grad_in = arr(self._addr(wid, "grad_in"))
+                v.grad_ready, v.grad_ack = iptr(self._addr(wid, "grad_ready")), iptr(self._addr(wid, "grad_ack"))
+            if st.replication > 1:
+                v.red_grad = arr(self._red_addrs(wid, "red_grad"))
+                v.red_bgrad = arr(self._red_addrs(wid, "red_bgrad"))
+                fl = self._addr(wid, "red_flags")
+                v.red_ready, v.red_done = fl[0], fl[1]
+            self._keep.append(v)
+            nat.check(L.pd_rt_add_view(rt, ctypes.byref(v)), "pd_rt_add_view")
+
+        reps = [st.replication for st in plan.stages]
         for b in self.bufs.values():
             t = b.tensors
+            wp = self.program.workers[b.wid]
             nl = len(b.dims) - 1
-            keep = []
-
-            def arr(ptrs):
-                a = self._parr(ptrs)
-                keep.append(a)
-                return ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p))
-
             dims = (ctypes.c_int64 * len(b.dims))(*b.dims)
-            keep.append(dims)
+            self._keep.append(dims)
             is_first, is_last = b.stage == 0, b.stage == n - 1
             d = nat.StageDesc()
-            d.stage, d.n_layers, d.dims, d.batch, d.dtype = b.stage, nl, dims, self.model.batch, self.pd_dtype
+            d.worker, d.stage, d.replica, d.rep = b.wid, b.stage, wp.replica, reps[b.stage]
+            d.first_worker = self.schedule.worker_id(b.stage, 0)
+            d.n_layers, d.dims, d.batch, d.dtype = nl, dims, self.model.batch, self.pd_dtype
             d.is_first, d.is_last, d.relu_last = int(is_first), int(is_last), int(not is_last)
             d.ring_depth, d.init_slot, d.act_depth = b.ring_depth, b.init_slot, b.act_depth
             d.in_depth, d.grad_depth, d.lr = b.in_depth, b.grad_depth, self.model.lr
+            d.n_data_blocks = self.model.n_blocks
+            # does any producer of my inboxes live in another process?
+            if not is_first:
+                prev = [self.schedule.worker_id(b.stage - 1, r) for r in range(reps[b.stage - 1])]
+                d.remote_prev = int(any(self.program.device_of[w] != self.rank for w in prev))
+            if not is_last:
+                nxt = [self.schedule.worker_id(b.stage + 1, r) for r in range(reps[b.stage + 1])]
+                d.remote_next = int(any(self.program.device_of[w] != self.rank for w in nxt))
             d.w_master = arr([w.data_ptr() for w in t["w_master"]])
             d.b_master = arr([x.data_ptr() for x in t["b_master"]])
             d.w_ring = arr([t["w_ring"][l][k].data_ptr() for l in range(nl) for k in range(b.ring_depth)])
             d.b_ring = arr([t["b_ring"][l][k].data_ptr() for l in range(nl) for k in range(b.ring_depth)])
             d.act = arr([t["act"][l][k].data_ptr() for l in range(nl - 1) for k in range(b.act_depth)])
             d.act_in = arr([x.data_ptr() for x in t["act_in"]])
-            d.n_data_blocks = self.model.n_blocks
             if not is_last:
                 d.grad_in = arr([x.data_ptr() for x in t["grad_in"]])
-                nw = self._neighbour(b.wid, +1)
-                d.next_act_in = arr(self._view(nw, "act_in"))
-                d.next_in_depth = self.program.workers[nw].in_depth
-                if self.program.device_of[nw] != self.rank:  # peer GPU: flag-ordered hand-off
-                    d.next_act_ready = self._view(nw, "act_ready")[0]
-                    d.next_act_ack = t["next_act_ack"].data_ptr()
-                    d.grad_ready = t["grad_ready"].data_ptr()
-                    d.grad_ack_remote = self._view(nw, "prev_grad_ack")[0]
+                d.grad_ready, d.grad_ack = t["grad_ready"].data_ptr(), t["grad_ack"].data_ptr()
             else:
                 d.dz_last = arr([x.data_ptr() for x in t["dz_last"]])
                 d.target = arr([x.data_ptr() for x in t["target"]])
                 d.loss = t["loss"].data_ptr()
             if not is_first:
-                pw = self._neighbour(b.wid, -1)
-                d.prev_grad_in = arr(self._view(pw, "grad_in"))
-                d.prev_grad_depth = self.program.workers[pw].grad_depth
-                if self.program.device_of[pw] != self.rank:
-                    d.prev_grad_ready = self._view(pw, "grad_ready")[0]
-                    d.prev_grad_ack = t["prev_grad_ack"].data_ptr()
-                    d.act_ready = t["act_ready"].data_ptr()
-                    d.act_ack_remote = self._view(pw, "next_act_ack")[0]
+                d.act_ready, d.act_ack = t["act_ready"].data_ptr(), t["act_ack"].data_ptr()
+            if d.rep > 1:
+                d.red_grad = arr([g.data_ptr() for pair in t["red_grad"] for g in pair])
+                d.red_bgrad = arr([g.data_ptr() for pair in t["red_bgrad"] for g in pair])
+                d.red_ready, d.red_done = t["red_flags"].data_ptr(), t["red_flags"].data_ptr() + 4
             d.tmp[0], d.tmp[1] = t["tmp"][0].data_ptr(), t["tmp"][1].data_ptr()
             d.err_word = t["err"].data_ptr()
-            b.desc, b.keep = d, keep
+            b.desc = d
             nat.check(L.pd_rt_add_stage(rt, ctypes.byref(d)), "pd_rt_add_stage")
         prog = np.ascontiguousarray(self.program.items_for_rank(self.rank))
         self._prog = prog
@@ -360,6 +402,8 @@ class Executor:
         evs = []
         for idx, t0, t1 in self.records():
             row = self._prog[idx]
+            if row[nat.IT_OP] == 2:  # replica reduction: part of the backward round, not a pass
+                continue
             evs.append(TraceEvent(
                 time_start=t0 * 1e-3, time_end=t1 * 1e-3, worker=int(row[nat.IT_WORKER]),
                 minibatch=int(row[nat.IT_MB]), stage=int(row[nat.IT_STAGE]),
@@ -375,6 +419,10 @@ class Executor:
         total = 0.0
         for row in self._prog:
             s = int(row[nat.IT_STAGE])
+            if row[nat.IT_OP] == 1 and plan.stages[s].replication > 1:  # one gradient per replica per round
+                w = sum(a * b for a, b in zip(m.widths[plan.stages[s].first_layer - 1: plan.stages[s].last_layer],
+                                              m.widths[plan.stages[s].first_layer: plan.stages[s].last_layer + 1]))
+                total += (plan.stages[s].replication - 1) * w * 4 / plan.stages[s].replication
             if row[nat.IT_OP] == 0 and s < plan.num_stages - 1:
                 total += m.batch * m.widths[plan.stages[s].last_layer] * m.bytes_per_elem
             if row[nat.IT_OP] == 1 and s > 0:

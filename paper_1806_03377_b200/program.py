@@ -34,6 +34,7 @@ from .ledger import Mode, VersionLedger
 from .orders import Direction, Schedule, replica_for, stage_inflight_caps
 
 F, B = Direction.FORWARD, Direction.BACKWARD
+ITEM_WIDTH = 20  # include/pd_b200.h PD_ITEM_WIDTH
 
 
 def resolve_versions(schedule: Schedule, mode) -> VersionLedger:
@@ -120,22 +121,24 @@ class Program:
     device_of: list[int]  # worker id -> rank
 
     def items_for_rank(self, rank: int) -> np.ndarray:
-        """int32 [n, 16] program for one process; dependency indices are rank-local."""
+        """int32 [n, ITEM_WIDTH] program for one process; dependency indices are rank-local."""
         mine = [it for it in self.items if self.device_of[it["worker"]] == rank]
         local_index = {it["key"]: i for i, it in enumerate(mine)}
-        out = np.full((len(mine), 16), -1, dtype=np.int32)
+        out = np.full((len(mine), ITEM_WIDTH), -1, dtype=np.int32)
         for i, it in enumerate(mine):
             dep = it["dep"]
             war = it["war"]
             dep_local = dep is not None and self.device_of[dep[0]] == rank
             war_local = war is not None and self.device_of[war[0]] == rank
+            op = 0 if it["dir"] is F else (1 if it["dir"] is B else 2)
             out[i] = [
-                0 if it["dir"] is F else 1, it["stage"], it["mb"], it["worker"], it["version"], it["wslot"],
+                op, it["stage"], it["mb"], it["worker"], it["version"], it["wslot"],
                 it["wnew"], it["act"], it["xslot"], it["gslot"], it["out"], it["block"],
                 local_index[dep] if dep_local else -1,
                 local_index[war] if war_local else -1,
                 it["mb"] if (dep is not None and not dep_local) else 0,
                 it["war_mb"] if (war is not None and not war_local) else 0,
+                it["dst"], it["src"], it["round"], 0,
             ]
         return out
 
@@ -192,10 +195,12 @@ def compile_program(schedule: Schedule, mode, *, n_blocks: int = 1, world_size: 
             wp.grad_depth = max(1, min(len(wp.mine), wp.cap))
 
     items: dict[tuple[int, int], dict] = {}
+    seqs: list[list[tuple[int, int]]] = []  # per worker: item keys in execution order
     for wp, order in zip(workers, schedule.orders):
         s = wp.stage
         rep = reps[s]
         rounds = 0
+        seq = []
         for p, it in enumerate(order):
             mb = it.minibatch_id
             j = index_in[wp.wid].get(mb)
@@ -206,9 +211,10 @@ def compile_program(schedule: Schedule, mode, *, n_blocks: int = 1, world_size: 
                 )
             v = ledger.version_used(s, mb, it.direction)
             rec = {
-                "key": (wp.wid, p), "worker": wp.wid, "stage": s, "mb": mb, "dir": it.direction, "version": v,
-                "wslot": wp.ring_slot[v], "wnew": -1, "act": j % wp.act_depth, "xslot": -1, "gslot": -1,
-                "out": -1, "block": (mb - 1) % n_blocks, "dep": None, "war": None, "war_mb": 0,
+                "key": (wp.wid, len(seq)), "worker": wp.wid, "stage": s, "mb": mb, "dir": it.direction,
+                "version": v, "wslot": wp.ring_slot[v], "wnew": -1, "act": j % wp.act_depth, "xslot": -1,
+                "gslot": -1, "out": -1, "block": (mb - 1) % n_blocks, "dep": None, "war": None, "war_mb": 0,
+                "dst": -1, "src": -1, "round": 0, "xdeps": [],
             }
             if s > 0:
                 rec["xslot"] = j % wp.in_depth
@@ -216,12 +222,14 @@ def compile_program(schedule: Schedule, mode, *, n_blocks: int = 1, world_size: 
                 rec["xslot"] = rec["block"]
             if it.direction is B:
                 rounds += 1
-                rec["wnew"] = wp.ring_slot[mb if rep == 1 else rounds * rep]
+                commit_slot = wp.ring_slot[mb if rep == 1 else rounds * rep]
                 if s < n - 1:
                     rec["gslot"] = j % wp.grad_depth
                     rec["dep"] = ("B", s + 1, mb)
+                    rec["src"] = wid_of(s + 1, mb)
                 if s > 0:
                     dst = workers[wid_of(s - 1, mb)]
+                    rec["dst"] = dst.wid
                     jd = index_in[dst.wid].get(mb)
                     if jd is None:
                         rec["out"], rec["war"] = 0, ("missing", ("F", s - 1, mb))
@@ -229,11 +237,22 @@ def compile_program(schedule: Schedule, mode, *, n_blocks: int = 1, world_size: 
                         rec["out"] = jd % dst.grad_depth
                         if jd >= dst.grad_depth:
                             rec["war"] = ("B", s - 1, dst.mine[jd - dst.grad_depth])
+                if rep == 1:
+                    rec["wnew"] = commit_slot
+                else:
+                    # replicated stage (round rule): the backward only produces this
+                    # replica's gradient; a REDUCE item sums all replicas' round-k gradients and commits
+                    rec["round"] = rounds
+                    if rounds >= 3:  # its gradient buffer (parity k % 2) was read by round k-2
+                        rec["xdeps"] = [("R", s, workers[schedule.worker_id(s, r)].mine[rounds - 3])
+                                        for r in range(rep) if rounds - 3 < len(workers[schedule.worker_id(s, r)].mine)]
             else:
                 if s > 0:
                     rec["dep"] = ("F", s - 1, mb)
+                    rec["src"] = wid_of(s - 1, mb)
                 if s < n - 1:
                     dst = workers[wid_of(s + 1, mb)]
+                    rec["dst"] = dst.wid
                     jd = index_in[dst.wid].get(mb)
                     if jd is None:
                         rec["out"], rec["war"] = 0, ("missing", ("F", s + 1, mb))
@@ -241,11 +260,22 @@ def compile_program(schedule: Schedule, mode, *, n_blocks: int = 1, world_size: 
                         rec["out"] = jd % dst.in_depth
                         if jd >= dst.in_depth:
                             rec["war"] = ("B", s + 1, dst.mine[jd - dst.in_depth])
-            items[(wp.wid, p)] = rec
+            items[rec["key"]] = rec
+            seq.append(rec["key"])
+            if it.direction is B and rep > 1:
+                red = dict(rec, key=(wp.wid, len(seq)), dir="R", wnew=commit_slot, dep=None, war=None, war_mb=0,
+                           dst=-1, out=-1,
+                           xdeps=[("B", s, workers[schedule.worker_id(s, r)].mine[rounds - 1])
+                                  for r in range(rep) if rounds - 1 < len(workers[schedule.worker_id(s, r)].mine)])
+                items[red["key"]] = red
+                seq.append(red["key"])
+        seqs.append(seq)
 
-    # resolve symbolic dependencies to (worker, pos) keys
-    where = {(("F" if it.direction is F else "B"), it.stage_index, it.minibatch_id): (wid, p)
-             for wid, order in enumerate(schedule.orders) for p, it in enumerate(order)}
+    # resolve symbolic dependencies to item keys
+    where = {}
+    for key, rec in items.items():
+        kind = "F" if rec["dir"] is F else ("B" if rec["dir"] is B else "R")
+        where[(kind, rec["stage"], rec["mb"])] = key
     for rec in items.values():
         for k in ("dep", "war"):
             sym = rec[k]
@@ -257,18 +287,19 @@ def compile_program(schedule: Schedule, mode, *, n_blocks: int = 1, world_size: 
                 if k == "war":
                     rec["war_mb"] = sym[2]
                 rec[k] = where[sym]
+        rec["xdeps"] = [where.get(x, ("missing", x)) for x in rec["xdeps"]]
 
     # ---- global topological issue order (round-robin list scheduling)
     pos = [0] * W
     done: set = set()
     order_out: list[dict] = []
-    total = sum(len(o) for o in schedule.orders)
+    total = len(items)
     while len(order_out) < total:
         progressed = False
         for w in range(W):
-            while pos[w] < len(schedule.orders[w]):
-                rec = items[(w, pos[w])]
-                deps = [d for d in (rec["dep"], rec["war"]) if d is not None]
+            while pos[w] < len(seqs[w]):
+                rec = items[seqs[w][pos[w]]]
+                deps = [d for d in (rec["dep"], rec["war"]) if d is not None] + list(rec["xdeps"])
                 if any(d[0] == "missing" or d not in done for d in deps):
                     break
                 order_out.append(rec)
@@ -276,12 +307,13 @@ def compile_program(schedule: Schedule, mode, *, n_blocks: int = 1, world_size: 
                 pos[w] += 1
                 progressed = True
         if not progressed:
-            blocked = [w for w in range(W) if pos[w] < len(schedule.orders[w])]
+            blocked = [w for w in range(W) if pos[w] < len(seqs[w])]
             w = blocked[0]
-            it = schedule.orders[w][pos[w]]
+            rec = items[seqs[w][pos[w]]]
             s, r = schedule.workers[w]
+            what = "reduce" if rec["dir"] == "R" else rec["dir"].value
             raise SimulationError(
-                f"deadlock: worker {w} (stage {s}, replica {r}) blocked waiting for {it.direction.value} of "
-                f"minibatch {it.minibatch_id} ({len(blocked)} workers blocked in total)"
+                f"deadlock: worker {w} (stage {s}, replica {r}) blocked waiting for {what} of "
+                f"minibatch {rec['mb']} ({len(blocked)} workers blocked in total)"
             )
     return Program(schedule=schedule, ledger=ledger, workers=workers, items=order_out, device_of=device_of)

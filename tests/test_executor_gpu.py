@@ -124,3 +124,36 @@ def test_executor_rejects_bad_inputs():
     ctx = pd.mlp_context(pd.mlp(64, 3, dtype="fp32"))
     with pytest.raises(pd.ValidationError):
         pd.run(cfg, ctx, model=spec)  # profile mismatch (simulator.py:153-156)
+
+
+@pytest.mark.parametrize("serial", [False, True])
+def test_replicated_stage_round_rule_parity(serial):
+    """2-1 plan on one GPU: stage 0 replicated twice (allreduce + SGD per round), stage 1 single."""
+    stages = (pd.Stage(1, 2, 2), pd.Stage(3, 4, 1))
+    plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=pd.noam_for(3, 2), machines_used=3)
+    cfg = pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=16)
+    spec = pd.mlp(256, 4, batch=128, dtype="bf16", lr=2e-3, n_blocks=4, seed=4)
+    ex = pd.Executor(cfg, model=spec)
+    try:
+        ex.set_serial(serial)
+        ex.step(trace=True)
+        res = ex.result()
+    finally:
+        ex.close()
+    X, T = pd.make_data(spec)
+    v = lambda s, mb, d: res.ledger.version_used(s, mb, pd.Direction(d))  # noqa: E731
+    want, final = mlp_train(pd.init_params(spec), X, T, spec.lr, [(1, 2), (3, 4)], v, 16, emulate="bf16",
+                            reps=[2, 1])
+    got = np.array(res.losses[:16])
+    assert np.max(np.abs(got - want) / np.abs(want)) <= 2e-2
+    # both replicas hold the same weights; compare replica 0's (worker 0) with the oracle
+    assert weight_delta_err(spec, res.weights, final) <= 1e-1
+    assert res.report is not None and res.report.steady_throughput > 0
+
+
+def test_replicated_requires_whole_rounds():
+    stages = (pd.Stage(1, 1, 2), pd.Stage(2, 2, 1))
+    plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=2, machines_used=3)
+    cfg = pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=15)
+    with pytest.raises(pd.ValidationError):
+        pd.run(cfg, model=pd.mlp(64, 2, dtype="fp32"))

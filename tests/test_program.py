@@ -73,7 +73,7 @@ def test_issue_order_is_topological_and_complete():
     sch = pd.build_schedule(plan, 20)
     prog = pd.compile_program(sch, "weight_stashing")
     arr = prog.items_for_rank(0)
-    assert arr.shape == (2 * 4 * 20, 16)
+    assert arr.shape == (2 * 4 * 20, pd.program.ITEM_WIDTH)
     for i, row in enumerate(arr):
         assert row[12] < i and row[13] < i  # dep / war issued earlier
         assert row[14] == 0 and row[15] == 0  # single process: no flag waits
@@ -131,3 +131,35 @@ def test_report_from_synthetic_trace():
     with pytest.raises(SimulationError, match="steady window"):
         plan8 = plan_from_stages([[i, i, 1] for i in range(1, 9)])
         pd.build_report(pd.SimConfig(plan=plan8, mode="weight_stashing", num_minibatches=18), trace, 8, 0.0)
+
+
+def test_replicated_program_has_reduce_rounds():
+    # 2-1 plan: stage 0 on two replicas (round rule), stage 1 unreplicated
+    plan = plan_from_stages([[1, 1, 2], [2, 2, 1]])
+    sch = pd.build_schedule(plan, 16)
+    prog = pd.compile_program(sch, "weight_stashing")
+    arr = prog.items_for_rank(0)
+    red = arr[arr[:, 0] == 2]
+    bwd0 = arr[(arr[:, 0] == 1) & (arr[:, 1] == 0)]
+    assert len(red) == len(bwd0) == 16  # one reduce per replica backward
+    assert all(r[18] >= 1 for r in red) and all(b[6] == -1 for b in bwd0)  # commit happens in the reduce
+    # every reduce is issued after both replicas' backwards of its round
+    pos = {(int(r[0]), int(r[3]), int(r[18])): i for i, r in enumerate(arr) if r[18] > 0}
+    for (op, w, k), i in pos.items():
+        if op == 2:
+            assert pos[(1, 0, k)] < i and pos[(1, 1, k)] < i
+    # forwards after round k read version 2k (replica-summed minibatches 1..2k)
+    led = prog.ledger
+    assert led.version_used(0, 5, pd.Direction.FORWARD) in (0, 2)
+    for wp in prog.workers:
+        if wp.stage == 0:
+            assert set(wp.ring_slot) >= {0, 2, 4}
+
+
+def test_replicated_protocol_world2():
+    from test_protocol_sim import World
+
+    plan = plan_from_stages([[1, 1, 2], [2, 2, 1]])
+    w = World(plan, 16, 2)
+    for epoch in (1, 2):
+        w.run_epoch(epoch)

@@ -16,69 +16,74 @@ import paper_1806_03377_b200 as pd
 from helpers_golden import plan_from_stages
 
 FIELDS = dict(op=0, stage=1, mb=2, worker=3, wslot=5, wnew=6, act=7, x=8, g=9, out=10, dep=12, war=13, rwait=14,
-              await_=15)
+              await_=15, dst=16, src=17, round=18)
 
 
 def f(row, name):
     return int(row[FIELDS[name]])
 
 
-def enqueue(rank, prog, n_stages, epoch):
-    """Per-stage op queues for one rank, mirroring pd_rt_run."""
+def enqueue(world, rank, prog, epoch):
+    """Per-worker op queues for one rank, mirroring pd_rt_run (receiver-owned flags)."""
     queues = {}
     val = lambda mb: epoch * 65536 + mb  # noqa: E731
-    last_ack = {}
+    last = {}
     for i, row in enumerate(prog):
-        s, mb, fwd = f(row, "stage"), f(row, "mb"), f(row, "op") == 0
-        q = queues.setdefault(s, [])
+        w, s, mb, op = f(row, "worker"), f(row, "stage"), f(row, "mb"), f(row, "op")
+        fwd = op == 0
+        q = queues.setdefault(w, [])
         if f(row, "dep") >= 0:
             q.append(("event", (rank, f(row, "dep"))))
         if f(row, "war") >= 0:
             q.append(("event", (rank, f(row, "war"))))
         if f(row, "rwait") > 0:
-            key = ("act_ready", s, f(row, "x")) if fwd else ("grad_ready", s, f(row, "g"))
+            key = ("act_ready", w, f(row, "x")) if fwd else ("grad_ready", w, f(row, "g"))
             q.append(("wait", key, val(f(row, "rwait"))))
         if f(row, "await_") > 0:
-            key = ("act_ack", s + 1, f(row, "out")) if fwd else ("grad_ack", s - 1, f(row, "out"))
+            key = ("act_ack" if fwd else "grad_ack", f(row, "dst"), f(row, "out"))
             q.append(("wait", key, val(f(row, "await_"))))
+        rep = world.reps[s]
+        k = f(row, "round")
+        if op == 1 and rep > 1 and k >= 3:
+            for r in range(rep):
+                q.append(("wait", ("red_done", world.first[s] + r), val(k - 2)))
+        if op == 2:
+            for r in range(rep):
+                q.append(("wait", ("red_ready", world.first[s] + r), val(k)))
         q.append(("exec", row))
         q.append(("record", (rank, i)))
         q.append(("signals", row, epoch))
-        if f(row, "out") >= 0:
-            k = ("act" if fwd else "grad", s, f(row, "out"))
-            last_ack[k] = max(last_ack.get(k, 0), mb)
-    return queues, last_ack
+        if op in (0, 1) and f(row, "out") >= 0:
+            kk = ("act_ack" if fwd else "grad_ack", f(row, "dst"), f(row, "out"))
+            last[(w, kk)] = max(last.get((w, kk), 0), mb)
+    return queues, last
 
 
 class World:
     def __init__(self, plan, K, world, mode="weight_stashing"):
         self.plan = plan
         self.n = plan.num_stages
+        self.reps = [st.replication for st in plan.stages]
         self.prog = pd.compile_program(pd.build_schedule(plan, K), mode, world_size=world)
         self.world = world
-        self.rank_of_stage = {wp.stage: self.prog.device_of[wp.wid] for wp in self.prog.workers}
+        self.first = [sum(self.reps[:s]) for s in range(self.n)]
         self.flags = {}
-        self.slots = {}  # (kind, receiver stage, slot) -> [occupant mb, consumed?]
+        self.slots = {}  # (kind, receiver worker, slot) -> [occupant mb, consumed?]
         self.events = set()
 
     def remote(self, a, b):
-        return self.rank_of_stage[a] != self.rank_of_stage[b]
+        return self.prog.device_of[a] != self.prog.device_of[b]
 
     def run_epoch(self, epoch):
         queues = {}
-        drains = {}
         for r in range(self.world):
-            q, last = enqueue(r, self.prog.items_for_rank(r), self.n, epoch)
-            for s, ops in q.items():
-                # end-of-run drain for peer-GPU outboxes (runtime.cu pd_rt_run)
-                for (kind, st, slot), mb in last.items():
-                    if st != s:
-                        continue
-                    if kind == "act" and s < self.n - 1 and self.remote(s, s + 1):
-                        ops.append(("wait", ("act_ack", s + 1, slot), epoch * 65536 + mb))
-                    if kind == "grad" and s > 0 and self.remote(s, s - 1):
-                        ops.append(("wait", ("grad_ack", s - 1, slot), epoch * 65536 + mb))
-                queues[(r, s)] = ops
+            q, last = enqueue(self, r, self.prog.items_for_rank(r), epoch)
+            for w, ops in q.items():
+                # end-of-run drain for outboxes in another process (runtime.cu pd_rt_run)
+                for (ww, key), mb in last.items():
+                    if ww == w and self.remote(w, key[1]):
+                        ops.append(("wait", key, epoch * 65536 + mb))
+                queues[(r, w)] = ops
         self.events = set()
         while any(queues.values()):
             progressed = False
@@ -101,40 +106,45 @@ class World:
             self.events.add(op[1])
         elif kind == "exec":
             row = op[1]
-            s, mb, fwd = f(row, "stage"), f(row, "mb"), f(row, "op") == 0
-            if fwd:
+            w, s, mb, o = f(row, "worker"), f(row, "stage"), f(row, "mb"), f(row, "op")
+            if o == 0:
                 if s > 0:
-                    occ = self.slots[("act", s, f(row, "x"))]
-                    assert occ[0] == mb, ("forward read wrong activation", s, mb, occ)
+                    occ = self.slots[("act", w, f(row, "x"))]
+                    assert occ[0] == mb, ("forward read wrong activation", w, mb, occ)
                 if s < self.n - 1:
-                    k = ("act", s + 1, f(row, "out"))
+                    k = ("act", f(row, "dst"), f(row, "out"))
                     assert k not in self.slots or self.slots[k][1], ("activation inbox overwritten", k, mb)
                     self.slots[k] = [mb, False]
-            else:
+            elif o == 1:
                 if s > 0:
-                    occ = self.slots[("act", s, f(row, "x"))]
+                    occ = self.slots[("act", w, f(row, "x"))]
                     assert occ[0] == mb
                     occ[1] = True  # stage input no longer needed after the backward (wgrad consumed it)
                 if s < self.n - 1:
-                    occ = self.slots[("grad", s, f(row, "g"))]
-                    assert occ[0] == mb, ("backward read wrong gradient", s, mb, occ)
+                    occ = self.slots[("grad", w, f(row, "g"))]
+                    assert occ[0] == mb, ("backward read wrong gradient", w, mb, occ)
                     occ[1] = True
                 if s > 0:
-                    k = ("grad", s - 1, f(row, "out"))
+                    k = ("grad", f(row, "dst"), f(row, "out"))
                     assert k not in self.slots or self.slots[k][1], ("gradient inbox overwritten", k, mb)
                     self.slots[k] = [mb, False]
         elif kind == "signals":
             row, epoch = op[1], op[2]
-            s, mb, fwd = f(row, "stage"), f(row, "mb"), f(row, "op") == 0
+            w, s, mb, o = f(row, "worker"), f(row, "stage"), f(row, "mb"), f(row, "op")
             v = epoch * 65536 + mb
-            if fwd and s < self.n - 1 and self.remote(s, s + 1):
-                self.flags[("act_ready", s + 1, f(row, "out"))] = v
-            if not fwd and s > 0 and self.remote(s, s - 1):
-                self.flags[("grad_ready", s - 1, f(row, "out"))] = v
-            if not fwd and s > 0 and self.remote(s, s - 1):
-                self.flags[("act_ack", s, f(row, "x"))] = v
-            if not fwd and s < self.n - 1 and self.remote(s, s + 1):
-                self.flags[("grad_ack", s, f(row, "g"))] = v
+            if o == 0 and s < self.n - 1 and self.remote(w, f(row, "dst")):
+                self.flags[("act_ready", f(row, "dst"), f(row, "out"))] = v
+            if o == 1 and s > 0 and self.remote(w, f(row, "dst")):
+                self.flags[("grad_ready", f(row, "dst"), f(row, "out"))] = v
+            if o == 1:  # receiver-owned acks (the runtime signals them when a producer is remote)
+                if s > 0:
+                    self.flags[("act_ack", w, f(row, "x"))] = v
+                if s < self.n - 1:
+                    self.flags[("grad_ack", w, f(row, "g"))] = v
+                if self.reps[s] > 1:
+                    self.flags[("red_ready", w)] = epoch * 65536 + f(row, "round")
+            if o == 2:
+                self.flags[("red_done", w)] = epoch * 65536 + f(row, "round")
 
 
 @pytest.mark.parametrize("n,world,K", [(4, 2, 20), (8, 2, 25), (8, 4, 25), (8, 8, 25), (3, 2, 16), (4, 4, 14)])
@@ -192,3 +202,14 @@ def test_world2_gloo_exchange_of_programs():
                 src = (r[1] - 1, r[2], 0) if r[0] == 0 else (r[1] + 1, r[2], 1)
                 assert src in produced
     assert sum(len(p) for p in parts) == 2 * 4 * 20
+
+
+@pytest.mark.parametrize("shape,world,K", [([[1, 1, 2], [2, 2, 1]], 1, 16), ([[1, 1, 2], [2, 2, 1]], 3, 16),
+                                           ([[1, 1, 1], [2, 2, 2], [3, 3, 1]], 4, 24),
+                                           ([[1, 13, 7], [14, 16, 1]], 8, 42)])
+def test_protocol_replicated_stages(shape, world, K):
+    """Replicated stages: per-round gradient-ready / reduction-done flags, parity buffers (7-1 at 8)."""
+    plan = plan_from_stages(shape)
+    w = World(plan, K, world)
+    for epoch in (1, 2):
+        w.run_epoch(epoch)
