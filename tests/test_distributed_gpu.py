@@ -13,14 +13,16 @@ pytestmark = pytest.mark.gpu
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("stages", [4, 3])
-def test_two_process_pipeline_matches_oracle(stages):
-    env = dict(os.environ, PD_STAGES=str(stages), PD_DIST_BACKEND="gloo")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+@pytest.mark.parametrize("reps,nproc", [("1-1-1-1", 2), ("1-1-1", 2), ("2-1", 3), ("1-2-1", 4)])
+def test_multi_process_pipeline_matches_oracle(reps, nproc):
+    """Straight plans over 2 processes; replicated plans with the replicas in different processes
+    (peer-mapped gradient reads in the fused allreduce+SGD, remote round flags)."""
+    env = dict(os.environ, PD_REPS=reps, PD_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", "--master-port=29517", os.path.join(REPO, "tools", "dist_check.py")]
     out = subprocess.run(cmd, cwd=REPO, env=env, capture_output=True, text=True, timeout=600)
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert out.returncode == 0 and lines, out.stdout[-3000:] + out.stderr[-3000:]
     res = json.loads(lines[-1])
-    assert res["world"] == 2
+    assert res["world"] == nproc
     assert res["ok"], res

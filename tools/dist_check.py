@@ -19,10 +19,12 @@ def main():
     backend = os.environ.get("PD_DIST_BACKEND", "gloo")
     torch.distributed.init_process_group(backend)
     rank = torch.distributed.get_rank()
-    n_stages = int(os.environ.get("PD_STAGES", "4"))
+    reps = [int(x) for x in os.environ.get("PD_REPS", "1-1-1-1").split("-")]  # replication per stage
+    n_stages = len(reps)
     K = 20
-    stages = tuple(pd.Stage(2 * s + 1, 2 * s + 2, 1) for s in range(n_stages))
-    plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=n_stages, machines_used=n_stages)
+    stages = tuple(pd.Stage(2 * s + 1, 2 * s + 2, r) for s, r in enumerate(reps))
+    used = sum(reps)
+    plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=pd.noam_for(used, reps[0]), machines_used=used)
     cfg = pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=K)
     spec = pd.mlp(256, 2 * n_stages, batch=128, dtype="bf16", lr=2e-3, n_blocks=4, seed=3)
     ex = pd.Executor(cfg, model=spec)
@@ -41,11 +43,11 @@ def main():
         P = pd.init_params(spec)
         worst = 0.0
         for res in runs:
-            want, P = mlp_train(P, X, T, spec.lr, bounds, v, K, emulate="bf16")
+            want, P = mlp_train(P, X, T, spec.lr, bounds, v, K, emulate="bf16", reps=reps)
             got = np.array(res.losses[:K])
             worst = max(worst, float(np.max(np.abs(got - want) / np.abs(want))))
         rep = runs[-1].report
-        print(json.dumps({"ok": bool(worst <= 3e-2), "max_rel_loss_err": worst, "world": ex.world,
+        print(json.dumps({"ok": bool(worst <= 3e-2), "max_rel_loss_err": worst, "world": ex.world, "reps": reps,
                           "device_of_worker": runs[-1].extras["device_of_worker"],
                           "bubble": runs[-1].extras["bubble_fraction"],
                           "steady_minibatches_per_s": rep.steady_throughput if rep else None}), flush=True)
