@@ -200,7 +200,7 @@ def run_ours(args, rank, world):
 
     import paper_1806_03377_b200 as pd
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     dev = torch.cuda.current_device()
     per = args.layers // args.stages
     stages = tuple(pd.Stage(s * per + 1, (s + 1) * per, 1) for s in range(args.stages))
@@ -289,7 +289,9 @@ def run_ours(args, rank, world):
     tpath = os.path.join(REPO, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
-            traffic = json.load(fh).get(dom_name)
+            tr = json.load(fh)
+        if tr.get("batch") == args.batch and tr.get("width") == args.width:  # captured at this shape
+            traffic = tr.get(dom_name)
     per_class = {k: {"launches": v["launches"], "avg_ms": round(v["avg_ms"], 4),
                      "tflops": round(v["flops_per_launch"] / (v["avg_ms"] * 1e-3) / 1e12, 1),
                      "frac_of_sustained_peak": round(v["flops_per_launch"] / (v["avg_ms"] * 1e-3) / 1e12 / peak, 3)}
@@ -331,8 +333,11 @@ def main():
     if world > 1:
         import torch
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        torch.distributed.init_process_group("nccl")
+        ngpu = torch.cuda.device_count()
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % ngpu)
+        # host plumbing only (IPC handle exchange, barriers, max-over-ranks); the data path is
+        # peer stores + flags.  Several ranks per GPU (functional testing) cannot use NCCL.
+        torch.distributed.init_process_group("nccl" if ngpu >= world else "gloo")
     args.gpus = world
     run_ours(args, rank, world)
     if world > 1:
