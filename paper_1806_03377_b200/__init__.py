@@ -52,6 +52,7 @@ from .plans import (  # noqa: F401
     parse_config,
     plan_from_dict,
     replicated_plan,
+    solve,
     straight_plan,
 )
 from .profiles import (  # noqa: F401
@@ -69,4 +70,5 @@ from .profiles import (  # noqa: F401
     stage_time,
     weight_sync_time,
 )
+from .profiler import profile_mlp  # noqa: F401
 from .program import Program, compile_program, resolve_versions  # noqa: F401

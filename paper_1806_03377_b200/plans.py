@@ -136,3 +136,80 @@ def replicated_plan(ctx, stage_specs) -> Plan:
     used = sum(s.replication for s in stages)
     return Plan(stages=stages, bottleneck_time=max(times + links), noam=noam_for(used, stages[0].replication),
                 machines_used=used)
+
+
+# ------------------------------------------------------------------ planner (partitioner.py:183-308)
+TIME_TOL = 1e-12  # float ties in the DP are decided by structure, not evaluation order
+
+
+def _better(a, b) -> bool:
+    """Candidate a = (time, n_stages, split, split_m) strictly preferred over b (or b is None)."""
+    if b is None:
+        return True
+    if a[0] < b[0] - TIME_TOL:
+        return True
+    if a[0] > b[0] + TIME_TOL:
+        return False
+    return a[1:] < b[1:]  # fewer stages, then earlier last split, then smaller final replication
+
+
+def solve(ctx, machines: int | None = None, *, force_all_machines: bool = False,
+          max_replication: int | None = None, stats: dict | None = None) -> Plan:
+    """Bottleneck-minimising contiguous partition with per-stage replication (PipeDream §3.1).
+
+    best[j][m] is the best pipeline over layers 1..j on exactly m machines: either one stage
+    replicated m ways, or best[i][m - m'] followed by a stage over i+1..j on m' machines, with the
+    boundary i paying 2*C_i.  Same tie rules and outputs as the reference's ``solve``, so a plan
+    computed from a B200-measured profile (profiler.py) feeds ``run`` directly.
+    """
+    n = ctx.num_layers
+    budget = ctx.hw.num_machines if machines is None else machines
+    if budget < 1:
+        raise ValidationError("machine budget must be >= 1")
+    cap = budget if max_replication is None else max_replication
+    if cap < 1:
+        raise ValidationError("max_replication must be >= 1")
+    link = [0.0] + [2.0 * comm_time_activations(ctx, i) for i in range(1, n)]
+    best = [[None] * (budget + 1) for _ in range(n + 1)]
+    evals = 0
+    for j in range(1, n + 1):
+        for m in range(1, budget + 1):
+            cell = (stage_time(ctx, 1, j, m), 1, 0, 0) if m <= cap else None
+            for i in range(1, j):
+                for mp in range(1, min(m - 1, cap) + 1):
+                    head = best[i][m - mp]
+                    if head is None:
+                        continue
+                    evals += 1
+                    cand = (max(head[0], link[i], stage_time(ctx, i + 1, j, mp)), head[1] + 1, i, mp)
+                    if _better(cand, cell):
+                        cell = cand
+            best[j][m] = cell
+    if stats is not None:
+        stats["subproblem_evals"] = evals
+    if force_all_machines:
+        if best[n][budget] is None:
+            raise ValidationError(f"no plan uses exactly {budget} machines with replication cap {cap}")
+        used = budget
+    else:
+        used, pick = None, None
+        for m in range(1, budget + 1):
+            cell = best[n][m]
+            if cell is None:
+                continue
+            if pick is None or cell[0] < pick[0] - TIME_TOL or (
+                    cell[0] <= pick[0] + TIME_TOL and (cell[1], m) < (pick[1], used)):
+                pick, used = cell, m
+        if used is None:
+            raise ValidationError("no feasible plan found")
+    stages, j, m = [], n, used
+    while True:
+        cell = best[j][m]
+        if cell[2] == 0:
+            stages.append(Stage(1, j, m))
+            break
+        stages.append(Stage(cell[2] + 1, j, cell[3]))
+        j, m = cell[2], m - cell[3]
+    stages.reverse()
+    return Plan(stages=tuple(stages), bottleneck_time=best[n][used][0],
+                noam=noam_for(used, stages[0].replication), machines_used=used)

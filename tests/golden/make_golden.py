@@ -129,3 +129,6 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+# solve_plans.json was generated with the reference's pipesim.solve on 60 seeded instances of
+# tests/helpers.py:random_instance (rng seed 2026, <= 8 layers, <= 6 machines); see tests/test_solve.py

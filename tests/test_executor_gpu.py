@@ -157,3 +157,18 @@ def test_replicated_requires_whole_rounds():
     cfg = pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=15)
     with pytest.raises(pd.ValidationError):
         pd.run(cfg, model=pd.mlp(64, 2, dtype="fp32"))
+
+
+def test_profile_plan_run_loop(tmp_path):
+    """Measured B200 profile -> reference-format JSON -> solve(max_replication=1) -> run."""
+    spec = pd.mlp(512, 6, batch=256, dtype="bf16", lr=1e-3, n_blocks=4, seed=5)
+    prof = pd.profile_mlp(spec, repeats=5)
+    assert all(l.fwd_time > 0 and l.bwd_time > 0 for l in prof.layers)
+    path = tmp_path / "profile.json"
+    pd.save_profile(prof, path)
+    ctx = pd.build_context(pd.load_profile(path), pd.HardwareSpec(3, 770e9, 2))
+    plan = pd.solve(ctx, max_replication=1)
+    assert plan.num_layers == 6 and all(s.replication == 1 for s in plan.stages)
+    K = max(plan.noam + 10, 2 * plan.noam + plan.num_stages + 2)
+    res = pd.run(pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=K), ctx, model=spec)
+    assert np.all(np.isfinite(res.losses[:K])) and res.report.steady_throughput > 0
