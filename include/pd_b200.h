@@ -85,6 +85,8 @@ int pd_cast(int dtype, const float* src, void* out, int64_t n, void* stream);
  * pointer when the consumer is on another GPU); these flags order them.
  * signal: system-scope release store of `value`; wait: acquire-poll until *flag >= value. */
 int pd_flag_signal(int* flag, int value, void* stream);
+/* SM-issued 16-byte-vector copy (dst may be a peer-mapped inbox): the store half of a hand-off. */
+int pd_copy(void* dst, const void* src, int64_t bytes, void* stream);
 int pd_flag_wait(const int* flag, int value, int* err_word, void* stream);
 /* CUDA IPC so a peer process can map an inbox: handle is 64 opaque bytes naming the whole
  * allocation that contains dev_ptr; *offset_out is dev_ptr's byte offset inside it. */

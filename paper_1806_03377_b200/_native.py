@@ -25,7 +25,7 @@ ITEM_WIDTH = 20
 # Symbols include/pd_b200.h declares; tests check every one is exported.
 EXPORTED = (
     "pd_abi_version", "pd_last_error", "pd_device_sm_count", "pd_gemm", "pd_bias_sgd", "pd_sgd_update", "pd_cast", "pd_allreduce_sgd", "pd_bias_grad",
-    "pd_flag_signal", "pd_flag_wait", "pd_ipc_get_handle", "pd_ipc_open", "pd_ipc_close",
+    "pd_flag_signal", "pd_flag_wait", "pd_copy", "pd_ipc_get_handle", "pd_ipc_open", "pd_ipc_close",
     "pd_enable_peer_access", "pd_rt_create", "pd_rt_add_stage", "pd_rt_add_view", "pd_rt_load_program", "pd_rt_run",
     "pd_rt_records", "pd_rt_set_serial", "pd_rt_kernel_timing", "pd_rt_kernel_stats", "pd_rt_launch_count", "pd_rt_destroy",
 )
@@ -89,6 +89,7 @@ def lib() -> ctypes.CDLL:
         L.pd_sgd_update.argtypes = [c_int, c_void_p, c_void_p, c_void_p, c_int64, c_float, c_void_p]
         L.pd_cast.argtypes = [c_int, c_void_p, c_void_p, c_int64, c_void_p]
         L.pd_flag_signal.argtypes = [c_void_p, c_int, c_void_p]
+        L.pd_copy.argtypes = [c_void_p, c_void_p, c_int64, c_void_p]
         L.pd_flag_wait.argtypes = [c_void_p, c_int, c_void_p, c_void_p]
         L.pd_ipc_get_handle.argtypes = [c_void_p, c_void_p, POINTER(c_int64)]
         L.pd_ipc_open.argtypes = [c_void_p, POINTER(c_void_p)]

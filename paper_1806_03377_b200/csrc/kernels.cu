@@ -181,6 +181,26 @@ int cast_f32(int dtype, const float* src, void* out, int64_t n, cudaStream_t st)
   return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "cast: %s", cudaGetErrorString(e));
 }
 
+// ---------------------------------------------------------------- payload copy (P2P microbench)
+__global__ void __launch_bounds__(256) k_copy16(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+int copy_bytes(void* dst, const void* src, int64_t bytes, cudaStream_t st) {
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | (uintptr_t)bytes) & 15)
+    return set_error(PD_ERR_INVALID, "copy: 16-byte alignment required");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n16 = bytes / 16;
+  const int64_t want = (n16 + 255) / 256;
+  const int grid = (int)(want < sms * 4 ? (want > 0 ? want : 1) : sms * 4);
+  k_copy16<<<grid, 256, 0, st>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "copy: %s", cudaGetErrorString(e));
+}
+
 // ---------------------------------------------------------------- flags
 __global__ void k_flag_signal(int* flag, int v) {
   __threadfence_system();
@@ -254,6 +274,10 @@ int pd_bias_grad(int dtype, const void* dz, int rows, int cols, int64_t ld, floa
 
 int pd_cast(int dtype, const float* src, void* out, int64_t n, void* stream) {
   return cast_f32(dtype, src, out, n, static_cast<cudaStream_t>(stream));
+}
+
+int pd_copy(void* dst, const void* src, int64_t bytes, void* stream) {
+  return copy_bytes(dst, src, bytes, static_cast<cudaStream_t>(stream));
 }
 
 int pd_flag_signal(int* flag, int value, void* stream) {
