@@ -79,6 +79,40 @@ int pd_bias_grad(int dtype, const void* dz, int rows, int cols, int64_t ld, floa
 /* out[i] = cast(src[i]) (fp32 -> dtype). */
 int pd_cast(int dtype, const float* src, void* out, int64_t n, void* stream);
 
+/* ------------------------------------------------------------------ convolutional stages
+ * VGG-style stages (configs[2]): 3x3 / stride 1 / pad 1 convolutions over NHWC bf16
+ * activations with weights stored tap-major, Wt[9*c_in][c_out] (row = (r*3+s)*c_in + c), as
+ * implicit GEMMs on the tcgen05 kernel whose activation operand is loaded by TMA im2col
+ * (the zero-filled halo is the padding; no im2col matrix is written).
+ *   PD_CONV_FWD  : act = X [n,h,w,c_in],  other = Wt;  ep STORE  -> out Y [n,h,w,c_out] (+bias, ReLU)
+ *   PD_CONV_DGRAD: act = dY [n,h,w,c_out], other = Wt; ep MASK   -> out dX [n,h,w,c_in] * (X > 0)
+ *   PD_CONV_WGRAD: act = X, other = dY;  ep GRADF32 -> out = split-K partials [splits][9*c_in][c_out]
+ *                  (ldo = c_out; splits from pd_splitk_plan(9*c_in, c_out, n*h*w)), summed by pd_reduce_sgd
+ *   PD_GEMM_WGRAD_SPLITK: act = cols [n*h*w, c_in] (the im2col'ed first layer), other = dY;
+ *                  partials [splits][c_in][c_out] (pd_splitk_plan(c_in, c_out, n*h*w))
+ * These replace the reference's per-stage numeric step (semantics.py:119-144) for conv layers. */
+enum pd_conv_pass { PD_CONV_FWD = 0, PD_CONV_DGRAD = 1, PD_CONV_WGRAD = 2, PD_GEMM_WGRAD_SPLITK = 3 };
+int pd_conv3x3(int pass, const void* act, const void* other, int n, int h, int w, int c_in, int c_out,
+               const pd_epilogue* ep, void* stream);
+int pd_splitk_plan(int M, int N, int K, int* splits);
+/* 2x2/stride-2 max pool over NHWC bf16; argmax[n,h/2,w/2,c] = window index (dh*2+dw), first max wins. */
+int pd_maxpool2(const void* x, void* y, uint8_t* argmax, int n, int h, int w, int c, void* stream);
+int pd_maxpool2_bwd(const void* dy, const uint8_t* argmax, void* dx, int n, int h, int w, int c, void* stream);
+/* First-layer im2col: cols[pix][(r*3+s)*c + ch] for k < 9c, zero up to kpad. */
+int pd_im2col3(const void* x, void* cols, int n, int h, int w, int c, int kpad, void* stream);
+/* g[i] = sum_{s<splits} part[s*stride+i] (fixed order); grad ? grad[i]=g : (master[i]-=lr*g; out[i]=cast(master[i])). */
+int pd_reduce_sgd(int dtype, const float* part, int splits, int64_t stride, int64_t n, float* grad, float* master,
+                  void* out, float lr, void* stream);
+/* Bias gradient of a tall [rows, c] bf16 gradient (conv layers): two-pass column sum through
+ * part[pd_colsum_blocks(rows,c) * c], then grad or SGD as pd_reduce_sgd. */
+int pd_colsum_blocks(int64_t rows, int c);
+int pd_bias_grad_tall(const void* dz, int64_t rows, int c, float* part, float* grad, float* master, float* out,
+                      float lr, void* stream);
+/* Softmax cross-entropy over fp32 logits [b, v] (row pitch ldz), int32 labels:
+ * loss += mean_r (logsumexp_r - z[r,label_r]);  dz = (softmax - onehot) / b (bf16). */
+int pd_softmax_ce(const float* logits, int64_t ldz, const int* labels, int b, int v, void* dz, int64_t ldd,
+                  float* loss, void* stream);
+
 /* ------------------------------------------------------------------ P2P transport
  * Replaces _Engine._send (simulator.py:284-292): payloads are stored by the
  * producing GEMM epilogue straight into the consumer's inbox slot (a peer-mapped
@@ -88,6 +122,8 @@ int pd_flag_signal(int* flag, int value, void* stream);
 /* SM-issued 16-byte-vector copy (dst may be a peer-mapped inbox): the store half of a hand-off. */
 int pd_copy(void* dst, const void* src, int64_t bytes, void* stream);
 int pd_flag_wait(const int* flag, int value, int* err_word, void* stream);
+/* Copy-engine device->device (or peer-mapped) copy: the comparison leg of the P2P microbench. */
+int pd_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
 /* CUDA IPC so a peer process can map an inbox: handle is 64 opaque bytes naming the whole
  * allocation that contains dev_ptr; *offset_out is dev_ptr's byte offset inside it. */
 int pd_ipc_get_handle(const void* dev_ptr, void* handle_out64, int64_t* offset_out);

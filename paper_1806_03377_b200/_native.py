@@ -28,7 +28,10 @@ EXPORTED = (
     "pd_flag_signal", "pd_flag_wait", "pd_copy", "pd_ipc_get_handle", "pd_ipc_open", "pd_ipc_close",
     "pd_enable_peer_access", "pd_rt_create", "pd_rt_add_stage", "pd_rt_add_view", "pd_rt_load_program", "pd_rt_run",
     "pd_rt_records", "pd_rt_set_serial", "pd_rt_kernel_timing", "pd_rt_kernel_stats", "pd_rt_launch_count", "pd_rt_destroy",
+    "pd_conv3x3", "pd_splitk_plan", "pd_maxpool2", "pd_maxpool2_bwd", "pd_im2col3", "pd_reduce_sgd",
+    "pd_colsum_blocks", "pd_bias_grad_tall", "pd_softmax_ce", "pd_memcpy_async",
 )
+PD_CONV_FWD, PD_CONV_DGRAD, PD_CONV_WGRAD, PD_GEMM_WGRAD_SPLITK = range(4)
 
 
 class Epilogue(Structure):
@@ -108,6 +111,19 @@ def lib() -> ctypes.CDLL:
         L.pd_rt_kernel_stats.argtypes = [c_void_p, POINTER(c_double)]
         L.pd_rt_launch_count.argtypes = [c_void_p, POINTER(c_int64)]
         L.pd_device_sm_count.argtypes = [c_int, POINTER(c_int)]
+        L.pd_conv3x3.argtypes = [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, POINTER(Epilogue),
+                                 c_void_p]
+        L.pd_splitk_plan.argtypes = [c_int, c_int, c_int, POINTER(c_int)]
+        L.pd_maxpool2.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p]
+        L.pd_maxpool2_bwd.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p]
+        L.pd_im2col3.argtypes = [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p]
+        L.pd_reduce_sgd.argtypes = [c_int, c_void_p, c_int, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_float,
+                                    c_void_p]
+        L.pd_colsum_blocks.argtypes = [c_int64, c_int]
+        L.pd_bias_grad_tall.argtypes = [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_float,
+                                        c_void_p]
+        L.pd_softmax_ce.argtypes = [c_void_p, c_int64, c_void_p, c_int, c_int, c_void_p, c_int64, c_void_p, c_void_p]
+        L.pd_memcpy_async.argtypes = [c_void_p, c_void_p, c_int64, c_void_p]
         _lib = L
     return _lib
 
@@ -192,3 +208,27 @@ def ipc_import(handle: bytes, offset: int) -> int:
         check(lib().pd_ipc_open(buf, ctypes.byref(out)), "pd_ipc_open")
         base = _ipc_bases[handle] = int(out.value)
     return base + offset
+
+
+def _epi(kind, out=None, ldo=0, bias=None, relu=False, mask=None, ldm=0, loss=None, master=None, ldw=0, lr=0.0):
+    return Epilogue(kind=kind, out=ptr(out), ldo=ldo, bias=ptr(bias), relu=int(bool(relu)), mask=ptr(mask), ldm=ldm,
+                    target=0, ldt=0, scale=1.0, loss=ptr(loss), master=ptr(master), ldw=ldw, lr=lr)
+
+
+def splitk_plan(M: int, N: int, K: int) -> int:
+    s = c_int(0)
+    check(lib().pd_splitk_plan(M, N, K, ctypes.byref(s)), "pd_splitk_plan")
+    return int(s.value)
+
+
+def conv3x3(pass_: int, act, other, n: int, h: int, w: int, c_in: int, c_out: int, *, out, bias=None,
+            relu=False, mask=None, stream=None) -> None:
+    """One implicit-GEMM 3x3 convolution pass (include/pd_b200.h PD_CONV_*) on torch tensors."""
+    if pass_ == PD_CONV_FWD:
+        ep = _epi(EPI_STORE, out, c_out, bias=bias, relu=relu)
+    elif pass_ == PD_CONV_DGRAD:
+        ep = _epi(EPI_MASK, out, c_in, mask=mask, ldm=c_in)
+    else:
+        ep = _epi(EPI_GRADF32, out, c_out)
+    check(lib().pd_conv3x3(pass_, ptr(act), ptr(other), n, h, w, c_in, c_out, ctypes.byref(ep),
+                           stream_ptr(stream)), "pd_conv3x3")

@@ -35,6 +35,23 @@ struct EpiArgs {
   float lr;             // SGD
 };
 
+// Operand sources of the tcgen05 GEMM (gemm.cu).  SRC_2D: both operands are 2-D row-major
+// matrices.  The three implicit-GEMM 3x3/stride-1/pad-1 convolution passes (NHWC activations,
+// weights stored tap-major as Wt[9*Cin][Cout]) load their activation operand with TMA im2col:
+//   SRC_CONV_FWD  : Y[pix,Cout]   = sum_{tap,c} X(pix+tap)[c] * Wt[tap*Cin+c][Cout]
+//   SRC_CONV_DGRAD: dX[pix,Cin]   = sum_{tap,k} dY(pix+flip(tap))[k] * Wt[(8-tap)*Cin+c][k]
+//   SRC_CONV_WGRAD: dWt[tap*Cin+c][Cout] = sum_pix X(pix+tap)[c] * dY[pix][Cout]   (split-K)
+enum GemmSrc : int { SRC_2D = 0, SRC_CONV_FWD = 1, SRC_CONV_DGRAD = 2, SRC_CONV_WGRAD = 3 };
+
+struct ConvArgs {
+  int H, W;          // spatial size of the im2col'ed activation (input == output size)
+  int C;             // its channels (multiple of 64)
+  int brows;         // DGRAD: weight rows per tap (= Cin)
+  int kb_per;        // k-blocks per K split
+  int splits;        // K splits (>= 1); split s writes out + s*split_stride (EPI_GRADF32)
+  int64_t split_stride;
+};
+
 template <typename T> __device__ __forceinline__ float to_f(T x);
 template <> __device__ __forceinline__ float to_f<float>(float x) { return x; }
 template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) {

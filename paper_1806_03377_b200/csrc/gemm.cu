@@ -69,10 +69,10 @@ struct TcCfg {
   static_assert(!B_MN || B_ROWS % 64 == 0, "MN-major B needs whole 64-wide atoms per CTA");
 };
 
-template <int CG, int BN, bool A_MN, bool B_MN, int KIND>
+template <int CG, int BN, bool A_MN, bool B_MN, int KIND, int SRC = SRC_2D>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ CUtensorMap tmW, int M, int N, int K, EpiArgs ep) {
+              const __grid_constant__ CUtensorMap tmW, int M, int N, int K, EpiArgs ep, ConvArgs cv) {
   using C = TcCfg<CG, BN, B_MN, KIND>;
   constexpr int UM = TC_BM * CG;  // tile rows per unit (CTA or CTA pair)
   extern __shared__ uint8_t smem_raw[];
@@ -95,6 +95,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int num_kb = (K + TC_BK - 1) / TC_BK;
+  // split-K: work unit u covers tile u % tiles over k-blocks [kb_lo(u), kb_hi(u))
+  const int work = tiles * cv.splits;
+  auto kb_lo = [&](int u) { return (u / tiles) * cv.kb_per; };
+  auto kb_hi = [&](int u) { const int e = (u / tiles + 1) * cv.kb_per; return e < num_kb ? e : num_kb; };
+  const int HW = cv.H * cv.W;
+  // bounding-box coordinate of output pixel `pix` for the im2col loads (lower corner -1, -1)
+  auto pix_coord = [&](int pix, int& w, int& h, int& n) {
+    n = pix / HW;
+    const int rem = pix - n * HW;
+    h = rem / cv.W;
+    w = rem - h * cv.W - 1;
+    h -= 1;
+  };
   // Rasterisation.  Forward/dgrad stream a large B (the weights) through L2, so co-resident
   // tiles share B (m fastest).  The wgrad+SGD operands (dZ, X) are L2-resident and its cost is
   // the fp32 master read-modify-write, so co-resident tiles walk along the rows (n fastest) and
@@ -128,10 +141,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint64_t keep = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = unit; t < tiles; t += units) {
+      for (int u = unit; u < work; u += units) {
+        const int t = u % tiles;
         const int m0 = tile_m(t) * UM + TC_BM * cta;
         const int n0 = tile_n(t) * BN + C::B_ROWS * cta;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        int aw = 0, ah = 0, an = 0;
+        if constexpr (SRC == SRC_CONV_FWD || SRC == SRC_CONV_DGRAD) pix_coord(m0, aw, ah, an);
+        const int kb_end = kb_hi(u);
+        for (int kb = kb_lo(u); kb < kb_end; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], CG * C::STAGE_BYTES);
           else mbar_arrive_cluster_relaxed(&full[stage], 0);
@@ -143,17 +160,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if constexpr (CG == 2) tma_load_2d_2sm(dst, map, &full[stage], c0, c1, keep);
             else tma_load_2d_hint(dst, map, &full[stage], c0, c1, keep);
           };
-          if constexpr (A_MN) {
+          if constexpr (SRC == SRC_CONV_FWD || SRC == SRC_CONV_DGRAD) {
+            // 128 output pixels x 64 channels of tap `tap` (dgrad reads dY at the flipped offset)
+            const int tap = k0 / cv.C, c0 = k0 - tap * cv.C;
+            tma_load_im2col_4d(a_dst, &tmA, &full[stage], c0, aw, ah, an, (uint16_t)(tap % 3), (uint16_t)(tap / 3));
+            if constexpr (SRC == SRC_CONV_DGRAD) {
+              load(b_dst, &tmB, c0, (8 - tap) * cv.brows + n0);  // Wt rows of the mirrored tap
+            } else {
 #pragma unroll
-            for (int i = 0; i < TC_BM / 64; ++i) load(a_dst + i * 8192, &tmA, m0 + 64 * i, k0);
-          } else {
-            load(a_dst, &tmA, k0, m0);
-          }
-          if constexpr (B_MN) {
+              for (int i = 0; i < C::BNL / 64; ++i) load(b_dst + i * 8192, &tmB, n0 + 64 * i, k0);
+            }
+          } else if constexpr (SRC == SRC_CONV_WGRAD) {
+            // A(m = tap*C + c, k = pixel): two 64-channel x 64-pixel im2col atoms (MN-major)
+            int pw, ph, pn;
+            pix_coord(k0, pw, ph, pn);
+#pragma unroll
+            for (int i = 0; i < TC_BM / 64; ++i) {
+              const int mm = m0 + 64 * i;
+              int tap = mm / cv.C;
+              tap = tap < 8 ? tap : 8;  // rows past 9*C are clipped by the epilogue
+              const int c0 = mm - tap * cv.C < cv.C ? mm - tap * cv.C : 0;
+              tma_load_im2col_4d(a_dst + i * 8192, &tmA, &full[stage], c0, pw, ph, pn, (uint16_t)(tap % 3),
+                                 (uint16_t)(tap / 3));
+            }
 #pragma unroll
             for (int i = 0; i < C::BNL / 64; ++i) load(b_dst + i * 8192, &tmB, n0 + 64 * i, k0);
           } else {
-            load(b_dst, &tmB, k0, n0);
+            if constexpr (A_MN) {
+#pragma unroll
+              for (int i = 0; i < TC_BM / 64; ++i) load(a_dst + i * 8192, &tmA, m0 + 64 * i, k0);
+            } else {
+              load(a_dst, &tmA, k0, m0);
+            }
+            if constexpr (B_MN) {
+#pragma unroll
+              for (int i = 0; i < C::BNL / 64; ++i) load(b_dst + i * 8192, &tmB, n0 + 64 * i, k0);
+            } else {
+              load(b_dst, &tmB, k0, n0);
+            }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -172,11 +216,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = unit; t < tiles; t += units) {
+      for (int u = unit; u < work; u += units) {
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * TC_ACC_STRIDE;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb_begin = kb_lo(u), kb_end = kb_hi(u);
+        for (int kb = kb_begin; kb < kb_end; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
@@ -185,8 +230,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int k = 0; k < TC_BK / 16; ++k) {
             uint64_t ad = make_sw128_desc(a_addr + k * A_KSTEP, A_LBO, A_SBO);
             uint64_t bd = make_sw128_desc(b_addr + k * B_KSTEP, B_LBO, B_SBO);
-            if constexpr (CG == 2) umma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0);
-            else umma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+            if constexpr (CG == 2) umma_bf16_2sm(d, ad, bd, idesc, (kb != kb_begin) | (k != 0));
+            else umma_bf16(d, ad, bd, idesc, (kb != kb_begin) | (k != 0));
           }
           if constexpr (CG == 2) umma_commit_2sm_mc(&empty[stage]); else umma_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -215,7 +260,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t bar_phase[2] = {0, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = unit; t < tiles; t += units) {
+    for (int u = unit; u < work; u += units) {
+      const int t = u % tiles;
       const int m0 = tile_m(t) * UM + TC_BM * cta;
       const int n0 = tile_n(t) * BN;
       const int row0 = m0 + 32 * q;
@@ -301,7 +347,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint64_t stream = l2_policy_evict_first();  // master / ring are touched once per GEMM
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = unit; t < tiles; t += units) {
+    for (int u = unit; u < work; u += units) {
+      const int t = u % tiles;
       const int m0 = tile_m(t) * UM + TC_BM * cta;
       const int n0 = tile_n(t) * BN;
       const int64_t row0 = m0 + 32 * q;
@@ -346,10 +393,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 po += ep.ldo;
               }
             } else {
-              float* po = static_cast<float*>(ep.out) + row0 * ep.ldo + col;
+              // fp32 result (+ per-column bias: logits); split-K partial s goes to out + s*split_stride
+              float* po = static_cast<float*>(ep.out) + (u / tiles) * cv.split_stride + row0 * ep.ldo + col;
+              const float bcol = ep.bias ? ep.bias[col] : 0.f;
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
-                if (i < rows) *po = stg[i * 33 + lane];
+                if (i < rows) *po = stg[i * 33 + lane] + bcol;
                 po += ep.ldo;
               }
             }
@@ -377,7 +426,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     float lsum = 0.f;
-    for (int t = unit; t < tiles; t += units) {
+    for (int u = unit; u < work; u += units) {
+      const int t = u % tiles;
       const int m0 = tile_m(t) * UM + TC_BM * cta;
       const int n0 = tile_n(t) * BN;
       const int64_t r = m0 + 32 * q + lane_id();
@@ -519,16 +569,58 @@ static int num_sms() {
   return n;
 }
 
-template <int CG, int BN, bool A_MN, bool B_MN, int KIND>
+// 4-D im2col map over an NHWC bf16 activation [n, H, W, C] for 3x3 / stride 1 / pad 1: bounding
+// box corners (-1, -1) .. (-1, -1) relative to the extent, 64 channels (128 B, swizzled) per pixel,
+// `pixels` pixels per load.
+static PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col_fn() {
+  static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(p);
+  });
+  return fn;
+}
+
+static int make_im2col_map(CUtensorMap* map, const void* ptr, int n, int H, int W, int C, int pixels) {
+  auto fn = encode_im2col_fn();
+  if (!fn) return set_error(PD_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable");
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  int lower[2] = {-1, -1}, upper[2] = {-1, -1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, lower, upper, 64,
+                  (cuuint32_t)pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(PD_ERR_CUDA, "cuTensorMapEncodeIm2col failed (%d)", (int)r);
+  // Drivers up to 13.1 mis-handle im2col maps over tensors smaller than 128 KiB unless this
+  // descriptor bit is cleared (the same workaround CUTLASS applies).
+  int drv = 0;
+  cudaDriverGetVersion(&drv);
+  if (drv <= 13010 && (int64_t)n * H * W * C * 2 < 131072) reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
+  return 0;
+}
+
+template <int CG, int BN, bool A_MN, bool B_MN, int KIND, int SRC = SRC_2D>
 static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
-                     cudaStream_t st) {
+                     cudaStream_t st, ConvArgs cv = ConvArgs{}) {
   using C = TcCfg<CG, BN, B_MN, KIND>;
   CUtensorMap ta, tb;
   int rc;
-  if (A_MN) rc = make_map(&ta, A, (uint64_t)M, (uint64_t)K, lda, 64, 64);
+  if (cv.splits < 1) {  // no split-K
+    cv.splits = 1;
+    cv.kb_per = (K + TC_BK - 1) / TC_BK;
+  }
+  if (SRC == SRC_CONV_FWD || SRC == SRC_CONV_DGRAD) rc = make_im2col_map(&ta, A, M / (cv.H * cv.W), cv.H, cv.W, cv.C, TC_BM);
+  else if (SRC == SRC_CONV_WGRAD) rc = make_im2col_map(&ta, A, K / (cv.H * cv.W), cv.H, cv.W, cv.C, 64);
+  else if (A_MN) rc = make_map(&ta, A, (uint64_t)M, (uint64_t)K, lda, 64, 64);
   else rc = make_map(&ta, A, (uint64_t)K, (uint64_t)M, lda, 64, TC_BM);
   if (rc) return rc;
-  if (B_MN) rc = make_map(&tb, B, (uint64_t)N, (uint64_t)K, ldb, 64, 64);
+  if (SRC == SRC_CONV_DGRAD) rc = make_map(&tb, B, (uint64_t)cv.C, 9ull * cv.brows, ldb, 64, C::B_ROWS);
+  else if (B_MN) rc = make_map(&tb, B, (uint64_t)N, (uint64_t)K, ldb, 64, 64);
   else rc = make_map(&tb, B, (uint64_t)K, (uint64_t)N, ldb, 64, C::B_ROWS);
   if (rc) return rc;
   CUtensorMap tw;
@@ -539,14 +631,14 @@ static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int
     rc = make_map(&tw, ep.master, (uint64_t)N, (uint64_t)M, ep.ldw, 32, 32, true);
     if (rc) return rc;
   }
-  auto kern = k_gemm_tc<CG, BN, A_MN, B_MN, KIND>;
+  auto kern = k_gemm_tc<CG, BN, A_MN, B_MN, KIND, SRC>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
       return set_error(PD_ERR_CUDA, "cudaFuncSetAttribute(smem=%d) failed", C::SMEM_BYTES);
     attr_set = true;
   }
-  const int units = ((M + TC_BM * CG - 1) / (TC_BM * CG)) * ((N + BN - 1) / BN);
+  const int units = ((M + TC_BM * CG - 1) / (TC_BM * CG)) * ((N + BN - 1) / BN) * cv.splits;
   const int max_units = num_sms() / CG;
   const int grid = CG * (units < max_units ? units : max_units);
   cudaLaunchConfig_t cfg{};
@@ -561,7 +653,7 @@ static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tw, M, N, K, ep);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tw, M, N, K, ep, cv);
   if (e != cudaSuccess) return set_error(PD_ERR_CUDA, "tcgen05 gemm launch: %s", cudaGetErrorString(e));
   return 0;
 }
@@ -620,6 +712,74 @@ static int dispatch_kind(int kind, const void* A, int64_t lda, const void* B, in
     case EPI_GRADF32: return launch_bn<A_MN, B_MN, EPI_GRADF32>(A, lda, B, ldb, M, N, K, ep, st);
   }
   return set_error(PD_ERR_INVALID, "unknown epilogue kind %d", kind);
+}
+
+// ============================================================== 3x3 convolution passes
+// Implicit GEMM on the same tcgen05 kernel; the activation operand comes from TMA im2col loads
+// (zero-filled halo = padding), so no im2col matrix is ever materialised in HBM.
+static int conv_bn(int N) { return N >= 256 ? 256 : (N >= 128 ? 128 : 64); }
+
+int splitk_plan(int M, int N, int K, int* splits, int* kb_per) {
+  const int bn = conv_bn(N);
+  const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + bn - 1) / bn);
+  const int num_kb = (K + TC_BK - 1) / TC_BK;
+  int s = (2 * num_sms() + tiles - 1) / tiles;  // about two waves of work units
+  const int cap = num_kb / 4 > 1 ? num_kb / 4 : 1;  // at least 4 k-blocks per split
+  s = s < 1 ? 1 : (s > cap ? cap : s);
+  const int per = (num_kb + s - 1) / s;
+  *kb_per = per;
+  *splits = (num_kb + per - 1) / per;  // no empty split
+  return 0;
+}
+
+template <int BN>
+static int conv_launch(int pass, const void* act, const void* other, int n, int H, int W, int cin, int cout,
+                       int kind, const EpiArgs& ep, cudaStream_t st) {
+  const int pix = n * H * W;
+  ConvArgs cv{};
+  cv.H = H;
+  cv.W = W;
+  if (pass == PD_CONV_FWD) {
+    if (kind != EPI_STORE) return set_error(PD_ERR_INVALID, "conv fwd: STORE epilogue only");
+    cv.C = cin;
+    return launch_tc<1, BN, false, true, EPI_STORE, SRC_CONV_FWD>(act, cin, other, cout, pix, cout, 9 * cin, ep, st,
+                                                                  cv);
+  }
+  if (pass == PD_CONV_DGRAD) {
+    if (kind != EPI_MASK) return set_error(PD_ERR_INVALID, "conv dgrad: MASK epilogue only");
+    cv.C = cout;
+    cv.brows = cin;
+    return launch_tc<1, BN, false, false, EPI_MASK, SRC_CONV_DGRAD>(act, cout, other, cout, pix, cin, 9 * cout, ep,
+                                                                   st, cv);
+  }
+  if (kind != EPI_GRADF32) return set_error(PD_ERR_INVALID, "conv wgrad: GRADF32 epilogue only");
+  const int M = pass == PD_CONV_WGRAD ? 9 * cin : cin;
+  splitk_plan(M, cout, pix, &cv.splits, &cv.kb_per);
+  cv.split_stride = (int64_t)M * ep.ldo;
+  if (pass == PD_CONV_WGRAD) {
+    cv.C = cin;
+    return launch_tc<1, BN, true, true, EPI_GRADF32, SRC_CONV_WGRAD>(act, cin, other, cout, M, cout, pix, ep, st, cv);
+  }
+  // PD_GEMM_WGRAD_SPLITK: plain dW^T[cin, cout] = X^T dY over `pix` rows (im2col'ed first layer)
+  return launch_tc<1, BN, true, true, EPI_GRADF32, SRC_2D>(act, cin, other, cout, M, cout, pix, ep, st, cv);
+}
+
+int conv3x3_tc(int pass, const void* act, const void* other, int n, int H, int W, int cin, int cout, int kind,
+               const EpiArgs& ep, cudaStream_t st) {
+  if (n < 1 || H < 1 || W < 1 || cin < 1 || cout < 1) return set_error(PD_ERR_INVALID, "conv: empty shape");
+  if (pass != PD_GEMM_WGRAD_SPLITK && (cin % 64 || cout % 64))
+    return set_error(PD_ERR_INVALID, "conv: channels must be multiples of 64 (got %d -> %d)", cin, cout);
+  if (pass == PD_GEMM_WGRAD_SPLITK && (cin % 8 || cout % 64))
+    return set_error(PD_ERR_INVALID, "split-K wgrad: cin %% 8, cout %% 64 required");
+  if ((int64_t)n * H * W >= (1ll << 31) / 64) return set_error(PD_ERR_INVALID, "conv: too many pixels");
+  if ((reinterpret_cast<uintptr_t>(act) | reinterpret_cast<uintptr_t>(other) | reinterpret_cast<uintptr_t>(ep.out)) & 15)
+    return set_error(PD_ERR_INVALID, "conv: 16-byte aligned operands required");
+  const int N = (pass == PD_CONV_DGRAD) ? cin : cout;
+  switch (conv_bn(N)) {
+    case 64: return conv_launch<64>(pass, act, other, n, H, W, cin, cout, kind, ep, st);
+    case 128: return conv_launch<128>(pass, act, other, n, H, W, cin, cout, kind, ep, st);
+    default: return conv_launch<256>(pass, act, other, n, H, W, cin, cout, kind, ep, st);
+  }
 }
 
 int gemm_bf16_tc(const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M, int N,

@@ -280,6 +280,11 @@ int pd_copy(void* dst, const void* src, int64_t bytes, void* stream) {
   return copy_bytes(dst, src, bytes, static_cast<cudaStream_t>(stream));
 }
 
+int pd_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "memcpy: %s", cudaGetErrorString(e));
+}
+
 int pd_flag_signal(int* flag, int value, void* stream) {
   return flag_signal(flag, value, static_cast<cudaStream_t>(stream));
 }

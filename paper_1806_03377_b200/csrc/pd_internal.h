@@ -20,6 +20,21 @@ int gemm_simt(int dtype, const void* A, int a_mn, int64_t lda, const void* B, in
 int gemm(int dtype, const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M, int N, int K,
          int kind, const EpiArgs& ep, cudaStream_t st);
 
+// Implicit-GEMM 3x3 convolution passes (PD_CONV_*), and the split-K plan they share.
+int conv3x3_tc(int pass, const void* act, const void* other, int n, int H, int W, int cin, int cout, int kind,
+               const EpiArgs& ep, cudaStream_t st);
+int splitk_plan(int M, int N, int K, int* splits, int* kb_per);
+int maxpool_fwd(const void* x, void* y, uint8_t* arg, int n, int H, int W, int C, cudaStream_t st);
+int maxpool_bwd(const void* dy, const uint8_t* arg, void* dx, int n, int H, int W, int C, cudaStream_t st);
+int im2col3(const void* x, void* cols, int n, int H, int W, int C, int kpad, cudaStream_t st);
+int reduce_sgd(int out_dtype, const float* part, int S, int64_t stride, int64_t n, float* grad, float* master,
+               void* out, float lr, cudaStream_t st);
+int colsum_blocks(int64_t rows, int C);
+int bias_grad_tall(const void* dz, int64_t rows, int C, float* part, float* grad, float* master, float* out, float lr,
+                   cudaStream_t st);
+int softmax_ce(const float* logits, int64_t ldz, const int* labels, int B, int V, void* dz, int64_t ldd, float* loss,
+               cudaStream_t st);
+
 int bias_sgd(int dtype, const void* dz, int rows, int cols, int64_t ld, float* b_master, float* b_out, float lr,
              cudaStream_t st);
 int sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n, float lr, cudaStream_t st);

@@ -69,6 +69,19 @@ PD_DEVICE void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar
       : "memory");
 }
 
+// 4-D im2col bulk tensor load (NHWC activation, implicit-GEMM convolution): `pixelsPerColumn`
+// consecutive output pixels starting at the bounding-box coordinate (w, h, n), each reading the
+// channelsPerPixel channels from c at input position (w + ow, h + oh); halo pixels outside the
+// tensor are zero-filled (the convolution's padding).
+PD_DEVICE void tma_load_im2col_4d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c, int w, int h, int n,
+                                  uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+      : "memory");
+}
+
 // L2 eviction-priority policies (createpolicy) and loads/stores / TMA that carry them.
 PD_DEVICE uint64_t l2_policy_evict_first() {
   uint64_t p;

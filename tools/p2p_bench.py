@@ -47,7 +47,7 @@ def main():
             for mode in ("store+flag", "memcpy"):
                 def once(i):
                     if mode == "memcpy":
-                        torch.cuda.cudart().cudaMemcpyAsync(peer_inbox, src.data_ptr(), n, 3, stream.cuda_stream)
+                        nat.check(lib.pd_memcpy_async(peer_inbox, src.data_ptr(), n, stream.cuda_stream), "memcpy")
                     else:
                         # the hand-off path: SM stores into the peer inbox (16-byte vectors), then the
                         # system-scope release flag the consumer acquire-polls
