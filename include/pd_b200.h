@@ -183,7 +183,37 @@ typedef struct pd_stage_desc {
   int* red_ready;           /* last round whose gradients are complete here */
   int* red_done;            /* last round whose reduction has finished reading every replica */
   int* err_word;            /* device int, set non-zero by a timed-out flag wait */
+  /* Layered stages (VGG-style conv / classifier stages).  layers == NULL: the MLP stage above
+   * (Linear + ReLU per layer, MSE at the model output).  Otherwise n_layers descriptors; the
+   * per-layer arrays above keep their meaning with
+   *   weights  LINEAR [c_out, c_in];  CONV3 Wt [9*c_in, c_out] (im2col layer: [64, c_out]);
+   *   act[l]   the layer's (pooled) output, [batch, out_features(l)] in NHWC order;
+   *   tmp[2]   [batch, max pre-pool features] (forward pre-pool scratch / gradient ping-pong). */
+  const struct pd_layer* layers;
+  int loss_kind;            /* last stage: PD_LOSS_MSE (target = fp32 [batch, out]) or PD_LOSS_CE
+                               (target = int32 labels [batch], logits below) */
+  float* logits;            /* PD_LOSS_CE: fp32 [batch, classes] */
+  float* part;              /* fp32 scratch for split-K partials and column-sum blocks (size from
+                               pd_layer_scratch_floats) */
 } pd_stage_desc;
+
+enum pd_layer_kind { PD_LAYER_LINEAR = 0, PD_LAYER_CONV3 = 1 };
+enum pd_loss_kind { PD_LOSS_MSE = 0, PD_LOSS_CE = 1 };
+
+typedef struct pd_layer {
+  int kind;                 /* pd_layer_kind */
+  int relu;                 /* ReLU after the layer */
+  int pool;                 /* CONV3: 2x2/2 max pool after the ReLU */
+  int im2col;               /* CONV3 with c_in < 64 (the image layer): explicit im2col to 64 columns */
+  int h, w;                 /* CONV3: input (= pre-pool output) spatial size */
+  int c_in, c_out;          /* channels (CONV3) or features (LINEAR) */
+  uint8_t* const* argmax;   /* pool: [act_depth] uint8 [batch, h/2, w/2, c_out] */
+  void* const* cols;        /* im2col: [act_depth] dtype [batch*h*w, 64] */
+} pd_layer;
+
+/* fp32 elements the stage's `part` scratch needs for this layer (split-K partials of the weight
+ * gradient, then the bias column-sum blocks; the larger of the two). */
+int64_t pd_layer_scratch_floats(const pd_layer* layer, int batch);
 
 /* What any worker (in this process or a peer-mapped one in another) exposes to the others. */
 typedef struct pd_worker_view {

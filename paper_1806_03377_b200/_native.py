@@ -29,7 +29,7 @@ EXPORTED = (
     "pd_enable_peer_access", "pd_rt_create", "pd_rt_add_stage", "pd_rt_add_view", "pd_rt_load_program", "pd_rt_run",
     "pd_rt_records", "pd_rt_set_serial", "pd_rt_kernel_timing", "pd_rt_kernel_stats", "pd_rt_launch_count", "pd_rt_destroy",
     "pd_conv3x3", "pd_splitk_plan", "pd_maxpool2", "pd_maxpool2_bwd", "pd_im2col3", "pd_reduce_sgd",
-    "pd_colsum_blocks", "pd_bias_grad_tall", "pd_softmax_ce", "pd_memcpy_async",
+    "pd_colsum_blocks", "pd_bias_grad_tall", "pd_softmax_ce", "pd_memcpy_async", "pd_layer_scratch_floats",
 )
 PD_CONV_FWD, PD_CONV_DGRAD, PD_CONV_WGRAD, PD_GEMM_WGRAD_SPLITK = range(4)
 
@@ -39,6 +39,17 @@ class Epilogue(Structure):
         ("kind", c_int), ("out", c_void_p), ("ldo", c_int64), ("bias", c_void_p), ("relu", c_int),
         ("mask", c_void_p), ("ldm", c_int64), ("target", c_void_p), ("ldt", c_int64), ("scale", c_float),
         ("loss", c_void_p), ("master", c_void_p), ("ldw", c_int64), ("lr", c_float),
+    ]
+
+
+PD_LAYER_LINEAR, PD_LAYER_CONV3 = 0, 1
+PD_LOSS_MSE, PD_LOSS_CE = 0, 1
+
+
+class LayerDesc(Structure):
+    _fields_ = [
+        ("kind", c_int), ("relu", c_int), ("pool", c_int), ("im2col", c_int), ("h", c_int), ("w", c_int),
+        ("c_in", c_int), ("c_out", c_int), ("argmax", POINTER(c_void_p)), ("cols", POINTER(c_void_p)),
     ]
 
 
@@ -56,6 +67,7 @@ class StageDesc(Structure):
         ("act_ready", c_void_p), ("act_ack", c_void_p), ("grad_ready", c_void_p), ("grad_ack", c_void_p),
         ("red_grad", POINTER(c_void_p)), ("red_bgrad", POINTER(c_void_p)), ("red_ready", c_void_p),
         ("red_done", c_void_p), ("err_word", c_void_p),
+        ("layers", POINTER(LayerDesc)), ("loss_kind", c_int), ("logits", c_void_p), ("part", c_void_p),
     ]
 
 
@@ -124,6 +136,8 @@ def lib() -> ctypes.CDLL:
                                         c_void_p]
         L.pd_softmax_ce.argtypes = [c_void_p, c_int64, c_void_p, c_int, c_int, c_void_p, c_int64, c_void_p, c_void_p]
         L.pd_memcpy_async.argtypes = [c_void_p, c_void_p, c_int64, c_void_p]
+        L.pd_layer_scratch_floats.argtypes = [POINTER(LayerDesc), c_int]
+        L.pd_layer_scratch_floats.restype = c_int64
         _lib = L
     return _lib
 

@@ -21,8 +21,15 @@ namespace {
 
 using namespace pd;
 
+struct Layer {
+  pd_layer d{};
+  std::vector<uint8_t*> argmax;
+  std::vector<void*> cols;
+};
+
 struct Stage {
   pd_stage_desc d{};
+  std::vector<Layer> layers;  // empty: MLP stage
   std::vector<int64_t> dims;
   std::vector<float*> w_master, b_master, b_ring, red_grad, red_bgrad;
   std::vector<void*> w_ring, act, act_in, grad_in, dz_last;
@@ -106,6 +113,15 @@ int timed_gemm(pd_runtime* rt, int cls, int dtype, const void* A, int a_mn, int6
   if (slot) PD_CHECK(cudaEventRecord(slot->b, st));
   return 0;
 }
+
+// Parameter sizes of layer l (MLP: dims; layered: per kind).
+int64_t w_numel(const Stage& S, int l) {
+  if (S.layers.empty()) return S.dims[l] * S.dims[l + 1];
+  const pd_layer& y = S.layers[l].d;
+  if (y.kind == PD_LAYER_LINEAR) return (int64_t)y.c_in * y.c_out;
+  return (int64_t)(y.im2col ? 64 : 9 * y.c_in) * y.c_out;
+}
+int64_t b_numel(const Stage& S, int l) { return S.layers.empty() ? S.dims[l + 1] : S.layers[l].d.c_out; }
 
 int wait_flag(pd_runtime* rt, Stage& S, const int* flag, int value) {
   PD_TRY(flag_wait(flag, flag_val(rt->epoch, value), S.d.err_word, stream_of(rt, S)));
@@ -208,6 +224,198 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
   return 0;
 }
 
+int timed_conv(pd_runtime* rt, int cls, int pass, const void* act, const void* other, int n, int h, int w, int cin,
+               int cout, int kind, const EpiArgs& ep, cudaStream_t st) {
+  pd_runtime::KT* slot = nullptr;
+  if (rt->ktiming) {
+    if (rt->kt_used == rt->kt.size()) {
+      pd_runtime::KT k{};
+      PD_CHECK(cudaEventCreate(&k.a));
+      PD_CHECK(cudaEventCreate(&k.b));
+      rt->kt.push_back(k);
+    }
+    slot = &rt->kt[rt->kt_used++];
+    slot->cls = cls;
+    slot->flops = 2.0 * (double)n * h * w * 9.0 * cin * cout;
+    PD_CHECK(cudaEventRecord(slot->a, st));
+  }
+  PD_TRY(conv3x3_tc(pass, act, other, n, h, w, cin, cout, kind, ep, st));
+  rt->launches += 1;
+  if (slot) PD_CHECK(cudaEventRecord(slot->b, st));
+  return 0;
+}
+
+// Layered stage forward (VGG-style): per layer Linear or implicit-GEMM conv (+bias, ReLU fused in
+// the epilogue), optional max pool; the stage's last layer writes the next stage's inbox slot,
+// or at the model output the loss (MSE epilogue, or fp32 logits + softmax cross-entropy).
+int run_forward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
+  cudaStream_t ST = stream_of(rt, S);
+  const pd_stage_desc& d = S.d;
+  const int L = d.n_layers, B = d.batch;
+  const int wslot = it[PD_IT_WSLOT], act = it[PD_IT_ACT], mb = it[PD_IT_MB];
+  const void* x = d.is_first ? S.act_in[it[PD_IT_BLOCK]] : S.act_in[it[PD_IT_XSLOT]];
+  for (int l = 0; l < L; ++l) {
+    const Layer& Y = S.layers[l];
+    const pd_layer& y = Y.d;
+    const bool last = l == L - 1;
+    void* out = !last ? S.act[(size_t)l * d.act_depth + act]
+                      : (d.is_last ? nullptr : rt->views.at(it[PD_IT_DST]).act_in[it[PD_IT_OUT]]);
+    const void* W = S.w_ring[(size_t)l * d.ring_depth + wslot];
+    const float* bias = S.b_ring[(size_t)l * d.ring_depth + wslot];
+    EpiArgs ep{};
+    ep.bias = bias;
+    ep.relu = y.relu;
+    if (y.kind == PD_LAYER_LINEAR) {
+      ep.ldo = y.c_out;
+      int kind = EPI_STORE;
+      if (last && d.is_last) {
+        if (d.loss_kind == PD_LOSS_CE) {
+          kind = EPI_GRADF32;  // fp32 logits (+ bias)
+          ep.out = d.logits;
+        } else {
+          kind = EPI_LOSS;
+          ep.out = S.dz_last[act];
+          ep.target = S.target[it[PD_IT_BLOCK]];
+          ep.ldt = y.c_out;
+          ep.scale = 1.0f / (float)B;
+          ep.loss = d.loss + mb;
+        }
+      } else {
+        ep.out = out;
+      }
+      PD_TRY(timed_gemm(rt, KC_FWD, d.dtype, x, 0, y.c_in, W, 0, y.c_in, B, y.c_out, y.c_in, kind, ep, ST));
+      if (last && d.is_last && d.loss_kind == PD_LOSS_CE) {
+        PD_TRY(softmax_ce(d.logits, y.c_out, reinterpret_cast<const int*>(S.target[it[PD_IT_BLOCK]]), B, y.c_out,
+                          S.dz_last[act], y.c_out, d.loss + mb, ST));
+        rt->launches += 1;
+      }
+      x = out;
+      continue;
+    }
+    // CONV3
+    if (last && d.is_last) return set_error(PD_ERR_INVALID, "worker %d: a conv layer cannot be the model output", d.worker);
+    void* conv_out = y.pool ? d.tmp[0] : out;
+    ep.out = conv_out;
+    ep.ldo = y.c_out;
+    const int pix = B * y.h * y.w;
+    if (y.im2col) {
+      void* cols = Y.cols[act];
+      PD_TRY(im2col3(x, cols, B, y.h, y.w, y.c_in, 64, ST));
+      rt->launches += 1;
+      PD_TRY(timed_gemm(rt, KC_FWD, d.dtype, cols, 0, 64, W, 1, y.c_out, pix, y.c_out, 64, EPI_STORE, ep, ST));
+    } else {
+      PD_TRY(timed_conv(rt, KC_FWD, PD_CONV_FWD, x, W, B, y.h, y.w, y.c_in, y.c_out, EPI_STORE, ep, ST));
+    }
+    if (y.pool) {
+      PD_TRY(maxpool_fwd(conv_out, out, Y.argmax[act], B, y.h, y.w, y.c_out, ST));
+      rt->launches += 1;
+    }
+    x = out;
+  }
+  return 0;
+}
+
+int run_backward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
+  cudaStream_t ST = stream_of(rt, S);
+  const pd_stage_desc& d = S.d;
+  const int L = d.n_layers, B = d.batch;
+  const int wslot = it[PD_IT_WSLOT], wnew = it[PD_IT_WNEW], act = it[PD_IT_ACT], round = it[PD_IT_ROUND];
+  const bool replicated = d.rep > 1;
+  const int par = round & 1;
+  if (replicated && round >= 3) {
+    for (int r = 0; r < d.rep; ++r) PD_TRY(wait_flag(rt, S, rt->views.at(d.first_worker + r).v.red_done, round - 2));
+  }
+  const bool update = replicated || wnew >= 0;
+  const void* dz = d.is_last ? S.dz_last[act] : S.grad_in[it[PD_IT_GSLOT]];
+  auto other_tmp = [&](const void* p) { return p == d.tmp[0] ? d.tmp[1] : d.tmp[0]; };
+  for (int l = L - 1; l >= 0; --l) {
+    const Layer& Y = S.layers[l];
+    const pd_layer& y = Y.d;
+    const void* X = (l == 0) ? (d.is_first ? S.act_in[it[PD_IT_BLOCK]] : S.act_in[it[PD_IT_XSLOT]])
+                             : S.act[(size_t)(l - 1) * d.act_depth + act];
+    const void* Wst = S.w_ring[(size_t)l * d.ring_depth + wslot];
+    const bool need_dx = !(d.is_first && l == 0);
+    float* gW = replicated ? S.red_grad[(size_t)l * 2 + par] : nullptr;
+    float* gb = replicated ? S.red_bgrad[(size_t)l * 2 + par] : nullptr;
+    void* ring_new = (!replicated && wnew >= 0) ? S.w_ring[(size_t)l * d.ring_depth + wnew] : nullptr;
+    float* bring_new = (!replicated && wnew >= 0) ? S.b_ring[(size_t)l * d.ring_depth + wnew] : nullptr;
+    void* dst = nullptr;
+    if (y.kind == PD_LAYER_LINEAR) {
+      if (need_dx) {
+        dst = (l == 0) ? rt->views.at(it[PD_IT_DST]).grad_in[it[PD_IT_OUT]] : other_tmp(dz);
+        EpiArgs ep{};
+        ep.out = dst;
+        ep.ldo = y.c_in;
+        ep.mask = X;
+        ep.ldm = y.c_in;
+        PD_TRY(timed_gemm(rt, KC_DGRAD, d.dtype, dz, 0, y.c_out, Wst, 1, y.c_in, B, y.c_in, y.c_out, EPI_MASK, ep, ST));
+      }
+      if (replicated) {
+        EpiArgs ep{};
+        ep.out = gW;
+        ep.ldo = y.c_in;
+        PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, y.c_out, X, 1, y.c_in, y.c_out, y.c_in, B, EPI_GRADF32, ep, ST));
+        PD_TRY(bias_grad(d.dtype, dz, B, y.c_out, y.c_out, gb, ST));
+        rt->launches += 1;
+      } else if (update) {
+        EpiArgs ep{};
+        ep.master = S.w_master[l];
+        ep.ldw = y.c_in;
+        ep.out = ring_new;
+        ep.ldo = y.c_in;
+        ep.lr = d.lr;
+        PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, y.c_out, X, 1, y.c_in, y.c_out, y.c_in, B, EPI_SGD, ep, ST));
+        PD_TRY(bias_sgd(d.dtype, dz, B, y.c_out, y.c_out, S.b_master[l], bring_new, d.lr, ST));
+        rt->launches += 1;
+      }
+      dz = dst;
+      continue;
+    }
+    // CONV3: route the pooled gradient back to the window maxima (dz is already ReLU-masked by
+    // the consumer's dgrad epilogue: pooled > 0 <=> the argmax pre-activation > 0)
+    const void* dy = dz;
+    if (y.pool) {
+      void* t = other_tmp(dz);
+      PD_TRY(maxpool_bwd(dz, Y.argmax[act], t, B, y.h, y.w, y.c_out, ST));
+      rt->launches += 1;
+      dy = t;
+    }
+    const int pix = B * y.h * y.w;
+    if (update) {
+      // weight gradient: split-K partials into `part`, summed in fixed order by the reduction,
+      // which either applies SGD into the new ring slot or hands the sum to the replica reduce
+      const int M = y.im2col ? 64 : 9 * y.c_in;
+      int splits = 1, per = 0;
+      PD_TRY(splitk_plan(M, y.c_out, pix, &splits, &per));
+      EpiArgs ep{};
+      ep.out = d.part;
+      ep.ldo = y.c_out;
+      if (y.im2col)
+        PD_TRY(timed_conv(rt, KC_WGRAD, PD_GEMM_WGRAD_SPLITK, Y.cols[act], dy, B, y.h, y.w, 64, y.c_out, EPI_GRADF32,
+                          ep, ST));
+      else
+        PD_TRY(timed_conv(rt, KC_WGRAD, PD_CONV_WGRAD, X, dy, B, y.h, y.w, y.c_in, y.c_out, EPI_GRADF32, ep, ST));
+      const int64_t n = (int64_t)M * y.c_out;
+      PD_TRY(reduce_sgd(d.dtype, d.part, splits, n, n, gW, S.w_master[l], ring_new, d.lr, ST));
+      PD_TRY(bias_grad_tall(dy, pix, y.c_out, d.part, gb, S.b_master[l], bring_new, d.lr, ST));
+      rt->launches += 3;
+    }
+    if (need_dx) {
+      if (y.im2col) return set_error(PD_ERR_INVALID, "worker %d: im2col layer must be the model input", d.worker);
+      dst = (l == 0) ? rt->views.at(it[PD_IT_DST]).grad_in[it[PD_IT_OUT]] : other_tmp(dy);
+      EpiArgs ep{};
+      ep.out = dst;
+      ep.ldo = y.c_in;
+      ep.mask = X;
+      ep.ldm = y.c_in;
+      PD_TRY(timed_conv(rt, KC_DGRAD, PD_CONV_DGRAD, dy, Wst, B, y.h, y.w, y.c_in, y.c_out, EPI_MASK, ep, ST));
+    }
+    dz = dst;
+  }
+  if (replicated) PD_TRY(signal_flag(rt, S, d.red_ready, round));
+  return 0;
+}
+
 // Replicated stage, round k: wait until every replica's round-k gradients exist, then the fused
 // allreduce (peer loads) + SGD kernel commits version k*rep into ring slot wnew on each replica.
 int run_reduce(pd_runtime* rt, Stage& S, const int32_t* it) {
@@ -222,11 +430,11 @@ int run_reduce(pd_runtime* rt, Stage& S, const int32_t* it) {
       g[r] = V.red_grad[(size_t)l * 2 + par];
       gb[r] = V.red_bgrad[(size_t)l * 2 + par];
     }
-    const int64_t n = S.dims[l] * S.dims[l + 1];
+    const int64_t n = w_numel(S, l);
     PD_TRY(allreduce_sgd(d.dtype, g.data(), d.rep, S.w_master[l], S.w_ring[(size_t)l * d.ring_depth + wnew], n,
                          d.lr, ST));
     PD_TRY(allreduce_sgd(PD_F32, gb.data(), d.rep, S.b_master[l], S.b_ring[(size_t)l * d.ring_depth + wnew],
-                         S.dims[l + 1], d.lr, ST));
+                         b_numel(S, l), d.lr, ST));
     rt->launches += 2;
   }
   PD_TRY(signal_flag(rt, S, d.red_done, round));
@@ -266,6 +474,34 @@ int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc) {
   S.d = d;
   const int L = d.n_layers;
   S.dims = copy_arr(d.dims, L + 1);
+  if (d.layers) {
+    for (int l = 0; l < L; ++l) {
+      Layer Y;
+      Y.d = d.layers[l];
+      const pd_layer& y = Y.d;
+      if (y.kind != PD_LAYER_LINEAR && y.kind != PD_LAYER_CONV3)
+        return set_error(PD_ERR_INVALID, "worker %d layer %d: bad kind %d", d.worker, l, y.kind);
+      if (y.c_in < 1 || y.c_out < 1 || (y.kind == PD_LAYER_CONV3 && (y.h < 2 || y.w < 2)))
+        return set_error(PD_ERR_INVALID, "worker %d layer %d: bad shape", d.worker, l);
+      if (d.dtype != PD_BF16) return set_error(PD_ERR_INVALID, "worker %d: layered stages are bf16", d.worker);
+      if (y.kind == PD_LAYER_CONV3 && !d.part)
+        return set_error(PD_ERR_INVALID, "worker %d: conv layers need the `part` scratch", d.worker);
+      if (y.pool) {
+        if (!y.argmax) return set_error(PD_ERR_INVALID, "worker %d layer %d: pool without argmax", d.worker, l);
+        Y.argmax.assign(y.argmax, y.argmax + d.act_depth);
+      }
+      if (y.im2col) {
+        if (!y.cols) return set_error(PD_ERR_INVALID, "worker %d layer %d: im2col without cols", d.worker, l);
+        Y.cols.assign(y.cols, y.cols + d.act_depth);
+      }
+      Y.d.argmax = nullptr;
+      Y.d.cols = nullptr;
+      S.layers.push_back(Y);
+    }
+    if (d.is_last && d.loss_kind == PD_LOSS_CE && !d.logits)
+      return set_error(PD_ERR_INVALID, "worker %d: cross-entropy needs the logits buffer", d.worker);
+  }
+  S.d.layers = nullptr;
   S.w_master = copy_arr(d.w_master, L);
   S.b_master = copy_arr(d.b_master, L);
   S.w_ring = copy_arr(d.w_ring, (int64_t)L * d.ring_depth);
@@ -373,11 +609,11 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
     PD_CHECK(cudaStreamWaitEvent(ST, rt->ev0, 0));
     // version 0 of this run = the current (latest) weights
     for (int l = 0; l < S.d.n_layers; ++l) {
-      const int64_t n = S.dims[l] * S.dims[l + 1];
+      const int64_t n = w_numel(S, l);
       PD_TRY(cast_f32(S.d.dtype, S.w_master[l], S.w_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], n, ST));
       rt->launches += 1;
       PD_CHECK(cudaMemcpyAsync(S.b_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], S.b_master[l],
-                               sizeof(float) * S.dims[l + 1], cudaMemcpyDeviceToDevice, ST));
+                               sizeof(float) * b_numel(S, l), cudaMemcpyDeviceToDevice, ST));
     }
     if (S.d.is_last && S.d.loss)  // losses are indexed by minibatch id
       PD_CHECK(cudaMemsetAsync(S.d.loss, 0, sizeof(float) * (size_t)(max_mb + 1), ST));
@@ -400,8 +636,9 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
       PD_TRY(wait_flag(rt, S, (fwd ? V.v.act_ack : V.v.grad_ack) + it[PD_IT_OUT], it[PD_IT_AWAIT]));
     }
     if (rt->traced) PD_CHECK(cudaEventRecord(rt->ev_start[i], ST));
-    if (op == 0) PD_TRY(run_forward(rt, S, it));
-    else if (op == 1) PD_TRY(run_backward(rt, S, it));
+    const bool layered = !S.layers.empty();
+    if (op == 0) PD_TRY(layered ? run_forward_layers(rt, S, it) : run_forward(rt, S, it));
+    else if (op == 1) PD_TRY(layered ? run_backward_layers(rt, S, it) : run_backward(rt, S, it));
     else PD_TRY(run_reduce(rt, S, it));
     // cross-process hand-off: publish the payload the epilogue stored into the peer inbox
     if ((op == 0 && !S.d.is_last) || (op == 1 && !S.d.is_first)) {
@@ -504,3 +741,16 @@ int pd_rt_destroy(pd_runtime* rt) {
 }
 
 }  // extern "C"
+
+extern "C" int64_t pd_layer_scratch_floats(const pd_layer* layer, int batch) {
+  if (!layer || batch < 1) return 0;
+  const pd_layer& y = *layer;
+  if (y.kind != PD_LAYER_CONV3) return 0;
+  const int M = y.im2col ? 64 : 9 * y.c_in;
+  const int64_t pix = (int64_t)batch * y.h * y.w;
+  int splits = 1, per = 0;
+  pd::splitk_plan(M, y.c_out, (int)pix, &splits, &per);
+  const int64_t wpart = (int64_t)splits * M * y.c_out;
+  const int64_t bpart = (int64_t)pd::colsum_blocks(pix, y.c_out) * y.c_out;
+  return wpart > bpart ? wpart : bpart;
+}

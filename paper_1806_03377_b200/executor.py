@@ -31,7 +31,7 @@ import numpy as np
 from . import _native as nat
 from .errors import SimulationError, ValidationError
 from .ledger import Mode, SimConfig, SimResult, TraceEvent, build_report
-from .models import MLPSpec, init_params, make_data
+from .models import ConvNetSpec, MLPSpec, init_params_any, make_data_any
 from .orders import Direction, Schedule, build_schedule, stage_inflight_caps
 from .program import Program, compile_program
 
@@ -57,6 +57,7 @@ class _StageBuf:
     tensors: dict = field(default_factory=dict)
     desc: object = None
     keep: list = field(default_factory=list)  # ctypes arrays referenced by desc
+    geoms: list | None = None  # layered stages: LayerGeom per layer
 
 
 def _validate(cfg: SimConfig, ctx, model: MLPSpec) -> None:
@@ -100,7 +101,10 @@ class Executor:
         self.hosted = [wp for wp in self.program.workers if self.program.device_of[wp.wid] == self.rank]
         self.dtype = torch.float32 if model.dtype == "fp32" else torch.bfloat16
         self.pd_dtype = nat.PD_F32 if model.dtype == "fp32" else nat.PD_BF16
-        n_params = sum(a * b for a, b in zip(model.widths[:-1], model.widths[1:]))
+        self.layered = isinstance(model, ConvNetSpec)
+        self.geoms = model.geoms() if self.layered else None
+        n_params = (model.n_params() if self.layered
+                    else sum(a * b for a, b in zip(model.widths[:-1], model.widths[1:])))
         self.init = init or ("host" if n_params <= HOST_INIT_LIMIT else "device")
         self._alloc()
         self._exchange()
@@ -108,13 +112,33 @@ class Executor:
         self.runs = 0
 
     # ------------------------------------------------------------------ setup
+    def _layer_desc(self, x, argmax=None, cols=None):
+        d = nat.LayerDesc()
+        d.kind = nat.PD_LAYER_CONV3 if x.kind == "conv" else nat.PD_LAYER_LINEAR
+        d.relu, d.pool, d.im2col = int(x.relu), int(x.pool), int(x.im2col)
+        d.h, d.w, d.c_in, d.c_out = x.h, x.w, x.c_in, x.c_out
+        if argmax is not None:
+            a = self._parr([p.data_ptr() for p in argmax])
+            self._keep.append(a)
+            d.argmax = ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p))
+        if cols is not None:
+            a = self._parr([p.data_ptr() for p in cols])
+            self._keep.append(a)
+            d.cols = ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p))
+        return d
+
+    def _scratch_floats(self, x) -> int:
+        self._keep = getattr(self, "_keep", [])
+        d = self._layer_desc(x)
+        return int(nat.lib().pd_layer_scratch_floats(ctypes.byref(d), self.model.batch))
+
     def _alloc(self) -> None:
         torch = _torch()
         dev, dt, m = self.device, self.dtype, self.model
         plan = self.cfg.plan
         if self.init == "host":
-            params = init_params(m)
-            X, T = make_data(m)
+            params = init_params_any(m)
+            X, T = make_data_any(m)
         else:
             params = None
             g = torch.Generator(device=dev).manual_seed(m.seed)
@@ -128,24 +152,31 @@ class Executor:
                           grad_depth=wp.grad_depth)
             L = len(dims) - 1
             t = b.tensors
+            geo = self.geoms[st.first_layer - 1: st.last_layer] if self.layered else None
+            b.geoms = geo
             t["w_master"], t["b_master"], t["w_ring"], t["b_ring"] = [], [], [], []
             for l in range(L):
                 din, dout = dims[l], dims[l + 1]
+                wshape = geo[l].w_shape if geo else (dout, din)
+                nb = geo[l].c_out if geo else dout
                 gl = st.first_layer - 1 + l
                 if params is not None:
                     W = torch.from_numpy(params[gl][0]).float().to(dev)
                     bias = torch.from_numpy(params[gl][1]).float().to(dev)
                 else:
-                    W = torch.randn(dout, din, device=dev, generator=g) * math.sqrt(2.0 / din)
-                    bias = torch.randn(dout, device=dev, generator=g) * 0.01
+                    fan = (9 * geo[l].c_in if geo[l].kind == "conv" else geo[l].c_in) if geo else din
+                    W = torch.randn(*wshape, device=dev, generator=g) * math.sqrt(2.0 / fan)
+                    if geo and geo[l].im2col:
+                        W[9 * geo[l].c_in:] = 0.0
+                    bias = torch.randn(nb, device=dev, generator=g) * 0.01
                 t["w_master"].append(W.contiguous())
                 t["b_master"].append(bias.contiguous())
-                t["w_ring"].append(torch.empty(b.ring_depth, dout, din, device=dev, dtype=dt))
-                t["b_ring"].append(torch.empty(b.ring_depth, dout, device=dev, dtype=torch.float32))
+                t["w_ring"].append(torch.empty(b.ring_depth, *wshape, device=dev, dtype=dt))
+                t["b_ring"].append(torch.empty(b.ring_depth, nb, device=dev, dtype=torch.float32))
             t["act"] = [torch.empty(b.act_depth, m.batch, dims[l + 1], device=dev, dtype=dt) for l in range(L - 1)]
             if wp.stage == 0:
                 if params is not None:
-                    t["act_in"] = torch.from_numpy(X).to(dev).to(dt).contiguous()
+                    t["act_in"] = torch.from_numpy(X.reshape(m.n_blocks, m.batch, -1)).to(dev).to(dt).contiguous()
                 else:
                     t["act_in"] = torch.randn(m.n_blocks, m.batch, dims[0], device=dev, generator=g).to(dt)
             else:
@@ -154,12 +185,27 @@ class Executor:
                 t["grad_in"] = torch.zeros(b.grad_depth, m.batch, dims[-1], device=dev, dtype=dt)
             else:
                 t["dz_last"] = torch.empty(b.act_depth, m.batch, dims[-1], device=dev, dtype=dt)
-                if params is not None:
+                if self.layered:  # cross-entropy: int32 labels and fp32 logits
+                    if params is not None:
+                        t["target"] = torch.from_numpy(T).to(dev).to(torch.int32).contiguous()
+                    else:
+                        t["target"] = torch.randint(0, m.classes, (m.n_blocks, m.batch), device=dev, generator=g,
+                                                    dtype=torch.int32)
+                    t["logits"] = torch.empty(m.batch, m.classes, device=dev, dtype=torch.float32)
+                elif params is not None:
                     t["target"] = torch.from_numpy(T).float().to(dev).contiguous()
                 else:
                     t["target"] = torch.randn(m.n_blocks, m.batch, dims[-1], device=dev, generator=g)
                 t["loss"] = torch.zeros(self.cfg.num_minibatches + 1, device=dev, dtype=torch.float32)
-            t["tmp"] = [torch.empty(m.batch, max(dims), device=dev, dtype=dt) for _ in range(2)]
+            tmp_feat = max(max(dims), max(x.pre_features for x in geo)) if geo else max(dims)
+            t["tmp"] = [torch.empty(m.batch, tmp_feat, device=dev, dtype=dt) for _ in range(2)]
+            if geo:
+                t["argmax"] = [torch.empty(b.act_depth, m.batch, x.out_features, device=dev, dtype=torch.uint8)
+                               if x.pool else None for x in geo]
+                t["cols"] = [torch.empty(b.act_depth, m.batch * x.h * x.w, 64, device=dev, dtype=dt)
+                             if x.im2col else None for x in geo]
+                scratch = max([self._scratch_floats(x) for x in geo] + [1])
+                t["part"] = torch.empty(scratch, device=dev, dtype=torch.float32)
             t["err"] = torch.zeros(1, device=dev, dtype=torch.int32)
             # receiver-owned inbox flags (zero = nothing delivered yet); used when a producer is remote
             i32 = dict(device=dev, dtype=torch.int32)
@@ -170,8 +216,9 @@ class Executor:
                 t["grad_ready"] = torch.zeros(b.grad_depth, **i32)
                 t["grad_ack"] = torch.zeros(b.grad_depth, **i32)
             if st.replication > 1:  # round-parity gradient buffers + reduction flags
-                t["red_grad"] = [[torch.zeros(dims[l + 1], dims[l], device=dev) for _ in range(2)] for l in range(L)]
-                t["red_bgrad"] = [[torch.zeros(dims[l + 1], device=dev) for _ in range(2)] for l in range(L)]
+                t["red_grad"] = [[torch.zeros(*t["w_master"][l].shape, device=dev) for _ in range(2)] for l in range(L)]
+                t["red_bgrad"] = [[torch.zeros(t["b_master"][l].numel(), device=dev) for _ in range(2)]
+                                  for l in range(L)]
                 t["red_flags"] = torch.zeros(2, **i32)
             self.bufs[wp.wid] = b
 
@@ -238,7 +285,7 @@ class Executor:
         rt = ctypes.c_void_p()
         nat.check(L.pd_rt_create(self.device.index, ctypes.byref(rt)), "pd_rt_create")
         self._rt = rt
-        self._keep = []
+        self._keep = getattr(self, "_keep", [])
 
         def arr(ptrs):
             a = self._parr(ptrs)
@@ -315,6 +362,15 @@ class Executor:
                 d.red_ready, d.red_done = t["red_flags"].data_ptr(), t["red_flags"].data_ptr() + 4
             d.tmp[0], d.tmp[1] = t["tmp"][0].data_ptr(), t["tmp"][1].data_ptr()
             d.err_word = t["err"].data_ptr()
+            if self.layered:
+                descs = (nat.LayerDesc * nl)(*[self._layer_desc(x, t["argmax"][l], t["cols"][l])
+                                               for l, x in enumerate(b.geoms)])
+                self._keep.append(descs)
+                d.layers = ctypes.cast(descs, ctypes.POINTER(nat.LayerDesc))
+                d.part = t["part"].data_ptr()
+                if is_last:
+                    d.loss_kind = nat.PD_LOSS_CE
+                    d.logits = t["logits"].data_ptr()
             b.desc = d
             nat.check(L.pd_rt_add_stage(rt, ctypes.byref(d)), "pd_rt_add_stage")
         prog = np.ascontiguousarray(self.program.items_for_rank(self.rank))
@@ -420,8 +476,11 @@ class Executor:
         for row in self._prog:
             s = int(row[nat.IT_STAGE])
             if row[nat.IT_OP] == 1 and plan.stages[s].replication > 1:  # one gradient per replica per round
-                w = sum(a * b for a, b in zip(m.widths[plan.stages[s].first_layer - 1: plan.stages[s].last_layer],
-                                              m.widths[plan.stages[s].first_layer: plan.stages[s].last_layer + 1]))
+                if self.layered:
+                    w = sum(x.w_numel for x in self.geoms[plan.stages[s].first_layer - 1: plan.stages[s].last_layer])
+                else:
+                    w = sum(a * b for a, b in zip(m.widths[plan.stages[s].first_layer - 1: plan.stages[s].last_layer],
+                                                  m.widths[plan.stages[s].first_layer: plan.stages[s].last_layer + 1]))
                 total += (plan.stages[s].replication - 1) * w * 4 / plan.stages[s].replication
             if row[nat.IT_OP] == 0 and s < plan.num_stages - 1:
                 total += m.batch * m.widths[plan.stages[s].last_layer] * m.bytes_per_elem

@@ -97,3 +97,166 @@ def mlp_profile(spec: MLPSpec, tflops: float = 1000.0) -> ModelProfile:
 def mlp_context(spec: MLPSpec, machines: int = 1, bandwidth: float = 770e9, tflops: float = 1000.0):
     """CostContext for an MLP spec (bandwidth default: measured B200 NVLink peer copy)."""
     return build_context(mlp_profile(spec, tflops), HardwareSpec(machines, bandwidth, spec.bytes_per_elem))
+
+
+# ---------------------------------------------------------------- convolutional networks (configs[2])
+@dataclass(frozen=True)
+class LayerDef:
+    """One profile layer of a ConvNetSpec: a 3x3/pad-1 convolution (+ReLU, optional 2x2 max pool)
+    or a Linear layer (+ReLU unless it is the model output)."""
+
+    kind: str  # "conv" | "linear"
+    c_out: int
+    pool: bool = False
+
+
+@dataclass(frozen=True)
+class LayerGeom:
+    kind: str
+    h: int  # conv input spatial size
+    w: int
+    c_in: int  # channels (conv) / features (linear)
+    c_out: int
+    pool: bool
+    relu: bool
+    im2col: bool  # first conv on an image with < 64 channels
+    in_features: int
+    out_features: int  # per-sample, after pooling
+    pre_features: int  # per-sample, before pooling
+    w_shape: tuple[int, int]  # conv: Wt [9*c_in (or 64), c_out]; linear: [c_out, c_in]
+
+    @property
+    def w_numel(self) -> int:
+        return self.w_shape[0] * self.w_shape[1]
+
+    @property
+    def macs_per_sample(self) -> int:
+        """Multiply-adds of the forward pass per sample (algorithmic, unpadded)."""
+        if self.kind == "conv":
+            return self.h * self.w * 9 * self.c_in * self.c_out
+        return self.c_in * self.c_out
+
+
+@dataclass(frozen=True)
+class ConvNetSpec:
+    """A VGG-style network: NHWC bf16 images, conv/pool feature stack, Linear classifier, softmax
+    cross-entropy (mean over the minibatch).  Profile layer l (1-based) is ``layers[l-1]``; pools
+    belong to the convolution they follow (PipeDream's VGG-16 has 16 profile layers)."""
+
+    image: tuple[int, int, int]  # (H, W, C)
+    layers: tuple[LayerDef, ...]
+    batch: int = 32
+    dtype: str = "bf16"
+    lr: float = 1e-3
+    n_blocks: int = 4
+    seed: int = 0
+
+    def __post_init__(self):
+        object.__setattr__(self, "layers", tuple(self.layers))
+        if self.dtype != "bf16":
+            raise ValidationError("convolutional networks run in bf16 (tcgen05)")
+        if not self.layers or self.layers[-1].kind != "linear":
+            raise ValidationError("the model output must be a Linear layer (softmax cross-entropy)")
+        self.geoms()  # validates the shapes
+
+    @property
+    def num_layers(self) -> int:
+        return len(self.layers)
+
+    @property
+    def bytes_per_elem(self) -> int:
+        return 2
+
+    @property
+    def classes(self) -> int:
+        return self.layers[-1].c_out
+
+    def geoms(self) -> list[LayerGeom]:
+        h, w, c = self.image
+        out, flat = [], False
+        for i, ld in enumerate(self.layers):
+            last = i == len(self.layers) - 1
+            if ld.kind == "conv":
+                if flat:
+                    raise ValidationError("conv after a linear layer")
+                im2col = i == 0 and c < 64
+                if not im2col and c % 64:
+                    raise ValidationError(f"layer {i + 1}: conv input channels must be a multiple of 64 (got {c})")
+                if ld.c_out % 64:
+                    raise ValidationError(f"layer {i + 1}: conv output channels must be a multiple of 64")
+                if im2col and 9 * c > 64:
+                    raise ValidationError("the im2col'ed image layer supports at most 7 input channels")
+                if ld.pool and (h % 2 or w % 2):
+                    raise ValidationError(f"layer {i + 1}: pooling needs even spatial sizes")
+                ho, wo = (h // 2, w // 2) if ld.pool else (h, w)
+                out.append(LayerGeom("conv", h, w, c, ld.c_out, ld.pool, True, im2col, h * w * c, ho * wo * ld.c_out,
+                                     h * w * ld.c_out, ((64 if im2col else 9 * c), ld.c_out)))
+                h, w, c = ho, wo, ld.c_out
+            elif ld.kind == "linear":
+                fin = h * w * c
+                if ld.c_out % 8 or fin % 8:
+                    raise ValidationError(f"layer {i + 1}: linear widths must be multiples of 8")
+                out.append(LayerGeom("linear", 1, 1, fin, ld.c_out, False, not last, False, fin, ld.c_out, ld.c_out,
+                                     (ld.c_out, fin)))
+                h, w, c, flat = 1, 1, ld.c_out, True
+            else:
+                raise ValidationError(f"unknown layer kind {ld.kind!r}")
+        return out
+
+    @property
+    def widths(self) -> tuple[int, ...]:
+        """Per-sample features at every layer boundary (d_0 = the image)."""
+        g = self.geoms()
+        return (g[0].in_features,) + tuple(x.out_features for x in g)
+
+    def n_params(self) -> int:
+        return sum(x.w_numel + x.c_out for x in self.geoms())
+
+    def flops_per_sample(self) -> float:
+        """Algorithmic fwd+bwd FLOPs per sample (6 x MACs), minus the first layer's unneeded dgrad."""
+        macs = [x.macs_per_sample for x in self.geoms()]
+        return 6.0 * sum(macs) - 2.0 * macs[0]
+
+
+def vgg16(batch: int = 32, classes: int = 1000, image: int = 224, **kw) -> ConvNetSpec:
+    """VGG-16 (13 conv + 5 max pool + 3 FC), the network of BASELINE configs[2] / PAPER.md:816."""
+    cfg = [64, 64, "P", 128, 128, "P", 256, 256, 256, "P", 512, 512, 512, "P", 512, 512, 512, "P"]
+    layers = []
+    for v in cfg:
+        if v == "P":
+            layers[-1] = LayerDef("conv", layers[-1].c_out, pool=True)
+        else:
+            layers.append(LayerDef("conv", v))
+    layers += [LayerDef("linear", 4096), LayerDef("linear", 4096), LayerDef("linear", classes)]
+    return ConvNetSpec(image=(image, image, 3), layers=tuple(layers), batch=batch, **kw)
+
+
+def init_params_any(spec) -> list[tuple[np.ndarray, np.ndarray]]:
+    """Initial parameters of an MLP or ConvNet spec, fp64.  Conv weights are stored tap-major
+    Wt [9*c_in, c_out] (row (r*3+s)*c_in + c); the im2col'ed image layer pads rows 9*c_in..63
+    with zeros.  He-normal weights, N(0, 0.01^2) biases, one seeded PCG64 stream."""
+    if isinstance(spec, MLPSpec):
+        return init_params(spec)
+    rng = np.random.default_rng(spec.seed)
+    out = []
+    for g in spec.geoms():
+        if g.kind == "conv":
+            fan = 9 * g.c_in
+            W = np.zeros(g.w_shape)
+            W[:fan] = rng.normal(0.0, np.sqrt(2.0 / fan), size=(fan, g.c_out))
+        else:
+            W = rng.normal(0.0, np.sqrt(2.0 / g.c_in), size=g.w_shape)
+        out.append((W, rng.normal(0.0, 0.01, size=g.c_out)))
+    return out
+
+
+def make_data_any(spec):
+    """MLP: (X, T) as make_data.  ConvNet: images X [n_blocks, B, H, W, C] ~ N(0, 1) (fp64) and
+    labels [n_blocks, B] uniform over the classes (int32)."""
+    if isinstance(spec, MLPSpec):
+        return make_data(spec)
+    rng = np.random.default_rng([spec.seed, 1])
+    H, W, C = spec.image
+    X = rng.normal(0.0, 1.0, size=(spec.n_blocks, spec.batch, H, W, C))
+    y = rng.integers(0, spec.classes, size=(spec.n_blocks, spec.batch)).astype(np.int32)
+    return X, y

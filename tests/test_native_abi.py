@@ -12,7 +12,7 @@ HEADER = Path(__file__).resolve().parents[1] / "include" / "pd_b200.h"
 
 def declared():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(pd_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(pd_\w+)\s*\(", text, re.M)))
 
 
 def test_header_and_binding_agree():
