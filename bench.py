@@ -36,6 +36,8 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", choices=["mlp", "vgg"], default="mlp",
+                   help="mlp: configs[1] MLP-8192 straight pipeline (headline); vgg: configs[2] VGG-16 7-1")
     p.add_argument("--batch", type=int, default=2048)
     p.add_argument("--minibatches", type=int, default=64)
     p.add_argument("--width", type=int, default=8192)
@@ -44,12 +46,28 @@ def parse():
     p.add_argument("--mode", default="weight_stashing")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=3)
-    p.add_argument("--serial", choices=["on", "off"], default="on",
-                   help="single-GPU: issue all hosted stages on one stream (on) or one stream per stage (off)")
+    p.add_argument("--serial", choices=["on", "off"], default="off",
+                   help="timed region: issue all hosted stages on one stream (on) or one stream per stage (off); "
+                        "the roofline pass is always serial so per-kernel events are not inflated by overlap")
     return p.parse_args()
 
 
 def workload(args):
+    if args.workload == "vgg":
+        return {
+            "workload": "cfg3: VGG-16 on synthetic 224x224 images, PipeDream 7-1 (conv stack replicated 7x with "
+                        "round-rule peer-memory allreduce, FC stage 1x), 1F1B-RR weight_stashing",
+            "minibatch": args.batch,
+            "minibatches_per_step": args.minibatches,
+            "stages": 2,
+            "workers": 8,
+            "workers_per_gpu": 8 // max(1, args.gpus),
+            "lr": 1e-3,
+            "l2": "working set > 100x L2 (126 MB); no flush needed",
+            "loss": "softmax cross-entropy, mean over the minibatch",
+            "streams": "one per GPU (workers in program order)" if args.serial == "on" else "one per worker",
+            "roofline_timing": "per-GEMM CUDA events over one extra serial step (no inter-worker overlap)",
+        }
     return {
         "workload": f"cfg2: {args.stages}-stage {args.layers}-layer MLP-{args.width} bf16 straight pipeline, "
                     f"1F1B {args.mode}",
@@ -61,6 +79,7 @@ def workload(args):
         "l2": "working set > 100x L2 (126 MB); no flush needed",
         "loss": "1/(2B) sum (Z-T)^2",
         "streams": "one per GPU (stages in program order)" if args.serial == "on" else "one per stage",
+        "roofline_timing": "per-GEMM CUDA events over one extra serial step (no inter-stage overlap)",
     }
 
 
@@ -169,24 +188,61 @@ def cpu_sample(args, seconds=12.0, batch=128, max_minibatches=3):
                       f"(fwd+bwd+SGD, numpy fp32, weight-stashing versions) in {el:.1f} s"}
 
 
+def cpu_sample_vgg(args, seconds=12.0, batch=4, max_minibatches=2):
+    """Time the conv-net oracle (torch CPU fp32, all host threads) on a bounded VGG-16 sample."""
+    import numpy as np
+    import torch
+
+    import paper_1806_03377_b200 as pd
+    from oracle.convnet_oracle import convnet_train
+
+    torch.set_num_threads(os.cpu_count())
+    spec = pd.vgg16(batch=batch)
+    key = ("vgg", batch)
+    if key not in _CPU_CACHE:
+        rng = np.random.default_rng(0)
+        params = [(rng.standard_normal(g.w_shape, dtype=np.float32) * np.float32(0.01),
+                   np.zeros(g.c_out, dtype=np.float32)) for g in spec.geoms()]
+        X = rng.standard_normal((1, batch, 224, 224, 3), dtype=np.float32)
+        y = rng.integers(0, 1000, size=(1, batch)).astype(np.int32)
+        _CPU_CACHE[key] = (params, X, y)
+    params, X, y = _CPU_CACHE[key]
+    done, t0 = 0, time.perf_counter()
+    while True:
+        convnet_train(spec.geoms(), params, X, y, 1e-3, [(1, 13), (14, 16)], lambda s, mb, d: 0, 1, emulate=None,
+                      dtype=torch.float32)
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or done >= max_minibatches:
+            break
+    return {"value": done * batch / el, "unit": "samples/s", "cores": torch.get_num_threads(), "kind": "port",
+            "sample": f"{done} minibatch(es) of {batch} images through all 16 VGG-16 layers "
+                      f"(fwd+bwd+SGD, torch-CPU fp32 conv-net oracle) in {el:.1f} s"}
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
     import numpy as np  # noqa: F401
 
     cfg = workload(args)
+    vgg = args.workload == "vgg"
+    one = (lambda: cpu_sample_vgg(args, seconds=0.0, max_minibatches=1)) if vgg else \
+        (lambda: cpu_sample(args, seconds=0.0, max_minibatches=1))
+    per_step = 4 if vgg else 128
     for _ in range(args.warmup):
-        cpu_sample(args, seconds=0.0, max_minibatches=1)
+        one()
     vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_sample(args, seconds=0.0, max_minibatches=1))
+        vals.append(one())
     el = time.perf_counter() - t0
-    samples = 128 * len(vals)
+    samples = per_step * len(vals)
     value = samples / el
     cb = dict(vals[-1])
     cb["value"] = value
-    cb["sample"] = f"{args.steps} steps x 1 minibatch of 128 samples, all {args.layers} layers, numpy fp32"
+    cb["sample"] = (f"{args.steps} steps x 1 minibatch of 4 images, all 16 VGG-16 layers, torch-CPU fp32" if vgg else
+                    f"{args.steps} steps x 1 minibatch of 128 samples, all {args.layers} layers, numpy fp32")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
@@ -202,11 +258,16 @@ def run_ours(args, rank, world):
 
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     dev = torch.cuda.current_device()
-    per = args.layers // args.stages
-    stages = tuple(pd.Stage(s * per + 1, (s + 1) * per, 1) for s in range(args.stages))
-    plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=args.stages, machines_used=args.stages)
+    if args.workload == "vgg":
+        # PipeDream's VGG-16 partition on 8 machines: conv stack x7, FC stage x1
+        plan = pd.Plan(stages=(pd.Stage(1, 13, 7), pd.Stage(14, 16, 1)), bottleneck_time=1.0, noam=2, machines_used=8)
+        spec = pd.vgg16(batch=args.batch, lr=1e-3, n_blocks=2, seed=0)
+    else:
+        per = args.layers // args.stages
+        stages = tuple(pd.Stage(s * per + 1, (s + 1) * per, 1) for s in range(args.stages))
+        plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=args.stages, machines_used=args.stages)
+        spec = pd.mlp(args.width, args.layers, batch=args.batch, dtype="bf16", lr=1e-5, n_blocks=4, seed=0)
     cfg = pd.SimConfig(plan=plan, mode=args.mode, num_minibatches=args.minibatches)
-    spec = pd.mlp(args.width, args.layers, batch=args.batch, dtype="bf16", lr=1e-5, n_blocks=4, seed=0)
     ex = pd.Executor(cfg, model=spec)
     ex.set_serial(args.serial == "on")
     dist = torch.distributed if world > 1 else None
@@ -221,7 +282,6 @@ def run_ours(args, rank, world):
     torch.cuda.synchronize()
     # ---------------- timed region (device events, max over ranks)
     launches0 = ex.launch_count()
-    ex.kernel_timing(True)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clocks:
         barrier()
@@ -238,8 +298,15 @@ def run_ours(args, rank, world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     launches = ex.launch_count() - launches0
+    # ---------------- roofline pass: one serial step with per-GEMM CUDA events on the launching stream
+    barrier()
+    ex.set_serial(True)
+    ex.kernel_timing(True)
+    ex.step(stream=stream)
+    torch.cuda.synchronize()
     kstats = ex.kernel_stats()
     ex.kernel_timing(False)
+    ex.set_serial(args.serial == "on")
     samples = args.steps * args.minibatches * args.batch
     value = samples / (ms * 1e-3)
     # ---------------- traced step: bubble / utilisation with the reference's window rule
@@ -249,10 +316,13 @@ def run_ours(args, rank, world):
     res = ex.result()
     # ---------------- e2e through the public API with host buffers
     X_host = torch.randn(spec.n_blocks, spec.batch, spec.widths[0]).to(torch.bfloat16).pin_memory()
-    T_host = torch.randn(spec.n_blocks, spec.batch, spec.widths[-1]).pin_memory()
+    if args.workload == "vgg":
+        T_host = torch.randint(0, spec.classes, (spec.n_blocks, spec.batch), dtype=torch.int32).pin_memory()
+    else:
+        T_host = torch.randn(spec.n_blocks, spec.batch, spec.widths[-1]).pin_memory()
     loss_host = torch.empty(args.minibatches + 1, dtype=torch.float32).pin_memory()
     hosts_first = ex.hosts_stage(0)
-    hosts_last = ex.hosts_stage(args.stages - 1)
+    hosts_last = ex.hosts_stage(cfg.plan.num_stages - 1)
     h2d = (X_host.numel() * X_host.element_size() if hosts_first else 0) + \
           (T_host.numel() * T_host.element_size() if hosts_last else 0)
     d2h = loss_host.numel() * 4 if hosts_last else 0
@@ -290,7 +360,7 @@ def run_ours(args, rank, world):
     if os.path.exists(tpath):
         with open(tpath) as fh:
             tr = json.load(fh)
-        if tr.get("batch") == args.batch and tr.get("width") == args.width:  # captured at this shape
+        if args.workload == "mlp" and tr.get("batch") == args.batch and tr.get("width") == args.width:
             traffic = tr.get(dom_name)
     per_class = {k: {"launches": v["launches"], "avg_ms": round(v["avg_ms"], 4),
                      "tflops": round(v["flops_per_launch"] / (v["avg_ms"] * 1e-3) / 1e12, 1),
@@ -302,7 +372,9 @@ def run_ours(args, rank, world):
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": workload(args),
-        "roofline": {"bound": "tensor", "kernel": f"k_gemm_tc ({dom_name})", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "tensor",
+                     "kernel": f"k_gemm_tc ({dom_name}{', conv + linear' if args.workload == 'vgg' else ''})",
+                     "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} bf16_tflops_sustained (MEASURED_PEAKS.json)"},
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -318,13 +390,18 @@ def run_ours(args, rank, world):
         "steady_minibatches_per_s": rep.steady_throughput if rep else None,
     }
     if not args.no_cpu_baseline and world == 1:
-        out["cpu_baseline"] = cpu_sample(args)
+        out["cpu_baseline"] = cpu_sample_vgg(args) if args.workload == "vgg" else cpu_sample(args)
     ex.close()
     print(json.dumps(out), flush=True)
 
 
 def main():
     args = parse()
+    if args.workload == "vgg":
+        if "--batch" not in sys.argv:
+            args.batch = 32
+        if "--minibatches" not in sys.argv:
+            args.minibatches = 42  # 6 allreduce rounds of 7; >= 37 for the reference's steady window
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":

@@ -95,7 +95,7 @@ def _backward(geoms, weights, saved, dz, q):
             dy = _pool_bwd(d, arg) if g.pool else d
             dW = torch.nn.grad.conv2d_weight(xin.permute(0, 3, 1, 2), (g.c_out, g.c_in, 3, 3), dy.permute(0, 3, 1, 2),
                                              padding=1)
-            gWt = torch.zeros(g.w_shape, dtype=torch.float64)
+            gWt = torch.zeros(g.w_shape, dtype=dW.dtype)
             gWt[: 9 * g.c_in] = dW.permute(2, 3, 1, 0).reshape(9 * g.c_in, g.c_out)
             grads[l] = (gWt, dy.reshape(-1, g.c_out).sum(0))
             if l > 0:
@@ -109,14 +109,16 @@ def _backward(geoms, weights, saved, dz, q):
     return grads
 
 
-def convnet_train(geoms, params, X, labels, lr, stage_bounds, versions, K, emulate: str | None = "bf16", reps=None):
+@torch.no_grad()
+def convnet_train(geoms, params, X, labels, lr, stage_bounds, versions, K, emulate: str | None = "bf16", reps=None,
+                  dtype=torch.float64):
     """Delayed-SGD pipeline training of a conv net (see module docstring).
 
     geoms: per-layer geometry objects (kind, h, w, c_in, c_out, pool, relu, w_shape);
     params: [(W, b)] fp64 numpy per layer; X [n_blocks, B, H, W, C]; labels [n_blocks, B].
+    dtype: arithmetic type (float64 for parity; float32 for the timed CPU baseline, no emulation).
     Returns (losses[K], final params list of numpy (W, b)).
     """
-    torch.set_grad_enabled(False)
     q = _q_t if emulate == "bf16" else (lambda a: a)
     master = _f32_t if emulate == "bf16" else (lambda a: a)
     n = len(stage_bounds)
@@ -125,15 +127,16 @@ def convnet_train(geoms, params, X, labels, lr, stage_bounds, versions, K, emula
     for s, (a, b) in enumerate(stage_bounds):
         for l in range(a, b + 1):
             layer_stage[l - 1] = s
-    archives = [{0: [(master(torch.from_numpy(np.asarray(params[l - 1][0], np.float64))),
-                      master(torch.from_numpy(np.asarray(params[l - 1][1], np.float64)))) for l in range(a, b + 1)]}
+    archives = [{0: [(master(torch.from_numpy(np.asarray(params[l - 1][0], np.float64)).to(dtype)),
+                      master(torch.from_numpy(np.asarray(params[l - 1][1], np.float64)).to(dtype)))
+                     for l in range(a, b + 1)]}
                 for (a, b) in stage_bounds]
     latest_v = [0] * n
     first = [a - 1 for a, _ in stage_bounds]
     losses, round_acc = [], {}
     for mb in range(1, K + 1):
         blk = (mb - 1) % X.shape[0]
-        x = torch.from_numpy(np.asarray(X[blk], np.float64))
+        x = torch.from_numpy(np.asarray(X[blk], np.float64)).to(dtype)
         y = torch.from_numpy(np.asarray(labels[blk], np.int64))
         B = x.shape[0]
         fv = [versions(s, mb, "forward") for s in range(n)]
@@ -167,5 +170,5 @@ def convnet_train(geoms, params, X, labels, lr, stage_bounds, versions, K, emula
             latest_v[s] = mb
     final = []
     for s in range(n):
-        final.extend((W.numpy(), b.numpy()) for W, b in archives[s][latest_v[s]])
+        final.extend((W.double().numpy(), b.double().numpy()) for W, b in archives[s][latest_v[s]])
     return np.array(losses), final

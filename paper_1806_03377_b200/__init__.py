@@ -31,7 +31,19 @@ from .ledger import (  # noqa: F401
     staleness_check,
     write_trace_csv,
 )
-from .models import MLPSpec, init_params, make_data, mlp, mlp_context, mlp_profile  # noqa: F401
+from .models import (  # noqa: F401
+    ConvNetSpec,
+    LayerDef,
+    MLPSpec,
+    init_params,
+    init_params_any,
+    make_data,
+    make_data_any,
+    mlp,
+    mlp_context,
+    mlp_profile,
+    vgg16,
+)
 from .orders import (  # noqa: F401
     Direction,
     Schedule,
