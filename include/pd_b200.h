@@ -32,7 +32,12 @@ extern "C" {
 
 enum pd_status { PD_OK = 0, PD_ERR_INVALID = 1, PD_ERR_CUDA = 2, PD_ERR_TIMEOUT = 3, PD_ERR_DEADLOCK = 4 };
 enum pd_dtype { PD_F32 = 0, PD_BF16 = 1 };
-enum pd_epi_kind { PD_EPI_STORE = 0, PD_EPI_LOSS = 1, PD_EPI_MASK = 2, PD_EPI_SGD = 3, PD_EPI_GRADF32 = 4 };
+enum pd_epi_kind {
+  PD_EPI_STORE = 0, PD_EPI_LOSS = 1, PD_EPI_MASK = 2, PD_EPI_SGD = 3, PD_EPI_GRADF32 = 4,
+  PD_EPI_GELU = 5,      /* z = acc + bias -> aux; out = gelu_tanh(z)        (A, B K-major) */
+  PD_EPI_GELU_BWD = 6,  /* out = acc * gelu_tanh'(mask)                     (A K-major, B MN-major) */
+  PD_EPI_RESID = 7      /* out = acc + bias + mask (residual stream)        (A, B K-major) */
+};
 
 /* ------------------------------------------------------------------ library */
 int pd_abi_version(void);
@@ -60,6 +65,7 @@ typedef struct pd_epilogue {
   float* master;        /* SGD: fp32 latest weights, master -= lr*acc, out = cast(master) */
   int64_t ldw;
   float lr;
+  void* aux;            /* GELU: pre-activation output, ld = ldo */
 } pd_epilogue;
 
 int pd_gemm(int dtype, const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M, int N,
@@ -197,23 +203,57 @@ typedef struct pd_stage_desc {
                                pd_layer_scratch_floats) */
 } pd_stage_desc;
 
-enum pd_layer_kind { PD_LAYER_LINEAR = 0, PD_LAYER_CONV3 = 1 };
+enum pd_layer_kind { PD_LAYER_LINEAR = 0, PD_LAYER_CONV3 = 1, PD_LAYER_EMBED = 2, PD_LAYER_BLOCK = 3, PD_LAYER_HEAD = 4 };
 enum pd_loss_kind { PD_LOSS_MSE = 0, PD_LOSS_CE = 1 };
 
+/* Transformer layers (GPT-2, configs[3]); T = batch * seq tokens, d = c_in:
+ *   EMBED  c_in = padded vocab Vp, c_out = d, h = seq.  input int32 tokens [T];
+ *          weights [wte Vp x d | wpe seq x d]; no biases.
+ *   BLOCK  pre-LN transformer block, c_in = c_out = d, h = seq, w = heads (head dim 64), ffn.
+ *          weights [Wqkv 3d x d | Wo d x d | W1 ffn x d | W2 d x ffn] ([out, in] each);
+ *          biases  [bqkv 3d | bo d | b1 ffn | b2 d | ln1 gamma,beta 2d | ln2 gamma,beta 2d].
+ *   HEAD   final LayerNorm + LM head + softmax cross-entropy over `vocab` of c_out = Vp logits;
+ *          c_in = d, h = seq; weights [W Vp x d]; biases [lnf gamma,beta 2d]; the stage's target
+ *          blocks are int32 next-token labels [T], dz_last holds dlogits [T, Vp], logits fp32 [T, Vp].
+ * save[act_depth]: per in-flight minibatch tensors the backward needs (pd_layer_save_bytes);
+ * work: per-stage backward scratch shared by the stage's layers (pd_layer_work_bytes). */
 typedef struct pd_layer {
   int kind;                 /* pd_layer_kind */
   int relu;                 /* ReLU after the layer */
   int pool;                 /* CONV3: 2x2/2 max pool after the ReLU */
   int im2col;               /* CONV3 with c_in < 64 (the image layer): explicit im2col to 64 columns */
-  int h, w;                 /* CONV3: input (= pre-pool output) spatial size */
-  int c_in, c_out;          /* channels (CONV3) or features (LINEAR) */
+  int h, w;                 /* CONV3: input (= pre-pool output) spatial size; transformer: seq, heads */
+  int c_in, c_out;          /* channels (CONV3) or features (LINEAR); see above for transformer kinds */
   uint8_t* const* argmax;   /* pool: [act_depth] uint8 [batch, h/2, w/2, c_out] */
   void* const* cols;        /* im2col: [act_depth] dtype [batch*h*w, 64] */
+  int ffn;                  /* BLOCK: hidden width */
+  int vocab;                /* HEAD: valid vocabulary (<= c_out) */
+  void* const* save;        /* transformer kinds: [act_depth] saved tensors */
+  void* work;               /* transformer kinds: backward scratch */
 } pd_layer;
 
 /* fp32 elements the stage's `part` scratch needs for this layer (split-K partials of the weight
  * gradient, then the bias column-sum blocks; the larger of the two). */
 int64_t pd_layer_scratch_floats(const pd_layer* layer, int batch);
+/* Bytes of one `save` slot and of the `work` scratch of a transformer layer (0 for others). */
+int64_t pd_layer_save_bytes(const pd_layer* layer, int batch);
+int64_t pd_layer_work_bytes(const pd_layer* layer, int batch);
+/* Transformer kernels (also used by the runtime): causal flash attention (head dim 64),
+ * LayerNorm, embeddings, vocabulary-padded cross-entropy.  See csrc/attention.cu, transformer.cu. */
+int pd_attention_fwd(const void* qkv, void* out, float* lse, int batch, int seq, int heads, void* stream);
+int pd_attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse, float* dvec,
+                     float* dq_acc, void* dqkv, int batch, int seq, int heads, void* stream);
+int pd_layernorm_fwd(const void* x, const float* gb, void* y, float* mean, float* rstd, int64_t rows, int d,
+                     void* stream);
+int pd_layernorm_bwd_blocks(int64_t rows);
+int pd_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gb,
+                     const void* dres, void* dx, float* part, int64_t rows, int d, void* stream);
+int pd_embedding_fwd(const int* tok, const void* wte, const void* wpe, void* x, int64_t tokens, int seq, int d,
+                     void* stream);
+int pd_embedding_bwd(const int* tok, const void* dx, float* gte, float* gpe, int64_t tokens, int seq, int d,
+                     void* stream);
+int pd_softmax_ce_vocab(const float* logits, int64_t ldz, const int* labels, int64_t rows, int v, int vpad, void* dz,
+                        int64_t ldd, float* loss, void* stream);
 
 /* What any worker (in this process or a peer-mapped one in another) exposes to the others. */
 typedef struct pd_worker_view {

@@ -33,7 +33,9 @@ from .ledger import (  # noqa: F401
 )
 from .models import (  # noqa: F401
     ConvNetSpec,
+    GPTSpec,
     LayerDef,
+    gpt2_medium,
     MLPSpec,
     init_params,
     init_params_any,

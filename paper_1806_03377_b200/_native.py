@@ -17,7 +17,7 @@ from .errors import NativeError, SimulationError, ValidationError
 LIB_PATH = Path(__file__).resolve().parent / "libpd_b200.so"
 
 PD_F32, PD_BF16 = 0, 1
-EPI_STORE, EPI_LOSS, EPI_MASK, EPI_SGD, EPI_GRADF32 = range(5)
+EPI_STORE, EPI_LOSS, EPI_MASK, EPI_SGD, EPI_GRADF32, EPI_GELU, EPI_GELU_BWD, EPI_RESID = range(8)
 ITEM_WIDTH = 20
 (IT_OP, IT_STAGE, IT_MB, IT_WORKER, IT_VERSION, IT_WSLOT, IT_WNEW, IT_ACT, IT_XSLOT, IT_GSLOT, IT_OUT,
  IT_BLOCK, IT_DEP, IT_WAR, IT_RWAIT, IT_AWAIT, IT_DST, IT_SRC, IT_ROUND) = range(19)
@@ -30,6 +30,8 @@ EXPORTED = (
     "pd_rt_records", "pd_rt_set_serial", "pd_rt_kernel_timing", "pd_rt_kernel_stats", "pd_rt_launch_count", "pd_rt_destroy",
     "pd_conv3x3", "pd_splitk_plan", "pd_maxpool2", "pd_maxpool2_bwd", "pd_im2col3", "pd_reduce_sgd",
     "pd_colsum_blocks", "pd_bias_grad_tall", "pd_softmax_ce", "pd_memcpy_async", "pd_layer_scratch_floats",
+    "pd_layer_save_bytes", "pd_layer_work_bytes", "pd_attention_fwd", "pd_attention_bwd", "pd_layernorm_fwd",
+    "pd_layernorm_bwd_blocks", "pd_layernorm_bwd", "pd_embedding_fwd", "pd_embedding_bwd", "pd_softmax_ce_vocab",
 )
 PD_CONV_FWD, PD_CONV_DGRAD, PD_CONV_WGRAD, PD_GEMM_WGRAD_SPLITK = range(4)
 
@@ -38,11 +40,11 @@ class Epilogue(Structure):
     _fields_ = [
         ("kind", c_int), ("out", c_void_p), ("ldo", c_int64), ("bias", c_void_p), ("relu", c_int),
         ("mask", c_void_p), ("ldm", c_int64), ("target", c_void_p), ("ldt", c_int64), ("scale", c_float),
-        ("loss", c_void_p), ("master", c_void_p), ("ldw", c_int64), ("lr", c_float),
+        ("loss", c_void_p), ("master", c_void_p), ("ldw", c_int64), ("lr", c_float), ("aux", c_void_p),
     ]
 
 
-PD_LAYER_LINEAR, PD_LAYER_CONV3 = 0, 1
+PD_LAYER_LINEAR, PD_LAYER_CONV3, PD_LAYER_EMBED, PD_LAYER_BLOCK, PD_LAYER_HEAD = range(5)
 PD_LOSS_MSE, PD_LOSS_CE = 0, 1
 
 
@@ -50,6 +52,7 @@ class LayerDesc(Structure):
     _fields_ = [
         ("kind", c_int), ("relu", c_int), ("pool", c_int), ("im2col", c_int), ("h", c_int), ("w", c_int),
         ("c_in", c_int), ("c_out", c_int), ("argmax", POINTER(c_void_p)), ("cols", POINTER(c_void_p)),
+        ("ffn", c_int), ("vocab", c_int), ("save", POINTER(c_void_p)), ("work", c_void_p),
     ]
 
 
@@ -138,6 +141,18 @@ def lib() -> ctypes.CDLL:
         L.pd_memcpy_async.argtypes = [c_void_p, c_void_p, c_int64, c_void_p]
         L.pd_layer_scratch_floats.argtypes = [POINTER(LayerDesc), c_int]
         L.pd_layer_scratch_floats.restype = c_int64
+        for fn in ("pd_layer_save_bytes", "pd_layer_work_bytes"):
+            getattr(L, fn).argtypes = [POINTER(LayerDesc), c_int]
+            getattr(L, fn).restype = c_int64
+        L.pd_attention_fwd.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p]
+        L.pd_attention_bwd.argtypes = [c_void_p] * 7 + [c_int, c_int, c_int, c_void_p]
+        L.pd_layernorm_fwd.argtypes = [c_void_p] * 5 + [c_int64, c_int, c_void_p]
+        L.pd_layernorm_bwd_blocks.argtypes = [c_int64]
+        L.pd_layernorm_bwd.argtypes = [c_void_p] * 8 + [c_int64, c_int, c_void_p]
+        L.pd_embedding_fwd.argtypes = [c_void_p] * 4 + [c_int64, c_int, c_int, c_void_p]
+        L.pd_embedding_bwd.argtypes = [c_void_p] * 4 + [c_int64, c_int, c_int, c_void_p]
+        L.pd_softmax_ce_vocab.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_int, c_int, c_void_p, c_int64,
+                                          c_void_p, c_void_p]
         _lib = L
     return _lib
 

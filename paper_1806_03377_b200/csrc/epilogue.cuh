@@ -17,7 +17,13 @@
 
 namespace pd {
 
-enum EpiKind : int { EPI_STORE = 0, EPI_LOSS = 1, EPI_MASK = 2, EPI_SGD = 3, EPI_GRADF32 = 4 };
+//   EPI_GELU   : z = acc + bias; aux = z; out = gelu(z)        (transformer FC1, tanh GELU)
+//   EPI_GELU_BWD: out = acc * gelu'(mask)                       (FC2 dgrad, mask = saved z)
+//   EPI_RESID  : out = acc + bias + mask                        (projection + residual stream)
+enum EpiKind : int {
+  EPI_STORE = 0, EPI_LOSS = 1, EPI_MASK = 2, EPI_SGD = 3, EPI_GRADF32 = 4,
+  EPI_GELU = 5, EPI_GELU_BWD = 6, EPI_RESID = 7
+};
 
 struct EpiArgs {
   void* out;            // activation dtype (fp32 for EPI_GRADF32)
@@ -33,7 +39,19 @@ struct EpiArgs {
   float* master;        // SGD: fp32 latest weights [M, N]
   int64_t ldw;
   float lr;             // SGD
+  void* aux;            // GELU: pre-activation output (activation dtype, ld = ldo)
 };
+
+// GPT-2's tanh GELU and its derivative.
+__device__ __forceinline__ float gelu_f(float x) {
+  const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+  return 0.5f * x * (1.f + tanhf(u));
+}
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+  const float t = tanhf(u);
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * 0.7978845608028654f * (1.f + 0.134145f * x * x);
+}
 
 // Operand sources of the tcgen05 GEMM (gemm.cu).  SRC_2D: both operands are 2-D row-major
 // matrices.  The three implicit-GEMM 3x3/stride-1/pad-1 convolution passes (NHWC activations,
@@ -79,13 +97,26 @@ __device__ __forceinline__ float epi_elem(const EpiArgs& ep, int64_t r, int64_t 
     float m = to_f<T>(static_cast<const T*>(ep.mask)[r * ep.ldm + c]);
     static_cast<T*>(ep.out)[r * ep.ldo + c] = from_f<T>(m > 0.f ? v : 0.f);
     return 0.f;
+  } else if constexpr (KIND == EPI_GELU) {
+    const float z = v + (ep.bias ? ep.bias[c] : 0.f);
+    static_cast<T*>(ep.aux)[r * ep.ldo + c] = from_f<T>(z);
+    static_cast<T*>(ep.out)[r * ep.ldo + c] = from_f<T>(gelu_f(to_f<T>(from_f<T>(z))));
+    return 0.f;
+  } else if constexpr (KIND == EPI_GELU_BWD) {
+    const float z = to_f<T>(static_cast<const T*>(ep.mask)[r * ep.ldm + c]);
+    static_cast<T*>(ep.out)[r * ep.ldo + c] = from_f<T>(v * gelu_grad_f(z));
+    return 0.f;
+  } else if constexpr (KIND == EPI_RESID) {
+    const float x = v + (ep.bias ? ep.bias[c] : 0.f) + to_f<T>(static_cast<const T*>(ep.mask)[r * ep.ldm + c]);
+    static_cast<T*>(ep.out)[r * ep.ldo + c] = from_f<T>(x);
+    return 0.f;
   } else if constexpr (KIND == EPI_SGD) {
     float w = ep.master[r * ep.ldw + c] - ep.lr * v;
     ep.master[r * ep.ldw + c] = w;
     static_cast<T*>(ep.out)[r * ep.ldo + c] = from_f<T>(w);
     return 0.f;
   } else {
-    static_cast<float*>(ep.out)[r * ep.ldo + c] = v;
+    static_cast<float*>(ep.out)[r * ep.ldo + c] = v + (ep.bias ? ep.bias[c] : 0.f);
     return 0.f;
   }
 }
@@ -108,6 +139,8 @@ template <int KIND> struct Aux { };
 template <> struct Aux<EPI_SGD> { float4 m[8]; };
 template <> struct Aux<EPI_MASK> { uint4 m[4]; };
 template <> struct Aux<EPI_LOSS> { float4 t[8]; };
+template <> struct Aux<EPI_GELU_BWD> { uint4 m[4]; };
+template <> struct Aux<EPI_RESID> { uint4 m[4]; };
 
 template <int KIND>
 __device__ __forceinline__ void aux_load(const EpiArgs& ep, int64_t r, int64_t c0, Aux<KIND>& a) {
@@ -115,7 +148,7 @@ __device__ __forceinline__ void aux_load(const EpiArgs& ep, int64_t r, int64_t c
     const float4* w4 = reinterpret_cast<const float4*>(ep.master + r * ep.ldw + c0);
 #pragma unroll
     for (int i = 0; i < 8; ++i) a.m[i] = w4[i];
-  } else if constexpr (KIND == EPI_MASK) {
+  } else if constexpr (KIND == EPI_MASK || KIND == EPI_GELU_BWD || KIND == EPI_RESID) {
     const uint4* m4 =
         reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(ep.mask) + r * ep.ldm + c0);
 #pragma unroll
@@ -174,6 +207,50 @@ __device__ __forceinline__ float apply_chunk(const EpiArgs& ep, int64_t r, int64
         unpack_bf16x2(mw[j], x0, x1);
         if (!(x0 > 0.f)) v[8 * i + 2 * j] = 0.f;
         if (!(x1 > 0.f)) v[8 * i + 2 * j + 1] = 0.f;
+      }
+    }
+    store32_bf16(ep.out, ep.ldo, r, c0, v);
+  } else if constexpr (KIND == EPI_GELU) {
+    if (ep.bias) {
+      const float4* b4 = reinterpret_cast<const float4*>(ep.bias + c0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 b = __ldg(b4 + i);
+        v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
+      }
+    }
+    store32_bf16(ep.aux, ep.ldo, r, c0, v);
+    // the stored (bf16) pre-activation is what the backward sees: apply GELU to the rounded value
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = gelu_f(__bfloat162float(__float2bfloat16_rn(v[i])));
+    store32_bf16(ep.out, ep.ldo, r, c0, v);
+  } else if constexpr (KIND == EPI_GELU_BWD || KIND == EPI_RESID) {
+    float bb[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) bb[i] = 0.f;
+    if (KIND == EPI_RESID && ep.bias) {
+      const float4* b4 = reinterpret_cast<const float4*>(ep.bias + c0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 b = __ldg(b4 + i);
+        bb[4 * i] = b.x; bb[4 * i + 1] = b.y; bb[4 * i + 2] = b.z; bb[4 * i + 3] = b.w;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t mw[4] = {a.m[i].x, a.m[i].y, a.m[i].z, a.m[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float x0, x1;
+        unpack_bf16x2(mw[j], x0, x1);
+        const int k = 8 * i + 2 * j;
+        if constexpr (KIND == EPI_GELU_BWD) {
+          v[k] *= gelu_grad_f(x0);
+          v[k + 1] *= gelu_grad_f(x1);
+        } else {
+          v[k] += bb[k] + x0;
+          v[k + 1] += bb[k + 1] + x1;
+        }
       }
     }
     store32_bf16(ep.out, ep.ldo, r, c0, v);

@@ -710,8 +710,20 @@ static int dispatch_kind(int kind, const void* A, int64_t lda, const void* B, in
     case EPI_MASK: return launch_bn<A_MN, B_MN, EPI_MASK>(A, lda, B, ldb, M, N, K, ep, st);
     case EPI_SGD: return launch_bn<A_MN, B_MN, EPI_SGD>(A, lda, B, ldb, M, N, K, ep, st);
     case EPI_GRADF32: return launch_bn<A_MN, B_MN, EPI_GRADF32>(A, lda, B, ldb, M, N, K, ep, st);
+    case EPI_GELU:
+      if constexpr (!A_MN && !B_MN) return launch_bn<A_MN, B_MN, EPI_GELU>(A, lda, B, ldb, M, N, K, ep, st);
+      break;
+    case EPI_RESID:
+      if constexpr (!A_MN && !B_MN) return launch_bn<A_MN, B_MN, EPI_RESID>(A, lda, B, ldb, M, N, K, ep, st);
+      break;
+    case EPI_GELU_BWD:
+      if constexpr (!A_MN && B_MN) return launch_bn<A_MN, B_MN, EPI_GELU_BWD>(A, lda, B, ldb, M, N, K, ep, st);
+      break;
+    default:
+      return set_error(PD_ERR_INVALID, "unknown epilogue kind %d", kind);
   }
-  return set_error(PD_ERR_INVALID, "unknown epilogue kind %d", kind);
+  return set_error(PD_ERR_INVALID, "epilogue kind %d is not instantiated for operand majors (%d, %d)", kind,
+                   (int)A_MN, (int)B_MN);
 }
 
 // ============================================================== 3x3 convolution passes
@@ -807,6 +819,9 @@ static int simt(const void* A, int a_mn, int64_t lda, const void* B, int b_mn, i
     case EPI_MASK: k_gemm_simt<T, EPI_MASK><<<grid, 256, 0, st>>>(a, a_mn, lda, b, b_mn, ldb, M, N, K, ep); break;
     case EPI_SGD: k_gemm_simt<T, EPI_SGD><<<grid, 256, 0, st>>>(a, a_mn, lda, b, b_mn, ldb, M, N, K, ep); break;
     case EPI_GRADF32: k_gemm_simt<T, EPI_GRADF32><<<grid, 256, 0, st>>>(a, a_mn, lda, b, b_mn, ldb, M, N, K, ep); break;
+    case EPI_GELU: k_gemm_simt<T, EPI_GELU><<<grid, 256, 0, st>>>(a, a_mn, lda, b, b_mn, ldb, M, N, K, ep); break;
+    case EPI_GELU_BWD: k_gemm_simt<T, EPI_GELU_BWD><<<grid, 256, 0, st>>>(a, a_mn, lda, b, b_mn, ldb, M, N, K, ep); break;
+    case EPI_RESID: k_gemm_simt<T, EPI_RESID><<<grid, 256, 0, st>>>(a, a_mn, lda, b, b_mn, ldb, M, N, K, ep); break;
     default: return set_error(PD_ERR_INVALID, "unknown epilogue kind %d", kind);
   }
   cudaError_t e = cudaGetLastError();

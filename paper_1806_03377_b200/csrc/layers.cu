@@ -155,6 +155,27 @@ __global__ void __launch_bounds__(CS_THREADS) k_colsum_part(const __nv_bfloat16*
                                                             int64_t rows_per, float* __restrict__ part) {
   extern __shared__ float red[];  // [CS_THREADS / (C/8)][C]
   const int C8 = C / 8;
+  if (C8 > CS_THREADS / 2) {  // wide rows: each thread owns column groups, walks all rows of the block
+    const int64_t r0 = blockIdx.x * rows_per;
+    const int64_t r1 = r0 + rows_per < rows ? r0 + rows_per : rows;
+    for (int cg = threadIdx.x; cg < C8; cg += CS_THREADS) {
+      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int64_t r = r0; r < r1; ++r) {
+        const uint4 v = *reinterpret_cast<const uint4*>(x + r * C + cg * 8);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float a, b;
+          unpack_bf16x2(w[j], a, b);
+          acc[2 * j] += a;
+          acc[2 * j + 1] += b;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) part[(int64_t)blockIdx.x * C + cg * 8 + j] = acc[j];
+    }
+    return;
+  }
   const int lanes = CS_THREADS / C8;  // row lanes per block
   const int cg = threadIdx.x % C8, rl = threadIdx.x / C8;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -216,8 +237,7 @@ int reduce_sgd(int out_dtype, const float* part, int S, int64_t stride, int64_t 
 }
 
 int colsum_blocks(int64_t rows, int C) {
-  (void)C;
-  const int64_t per = 2048;
+  const int64_t per = C / 8 > CS_THREADS / 2 ? 32 : 2048;
   int64_t b = (rows + per - 1) / per;
   const int64_t cap = (int64_t)sm_count() * 4;
   return (int)(b < 1 ? 1 : (b < cap ? b : cap));
@@ -226,11 +246,11 @@ int colsum_blocks(int64_t rows, int C) {
 // Bias gradient of a [rows, C] bf16 gradient; part must hold colsum_blocks(rows, C) * C floats.
 int bias_grad_tall(const void* dz, int64_t rows, int C, float* part, float* grad, float* master, float* out, float lr,
                    cudaStream_t st) {
-  if (C % 8 || C > 8 * CS_THREADS) return set_error(PD_ERR_INVALID, "bias_grad_tall: C %% 8 == 0, C <= 2048");
+  if (C % 8) return set_error(PD_ERR_INVALID, "bias_grad_tall: C %% 8 == 0");
   const int blocks = colsum_blocks(rows, C);
   const int64_t per = (rows + blocks - 1) / blocks;
   const int lanes = CS_THREADS / (C / 8);
-  const size_t smem = (size_t)(lanes > 0 ? lanes : 1) * C * sizeof(float);
+  const size_t smem = C / 8 > CS_THREADS / 2 ? 0 : (size_t)(lanes > 0 ? lanes : 1) * C * sizeof(float);
   k_colsum_part<<<blocks, CS_THREADS, smem, st>>>(static_cast<const __nv_bfloat16*>(dz), rows, C, per, part);
   int rc = launch_status("colsum_part");
   if (rc) return rc;

@@ -35,6 +35,18 @@ int bias_grad_tall(const void* dz, int64_t rows, int C, float* part, float* grad
 int softmax_ce(const float* logits, int64_t ldz, const int* labels, int B, int V, void* dz, int64_t ldd, float* loss,
                cudaStream_t st);
 
+int attn_fwd(const void* qkv, void* out, float* lse, int B, int S, int H, cudaStream_t st);
+int attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, float* Dv, float* dq_acc,
+             void* dqkv, int B, int S, int H, cudaStream_t st);
+int ln_fwd(const void* x, const float* gb, void* y, float* mean, float* rstd, int64_t T, int D, cudaStream_t st);
+int ln_bwd_blocks(int64_t T);
+int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gb, const void* dres,
+           void* dx, float* part, int64_t T, int D, cudaStream_t st);
+int embed_fwd(const int* tok, const void* wte, const void* wpe, void* x, int64_t T, int S, int D, cudaStream_t st);
+int embed_bwd(const int* tok, const void* dx, float* gte, float* gpe, int64_t T, int S, int D, cudaStream_t st);
+int softmax_ce_v(const float* logits, int64_t ldz, const int* labels, int64_t rows, int V, int Vp, void* dz,
+                 int64_t ldd, float* loss, cudaStream_t st);
+
 int bias_sgd(int dtype, const void* dz, int rows, int cols, int64_t ld, float* b_master, float* b_out, float lr,
              cudaStream_t st);
 int sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n, float lr, cudaStream_t st);
@@ -49,7 +61,7 @@ inline EpiArgs to_epi(const pd_epilogue& e) {
   EpiArgs a{};
   a.out = e.out; a.ldo = e.ldo; a.bias = e.bias; a.relu = e.relu; a.mask = e.mask; a.ldm = e.ldm;
   a.target = e.target; a.ldt = e.ldt; a.scale = e.scale; a.loss = e.loss; a.master = e.master;
-  a.ldw = e.ldw; a.lr = e.lr;
+  a.ldw = e.ldw; a.lr = e.lr; a.aux = e.aux;
   return a;
 }
 

@@ -21,10 +21,76 @@ namespace {
 
 using namespace pd;
 
+// Byte layout of a transformer layer's per-minibatch `save` slot and shared `work` scratch.
+struct TLayout {
+  int64_t T = 0;
+  int d = 0, f = 0, H = 0;
+  // save (bf16 element offsets, then fp32 float offsets from f32_base)
+  int64_t h1 = 0, qkv = 0, a = 0, x2 = 0, h2 = 0, z = 0, u = 0;
+  int64_t f32_base = 0;  // bytes
+  int64_t lse = 0, mean1 = 0, rstd1 = 0, mean2 = 0, rstd2 = 0;
+  int64_t save_bytes = 0;
+  // work (bf16 element offsets, fp32 after w32_base)
+  int64_t dz1 = 0, dh = 0, dx2 = 0, da = 0, dqkv = 0;
+  int64_t w32_base = 0, dq_acc = 0, dvec = 0;
+  int64_t work_bytes = 0;
+};
+
+inline int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
+
+TLayout tlayout(const pd_layer& y, int batch) {
+  TLayout L;
+  L.T = (int64_t)batch * y.h;
+  L.d = y.kind == PD_LAYER_EMBED ? y.c_out : y.c_in;
+  L.f = y.ffn;
+  L.H = y.w;
+  const int64_t T = L.T, d = L.d, f = L.f;
+  if (y.kind == PD_LAYER_BLOCK) {
+    int64_t o = 0;
+    L.h1 = o; o += T * d;
+    L.qkv = o; o += 3 * T * d;
+    L.a = o; o += T * d;
+    L.x2 = o; o += T * d;
+    L.h2 = o; o += T * d;
+    L.z = o; o += T * f;
+    L.u = o; o += T * f;
+    L.f32_base = align256(o * 2);
+    int64_t q = 0;
+    L.lse = q; q += T * L.H;
+    L.mean1 = q; q += T;
+    L.rstd1 = q; q += T;
+    L.mean2 = q; q += T;
+    L.rstd2 = q; q += T;
+    L.save_bytes = L.f32_base + q * 4;
+    o = 0;
+    L.dz1 = o; o += T * f;
+    L.dh = o; o += T * d;
+    L.dx2 = o; o += T * d;
+    L.da = o; o += T * d;
+    L.dqkv = o; o += 3 * T * d;
+    L.w32_base = align256(o * 2);
+    q = 0;
+    L.dq_acc = q; q += T * d;
+    L.dvec = q; q += T * L.H;
+    L.work_bytes = L.w32_base + q * 4;
+  } else if (y.kind == PD_LAYER_HEAD) {
+    L.h1 = 0;
+    L.f32_base = align256(T * d * 2);
+    L.mean1 = 0;
+    L.rstd1 = T;
+    L.save_bytes = L.f32_base + 2 * T * 4;
+    L.dh = 0;
+    L.work_bytes = T * d * 2;
+  }
+  return L;
+}
+
 struct Layer {
   pd_layer d{};
   std::vector<uint8_t*> argmax;
   std::vector<void*> cols;
+  std::vector<void*> save;
+  TLayout t;
 };
 
 struct Stage {
@@ -119,9 +185,19 @@ int64_t w_numel(const Stage& S, int l) {
   if (S.layers.empty()) return S.dims[l] * S.dims[l + 1];
   const pd_layer& y = S.layers[l].d;
   if (y.kind == PD_LAYER_LINEAR) return (int64_t)y.c_in * y.c_out;
+  if (y.kind == PD_LAYER_EMBED) return (int64_t)(y.c_in + y.h) * y.c_out;
+  if (y.kind == PD_LAYER_BLOCK) return (4ll * y.c_in + 2ll * y.ffn) * y.c_in;
+  if (y.kind == PD_LAYER_HEAD) return (int64_t)y.c_out * y.c_in;
   return (int64_t)(y.im2col ? 64 : 9 * y.c_in) * y.c_out;
 }
-int64_t b_numel(const Stage& S, int l) { return S.layers.empty() ? S.dims[l + 1] : S.layers[l].d.c_out; }
+int64_t b_numel(const Stage& S, int l) {
+  if (S.layers.empty()) return S.dims[l + 1];
+  const pd_layer& y = S.layers[l].d;
+  if (y.kind == PD_LAYER_EMBED) return 0;
+  if (y.kind == PD_LAYER_BLOCK) return 9ll * y.c_in + y.ffn;
+  if (y.kind == PD_LAYER_HEAD) return 2ll * y.c_in;
+  return y.c_out;
+}
 
 int wait_flag(pd_runtime* rt, Stage& S, const int* flag, int value) {
   PD_TRY(flag_wait(flag, flag_val(rt->epoch, value), S.d.err_word, stream_of(rt, S)));
@@ -245,6 +321,224 @@ int timed_conv(pd_runtime* rt, int cls, int pass, const void* act, const void* o
   return 0;
 }
 
+inline void* bf16_at(void* base, int64_t elems) { return static_cast<__nv_bfloat16*>(base) + elems; }
+inline float* f32_at(void* base, int64_t byte_base, int64_t floats) {
+  return reinterpret_cast<float*>(static_cast<uint8_t*>(base) + byte_base) + floats;
+}
+
+int gemm_t(pd_runtime* rt, int cls, const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M,
+           int N, int K, int kind, const EpiArgs& ep, cudaStream_t st) {
+  return timed_gemm(rt, cls, PD_BF16, A, a_mn, lda, B, b_mn, ldb, M, N, K, kind, ep, st);
+}
+
+// wgrad + SGD of one [M, N] weight matrix inside a flat parameter buffer: dW = A^T B over T rows
+// (A = dY [T, M], B = X [T, N], both row-major = MN-major operands).
+int wgrad_sgd(pd_runtime* rt, Stage& S, int l, int wnew, int64_t woff, const void* dY, const void* X, int M, int N,
+              int64_t T, cudaStream_t st) {
+  const pd_stage_desc& d = S.d;
+  EpiArgs ep{};
+  ep.master = S.w_master[l] + woff;
+  ep.ldw = N;
+  ep.out = bf16_at(S.w_ring[(size_t)l * d.ring_depth + wnew], woff);
+  ep.ldo = N;
+  ep.lr = d.lr;
+  return gemm_t(rt, KC_WGRAD, dY, 1, M, X, 1, N, M, N, (int)T, EPI_SGD, ep, st);
+}
+
+// bias gradient (column sum over T rows) + SGD of a bias slice at boff
+int bias_update(pd_runtime* rt, Stage& S, int l, int wnew, int64_t boff, const void* dY, int64_t T, int C,
+                cudaStream_t st) {
+  const pd_stage_desc& d = S.d;
+  rt->launches += 2;
+  return bias_grad_tall(dY, T, C, d.part, nullptr, S.b_master[l] + boff,
+                        S.b_ring[(size_t)l * d.ring_depth + wnew] + boff, d.lr, st);
+}
+
+// LayerNorm backward fused with the residual gradient, then the gamma/beta update at goff
+int ln_backward(pd_runtime* rt, Stage& S, int l, int wslot, int wnew, int64_t goff, const void* dy, const void* x,
+                const float* mean, const float* rstd, const void* dres, void* dx, int64_t T, int D, bool update,
+                cudaStream_t st) {
+  const pd_stage_desc& d = S.d;
+  const float* gb = S.b_ring[(size_t)l * d.ring_depth + wslot] + goff;
+  PD_TRY(ln_bwd(dy, x, mean, rstd, gb, dres, dx, d.part, T, D, st));
+  rt->launches += 1;
+  if (!update) return 0;
+  rt->launches += 1;
+  return reduce_sgd(PD_F32, d.part, ln_bwd_blocks(T), 2ll * D, 2ll * D, nullptr, S.b_master[l] + goff,
+                    S.b_ring[(size_t)l * d.ring_depth + wnew] + goff, d.lr, st);
+}
+
+// Transformer layer forward.  x: layer input (tokens for EMBED), out: layer output [T, d]
+// (next layer's stash, or the next stage's inbox slot).
+int tfwd(pd_runtime* rt, Stage& S, const Layer& Y, int l, const int32_t* it, const void* x, void* out) {
+  cudaStream_t ST = stream_of(rt, S);
+  const pd_stage_desc& d = S.d;
+  const pd_layer& y = Y.d;
+  const int wslot = it[PD_IT_WSLOT], act = it[PD_IT_ACT], mb = it[PD_IT_MB];
+  void* W = S.w_ring[(size_t)l * d.ring_depth + wslot];
+  const float* b = S.b_ring[(size_t)l * d.ring_depth + wslot];
+  const TLayout& L = Y.t;
+  const int64_t T = L.T;
+  const int D = L.d, F = L.f;
+  if (y.kind == PD_LAYER_EMBED) {
+    rt->launches += 1;
+    return embed_fwd(static_cast<const int*>(x), W, bf16_at(W, (int64_t)y.c_in * D), out, T, y.h, D, ST);
+  }
+  void* sv = Y.save[act];
+  if (y.kind == PD_LAYER_HEAD) {
+    void* h = bf16_at(sv, 0);
+    float* mean = f32_at(sv, L.f32_base, L.mean1);
+    float* rstd = f32_at(sv, L.f32_base, L.rstd1);
+    PD_TRY(ln_fwd(x, b, h, mean, rstd, T, D, ST));
+    EpiArgs ep{};
+    ep.out = d.logits;
+    ep.ldo = y.c_out;
+    PD_TRY(gemm_t(rt, KC_FWD, h, 0, D, W, 0, D, (int)T, y.c_out, D, EPI_GRADF32, ep, ST));
+    rt->launches += 2;
+    return softmax_ce_v(d.logits, y.c_out, reinterpret_cast<const int*>(S.target[it[PD_IT_BLOCK]]), T, y.vocab, y.c_out,
+                        S.dz_last[act], y.c_out, d.loss + mb, ST);
+  }
+  // BLOCK (pre-LN): x2 = x + attn(LN1 x) Wo^T + bo ; out = x2 + gelu(LN2 x2 W1^T + b1) W2^T + b2
+  const int64_t oWo = 3ll * D * D, oW1 = 4ll * D * D, oW2 = 4ll * D * D + (int64_t)F * D;
+  const int64_t obo = 3ll * D, ob1 = 4ll * D, ob2 = 4ll * D + F, oln1 = 5ll * D + F, oln2 = 7ll * D + F;
+  void* h1 = bf16_at(sv, L.h1);
+  void* qkv = bf16_at(sv, L.qkv);
+  void* a = bf16_at(sv, L.a);
+  void* x2 = bf16_at(sv, L.x2);
+  void* h2 = bf16_at(sv, L.h2);
+  void* z = bf16_at(sv, L.z);
+  void* u = bf16_at(sv, L.u);
+  PD_TRY(ln_fwd(x, b + oln1, h1, f32_at(sv, L.f32_base, L.mean1), f32_at(sv, L.f32_base, L.rstd1), T, D, ST));
+  EpiArgs ep{};
+  ep.out = qkv;
+  ep.ldo = 3 * D;
+  ep.bias = b;
+  PD_TRY(gemm_t(rt, KC_FWD, h1, 0, D, W, 0, D, (int)T, 3 * D, D, EPI_STORE, ep, ST));
+  PD_TRY(attn_fwd(qkv, a, f32_at(sv, L.f32_base, L.lse), (int)(T / y.h), y.h, L.H, ST));
+  ep = EpiArgs{};
+  ep.out = x2;
+  ep.ldo = D;
+  ep.bias = b + obo;
+  ep.mask = x;
+  ep.ldm = D;
+  PD_TRY(gemm_t(rt, KC_FWD, a, 0, D, bf16_at(W, oWo), 0, D, (int)T, D, D, EPI_RESID, ep, ST));
+  PD_TRY(ln_fwd(x2, b + oln2, h2, f32_at(sv, L.f32_base, L.mean2), f32_at(sv, L.f32_base, L.rstd2), T, D, ST));
+  ep = EpiArgs{};
+  ep.out = u;
+  ep.aux = z;
+  ep.ldo = F;
+  ep.bias = b + ob1;
+  PD_TRY(gemm_t(rt, KC_FWD, h2, 0, D, bf16_at(W, oW1), 0, D, (int)T, F, D, EPI_GELU, ep, ST));
+  ep = EpiArgs{};
+  ep.out = out;
+  ep.ldo = D;
+  ep.bias = b + ob2;
+  ep.mask = x2;
+  ep.ldm = D;
+  PD_TRY(gemm_t(rt, KC_FWD, u, 0, F, bf16_at(W, oW2), 0, F, (int)T, D, F, EPI_RESID, ep, ST));
+  rt->launches += 3;
+  return 0;
+}
+
+// Transformer layer backward.  dout: gradient of the layer output; X: layer input; dst: where the
+// input gradient goes (nullptr: none needed).
+int tbwd(pd_runtime* rt, Stage& S, const Layer& Y, int l, const int32_t* it, const void* dout, const void* X,
+         void* dst) {
+  cudaStream_t ST = stream_of(rt, S);
+  const pd_stage_desc& d = S.d;
+  const pd_layer& y = Y.d;
+  const int wslot = it[PD_IT_WSLOT], wnew = it[PD_IT_WNEW], act = it[PD_IT_ACT];
+  const bool update = wnew >= 0;
+  void* W = S.w_ring[(size_t)l * d.ring_depth + wslot];
+  const TLayout& L = Y.t;
+  const int64_t T = L.T;
+  const int D = L.d, F = L.f;
+  if (y.kind == PD_LAYER_EMBED) {
+    if (!update) return 0;
+    const int64_t n = w_numel(S, l);
+    PD_CHECK(cudaMemsetAsync(d.part, 0, sizeof(float) * n, ST));
+    PD_TRY(embed_bwd(static_cast<const int*>(X), dout, d.part, d.part + (int64_t)y.c_in * D, T, y.h, D, ST));
+    rt->launches += 2;
+    return reduce_sgd(PD_BF16, d.part, 1, n, n, nullptr, S.w_master[l], S.w_ring[(size_t)l * d.ring_depth + wnew],
+                      d.lr, ST);
+  }
+  void* sv = Y.save[act];
+  if (y.kind == PD_LAYER_HEAD) {
+    void* h = bf16_at(sv, 0);
+    void* dh = bf16_at(y.work, L.dh);
+    EpiArgs ep{};
+    ep.out = dh;
+    ep.ldo = D;
+    PD_TRY(gemm_t(rt, KC_DGRAD, dout, 0, y.c_out, W, 1, D, (int)T, D, y.c_out, EPI_STORE, ep, ST));
+    if (update) PD_TRY(wgrad_sgd(rt, S, l, wnew, 0, dout, h, y.c_out, D, T, ST));
+    return ln_backward(rt, S, l, wslot, wnew, 0, dh, X, f32_at(sv, L.f32_base, L.mean1),
+                       f32_at(sv, L.f32_base, L.rstd1), nullptr, dst, T, D, update, ST);
+  }
+  // BLOCK
+  const int64_t oWo = 3ll * D * D, oW1 = 4ll * D * D, oW2 = 4ll * D * D + (int64_t)F * D;
+  const int64_t obo = 3ll * D, ob1 = 4ll * D, ob2 = 4ll * D + F, oln1 = 5ll * D + F, oln2 = 7ll * D + F;
+  void* h1 = bf16_at(sv, L.h1);
+  void* qkv = bf16_at(sv, L.qkv);
+  void* a = bf16_at(sv, L.a);
+  void* x2 = bf16_at(sv, L.x2);
+  void* h2 = bf16_at(sv, L.h2);
+  void* z = bf16_at(sv, L.z);
+  void* u = bf16_at(sv, L.u);
+  void* dz1 = bf16_at(y.work, L.dz1);
+  void* dh = bf16_at(y.work, L.dh);
+  void* dx2 = bf16_at(y.work, L.dx2);
+  void* da = bf16_at(y.work, L.da);
+  void* dqkv = bf16_at(y.work, L.dqkv);
+  // FC2: dz1 = (dout W2) * gelu'(z)
+  EpiArgs ep{};
+  ep.out = dz1;
+  ep.ldo = F;
+  ep.mask = z;
+  ep.ldm = F;
+  PD_TRY(gemm_t(rt, KC_DGRAD, dout, 0, D, bf16_at(W, oW2), 1, F, (int)T, F, D, EPI_GELU_BWD, ep, ST));
+  if (update) {
+    PD_TRY(wgrad_sgd(rt, S, l, wnew, oW2, dout, u, D, F, T, ST));
+    PD_TRY(bias_update(rt, S, l, wnew, ob2, dout, T, D, ST));
+  }
+  // FC1: dh2 = dz1 W1
+  ep = EpiArgs{};
+  ep.out = dh;
+  ep.ldo = D;
+  PD_TRY(gemm_t(rt, KC_DGRAD, dz1, 0, F, bf16_at(W, oW1), 1, D, (int)T, D, F, EPI_STORE, ep, ST));
+  if (update) {
+    PD_TRY(wgrad_sgd(rt, S, l, wnew, oW1, dz1, h2, F, D, T, ST));
+    PD_TRY(bias_update(rt, S, l, wnew, ob1, dz1, T, F, ST));
+  }
+  // LN2 (+ the residual path): dx2 = dout + LN2'(dh2)
+  PD_TRY(ln_backward(rt, S, l, wslot, wnew, oln2, dh, x2, f32_at(sv, L.f32_base, L.mean2),
+                     f32_at(sv, L.f32_base, L.rstd2), dout, dx2, T, D, update, ST));
+  // out projection: da = dx2 Wo
+  ep = EpiArgs{};
+  ep.out = da;
+  ep.ldo = D;
+  PD_TRY(gemm_t(rt, KC_DGRAD, dx2, 0, D, bf16_at(W, oWo), 1, D, (int)T, D, D, EPI_STORE, ep, ST));
+  if (update) {
+    PD_TRY(wgrad_sgd(rt, S, l, wnew, oWo, dx2, a, D, D, T, ST));
+    PD_TRY(bias_update(rt, S, l, wnew, obo, dx2, T, D, ST));
+  }
+  // attention
+  PD_TRY(attn_bwd(qkv, a, da, f32_at(sv, L.f32_base, L.lse), f32_at(y.work, L.w32_base, L.dvec),
+                  f32_at(y.work, L.w32_base, L.dq_acc), dqkv, (int)(T / y.h), y.h, L.H, ST));
+  rt->launches += 3;
+  // QKV: dh1 = dqkv Wqkv
+  ep = EpiArgs{};
+  ep.out = dh;
+  ep.ldo = D;
+  PD_TRY(gemm_t(rt, KC_DGRAD, dqkv, 0, 3 * D, W, 1, D, (int)T, D, 3 * D, EPI_STORE, ep, ST));
+  if (update) {
+    PD_TRY(wgrad_sgd(rt, S, l, wnew, 0, dqkv, h1, 3 * D, D, T, ST));
+    PD_TRY(bias_update(rt, S, l, wnew, 0, dqkv, T, 3 * D, ST));
+  }
+  // LN1 (+ the residual path): dx = dx2 + LN1'(dh1)
+  return ln_backward(rt, S, l, wslot, wnew, oln1, dh, X, f32_at(sv, L.f32_base, L.mean1),
+                     f32_at(sv, L.f32_base, L.rstd1), dx2, dst, T, D, update, ST);
+}
+
 // Layered stage forward (VGG-style): per layer Linear or implicit-GEMM conv (+bias, ReLU fused in
 // the epilogue), optional max pool; the stage's last layer writes the next stage's inbox slot,
 // or at the model output the loss (MSE epilogue, or fp32 logits + softmax cross-entropy).
@@ -262,6 +556,11 @@ int run_forward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
                       : (d.is_last ? nullptr : rt->views.at(it[PD_IT_DST]).act_in[it[PD_IT_OUT]]);
     const void* W = S.w_ring[(size_t)l * d.ring_depth + wslot];
     const float* bias = S.b_ring[(size_t)l * d.ring_depth + wslot];
+    if (y.kind >= PD_LAYER_EMBED) {
+      PD_TRY(tfwd(rt, S, Y, l, it, x, out));
+      x = out;
+      continue;
+    }
     EpiArgs ep{};
     ep.bias = bias;
     ep.relu = y.relu;
@@ -340,6 +639,12 @@ int run_backward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
     void* ring_new = (!replicated && wnew >= 0) ? S.w_ring[(size_t)l * d.ring_depth + wnew] : nullptr;
     float* bring_new = (!replicated && wnew >= 0) ? S.b_ring[(size_t)l * d.ring_depth + wnew] : nullptr;
     void* dst = nullptr;
+    if (y.kind >= PD_LAYER_EMBED) {
+      if (need_dx) dst = (l == 0) ? rt->views.at(it[PD_IT_DST]).grad_in[it[PD_IT_OUT]] : other_tmp(dz);
+      PD_TRY(tbwd(rt, S, Y, l, it, dz, X, dst));
+      dz = dst;
+      continue;
+    }
     if (y.kind == PD_LAYER_LINEAR) {
       if (need_dx) {
         dst = (l == 0) ? rt->views.at(it[PD_IT_DST]).grad_in[it[PD_IT_OUT]] : other_tmp(dz);
@@ -479,10 +784,26 @@ int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc) {
       Layer Y;
       Y.d = d.layers[l];
       const pd_layer& y = Y.d;
-      if (y.kind != PD_LAYER_LINEAR && y.kind != PD_LAYER_CONV3)
+      if (y.kind < PD_LAYER_LINEAR || y.kind > PD_LAYER_HEAD)
         return set_error(PD_ERR_INVALID, "worker %d layer %d: bad kind %d", d.worker, l, y.kind);
       if (y.c_in < 1 || y.c_out < 1 || (y.kind == PD_LAYER_CONV3 && (y.h < 2 || y.w < 2)))
         return set_error(PD_ERR_INVALID, "worker %d layer %d: bad shape", d.worker, l);
+      const bool tkind = y.kind == PD_LAYER_EMBED || y.kind == PD_LAYER_BLOCK || y.kind == PD_LAYER_HEAD;
+      if (tkind) {
+        if (d.rep > 1) return set_error(PD_ERR_INVALID, "worker %d: transformer stages are not replicated", d.worker);
+        if (y.h < 64 || y.h % 64) return set_error(PD_ERR_INVALID, "worker %d layer %d: seq %% 64", d.worker, l);
+        if (y.kind == PD_LAYER_BLOCK && (y.w * 64 != y.c_in || y.ffn < 1))
+          return set_error(PD_ERR_INVALID, "worker %d layer %d: d = 64 * heads required", d.worker, l);
+        if (y.kind == PD_LAYER_HEAD && (y.vocab < 1 || y.vocab > y.c_out || !d.is_last || !d.logits))
+          return set_error(PD_ERR_INVALID, "worker %d layer %d: bad head", d.worker, l);
+        if (y.kind == PD_LAYER_EMBED && !(d.is_first && l == 0))
+          return set_error(PD_ERR_INVALID, "worker %d: the embedding must be the model input", d.worker);
+        if (y.kind != PD_LAYER_EMBED && (!y.save || !y.work))
+          return set_error(PD_ERR_INVALID, "worker %d layer %d: missing save/work buffers", d.worker, l);
+        if (!d.part) return set_error(PD_ERR_INVALID, "worker %d: transformer layers need `part`", d.worker);
+        Y.t = tlayout(y, d.batch);
+        if (y.save) Y.save.assign(y.save, y.save + d.act_depth);
+      }
       if (d.dtype != PD_BF16) return set_error(PD_ERR_INVALID, "worker %d: layered stages are bf16", d.worker);
       if (y.kind == PD_LAYER_CONV3 && !d.part)
         return set_error(PD_ERR_INVALID, "worker %d: conv layers need the `part` scratch", d.worker);
@@ -496,9 +817,10 @@ int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc) {
       }
       Y.d.argmax = nullptr;
       Y.d.cols = nullptr;
+      Y.d.save = nullptr;
       S.layers.push_back(Y);
     }
-    if (d.is_last && d.loss_kind == PD_LOSS_CE && !d.logits)
+    if (d.is_last && d.loss_kind == PD_LOSS_CE && !d.logits && S.layers.back().d.kind != PD_LAYER_HEAD)
       return set_error(PD_ERR_INVALID, "worker %d: cross-entropy needs the logits buffer", d.worker);
   }
   S.d.layers = nullptr;
@@ -612,8 +934,9 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
       const int64_t n = w_numel(S, l);
       PD_TRY(cast_f32(S.d.dtype, S.w_master[l], S.w_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], n, ST));
       rt->launches += 1;
-      PD_CHECK(cudaMemcpyAsync(S.b_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], S.b_master[l],
-                               sizeof(float) * b_numel(S, l), cudaMemcpyDeviceToDevice, ST));
+      if (b_numel(S, l) > 0)
+        PD_CHECK(cudaMemcpyAsync(S.b_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], S.b_master[l],
+                                 sizeof(float) * b_numel(S, l), cudaMemcpyDeviceToDevice, ST));
     }
     if (S.d.is_last && S.d.loss)  // losses are indexed by minibatch id
       PD_CHECK(cudaMemsetAsync(S.d.loss, 0, sizeof(float) * (size_t)(max_mb + 1), ST));
@@ -742,9 +1065,32 @@ int pd_rt_destroy(pd_runtime* rt) {
 
 }  // extern "C"
 
+extern "C" int64_t pd_layer_save_bytes(const pd_layer* layer, int batch) {
+  if (!layer || batch < 1) return 0;
+  return tlayout(*layer, batch).save_bytes;
+}
+
+extern "C" int64_t pd_layer_work_bytes(const pd_layer* layer, int batch) {
+  if (!layer || batch < 1) return 0;
+  return tlayout(*layer, batch).work_bytes;
+}
+
 extern "C" int64_t pd_layer_scratch_floats(const pd_layer* layer, int batch) {
   if (!layer || batch < 1) return 0;
   const pd_layer& y = *layer;
+  if (y.kind == PD_LAYER_EMBED) return (int64_t)(y.c_in + y.h) * y.c_out;
+  if (y.kind == PD_LAYER_BLOCK || y.kind == PD_LAYER_HEAD) {
+    const int64_t T = (int64_t)batch * y.h;
+    const int64_t D = y.c_in;
+    int64_t need = (int64_t)pd::ln_bwd_blocks(T) * 2 * D;
+    const int64_t widest = y.kind == PD_LAYER_BLOCK ? (3 * D > y.ffn ? 3 * D : y.ffn) : 0;
+    for (int64_t c : {D, widest}) {
+      if (c <= 0) continue;
+      const int64_t cs = (int64_t)pd::colsum_blocks(T, (int)c) * c;
+      need = cs > need ? cs : need;
+    }
+    return need;
+  }
   if (y.kind != PD_LAYER_CONV3) return 0;
   const int M = y.im2col ? 64 : 9 * y.c_in;
   const int64_t pix = (int64_t)batch * y.h * y.w;

@@ -1,0 +1,327 @@
+// Non-GEMM kernels of the GPT-2 stages (BASELINE configs[3]): LayerNorm
+// forward / backward (the backward fused with the residual-stream gradient add and the
+// gamma/beta column sums), token + position embedding gather / scatter-add, and the
+// vocabulary-padded softmax cross-entropy.  One warp per row, 16-byte vector accesses; the
+// column-sum partials go through the fixed-order reduction of layers.cu (reduce_sgd).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "pd_internal.h"
+
+namespace pd {
+
+namespace {
+
+int sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+int status(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+constexpr int LN_WARPS = 8;
+constexpr int LN_MAXV = 8;  // up to 8 x 256 = 2048 features per row (NV = D / 256 is a template parameter)
+
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&v)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) unpack_bf16x2(w[j], v[2 * j], v[2 * j + 1]);
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&v)[8]) {
+  *reinterpret_cast<uint4*>(p) = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
+                                            pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+}
+
+// y = (x - mean) * rstd * gamma + beta ; gamma/beta = gb[0:D], gb[D:2D] (fp32)
+template <int NV>
+__global__ void __launch_bounds__(LN_WARPS * 32) k_ln_fwd(const __nv_bfloat16* __restrict__ x, const float* __restrict__ gb,
+                                                          __nv_bfloat16* __restrict__ y, float* __restrict__ mean,
+                                                          float* __restrict__ rstd, int64_t T, int D, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * (int64_t)LN_WARPS + (threadIdx.x >> 5);
+  if (row >= T) return;
+  constexpr int nv = NV;
+  float v[NV][8];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    if (i < nv) {
+      load8(x + row * D + i * 256 + lane * 8, v[i]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += v[i][j];
+    }
+  s = warp_sum(s);
+  const float mu = s / D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    if (i < nv)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float d = v[i][j] - mu;
+        q += d * d;
+      }
+  q = warp_sum(q);
+  const float rs = rsqrtf(q / D + eps);
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    if (i < nv) {
+      const int c = i * 256 + lane * 8;
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mu) * rs * gb[c + j] + gb[D + c + j];
+      store8(y + row * D + c, o);
+    }
+  if (lane == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
+// dx = dres + rstd * (g*dy - mean(g*dy) - xhat * mean(g*dy*xhat));  part[block] += (dy*xhat, dy)
+template <int NV>
+__global__ void __launch_bounds__(LN_WARPS * 32) k_ln_bwd(const __nv_bfloat16* __restrict__ dy,
+                                                          const __nv_bfloat16* __restrict__ x,
+                                                          const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                          const float* __restrict__ gb,
+                                                          const __nv_bfloat16* __restrict__ dres,
+                                                          __nv_bfloat16* __restrict__ dx, float* __restrict__ part,
+                                                          int64_t T, int D, int64_t rows_per_block) {
+  extern __shared__ float red[];  // [LN_WARPS][2*D]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int nv = NV;
+  float pg[NV][8], pb[NV][8];
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) pg[i][j] = pb[i][j] = 0.f;
+  const int64_t r0 = blockIdx.x * rows_per_block;
+  const int64_t r1 = r0 + rows_per_block < T ? r0 + rows_per_block : T;
+  for (int64_t row = r0 + warp; row < r1; row += LN_WARPS) {
+    const float mu = mean[row], rs = rstd[row];
+    float g[NV][8], xh[NV][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (i < nv) {
+        const int c = i * 256 + lane * 8;
+        float dv[8], xv[8];
+        load8(dy + row * D + c, dv);
+        load8(x + row * D + c, xv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          xh[i][j] = (xv[j] - mu) * rs;
+          g[i][j] = dv[j] * gb[c + j];
+          s1 += g[i][j];
+          s2 += g[i][j] * xh[i][j];
+          pg[i][j] += dv[j] * xh[i][j];
+          pb[i][j] += dv[j];
+        }
+      }
+    s1 = warp_sum(s1) / D;
+    s2 = warp_sum(s2) / D;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (i < nv) {
+        const int c = i * 256 + lane * 8;
+        float o[8], r[8];
+        if (dres) load8(dres + row * D + c, r);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = rs * (g[i][j] - s1 - xh[i][j] * s2) + (dres ? r[j] : 0.f);
+        store8(dx + row * D + c, o);
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    if (i < nv)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = i * 256 + lane * 8 + j;
+        red[warp * 2 * D + c] = pg[i][j];
+        red[warp * 2 * D + D + c] = pb[i][j];
+      }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 2 * D; c += LN_WARPS * 32) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < LN_WARPS; ++w) s += red[w * 2 * D + c];
+    part[blockIdx.x * 2 * (int64_t)D + c] = s;
+  }
+}
+
+// x[t] = wte[tok[t]] + wpe[t % S]
+__global__ void __launch_bounds__(256) k_embed_fwd(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ wte,
+                                                   const __nv_bfloat16* __restrict__ wpe, __nv_bfloat16* __restrict__ x,
+                                                   int64_t T, int S, int D) {
+  const int D8 = D / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T * D8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / D8;
+    const int c = (int)(i % D8) * 8;
+    float a[8], b[8];
+    load8(wte + (int64_t)tok[t] * D + c, a);
+    load8(wpe + (t % S) * D + c, b);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] += b[j];
+    store8(x + t * D + c, a);
+  }
+}
+
+// gte[tok[t]] += dx[t]; gpe[t % S] += dx[t]   (fp32 atomics into zeroed gradient buffers)
+__global__ void __launch_bounds__(256) k_embed_bwd(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ dx,
+                                                   float* __restrict__ gte, float* __restrict__ gpe, int64_t T, int S,
+                                                   int D) {
+  const int D8 = D / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T * D8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / D8;
+    const int c = (int)(i % D8) * 8;
+    float g[8];
+    load8(dx + t * D + c, g);
+    float* a = gte + (int64_t)tok[t] * D + c;
+    float* b = gpe + (t % S) * D + c;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      atomicAdd(a + j, g[j]);
+      atomicAdd(b + j, g[j]);
+    }
+  }
+}
+
+// Softmax cross-entropy over the first V of Vp fp32 logit columns; columns >= V get dz = 0.
+__global__ void __launch_bounds__(512) k_softmax_ce_v(const float* __restrict__ z, int64_t ldz,
+                                                      const int* __restrict__ labels, int V, int Vp, float inv_n,
+                                                      __nv_bfloat16* __restrict__ dz, int64_t ldd,
+                                                      float* __restrict__ loss) {
+  __shared__ float sh[32];
+  const int64_t r = blockIdx.x;
+  const float* row = z + r * ldz;
+  const int nw = blockDim.x >> 5;
+  float m = -INFINITY;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) m = fmaxf(m, row[j]);
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = sh[0];
+  for (int w = 1; w < nw; ++w) m = fmaxf(m, sh[w]);
+  __syncthreads();
+  float s = 0.f;
+  for (int j = threadIdx.x; j < V; j += blockDim.x) s += __expf(row[j] - m);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  s = 0.f;
+  for (int w = 0; w < nw; ++w) s += sh[w];
+  const int lab = labels[r];
+  const float inv_s = 1.f / s;
+  __nv_bfloat16* drow = dz + r * ldd;
+  for (int j = threadIdx.x; j < Vp; j += blockDim.x) {
+    const float p = j < V ? __expf(row[j] - m) * inv_s : 0.f;
+    drow[j] = __float2bfloat16_rn((p - (j == lab ? 1.f : 0.f)) * inv_n);
+  }
+  if (threadIdx.x == 0) atomicAdd(loss, inv_n * (m + __logf(s) - row[lab]));
+}
+
+}  // namespace
+
+int ln_fwd(const void* x, const float* gb, void* y, float* mean, float* rstd, int64_t T, int D, cudaStream_t st) {
+  if (D % 256 || D > 256 * LN_MAXV) return set_error(PD_ERR_INVALID, "layernorm: D %% 256 == 0, D <= 2048");
+  const unsigned g = (unsigned)((T + LN_WARPS - 1) / LN_WARPS);
+  auto X = static_cast<const __nv_bfloat16*>(x);
+  auto Y = static_cast<__nv_bfloat16*>(y);
+  switch (D / 256) {
+    case 1: k_ln_fwd<1><<<g, LN_WARPS * 32, 0, st>>>(X, gb, Y, mean, rstd, T, D, 1e-5f); break;
+    case 2: k_ln_fwd<2><<<g, LN_WARPS * 32, 0, st>>>(X, gb, Y, mean, rstd, T, D, 1e-5f); break;
+    case 4: k_ln_fwd<4><<<g, LN_WARPS * 32, 0, st>>>(X, gb, Y, mean, rstd, T, D, 1e-5f); break;
+    case 8: k_ln_fwd<8><<<g, LN_WARPS * 32, 0, st>>>(X, gb, Y, mean, rstd, T, D, 1e-5f); break;
+    default: return set_error(PD_ERR_INVALID, "layernorm: D/256 must be 1, 2, 4 or 8");
+  }
+  return status("ln_fwd");
+}
+
+int ln_bwd_blocks(int64_t T) {
+  int64_t b = (T + 31) / 32;
+  const int64_t cap = (int64_t)sms() * 2;
+  return (int)(b < 1 ? 1 : (b < cap ? b : cap));
+}
+
+int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gb, const void* dres,
+           void* dx, float* part, int64_t T, int D, cudaStream_t st) {
+  if (D % 256 || D > 256 * LN_MAXV) return set_error(PD_ERR_INVALID, "layernorm: D %% 256 == 0, D <= 2048");
+  const int blocks = ln_bwd_blocks(T);
+  const int64_t per = (T + blocks - 1) / blocks;
+  const size_t smem = (size_t)LN_WARPS * 2 * D * sizeof(float);
+  auto launch = [&](auto kern) -> int {
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return set_error(PD_ERR_CUDA, "ln_bwd: shared memory attribute");
+    kern<<<blocks, LN_WARPS * 32, smem, st>>>(static_cast<const __nv_bfloat16*>(dy),
+                                              static_cast<const __nv_bfloat16*>(x), mean, rstd, gb,
+                                              static_cast<const __nv_bfloat16*>(dres), static_cast<__nv_bfloat16*>(dx),
+                                              part, T, D, per);
+    return status("ln_bwd");
+  };
+  switch (D / 256) {
+    case 1: return launch(k_ln_bwd<1>);
+    case 2: return launch(k_ln_bwd<2>);
+    case 4: return launch(k_ln_bwd<4>);
+    case 8: return launch(k_ln_bwd<8>);
+  }
+  return set_error(PD_ERR_INVALID, "layernorm: D/256 must be 1, 2, 4 or 8");
+}
+
+int embed_fwd(const int* tok, const void* wte, const void* wpe, void* x, int64_t T, int S, int D, cudaStream_t st) {
+  if (D % 8) return set_error(PD_ERR_INVALID, "embedding: D %% 8 == 0");
+  k_embed_fwd<<<sms() * 8, 256, 0, st>>>(tok, static_cast<const __nv_bfloat16*>(wte),
+                                        static_cast<const __nv_bfloat16*>(wpe), static_cast<__nv_bfloat16*>(x), T, S, D);
+  return status("embed_fwd");
+}
+
+int embed_bwd(const int* tok, const void* dx, float* gte, float* gpe, int64_t T, int S, int D, cudaStream_t st) {
+  if (D % 8) return set_error(PD_ERR_INVALID, "embedding: D %% 8 == 0");
+  k_embed_bwd<<<sms() * 8, 256, 0, st>>>(tok, static_cast<const __nv_bfloat16*>(dx), gte, gpe, T, S, D);
+  return status("embed_bwd");
+}
+
+int softmax_ce_v(const float* logits, int64_t ldz, const int* labels, int64_t rows, int V, int Vp, void* dz,
+                 int64_t ldd, float* loss, cudaStream_t st) {
+  if (rows < 1 || V < 1 || Vp < V) return set_error(PD_ERR_INVALID, "softmax_ce: bad shape");
+  k_softmax_ce_v<<<(unsigned)rows, 512, 0, st>>>(logits, ldz, labels, V, Vp, 1.f / (float)rows,
+                                                 static_cast<__nv_bfloat16*>(dz), ldd, loss);
+  return status("softmax_ce_v");
+}
+
+}  // namespace pd
+
+extern "C" {
+
+int pd_layernorm_fwd(const void* x, const float* gb, void* y, float* mean, float* rstd, int64_t rows, int d,
+                     void* stream) {
+  return pd::ln_fwd(x, gb, y, mean, rstd, rows, d, static_cast<cudaStream_t>(stream));
+}
+int pd_layernorm_bwd_blocks(int64_t rows) { return pd::ln_bwd_blocks(rows); }
+int pd_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gb,
+                     const void* dres, void* dx, float* part, int64_t rows, int d, void* stream) {
+  return pd::ln_bwd(dy, x, mean, rstd, gb, dres, dx, part, rows, d, static_cast<cudaStream_t>(stream));
+}
+int pd_embedding_fwd(const int* tok, const void* wte, const void* wpe, void* x, int64_t tokens, int seq, int d,
+                     void* stream) {
+  return pd::embed_fwd(tok, wte, wpe, x, tokens, seq, d, static_cast<cudaStream_t>(stream));
+}
+int pd_embedding_bwd(const int* tok, const void* dx, float* gte, float* gpe, int64_t tokens, int seq, int d,
+                     void* stream) {
+  return pd::embed_bwd(tok, dx, gte, gpe, tokens, seq, d, static_cast<cudaStream_t>(stream));
+}
+int pd_softmax_ce_vocab(const float* logits, int64_t ldz, const int* labels, int64_t rows, int v, int vpad, void* dz,
+                        int64_t ldd, float* loss, void* stream) {
+  return pd::softmax_ce_v(logits, ldz, labels, rows, v, vpad, dz, ldd, loss, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

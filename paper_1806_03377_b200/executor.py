@@ -31,7 +31,7 @@ import numpy as np
 from . import _native as nat
 from .errors import SimulationError, ValidationError
 from .ledger import Mode, SimConfig, SimResult, TraceEvent, build_report
-from .models import ConvNetSpec, MLPSpec, init_params_any, make_data_any
+from .models import ConvNetSpec, GPTSpec, MLPSpec, init_params_any, make_data_any
 from .orders import Direction, Schedule, build_schedule, stage_inflight_caps
 from .program import Program, compile_program
 
@@ -101,7 +101,8 @@ class Executor:
         self.hosted = [wp for wp in self.program.workers if self.program.device_of[wp.wid] == self.rank]
         self.dtype = torch.float32 if model.dtype == "fp32" else torch.bfloat16
         self.pd_dtype = nat.PD_F32 if model.dtype == "fp32" else nat.PD_BF16
-        self.layered = isinstance(model, ConvNetSpec)
+        self.layered = isinstance(model, (ConvNetSpec, GPTSpec))
+        self.is_gpt = isinstance(model, GPTSpec)
         self.geoms = model.geoms() if self.layered else None
         n_params = (model.n_params() if self.layered
                     else sum(a * b for a, b in zip(model.widths[:-1], model.widths[1:])))
@@ -112,11 +113,21 @@ class Executor:
         self.runs = 0
 
     # ------------------------------------------------------------------ setup
-    def _layer_desc(self, x, argmax=None, cols=None):
+    KINDS = {"linear": nat.PD_LAYER_LINEAR, "conv": nat.PD_LAYER_CONV3, "embed": nat.PD_LAYER_EMBED,
+             "block": nat.PD_LAYER_BLOCK, "head": nat.PD_LAYER_HEAD}
+
+    def _layer_desc(self, x, argmax=None, cols=None, save=None, work=None):
         d = nat.LayerDesc()
-        d.kind = nat.PD_LAYER_CONV3 if x.kind == "conv" else nat.PD_LAYER_LINEAR
+        d.kind = self.KINDS[x.kind]
         d.relu, d.pool, d.im2col = int(x.relu), int(x.pool), int(x.im2col)
         d.h, d.w, d.c_in, d.c_out = x.h, x.w, x.c_in, x.c_out
+        d.ffn, d.vocab = x.ffn, x.vocab
+        if save is not None:
+            a = self._parr([p.data_ptr() for p in save])
+            self._keep.append(a)
+            d.save = ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p))
+        if work is not None:
+            d.work = work.data_ptr()
         if argmax is not None:
             a = self._parr([p.data_ptr() for p in argmax])
             self._keep.append(a)
@@ -131,6 +142,36 @@ class Executor:
         self._keep = getattr(self, "_keep", [])
         d = self._layer_desc(x)
         return int(nat.lib().pd_layer_scratch_floats(ctypes.byref(d), self.model.batch))
+
+    def _layer_bytes(self, x, which: str) -> int:
+        d = self._layer_desc(x)
+        fn = nat.lib().pd_layer_save_bytes if which == "save" else nat.lib().pd_layer_work_bytes
+        return int(fn(ctypes.byref(d), self.model.batch))
+
+    @staticmethod
+    def _device_init(x, g, dev, torch, layers: int):
+        """Seeded on-device initialisation of one layer's (W, b) for models too large for the host."""
+        if x.kind in ("conv", "linear"):
+            fan = 9 * x.c_in if x.kind == "conv" else x.c_in
+            W = torch.randn(*x.w_shape, device=dev, generator=g) * math.sqrt(2.0 / fan)
+            if x.im2col:
+                W[9 * x.c_in:] = 0.0
+            return W, torch.randn(x.c_out, device=dev, generator=g) * 0.01
+        W = torch.randn(*x.w_shape, device=dev, generator=g) * 0.02
+        d = x.c_in if x.kind != "embed" else x.c_out
+        if x.kind == "block":
+            f = x.ffn
+            flat = W.view(-1)
+            scale = 1.0 / math.sqrt(2.0 * layers)
+            flat[3 * d * d: 4 * d * d] *= scale
+            flat[4 * d * d + f * d:] *= scale
+            b = torch.zeros(x.b_numel, device=dev)
+            b[5 * d + f: 6 * d + f] = 1.0
+            b[7 * d + f: 8 * d + f] = 1.0
+            return W, b
+        if x.kind == "head":
+            return W, torch.cat([torch.ones(d, device=dev), torch.zeros(d, device=dev)])
+        return W, torch.zeros(0, device=dev)
 
     def _alloc(self) -> None:
         torch = _torch()
@@ -158,23 +199,28 @@ class Executor:
             for l in range(L):
                 din, dout = dims[l], dims[l + 1]
                 wshape = geo[l].w_shape if geo else (dout, din)
-                nb = geo[l].c_out if geo else dout
+                nb = geo[l].b_numel if geo else dout
                 gl = st.first_layer - 1 + l
                 if params is not None:
                     W = torch.from_numpy(params[gl][0]).float().to(dev)
                     bias = torch.from_numpy(params[gl][1]).float().to(dev)
+                elif geo:
+                    W, bias = self._device_init(geo[l], g, dev, torch, getattr(m, "layers", 0))
                 else:
-                    fan = (9 * geo[l].c_in if geo[l].kind == "conv" else geo[l].c_in) if geo else din
-                    W = torch.randn(*wshape, device=dev, generator=g) * math.sqrt(2.0 / fan)
-                    if geo and geo[l].im2col:
-                        W[9 * geo[l].c_in:] = 0.0
+                    W = torch.randn(*wshape, device=dev, generator=g) * math.sqrt(2.0 / din)
                     bias = torch.randn(nb, device=dev, generator=g) * 0.01
                 t["w_master"].append(W.contiguous())
                 t["b_master"].append(bias.contiguous())
                 t["w_ring"].append(torch.empty(b.ring_depth, *wshape, device=dev, dtype=dt))
                 t["b_ring"].append(torch.empty(b.ring_depth, nb, device=dev, dtype=torch.float32))
             t["act"] = [torch.empty(b.act_depth, m.batch, dims[l + 1], device=dev, dtype=dt) for l in range(L - 1)]
-            if wp.stage == 0:
+            if wp.stage == 0 and self.is_gpt:  # int32 token ids
+                if params is not None:
+                    t["act_in"] = torch.from_numpy(X).to(dev).to(torch.int32).contiguous()
+                else:
+                    t["act_in"] = torch.randint(0, m.vocab, (m.n_blocks, m.batch, m.seq), device=dev, generator=g,
+                                                dtype=torch.int32)
+            elif wp.stage == 0:
                 if params is not None:
                     t["act_in"] = torch.from_numpy(X.reshape(m.n_blocks, m.batch, -1)).to(dev).to(dt).contiguous()
                 else:
@@ -185,7 +231,14 @@ class Executor:
                 t["grad_in"] = torch.zeros(b.grad_depth, m.batch, dims[-1], device=dev, dtype=dt)
             else:
                 t["dz_last"] = torch.empty(b.act_depth, m.batch, dims[-1], device=dev, dtype=dt)
-                if self.layered:  # cross-entropy: int32 labels and fp32 logits
+                if self.is_gpt:  # next-token labels and fp32 logits [tokens, padded vocab]
+                    if params is not None:
+                        t["target"] = torch.from_numpy(T).to(dev).to(torch.int32).contiguous()
+                    else:
+                        t["target"] = torch.randint(0, m.vocab, (m.n_blocks, m.batch, m.seq), device=dev,
+                                                    generator=g, dtype=torch.int32)
+                    t["logits"] = torch.empty(m.tokens, m.vocab_pad, device=dev, dtype=torch.float32)
+                elif self.layered:  # cross-entropy: int32 labels and fp32 logits
                     if params is not None:
                         t["target"] = torch.from_numpy(T).to(dev).to(torch.int32).contiguous()
                     else:
@@ -197,7 +250,8 @@ class Executor:
                 else:
                     t["target"] = torch.randn(m.n_blocks, m.batch, dims[-1], device=dev, generator=g)
                 t["loss"] = torch.zeros(self.cfg.num_minibatches + 1, device=dev, dtype=torch.float32)
-            tmp_feat = max(max(dims), max(x.pre_features for x in geo)) if geo else max(dims)
+            tmp_feat = (max(max(x.pre_features for x in geo), max(x.in_features for x in geo)) if geo
+                        else max(dims))
             t["tmp"] = [torch.empty(m.batch, tmp_feat, device=dev, dtype=dt) for _ in range(2)]
             if geo:
                 t["argmax"] = [torch.empty(b.act_depth, m.batch, x.out_features, device=dev, dtype=torch.uint8)
@@ -206,6 +260,10 @@ class Executor:
                              if x.im2col else None for x in geo]
                 scratch = max([self._scratch_floats(x) for x in geo] + [1])
                 t["part"] = torch.empty(scratch, device=dev, dtype=torch.float32)
+                t["save"] = [[torch.empty(self._layer_bytes(x, "save"), device=dev, dtype=torch.uint8)
+                              for _ in range(b.act_depth)] if self._layer_bytes(x, "save") else None for x in geo]
+                work = max([self._layer_bytes(x, "work") for x in geo] + [0])
+                t["work"] = torch.empty(max(work, 256), device=dev, dtype=torch.uint8)
             t["err"] = torch.zeros(1, device=dev, dtype=torch.int32)
             # receiver-owned inbox flags (zero = nothing delivered yet); used when a producer is remote
             i32 = dict(device=dev, dtype=torch.int32)
@@ -363,8 +421,8 @@ class Executor:
             d.tmp[0], d.tmp[1] = t["tmp"][0].data_ptr(), t["tmp"][1].data_ptr()
             d.err_word = t["err"].data_ptr()
             if self.layered:
-                descs = (nat.LayerDesc * nl)(*[self._layer_desc(x, t["argmax"][l], t["cols"][l])
-                                               for l, x in enumerate(b.geoms)])
+                descs = (nat.LayerDesc * nl)(*[self._layer_desc(x, t["argmax"][l], t["cols"][l], t["save"][l],
+                                                                t["work"]) for l, x in enumerate(b.geoms)])
                 self._keep.append(descs)
                 d.layers = ctypes.cast(descs, ctypes.POINTER(nat.LayerDesc))
                 d.part = t["part"].data_ptr()

@@ -123,11 +123,23 @@ class LayerGeom:
     in_features: int
     out_features: int  # per-sample, after pooling
     pre_features: int  # per-sample, before pooling
-    w_shape: tuple[int, int]  # conv: Wt [9*c_in (or 64), c_out]; linear: [c_out, c_in]
+    w_shape: tuple[int, int]  # conv: Wt [9*c_in (or 64), c_out]; linear: [c_out, c_in]; transformer: flat
+    ffn: int = 0  # transformer block hidden width
+    vocab: int = 0  # head: valid vocabulary (c_out is the padded one)
 
     @property
     def w_numel(self) -> int:
         return self.w_shape[0] * self.w_shape[1]
+
+    @property
+    def b_numel(self) -> int:
+        if self.kind == "embed":
+            return 0
+        if self.kind == "block":
+            return 9 * self.c_in + self.ffn
+        if self.kind == "head":
+            return 2 * self.c_in
+        return self.c_out
 
     @property
     def macs_per_sample(self) -> int:
@@ -231,6 +243,87 @@ def vgg16(batch: int = 32, classes: int = 1000, image: int = 224, **kw) -> ConvN
     return ConvNetSpec(image=(image, image, 3), layers=tuple(layers), batch=batch, **kw)
 
 
+# ---------------------------------------------------------------- GPT-2 (configs[3])
+@dataclass(frozen=True)
+class GPTSpec:
+    """GPT-2-style decoder: token + position embedding, pre-LN blocks (causal attention with
+    64-wide heads, tanh-GELU MLP), final LayerNorm and an (untied) LM head trained with next-token
+    softmax cross-entropy (mean over tokens).  Profile layers: 1 = embedding, 2..L+1 = blocks,
+    L+2 = head.  The head is untied from the token embedding because they live on different
+    pipeline stages (PipeDream keeps one copy of each parameter per stage).  The vocabulary is
+    padded to a multiple of 128 (50257 -> 50304); padded logits are excluded from the softmax."""
+
+    vocab: int = 50257
+    d: int = 1024
+    heads: int = 16
+    layers: int = 24
+    seq: int = 1024
+    ffn: int = 0  # 0: 4*d
+    batch: int = 8  # sequences per minibatch
+    dtype: str = "bf16"
+    lr: float = 1e-4
+    n_blocks: int = 2
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.ffn == 0:
+            object.__setattr__(self, "ffn", 4 * self.d)
+        if self.dtype != "bf16":
+            raise ValidationError("transformer stages run in bf16 (tcgen05)")
+        if self.d != 64 * self.heads:
+            raise ValidationError("head dim must be 64 (d == 64 * heads)")
+        if self.d % 256 or self.d > 2048:
+            raise ValidationError("d must be a multiple of 256 and <= 2048 (LayerNorm kernel)")
+        if self.seq % 64:
+            raise ValidationError("seq must be a multiple of 64 (attention tiles)")
+        if self.ffn % 8:
+            raise ValidationError("ffn must be a multiple of 8")
+
+    @property
+    def vocab_pad(self) -> int:
+        return -(-self.vocab // 128) * 128
+
+    @property
+    def num_layers(self) -> int:
+        return self.layers + 2
+
+    @property
+    def bytes_per_elem(self) -> int:
+        return 2
+
+    @property
+    def tokens(self) -> int:
+        return self.batch * self.seq
+
+    def geoms(self) -> list[LayerGeom]:
+        S, d, f, Vp = self.seq, self.d, self.ffn, self.vocab_pad
+        emb = LayerGeom("embed", S, self.heads, Vp, d, False, False, False, S, S * d, S * d, (Vp + S, d))
+        blk = LayerGeom("block", S, self.heads, d, d, False, False, False, S * d, S * d, S * d, (4 * d + 2 * f, d),
+                        ffn=f)
+        head = LayerGeom("head", S, self.heads, d, Vp, False, False, False, S * d, S * Vp, S * d, (Vp, d),
+                         vocab=self.vocab)
+        return [emb] + [blk] * self.layers + [head]
+
+    @property
+    def widths(self) -> tuple[int, ...]:
+        g = self.geoms()
+        return (self.seq,) + tuple(x.out_features for x in g)
+
+    def n_params(self) -> int:
+        return sum(x.w_numel + x.b_numel for x in self.geoms())
+
+    def flops_per_sample(self) -> float:
+        """Algorithmic fwd+bwd FLOPs per sequence: 6 x (linear MACs + causal attention S^2 d + head)."""
+        S, d, f = self.seq, self.d, self.ffn
+        block = S * (4 * d * d + 2 * d * f) + S * S * d
+        return 6.0 * (self.layers * block + S * d * self.vocab)
+
+
+def gpt2_medium(batch: int = 8, seq: int = 1024, **kw) -> GPTSpec:
+    """GPT-2 medium: 24 layers, d 1024, 16 heads, vocab 50257 (BASELINE configs[3])."""
+    return GPTSpec(vocab=50257, d=1024, heads=16, layers=24, seq=seq, batch=batch, **kw)
+
+
 def init_params_any(spec) -> list[tuple[np.ndarray, np.ndarray]]:
     """Initial parameters of an MLP or ConvNet spec, fp64.  Conv weights are stored tap-major
     Wt [9*c_in, c_out] (row (r*3+s)*c_in + c); the im2col'ed image layer pads rows 9*c_in..63
@@ -239,6 +332,21 @@ def init_params_any(spec) -> list[tuple[np.ndarray, np.ndarray]]:
         return init_params(spec)
     rng = np.random.default_rng(spec.seed)
     out = []
+    if isinstance(spec, GPTSpec):
+        d, f, Vp, S = spec.d, spec.ffn, spec.vocab_pad, spec.seq
+        proj = 0.02 / np.sqrt(2.0 * spec.layers)
+        for g in spec.geoms():
+            if g.kind == "embed":
+                W = np.concatenate([rng.normal(0.0, 0.02, size=(Vp, d)), rng.normal(0.0, 0.01, size=(S, d))])
+                out.append((W, np.zeros(0)))
+            elif g.kind == "block":
+                W = np.concatenate([rng.normal(0.0, 0.02, size=3 * d * d), rng.normal(0.0, proj, size=d * d),
+                                    rng.normal(0.0, 0.02, size=f * d), rng.normal(0.0, proj, size=d * f)])
+                b = np.concatenate([np.zeros(3 * d + d + f + d), np.ones(d), np.zeros(d), np.ones(d), np.zeros(d)])
+                out.append((W.reshape(g.w_shape), b))
+            else:
+                out.append((rng.normal(0.0, 0.02, size=g.w_shape), np.concatenate([np.ones(d), np.zeros(d)])))
+        return out
     for g in spec.geoms():
         if g.kind == "conv":
             fan = 9 * g.c_in
@@ -256,6 +364,9 @@ def make_data_any(spec):
     if isinstance(spec, MLPSpec):
         return make_data(spec)
     rng = np.random.default_rng([spec.seed, 1])
+    if isinstance(spec, GPTSpec):  # next-token prediction on synthetic token streams
+        tok = rng.integers(0, spec.vocab, size=(spec.n_blocks, spec.batch, spec.seq + 1)).astype(np.int32)
+        return tok[:, :, :-1].copy(), tok[:, :, 1:].copy()
     H, W, C = spec.image
     X = rng.normal(0.0, 1.0, size=(spec.n_blocks, spec.batch, H, W, C))
     y = rng.integers(0, spec.classes, size=(spec.n_blocks, spec.batch)).astype(np.int32)

@@ -30,7 +30,7 @@ def test_library_loads_and_exports():
 
 def test_struct_layouts():
     # field order of the ctypes mirrors must match the C structs (sizes on x86-64)
-    assert ctypes.sizeof(nat.Epilogue) == 4 + 4 + 8 + 8 + 8 + 4 + 4 + 8 + 8 + 8 + 8 + 4 + 4 + 8 + 8 + 8 + 4 + 4
+    assert ctypes.sizeof(nat.Epilogue) == 4 + 4 + 8 + 8 + 8 + 4 + 4 + 8 + 8 + 8 + 8 + 4 + 4 + 8 + 8 + 8 + 4 + 4 + 8
     assert ctypes.sizeof(nat.Record) == 24
 
 
