@@ -36,8 +36,9 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--workload", choices=["mlp", "vgg"], default="mlp",
-                   help="mlp: configs[1] MLP-8192 straight pipeline (headline); vgg: configs[2] VGG-16 7-1")
+    p.add_argument("--workload", choices=["mlp", "vgg", "gpt"], default="mlp",
+                   help="mlp: configs[1] MLP-8192 straight pipeline (headline); vgg: configs[2] VGG-16 7-1; "
+                        "gpt: configs[3] GPT-2 medium 8-stage")
     p.add_argument("--batch", type=int, default=2048)
     p.add_argument("--minibatches", type=int, default=64)
     p.add_argument("--width", type=int, default=8192)
@@ -52,7 +53,26 @@ def parse():
     return p.parse_args()
 
 
+GPT_BOUNDS = [(1, 4), (5, 7), (8, 10), (11, 13), (14, 17), (18, 21), (22, 25), (26, 26)]
+
+
 def workload(args):
+    if args.workload == "gpt":
+        return {
+            "workload": "cfg4: GPT-2 medium (24 layers, d 1024, 16 heads, vocab 50257 padded to 50304, untied head), "
+                        "seq 1024, bf16, synthetic tokens, 8-stage 1F1B weight_stashing",
+            "minibatch": args.batch,
+            "minibatch_unit": "sequences of 1024 tokens",
+            "minibatches_per_step": args.minibatches,
+            "stages": 8,
+            "stage_layers": GPT_BOUNDS,
+            "stages_per_gpu": 8 // max(1, args.gpus),
+            "lr": 1e-4,
+            "l2": "working set > 100x L2 (126 MB); no flush needed",
+            "loss": "next-token softmax cross-entropy, mean over tokens",
+            "streams": "one per GPU (stages in program order)" if args.serial == "on" else "one per stage",
+            "roofline_timing": "per-GEMM CUDA events over one extra serial step (no inter-stage overlap)",
+        }
     if args.workload == "vgg":
         return {
             "workload": "cfg3: VGG-16 on synthetic 224x224 images, PipeDream 7-1 (conv stack replicated 7x with "
@@ -220,6 +240,37 @@ def cpu_sample_vgg(args, seconds=12.0, batch=4, max_minibatches=2):
                       f"(fwd+bwd+SGD, torch-CPU fp32 conv-net oracle) in {el:.1f} s"}
 
 
+def cpu_sample_gpt(args, seconds=12.0, max_minibatches=1):
+    """Time the GPT oracle (torch CPU fp32 autograd, all host threads) on one GPT-2 medium sequence."""
+    import numpy as np
+    import torch
+
+    import paper_1806_03377_b200 as pd
+    from oracle.gpt_oracle import gpt_train
+
+    torch.set_num_threads(os.cpu_count())
+    spec = pd.gpt2_medium(batch=1)
+    key = ("gpt", 1)
+    if key not in _CPU_CACHE:
+        rng = np.random.default_rng(0)
+        params = [(rng.standard_normal(g.w_shape, dtype=np.float32) * np.float32(0.02),
+                   np.zeros(g.b_numel, dtype=np.float32)) for g in spec.geoms()]
+        tok = rng.integers(0, spec.vocab, size=(1, 1, spec.seq + 1)).astype(np.int32)
+        _CPU_CACHE[key] = (params, tok[:, :, :-1], tok[:, :, 1:])
+    params, X, y = _CPU_CACHE[key]
+    bounds = [(1, spec.num_layers)]
+    done, t0 = 0, time.perf_counter()
+    while True:
+        gpt_train(spec, params, X, y, 1e-4, bounds, lambda s, mb, d: 0, 1, emulate=None, dtype=torch.float32)
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or done >= max_minibatches:
+            break
+    return {"value": done / el, "unit": "samples/s", "cores": torch.get_num_threads(), "kind": "port",
+            "sample": f"{done} sequence(s) of 1024 tokens through all 26 GPT-2 medium layers "
+                      f"(fwd+bwd+SGD, torch-CPU fp32 autograd oracle) in {el:.1f} s"}
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
@@ -227,9 +278,14 @@ def run_reference(args, rank):
 
     cfg = workload(args)
     vgg = args.workload == "vgg"
-    one = (lambda: cpu_sample_vgg(args, seconds=0.0, max_minibatches=1)) if vgg else \
-        (lambda: cpu_sample(args, seconds=0.0, max_minibatches=1))
-    per_step = 4 if vgg else 128
+    gpt = args.workload == "gpt"
+    if gpt:
+        one = lambda: cpu_sample_gpt(args, seconds=0.0)  # noqa: E731
+    elif vgg:
+        one = lambda: cpu_sample_vgg(args, seconds=0.0, max_minibatches=1)  # noqa: E731
+    else:
+        one = lambda: cpu_sample(args, seconds=0.0, max_minibatches=1)  # noqa: E731
+    per_step = 1 if gpt else (4 if vgg else 128)
     for _ in range(args.warmup):
         one()
     vals = []
@@ -241,7 +297,9 @@ def run_reference(args, rank):
     value = samples / el
     cb = dict(vals[-1])
     cb["value"] = value
-    cb["sample"] = (f"{args.steps} steps x 1 minibatch of 4 images, all 16 VGG-16 layers, torch-CPU fp32" if vgg else
+    cb["sample"] = (f"{args.steps} steps x 1 sequence of 1024 tokens, all 26 GPT-2 medium layers, torch-CPU fp32"
+                    if gpt else
+                    f"{args.steps} steps x 1 minibatch of 4 images, all 16 VGG-16 layers, torch-CPU fp32" if vgg else
                     f"{args.steps} steps x 1 minibatch of 128 samples, all {args.layers} layers, numpy fp32")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
@@ -258,7 +316,11 @@ def run_ours(args, rank, world):
 
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     dev = torch.cuda.current_device()
-    if args.workload == "vgg":
+    if args.workload == "gpt":
+        stages = tuple(pd.Stage(a, b, 1) for a, b in GPT_BOUNDS)
+        plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=8, machines_used=8)
+        spec = pd.gpt2_medium(batch=args.batch, lr=1e-4, n_blocks=2, seed=0)
+    elif args.workload == "vgg":
         # PipeDream's VGG-16 partition on 8 machines: conv stack x7, FC stage x1
         plan = pd.Plan(stages=(pd.Stage(1, 13, 7), pd.Stage(14, 16, 1)), bottleneck_time=1.0, noam=2, machines_used=8)
         spec = pd.vgg16(batch=args.batch, lr=1e-3, n_blocks=2, seed=0)
@@ -315,8 +377,13 @@ def run_ours(args, rank, world):
     ex.step(stream=stream, trace=True)
     res = ex.result()
     # ---------------- e2e through the public API with host buffers
-    X_host = torch.randn(spec.n_blocks, spec.batch, spec.widths[0]).to(torch.bfloat16).pin_memory()
-    if args.workload == "vgg":
+    if args.workload == "gpt":
+        X_host = torch.randint(0, spec.vocab, (spec.n_blocks, spec.batch, spec.seq), dtype=torch.int32).pin_memory()
+    else:
+        X_host = torch.randn(spec.n_blocks, spec.batch, spec.widths[0]).to(torch.bfloat16).pin_memory()
+    if args.workload == "gpt":
+        T_host = torch.randint(0, spec.vocab, (spec.n_blocks, spec.batch, spec.seq), dtype=torch.int32).pin_memory()
+    elif args.workload == "vgg":
         T_host = torch.randint(0, spec.classes, (spec.n_blocks, spec.batch), dtype=torch.int32).pin_memory()
     else:
         T_host = torch.randn(spec.n_blocks, spec.batch, spec.widths[-1]).pin_memory()
@@ -374,6 +441,7 @@ def run_ours(args, rank, world):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": workload(args),
         "roofline": {"bound": "tensor",
                      "kernel": f"k_gemm_tc ({dom_name}{', conv + linear' if args.workload == 'vgg' else ''})",
+                     "flops_per_launch": dom["flops_per_launch"], "avg_launch_ms": dom["avg_ms"],
                      "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} bf16_tflops_sustained (MEASURED_PEAKS.json)"},
@@ -390,13 +458,19 @@ def run_ours(args, rank, world):
         "steady_minibatches_per_s": rep.steady_throughput if rep else None,
     }
     if not args.no_cpu_baseline and world == 1:
-        out["cpu_baseline"] = cpu_sample_vgg(args) if args.workload == "vgg" else cpu_sample(args)
+        out["cpu_baseline"] = (cpu_sample_vgg(args) if args.workload == "vgg" else
+                               cpu_sample_gpt(args) if args.workload == "gpt" else cpu_sample(args))
     ex.close()
     print(json.dumps(out), flush=True)
 
 
 def main():
     args = parse()
+    if args.workload == "gpt":
+        if "--batch" not in sys.argv:
+            args.batch = 8  # sequences of 1024 tokens per minibatch
+        if "--minibatches" not in sys.argv:
+            args.minibatches = 32  # >= 25 for the reference's steady window at 8 stages
     if args.workload == "vgg":
         if "--batch" not in sys.argv:
             args.batch = 32

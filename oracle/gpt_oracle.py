@@ -129,10 +129,12 @@ class _QFP32(torch.autograd.Function):
         return g
 
 
-def gpt_train(spec, params, X, labels, lr, stage_bounds, versions, K, emulate: str | None = "bf16"):
+def gpt_train(spec, params, X, labels, lr, stage_bounds, versions, K, emulate: str | None = "bf16",
+              dtype=torch.float64):
     """Delayed-SGD pipeline training of a GPTSpec model (see module docstring).
 
     params: [(W, b)] numpy per profile layer (device layout); X, labels: [n_blocks, B, S] ints.
+    dtype: arithmetic type (float64 for parity; float32 for the timed CPU baseline, no emulation).
     Returns (losses[K], final params list of numpy (W, b)).
     """
     emul = emulate == "bf16"
@@ -143,8 +145,8 @@ def gpt_train(spec, params, X, labels, lr, stage_bounds, versions, K, emulate: s
         for l in range(a, b + 1):
             layer_stage[l - 1] = s
     first = [a - 1 for a, _ in stage_bounds]
-    archives = [{0: [(master(torch.from_numpy(np.asarray(params[l - 1][0], np.float64)).clone()),
-                      master(torch.from_numpy(np.asarray(params[l - 1][1], np.float64)).clone()))
+    archives = [{0: [(master(torch.from_numpy(np.asarray(params[l - 1][0])).to(dtype).clone()),
+                      master(torch.from_numpy(np.asarray(params[l - 1][1])).to(dtype).clone()))
                      for l in range(a, b + 1)]} for (a, b) in stage_bounds]
     latest_v = [0] * n
     losses = []
@@ -177,5 +179,5 @@ def gpt_train(spec, params, X, labels, lr, stage_bounds, versions, K, emulate: s
             latest_v[s] = mb
     final = []
     for s in range(n):
-        final.extend((W.numpy(), b.numpy()) for W, b in archives[s][latest_v[s]])
+        final.extend((W.double().numpy(), b.double().numpy()) for W, b in archives[s][latest_v[s]])
     return np.array(losses), final
