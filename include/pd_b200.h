@@ -201,6 +201,7 @@ typedef struct pd_stage_desc {
   float* logits;            /* PD_LOSS_CE: fp32 [batch, classes] */
   float* part;              /* fp32 scratch for split-K partials and column-sum blocks (size from
                                pd_layer_scratch_floats) */
+  int* sync;                /* 16 zeroed int32: self-resetting counters of single-launch reductions */
 } pd_stage_desc;
 
 enum pd_layer_kind { PD_LAYER_LINEAR = 0, PD_LAYER_CONV3 = 1, PD_LAYER_EMBED = 2, PD_LAYER_BLOCK = 3, PD_LAYER_HEAD = 4 };
@@ -307,10 +308,12 @@ int pd_rt_records(pd_runtime* rt, pd_record* out, int cap, int* n_out);
 /* serial=1: every hosted stage issues on one stream in program order (single-GPU mode;
  * the per-item dependencies are then satisfied by stream order). */
 int pd_rt_set_serial(pd_runtime* rt, int on);
-/* Per-GEMM CUDA-event timing on the launching stage stream (resets the counters).
- * stats: 3 classes (forward, dgrad, wgrad+SGD) x {launches, total ms, algorithmic flops}. */
+/* Per-kernel CUDA-event timing on the launching stage stream (resets the counters).
+ * stats: n_classes (<= 8) classes x {launches, total ms, algorithmic flops}; classes are
+ * 0 forward GEMM, 1 dgrad GEMM, 2 wgrad(+SGD) GEMM, 3 attention, 4 LayerNorm, 5 loss,
+ * 6 update/reduction (bias sums, split-K / allreduce + SGD), 7 other (pool, im2col, embedding, cast). */
 int pd_rt_kernel_timing(pd_runtime* rt, int on);
-int pd_rt_kernel_stats(pd_runtime* rt, double* out9);
+int pd_rt_kernel_stats(pd_runtime* rt, double* out, int n_classes);
 /* Kernels of this library launched by the runtime since creation. */
 int pd_rt_launch_count(pd_runtime* rt, int64_t* out);
 int pd_rt_destroy(pd_runtime* rt);

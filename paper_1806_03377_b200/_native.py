@@ -71,6 +71,7 @@ class StageDesc(Structure):
         ("red_grad", POINTER(c_void_p)), ("red_bgrad", POINTER(c_void_p)), ("red_ready", c_void_p),
         ("red_done", c_void_p), ("err_word", c_void_p),
         ("layers", POINTER(LayerDesc)), ("loss_kind", c_int), ("logits", c_void_p), ("part", c_void_p),
+        ("sync", c_void_p),
     ]
 
 
@@ -123,7 +124,7 @@ def lib() -> ctypes.CDLL:
         L.pd_rt_destroy.argtypes = [c_void_p]
         L.pd_rt_kernel_timing.argtypes = [c_void_p, c_int]
         L.pd_rt_set_serial.argtypes = [c_void_p, c_int]
-        L.pd_rt_kernel_stats.argtypes = [c_void_p, POINTER(c_double)]
+        L.pd_rt_kernel_stats.argtypes = [c_void_p, POINTER(c_double), c_int]
         L.pd_rt_launch_count.argtypes = [c_void_p, POINTER(c_int64)]
         L.pd_device_sm_count.argtypes = [c_int, POINTER(c_int)]
         L.pd_conv3x3.argtypes = [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, POINTER(Epilogue),

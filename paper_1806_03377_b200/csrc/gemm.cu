@@ -687,6 +687,11 @@ static void pick_cfg(int M, int N, bool b_mn, int* cg, int* bn) {
 template <bool A_MN, bool B_MN, int KIND>
 static int launch_bn(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
                      cudaStream_t st) {
+  if constexpr (!A_MN && B_MN && KIND == EPI_STORE) {
+    // narrow outputs (the im2col'ed first convolution, c_out = 64): a 256-wide tile would be 3/4 padding
+    if (N <= 64) return launch_tc<1, 64, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
+    if (N <= 128) return launch_tc<1, 128, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
+  }
   int cg, bn;
   pick_cfg(M, N, B_MN, &cg, &bn);
   if (cg == 2) {

@@ -121,43 +121,74 @@ int maxpool_bwd(const void* dy, const uint8_t* arg, void* dx, int n, int H, int 
 // cols[pix, k] for k = (r*3+s)*C + c < 9C: x[n, p+r-1, q+s-1, c] (0 outside); k >= 9C: 0.
 // Only the first convolution (C = 3 image channels) uses it: its 27-wide K would waste a
 // 64-channel im2col TMA box; every other layer reads im2col tiles straight from the activation.
+// One thread per output pixel: gathers its 9*C inputs (C <= 7) and writes the 128-byte cols row
+// with eight 16-byte stores (the output stream is what bounds this kernel).
 __global__ void __launch_bounds__(256) k_im2col3(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ cols,
                                                  int n, int H, int W, int C, int kpad) {
-  const int64_t total = (int64_t)n * H * W * kpad;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(i % kpad);
-    const int64_t pix = i / kpad;
-    __nv_bfloat16 v = __float2bfloat16_rn(0.f);
-    if (k < 9 * C) {
-      const int tap = k / C, c = k - tap * C;
-      const int q = (int)(pix % W), p = (int)((pix / W) % H);
-      const int64_t b = pix / ((int64_t)H * W);
+  const int64_t pixels = (int64_t)n * H * W;
+  for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < pixels;
+       pix += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(pix % W), p = (int)((pix / W) % H);
+    const int64_t b = pix / ((int64_t)H * W);
+    uint32_t w[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) w[i] = 0;
+    int k = 0;
+    for (int tap = 0; tap < 9; ++tap) {
       const int hh = p + tap / 3 - 1, ww = q + tap % 3 - 1;
-      if (hh >= 0 && hh < H && ww >= 0 && ww < W) v = x[((b * H + hh) * W + ww) * C + c];
+      const bool ok = hh >= 0 && hh < H && ww >= 0 && ww < W;
+      const __nv_bfloat16* src = x + ((b * H + hh) * W + ww) * C;
+      for (int c = 0; c < C; ++c, ++k) {
+        const uint16_t v = ok ? __bfloat16_as_ushort(src[c]) : (uint16_t)0;
+        w[k >> 1] |= (uint32_t)v << ((k & 1) * 16);
+      }
     }
-    cols[i] = v;
+    uint4* dst = reinterpret_cast<uint4*>(cols + pix * kpad);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
   }
 }
 
 int im2col3(const void* x, void* cols, int n, int H, int W, int C, int kpad, cudaStream_t st) {
-  if (9 * C > kpad) return set_error(PD_ERR_INVALID, "im2col: kpad %d < 9*C", kpad);
-  const int64_t total = (int64_t)n * H * W * kpad;
+  if (9 * C > kpad || kpad != 64) return set_error(PD_ERR_INVALID, "im2col: kpad must be 64 and >= 9*C (%d)", kpad);
+  const int64_t total = (int64_t)n * H * W;
   k_im2col3<<<grid_for(total, 256), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x),
                                                   static_cast<__nv_bfloat16*>(cols), n, H, W, C, kpad);
   return launch_status("im2col3");
 }
 
-// ---------------------------------------------------------------- column sums (conv bias grads)
-// Pass 1: block b sums rows [b*rows_per, ...) of a [rows, C] bf16 matrix into part[b][C] (fp32);
-// each thread owns 8 columns (one 16-byte vector) and a strided set of rows.
+// ---------------------------------------------------------------- column sums (bias gradients)
+// Block b sums rows [b*rows_per, ...) of a [rows, C] bf16 matrix into part[b][C] (fp32); narrow
+// rows: each thread owns 8 columns (one 16-byte vector) and a strided set of rows; wide rows
+// (C/8 > 128): each thread owns column groups and walks the block's rows.  With a counter, the
+// last block to finish (threadfence + atomic ticket) sums the partials in block order and applies
+// the update itself (grad, or SGD into master/out), so the whole bias gradient is one launch;
+// the counter resets itself for the next launch on the stream.
 constexpr int CS_THREADS = 256;
+__device__ __forceinline__ void finish_update(const float* part, int S, int C, float* grad, float* master, float* out,
+                                              float lr) {
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float g = 0.f;
+    for (int b = 0; b < S; ++b) g += __ldcg(part + (int64_t)b * C + c);
+    if (grad) {
+      grad[c] = g;
+    } else {
+      const float w = master[c] - lr * g;
+      master[c] = w;
+      out[c] = w;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(CS_THREADS) k_colsum_part(const __nv_bfloat16* __restrict__ x, int64_t rows, int C,
-                                                            int64_t rows_per, float* __restrict__ part) {
-  extern __shared__ float red[];  // [CS_THREADS / (C/8)][C]
+                                                            int64_t rows_per, float* __restrict__ part, int* counter,
+                                                            float* grad, float* master, float* out, float lr) {
+  extern __shared__ float red[];  // narrow rows: [CS_THREADS / (C/8)][C]
+  __shared__ bool last;
   const int C8 = C / 8;
-  if (C8 > CS_THREADS / 2) {  // wide rows: each thread owns column groups, walks all rows of the block
-    const int64_t r0 = blockIdx.x * rows_per;
-    const int64_t r1 = r0 + rows_per < rows ? r0 + rows_per : rows;
+  const int64_t r0 = blockIdx.x * rows_per;
+  const int64_t r1 = r0 + rows_per < rows ? r0 + rows_per : rows;
+  if (C8 > CS_THREADS / 2) {
     for (int cg = threadIdx.x; cg < C8; cg += CS_THREADS) {
       float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int64_t r = r0; r < r1; ++r) {
@@ -171,37 +202,45 @@ __global__ void __launch_bounds__(CS_THREADS) k_colsum_part(const __nv_bfloat16*
           acc[2 * j + 1] += b;
         }
       }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) part[(int64_t)blockIdx.x * C + cg * 8 + j] = acc[j];
+      float4* dst = reinterpret_cast<float4*>(part + (int64_t)blockIdx.x * C + cg * 8);
+      dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
     }
-    return;
-  }
-  const int lanes = CS_THREADS / C8;  // row lanes per block
-  const int cg = threadIdx.x % C8, rl = threadIdx.x / C8;
-  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const int64_t r0 = blockIdx.x * rows_per;
-  const int64_t r1 = r0 + rows_per < rows ? r0 + rows_per : rows;
-  if (rl < lanes)
-    for (int64_t r = r0 + rl; r < r1; r += lanes) {
-      const uint4 v = *reinterpret_cast<const uint4*>(x + r * C + cg * 8);
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  } else {
+    const int lanes = CS_THREADS / C8;  // row lanes per block
+    const int cg = threadIdx.x % C8, rl = threadIdx.x / C8;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (rl < lanes)
+      for (int64_t r = r0 + rl; r < r1; r += lanes) {
+        const uint4 v = *reinterpret_cast<const uint4*>(x + r * C + cg * 8);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float a, b;
-        unpack_bf16x2(w[j], a, b);
-        acc[2 * j] += a;
-        acc[2 * j + 1] += b;
+        for (int j = 0; j < 4; ++j) {
+          float a, b;
+          unpack_bf16x2(w[j], a, b);
+          acc[2 * j] += a;
+          acc[2 * j + 1] += b;
+        }
       }
-    }
-  if (rl < lanes)
+    if (rl < lanes)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) red[rl * C + cg * 8 + j] = acc[j];
-  __syncthreads();
-  for (int c = threadIdx.x; c < C; c += CS_THREADS) {
-    float s = 0.f;
-    for (int l = 0; l < lanes; ++l) s += red[l * C + c];
-    part[(int64_t)blockIdx.x * C + c] = s;
+      for (int j = 0; j < 8; ++j) red[rl * C + cg * 8 + j] = acc[j];
+    __syncthreads();
+    for (int c = threadIdx.x; c < C; c += CS_THREADS) {
+      float s = 0.f;
+      for (int l = 0; l < lanes; ++l) s += red[l * C + c];
+      part[(int64_t)blockIdx.x * C + c] = s;
+    }
   }
+  if (!counter) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  finish_update(part, gridDim.x, C, grad, master, out, lr);
+  if (threadIdx.x == 0) *counter = 0;
 }
 
 // Pass 2 (shared with split-K): g[i] = sum_s part[s*stride + i] in order s = 0..S-1, then
@@ -236,24 +275,27 @@ int reduce_sgd(int out_dtype, const float* part, int S, int64_t stride, int64_t 
   return launch_status("reduce_sgd");
 }
 
+// One wave of blocks (at least 16 rows each): enough parallelism to stream the matrix at HBM
+// rate, few enough partials that the fixed-order final sum stays cheap.
 int colsum_blocks(int64_t rows, int C) {
-  const int64_t per = C / 8 > CS_THREADS / 2 ? 32 : 2048;
-  int64_t b = (rows + per - 1) / per;
-  const int64_t cap = (int64_t)sm_count() * 4;
+  (void)C;
+  int64_t b = (rows + 15) / 16;
+  const int64_t cap = (int64_t)sm_count() * 2;
   return (int)(b < 1 ? 1 : (b < cap ? b : cap));
 }
 
 // Bias gradient of a [rows, C] bf16 gradient; part must hold colsum_blocks(rows, C) * C floats.
 int bias_grad_tall(const void* dz, int64_t rows, int C, float* part, float* grad, float* master, float* out, float lr,
-                   cudaStream_t st) {
+                   cudaStream_t st, int* counter) {
   if (C % 8) return set_error(PD_ERR_INVALID, "bias_grad_tall: C %% 8 == 0");
   const int blocks = colsum_blocks(rows, C);
   const int64_t per = (rows + blocks - 1) / blocks;
   const int lanes = CS_THREADS / (C / 8);
   const size_t smem = C / 8 > CS_THREADS / 2 ? 0 : (size_t)(lanes > 0 ? lanes : 1) * C * sizeof(float);
-  k_colsum_part<<<blocks, CS_THREADS, smem, st>>>(static_cast<const __nv_bfloat16*>(dz), rows, C, per, part);
+  k_colsum_part<<<blocks, CS_THREADS, smem, st>>>(static_cast<const __nv_bfloat16*>(dz), rows, C, per, part, counter,
+                                                  grad, master, out, lr);
   int rc = launch_status("colsum_part");
-  if (rc) return rc;
+  if (rc || counter) return rc;
   return reduce_sgd(PD_F32, part, blocks, C, C, grad, master, out, lr, st);
 }
 

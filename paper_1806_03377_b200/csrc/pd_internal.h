@@ -30,8 +30,9 @@ int im2col3(const void* x, void* cols, int n, int H, int W, int C, int kpad, cud
 int reduce_sgd(int out_dtype, const float* part, int S, int64_t stride, int64_t n, float* grad, float* master,
                void* out, float lr, cudaStream_t st);
 int colsum_blocks(int64_t rows, int C);
+// counter != nullptr: single launch, the last block reduces and applies (self-resetting int).
 int bias_grad_tall(const void* dz, int64_t rows, int C, float* part, float* grad, float* master, float* out, float lr,
-                   cudaStream_t st);
+                   cudaStream_t st, int* counter = nullptr);
 int softmax_ce(const float* logits, int64_t ldz, const int* labels, int B, int V, void* dz, int64_t ldd, float* loss,
                cudaStream_t st);
 
@@ -40,8 +41,10 @@ int attn_bwd(const void* qkv, const void* out, const void* dout, const float* ls
              void* dqkv, int B, int S, int H, cudaStream_t st);
 int ln_fwd(const void* x, const float* gb, void* y, float* mean, float* rstd, int64_t T, int D, cudaStream_t st);
 int ln_bwd_blocks(int64_t T);
+// counter != nullptr: the last block sums the gamma/beta partials and applies SGD to master/out.
 int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gb, const void* dres,
-           void* dx, float* part, int64_t T, int D, cudaStream_t st);
+           void* dx, float* part, int64_t T, int D, cudaStream_t st, int* counter = nullptr, float* master = nullptr,
+           float* out = nullptr, float lr = 0.f);
 int embed_fwd(const int* tok, const void* wte, const void* wpe, void* x, int64_t T, int S, int D, cudaStream_t st);
 int embed_bwd(const int* tok, const void* dx, float* gte, float* gpe, int64_t T, int S, int D, cudaStream_t st);
 int softmax_ce_v(const float* logits, int64_t ldz, const int* labels, int64_t rows, int V, int Vp, void* dz,

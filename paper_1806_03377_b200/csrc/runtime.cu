@@ -155,7 +155,9 @@ namespace {
 
 inline int flag_val(int epoch, int v) { return epoch * 65536 + v; }
 
-enum { KC_FWD = 0, KC_DGRAD = 1, KC_WGRAD = 2, KC_N = 3 };
+// Kernel-time classes (pd_rt_kernel_stats): the three GEMM passes, then the non-GEMM kernels.
+enum { KC_FWD = 0, KC_DGRAD = 1, KC_WGRAD = 2, KC_ATTN = 3, KC_NORM = 4, KC_LOSS = 5, KC_UPDATE = 6, KC_OTHER = 7,
+       KC_N = 8 };
 
 inline cudaStream_t stream_of(pd_runtime* rt, Stage& S) { return rt->serial ? rt->shared : S.stream; }
 
@@ -197,6 +199,27 @@ int64_t b_numel(const Stage& S, int l) {
   if (y.kind == PD_LAYER_BLOCK) return 9ll * y.c_in + y.ffn;
   if (y.kind == PD_LAYER_HEAD) return 2ll * y.c_in;
   return y.c_out;
+}
+
+// CUDA events around one non-GEMM kernel call on its stream when kernel timing is on.
+template <class Fn>
+int timed_call(pd_runtime* rt, int cls, cudaStream_t st, Fn&& fn) {
+  pd_runtime::KT* slot = nullptr;
+  if (rt->ktiming) {
+    if (rt->kt_used == rt->kt.size()) {
+      pd_runtime::KT k{};
+      PD_CHECK(cudaEventCreate(&k.a));
+      PD_CHECK(cudaEventCreate(&k.b));
+      rt->kt.push_back(k);
+    }
+    slot = &rt->kt[rt->kt_used++];
+    slot->cls = cls;
+    slot->flops = 0.0;
+    PD_CHECK(cudaEventRecord(slot->a, st));
+  }
+  const int rc = fn();
+  if (slot) PD_CHECK(cudaEventRecord(slot->b, st));
+  return rc;
 }
 
 int wait_flag(pd_runtime* rt, Stage& S, const int* flag, int value) {
@@ -279,7 +302,7 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.out = S.red_grad[(size_t)l * 2 + par];
       ep.ldo = Kin;
       PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, Nout, X, 1, Kin, Nout, Kin, B, EPI_GRADF32, ep, ST));
-      PD_TRY(bias_grad(d.dtype, dz, B, Nout, Nout, S.red_bgrad[(size_t)l * 2 + par], ST));
+      PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return bias_grad(d.dtype, dz, B, Nout, Nout, S.red_bgrad[(size_t)l * 2 + par], ST); }));
       rt->launches += 1;
     } else if (wnew >= 0) {
       // wgrad + SGD onto the latest weights, written as version mb into ring slot wnew
@@ -290,8 +313,8 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.ldo = Kin;
       ep.lr = d.lr;
       PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, Nout, X, 1, Kin, Nout, Kin, B, EPI_SGD, ep, ST));
-      PD_TRY(bias_sgd(d.dtype, dz, B, Nout, Nout, S.b_master[l], S.b_ring[(size_t)l * d.ring_depth + wnew], d.lr,
-                      ST));
+      PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return bias_sgd(d.dtype, dz, B, Nout, Nout, S.b_master[l], S.b_ring[(size_t)l * d.ring_depth + wnew], d.lr,
+                      ST); }));
       rt->launches += 1;
     }
     dz = out;
@@ -351,7 +374,7 @@ int bias_update(pd_runtime* rt, Stage& S, int l, int wnew, int64_t boff, const v
   const pd_stage_desc& d = S.d;
   rt->launches += 2;
   return bias_grad_tall(dY, T, C, d.part, nullptr, S.b_master[l] + boff,
-                        S.b_ring[(size_t)l * d.ring_depth + wnew] + boff, d.lr, st);
+                        S.b_ring[(size_t)l * d.ring_depth + wnew] + boff, d.lr, st, d.sync);
 }
 
 // LayerNorm backward fused with the residual gradient, then the gamma/beta update at goff
@@ -360,12 +383,11 @@ int ln_backward(pd_runtime* rt, Stage& S, int l, int wslot, int wnew, int64_t go
                 cudaStream_t st) {
   const pd_stage_desc& d = S.d;
   const float* gb = S.b_ring[(size_t)l * d.ring_depth + wslot] + goff;
-  PD_TRY(ln_bwd(dy, x, mean, rstd, gb, dres, dx, d.part, T, D, st));
   rt->launches += 1;
-  if (!update) return 0;
-  rt->launches += 1;
-  return reduce_sgd(PD_F32, d.part, ln_bwd_blocks(T), 2ll * D, 2ll * D, nullptr, S.b_master[l] + goff,
-                    S.b_ring[(size_t)l * d.ring_depth + wnew] + goff, d.lr, st);
+  // the gamma/beta update is fused: the last block reduces the partials and applies SGD
+  return ln_bwd(dy, x, mean, rstd, gb, dres, dx, d.part, T, D, st, update ? d.sync : nullptr,
+                update ? S.b_master[l] + goff : nullptr, update ? S.b_ring[(size_t)l * d.ring_depth + wnew] + goff : nullptr,
+                d.lr);
 }
 
 // Transformer layer forward.  x: layer input (tokens for EMBED), out: layer output [T, d]
@@ -382,21 +404,21 @@ int tfwd(pd_runtime* rt, Stage& S, const Layer& Y, int l, const int32_t* it, con
   const int D = L.d, F = L.f;
   if (y.kind == PD_LAYER_EMBED) {
     rt->launches += 1;
-    return embed_fwd(static_cast<const int*>(x), W, bf16_at(W, (int64_t)y.c_in * D), out, T, y.h, D, ST);
+    return timed_call(rt, KC_OTHER, ST, [&]() { return embed_fwd(static_cast<const int*>(x), W, bf16_at(W, (int64_t)y.c_in * D), out, T, y.h, D, ST); });
   }
   void* sv = Y.save[act];
   if (y.kind == PD_LAYER_HEAD) {
     void* h = bf16_at(sv, 0);
     float* mean = f32_at(sv, L.f32_base, L.mean1);
     float* rstd = f32_at(sv, L.f32_base, L.rstd1);
-    PD_TRY(ln_fwd(x, b, h, mean, rstd, T, D, ST));
+    PD_TRY(timed_call(rt, KC_NORM, ST, [&]() { return ln_fwd(x, b, h, mean, rstd, T, D, ST); }));
     EpiArgs ep{};
     ep.out = d.logits;
     ep.ldo = y.c_out;
     PD_TRY(gemm_t(rt, KC_FWD, h, 0, D, W, 0, D, (int)T, y.c_out, D, EPI_GRADF32, ep, ST));
     rt->launches += 2;
-    return softmax_ce_v(d.logits, y.c_out, reinterpret_cast<const int*>(S.target[it[PD_IT_BLOCK]]), T, y.vocab, y.c_out,
-                        S.dz_last[act], y.c_out, d.loss + mb, ST);
+    return timed_call(rt, KC_LOSS, ST, [&]() { return softmax_ce_v(d.logits, y.c_out, reinterpret_cast<const int*>(S.target[it[PD_IT_BLOCK]]), T, y.vocab, y.c_out,
+                        S.dz_last[act], y.c_out, d.loss + mb, ST); });
   }
   // BLOCK (pre-LN): x2 = x + attn(LN1 x) Wo^T + bo ; out = x2 + gelu(LN2 x2 W1^T + b1) W2^T + b2
   const int64_t oWo = 3ll * D * D, oW1 = 4ll * D * D, oW2 = 4ll * D * D + (int64_t)F * D;
@@ -408,13 +430,13 @@ int tfwd(pd_runtime* rt, Stage& S, const Layer& Y, int l, const int32_t* it, con
   void* h2 = bf16_at(sv, L.h2);
   void* z = bf16_at(sv, L.z);
   void* u = bf16_at(sv, L.u);
-  PD_TRY(ln_fwd(x, b + oln1, h1, f32_at(sv, L.f32_base, L.mean1), f32_at(sv, L.f32_base, L.rstd1), T, D, ST));
+  PD_TRY(timed_call(rt, KC_NORM, ST, [&]() { return ln_fwd(x, b + oln1, h1, f32_at(sv, L.f32_base, L.mean1), f32_at(sv, L.f32_base, L.rstd1), T, D, ST); }));
   EpiArgs ep{};
   ep.out = qkv;
   ep.ldo = 3 * D;
   ep.bias = b;
   PD_TRY(gemm_t(rt, KC_FWD, h1, 0, D, W, 0, D, (int)T, 3 * D, D, EPI_STORE, ep, ST));
-  PD_TRY(attn_fwd(qkv, a, f32_at(sv, L.f32_base, L.lse), (int)(T / y.h), y.h, L.H, ST));
+  PD_TRY(timed_call(rt, KC_ATTN, ST, [&]() { return attn_fwd(qkv, a, f32_at(sv, L.f32_base, L.lse), (int)(T / y.h), y.h, L.H, ST); }));
   ep = EpiArgs{};
   ep.out = x2;
   ep.ldo = D;
@@ -422,7 +444,7 @@ int tfwd(pd_runtime* rt, Stage& S, const Layer& Y, int l, const int32_t* it, con
   ep.mask = x;
   ep.ldm = D;
   PD_TRY(gemm_t(rt, KC_FWD, a, 0, D, bf16_at(W, oWo), 0, D, (int)T, D, D, EPI_RESID, ep, ST));
-  PD_TRY(ln_fwd(x2, b + oln2, h2, f32_at(sv, L.f32_base, L.mean2), f32_at(sv, L.f32_base, L.rstd2), T, D, ST));
+  PD_TRY(timed_call(rt, KC_NORM, ST, [&]() { return ln_fwd(x2, b + oln2, h2, f32_at(sv, L.f32_base, L.mean2), f32_at(sv, L.f32_base, L.rstd2), T, D, ST); }));
   ep = EpiArgs{};
   ep.out = u;
   ep.aux = z;
@@ -457,10 +479,10 @@ int tbwd(pd_runtime* rt, Stage& S, const Layer& Y, int l, const int32_t* it, con
     if (!update) return 0;
     const int64_t n = w_numel(S, l);
     PD_CHECK(cudaMemsetAsync(d.part, 0, sizeof(float) * n, ST));
-    PD_TRY(embed_bwd(static_cast<const int*>(X), dout, d.part, d.part + (int64_t)y.c_in * D, T, y.h, D, ST));
+    PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return embed_bwd(static_cast<const int*>(X), dout, d.part, d.part + (int64_t)y.c_in * D, T, y.h, D, ST); }));
     rt->launches += 2;
-    return reduce_sgd(PD_BF16, d.part, 1, n, n, nullptr, S.w_master[l], S.w_ring[(size_t)l * d.ring_depth + wnew],
-                      d.lr, ST);
+    return timed_call(rt, KC_UPDATE, ST, [&]() { return reduce_sgd(PD_BF16, d.part, 1, n, n, nullptr, S.w_master[l], S.w_ring[(size_t)l * d.ring_depth + wnew],
+                      d.lr, ST); });
   }
   void* sv = Y.save[act];
   if (y.kind == PD_LAYER_HEAD) {
@@ -522,8 +544,8 @@ int tbwd(pd_runtime* rt, Stage& S, const Layer& Y, int l, const int32_t* it, con
     PD_TRY(bias_update(rt, S, l, wnew, obo, dx2, T, D, ST));
   }
   // attention
-  PD_TRY(attn_bwd(qkv, a, da, f32_at(sv, L.f32_base, L.lse), f32_at(y.work, L.w32_base, L.dvec),
-                  f32_at(y.work, L.w32_base, L.dq_acc), dqkv, (int)(T / y.h), y.h, L.H, ST));
+  PD_TRY(timed_call(rt, KC_ATTN, ST, [&]() { return attn_bwd(qkv, a, da, f32_at(sv, L.f32_base, L.lse), f32_at(y.work, L.w32_base, L.dvec),
+                  f32_at(y.work, L.w32_base, L.dq_acc), dqkv, (int)(T / y.h), y.h, L.H, ST); }));
   rt->launches += 3;
   // QKV: dh1 = dqkv Wqkv
   ep = EpiArgs{};
@@ -584,8 +606,8 @@ int run_forward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
       }
       PD_TRY(timed_gemm(rt, KC_FWD, d.dtype, x, 0, y.c_in, W, 0, y.c_in, B, y.c_out, y.c_in, kind, ep, ST));
       if (last && d.is_last && d.loss_kind == PD_LOSS_CE) {
-        PD_TRY(softmax_ce(d.logits, y.c_out, reinterpret_cast<const int*>(S.target[it[PD_IT_BLOCK]]), B, y.c_out,
-                          S.dz_last[act], y.c_out, d.loss + mb, ST));
+        PD_TRY(timed_call(rt, KC_LOSS, ST, [&]() { return softmax_ce(d.logits, y.c_out, reinterpret_cast<const int*>(S.target[it[PD_IT_BLOCK]]), B, y.c_out,
+                          S.dz_last[act], y.c_out, d.loss + mb, ST); }));
         rt->launches += 1;
       }
       x = out;
@@ -599,14 +621,14 @@ int run_forward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
     const int pix = B * y.h * y.w;
     if (y.im2col) {
       void* cols = Y.cols[act];
-      PD_TRY(im2col3(x, cols, B, y.h, y.w, y.c_in, 64, ST));
+      PD_TRY(timed_call(rt, KC_OTHER, ST, [&]() { return im2col3(x, cols, B, y.h, y.w, y.c_in, 64, ST); }));
       rt->launches += 1;
       PD_TRY(timed_gemm(rt, KC_FWD, d.dtype, cols, 0, 64, W, 1, y.c_out, pix, y.c_out, 64, EPI_STORE, ep, ST));
     } else {
       PD_TRY(timed_conv(rt, KC_FWD, PD_CONV_FWD, x, W, B, y.h, y.w, y.c_in, y.c_out, EPI_STORE, ep, ST));
     }
     if (y.pool) {
-      PD_TRY(maxpool_fwd(conv_out, out, Y.argmax[act], B, y.h, y.w, y.c_out, ST));
+      PD_TRY(timed_call(rt, KC_OTHER, ST, [&]() { return maxpool_fwd(conv_out, out, Y.argmax[act], B, y.h, y.w, y.c_out, ST); }));
       rt->launches += 1;
     }
     x = out;
@@ -660,7 +682,7 @@ int run_backward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
         ep.out = gW;
         ep.ldo = y.c_in;
         PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, y.c_out, X, 1, y.c_in, y.c_out, y.c_in, B, EPI_GRADF32, ep, ST));
-        PD_TRY(bias_grad(d.dtype, dz, B, y.c_out, y.c_out, gb, ST));
+        PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return bias_grad(d.dtype, dz, B, y.c_out, y.c_out, gb, ST); }));
         rt->launches += 1;
       } else if (update) {
         EpiArgs ep{};
@@ -670,7 +692,7 @@ int run_backward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
         ep.ldo = y.c_in;
         ep.lr = d.lr;
         PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, y.c_out, X, 1, y.c_in, y.c_out, y.c_in, B, EPI_SGD, ep, ST));
-        PD_TRY(bias_sgd(d.dtype, dz, B, y.c_out, y.c_out, S.b_master[l], bring_new, d.lr, ST));
+        PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return bias_sgd(d.dtype, dz, B, y.c_out, y.c_out, S.b_master[l], bring_new, d.lr, ST); }));
         rt->launches += 1;
       }
       dz = dst;
@@ -681,7 +703,7 @@ int run_backward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
     const void* dy = dz;
     if (y.pool) {
       void* t = other_tmp(dz);
-      PD_TRY(maxpool_bwd(dz, Y.argmax[act], t, B, y.h, y.w, y.c_out, ST));
+      PD_TRY(timed_call(rt, KC_OTHER, ST, [&]() { return maxpool_bwd(dz, Y.argmax[act], t, B, y.h, y.w, y.c_out, ST); }));
       rt->launches += 1;
       dy = t;
     }
@@ -701,8 +723,8 @@ int run_backward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
       else
         PD_TRY(timed_conv(rt, KC_WGRAD, PD_CONV_WGRAD, X, dy, B, y.h, y.w, y.c_in, y.c_out, EPI_GRADF32, ep, ST));
       const int64_t n = (int64_t)M * y.c_out;
-      PD_TRY(reduce_sgd(d.dtype, d.part, splits, n, n, gW, S.w_master[l], ring_new, d.lr, ST));
-      PD_TRY(bias_grad_tall(dy, pix, y.c_out, d.part, gb, S.b_master[l], bring_new, d.lr, ST));
+      PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return reduce_sgd(d.dtype, d.part, splits, n, n, gW, S.w_master[l], ring_new, d.lr, ST); }));
+      PD_TRY(bias_grad_tall(dy, pix, y.c_out, d.part, gb, S.b_master[l], bring_new, d.lr, ST, d.sync));
       rt->launches += 3;
     }
     if (need_dx) {
@@ -736,10 +758,10 @@ int run_reduce(pd_runtime* rt, Stage& S, const int32_t* it) {
       gb[r] = V.red_bgrad[(size_t)l * 2 + par];
     }
     const int64_t n = w_numel(S, l);
-    PD_TRY(allreduce_sgd(d.dtype, g.data(), d.rep, S.w_master[l], S.w_ring[(size_t)l * d.ring_depth + wnew], n,
-                         d.lr, ST));
-    PD_TRY(allreduce_sgd(PD_F32, gb.data(), d.rep, S.b_master[l], S.b_ring[(size_t)l * d.ring_depth + wnew],
-                         b_numel(S, l), d.lr, ST));
+    PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return allreduce_sgd(d.dtype, g.data(), d.rep, S.w_master[l], S.w_ring[(size_t)l * d.ring_depth + wnew], n,
+                         d.lr, ST); }));
+    PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return allreduce_sgd(PD_F32, gb.data(), d.rep, S.b_master[l], S.b_ring[(size_t)l * d.ring_depth + wnew],
+                         b_numel(S, l), d.lr, ST); }));
     rt->launches += 2;
   }
   PD_TRY(signal_flag(rt, S, d.red_done, round));
@@ -800,13 +822,14 @@ int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc) {
           return set_error(PD_ERR_INVALID, "worker %d: the embedding must be the model input", d.worker);
         if (y.kind != PD_LAYER_EMBED && (!y.save || !y.work))
           return set_error(PD_ERR_INVALID, "worker %d layer %d: missing save/work buffers", d.worker, l);
-        if (!d.part) return set_error(PD_ERR_INVALID, "worker %d: transformer layers need `part`", d.worker);
+        if (!d.part || !d.sync)
+          return set_error(PD_ERR_INVALID, "worker %d: transformer layers need `part` and `sync`", d.worker);
         Y.t = tlayout(y, d.batch);
         if (y.save) Y.save.assign(y.save, y.save + d.act_depth);
       }
       if (d.dtype != PD_BF16) return set_error(PD_ERR_INVALID, "worker %d: layered stages are bf16", d.worker);
-      if (y.kind == PD_LAYER_CONV3 && !d.part)
-        return set_error(PD_ERR_INVALID, "worker %d: conv layers need the `part` scratch", d.worker);
+      if (y.kind == PD_LAYER_CONV3 && (!d.part || !d.sync))
+        return set_error(PD_ERR_INVALID, "worker %d: conv layers need the `part` and `sync` scratch", d.worker);
       if (y.pool) {
         if (!y.argmax) return set_error(PD_ERR_INVALID, "worker %d layer %d: pool without argmax", d.worker, l);
         Y.argmax.assign(y.argmax, y.argmax + d.act_depth);
@@ -932,7 +955,7 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
     // version 0 of this run = the current (latest) weights
     for (int l = 0; l < S.d.n_layers; ++l) {
       const int64_t n = w_numel(S, l);
-      PD_TRY(cast_f32(S.d.dtype, S.w_master[l], S.w_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], n, ST));
+      PD_TRY(timed_call(rt, KC_OTHER, ST, [&]() { return cast_f32(S.d.dtype, S.w_master[l], S.w_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], n, ST); }));
       rt->launches += 1;
       if (b_numel(S, l) > 0)
         PD_CHECK(cudaMemcpyAsync(S.b_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], S.b_master[l],
@@ -1018,15 +1041,16 @@ int pd_rt_kernel_timing(pd_runtime* rt, int on) {
   return 0;
 }
 
-int pd_rt_kernel_stats(pd_runtime* rt, double* out9) {
-  if (!rt || !out9) return set_error(PD_ERR_INVALID, "pd_rt_kernel_stats: null argument");
-  for (int i = 0; i < 3 * KC_N; ++i) out9[i] = 0.0;
+int pd_rt_kernel_stats(pd_runtime* rt, double* out9, int n_classes) {
+  if (!rt || !out9 || n_classes < 1) return set_error(PD_ERR_INVALID, "pd_rt_kernel_stats: null argument");
+  for (int i = 0; i < 3 * n_classes; ++i) out9[i] = 0.0;
   PD_CHECK(cudaSetDevice(rt->device));
   for (size_t i = 0; i < rt->kt_used; ++i) {
     auto& k = rt->kt[i];
     float ms = 0.f;
     PD_CHECK(cudaEventSynchronize(k.b));
     PD_CHECK(cudaEventElapsedTime(&ms, k.a, k.b));
+    if (k.cls >= n_classes) continue;
     out9[3 * k.cls + 0] += 1.0;
     out9[3 * k.cls + 1] += ms;
     out9[3 * k.cls + 2] += k.flops;

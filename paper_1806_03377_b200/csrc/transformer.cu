@@ -95,8 +95,10 @@ __global__ void __launch_bounds__(LN_WARPS * 32) k_ln_bwd(const __nv_bfloat16* _
                                                           const float* __restrict__ gb,
                                                           const __nv_bfloat16* __restrict__ dres,
                                                           __nv_bfloat16* __restrict__ dx, float* __restrict__ part,
-                                                          int64_t T, int D, int64_t rows_per_block) {
+                                                          int64_t T, int D, int64_t rows_per_block, int* counter,
+                                                          float* master, float* mout, float lr) {
   extern __shared__ float red[];  // [LN_WARPS][2*D]
+  __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int nv = NV;
   float pg[NV][8], pb[NV][8];
@@ -156,6 +158,21 @@ __global__ void __launch_bounds__(LN_WARPS * 32) k_ln_bwd(const __nv_bfloat16* _
     for (int w = 0; w < LN_WARPS; ++w) s += red[w * 2 * D + c];
     part[blockIdx.x * 2 * (int64_t)D + c] = s;
   }
+  if (!counter) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int c = threadIdx.x; c < 2 * D; c += LN_WARPS * 32) {  // fixed block order
+    float g = 0.f;
+    for (int b = 0; b < (int)gridDim.x; ++b) g += __ldcg(part + (int64_t)b * 2 * D + c);
+    const float w = master[c] - lr * g;
+    master[c] = w;
+    mout[c] = w;
+  }
+  if (threadIdx.x == 0) *counter = 0;
 }
 
 // x[t] = wte[tok[t]] + wpe[t % S]
@@ -253,7 +270,8 @@ int ln_bwd_blocks(int64_t T) {
 }
 
 int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const float* gb, const void* dres,
-           void* dx, float* part, int64_t T, int D, cudaStream_t st) {
+           void* dx, float* part, int64_t T, int D, cudaStream_t st, int* counter, float* master, float* out,
+           float lr) {
   if (D % 256 || D > 256 * LN_MAXV) return set_error(PD_ERR_INVALID, "layernorm: D %% 256 == 0, D <= 2048");
   const int blocks = ln_bwd_blocks(T);
   const int64_t per = (T + blocks - 1) / blocks;
@@ -265,7 +283,7 @@ int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, 
     kern<<<blocks, LN_WARPS * 32, smem, st>>>(static_cast<const __nv_bfloat16*>(dy),
                                               static_cast<const __nv_bfloat16*>(x), mean, rstd, gb,
                                               static_cast<const __nv_bfloat16*>(dres), static_cast<__nv_bfloat16*>(dx),
-                                              part, T, D, per);
+                                              part, T, D, per, counter, master, out, lr);
     return status("ln_bwd");
   };
   switch (D / 256) {

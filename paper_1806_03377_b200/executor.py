@@ -265,6 +265,7 @@ class Executor:
                 work = max([self._layer_bytes(x, "work") for x in geo] + [0])
                 t["work"] = torch.empty(max(work, 256), device=dev, dtype=torch.uint8)
             t["err"] = torch.zeros(1, device=dev, dtype=torch.int32)
+            t["sync"] = torch.zeros(16, device=dev, dtype=torch.int32)
             # receiver-owned inbox flags (zero = nothing delivered yet); used when a producer is remote
             i32 = dict(device=dev, dtype=torch.int32)
             if wp.stage > 0:
@@ -420,6 +421,7 @@ class Executor:
                 d.red_ready, d.red_done = t["red_flags"].data_ptr(), t["red_flags"].data_ptr() + 4
             d.tmp[0], d.tmp[1] = t["tmp"][0].data_ptr(), t["tmp"][1].data_ptr()
             d.err_word = t["err"].data_ptr()
+            d.sync = t["sync"].data_ptr()
             if self.layered:
                 descs = (nat.LayerDesc * nl)(*[self._layer_desc(x, t["argmax"][l], t["cols"][l], t["save"][l],
                                                                 t["work"]) for l, x in enumerate(b.geoms)])
@@ -485,12 +487,16 @@ class Executor:
         """Per-GEMM CUDA events on the launching stage streams (resets the counters)."""
         nat.check(nat.lib().pd_rt_kernel_timing(self._rt, int(on)), "pd_rt_kernel_timing")
 
+    KERNEL_CLASSES = ("fwd", "dgrad", "wgrad_sgd", "attention", "layernorm", "loss", "update", "other")
+
     def kernel_stats(self) -> dict:
-        """{class: (launches, avg ms, algorithmic flops per launch)} for forward / dgrad / wgrad+SGD GEMMs."""
-        buf = (ctypes.c_double * 9)()
-        nat.check(nat.lib().pd_rt_kernel_stats(self._rt, buf), "pd_rt_kernel_stats")
+        """{class: launches, avg ms, algorithmic flops per launch, total ms} per kernel class
+        (GEMM passes fwd / dgrad / wgrad_sgd, then attention, layernorm, loss, update, other)."""
+        n = len(self.KERNEL_CLASSES)
+        buf = (ctypes.c_double * (3 * n))()
+        nat.check(nat.lib().pd_rt_kernel_stats(self._rt, buf, n), "pd_rt_kernel_stats")
         out = {}
-        for i, name in enumerate(("fwd", "dgrad", "wgrad_sgd")):
+        for i, name in enumerate(self.KERNEL_CLASSES):
             n, ms, fl = buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]
             if n:
                 out[name] = {"launches": int(n), "avg_ms": ms / n, "flops_per_launch": fl / n, "total_ms": ms}
