@@ -15,7 +15,7 @@ PKG_DIR = Path(__file__).resolve().parent
 REPO = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 LIB_PATH = PKG_DIR / "libpd_b200.so"
-SOURCES = ["gemm.cu", "kernels.cu", "layers.cu", "attention.cu", "transformer.cu", "runtime.cu"]
+SOURCES = ["gemm.cu", "kernels.cu", "layers.cu", "attention.cu", "attention_tc.cu", "transformer.cu", "runtime.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(REPO / "include")]
 

@@ -1,0 +1,574 @@
+// Causal flash attention on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), head_dim 64.
+//
+// Forward, one CTA per (128-query tile, head, sequence), two CTAs per SM:
+//   warp 0  TMA producer: Q tile once, then K_j / V_j tiles (128 keys x 64 dims, 128B swizzle)
+//   warp 1  MMA issuer (one elected thread) + TMEM owner:
+//             S_j = Q K_j^T       tcgen05.mma M=128 N=128 K=64   -> TMEM cols [0,128)
+//             O  += P_j V_j       tcgen05.mma M=128 N=64  K=128  -> TMEM cols [128,192)
+//   warps 2-5  softmax, one thread per query row (its TMEM lane): tcgen05.ld the S row, online
+//             max / exp2 / sum in fp32, rescale the O row in TMEM (tcgen05.ld/st) when the max
+//             moved, write P (bf16) into shared memory in the K-major SW128 layout the PV MMA
+//             reads, then signal the MMA warp.  At the end O/l is written to HBM and the row's
+//             log-sum-exp (log2 domain) is kept for the backward.
+// S_{j+1} is issued before PV_j so the next tile's scores are ready as soon as the softmax
+// warps finish writing P_j; the second CTA on the SM overlaps its MMAs with this CTA's softmax.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "epilogue.cuh"
+#include "pd_internal.h"
+#include "ptx.cuh"
+
+namespace pd {
+
+namespace {
+
+constexpr int TQ = 128;     // queries per tile (TMEM lanes)
+constexpr int TK = 128;     // keys per tile
+constexpr int HDIM = 64;    // head dim = one 128-byte swizzle row
+constexpr int FWD_THREADS = 192;
+constexpr int TILE_BYTES = 128 * 128;  // 128 rows x 64 bf16
+
+struct FwdSmem {
+  static constexpr int Q = 0;
+  static constexpr int K = Q + TILE_BYTES;
+  static constexpr int V = K + TILE_BYTES;
+  static constexpr int P = V + TILE_BYTES;          // two K-major atoms: keys 0..63, 64..127
+  static constexpr int BAR = P + 2 * TILE_BYTES;
+  static constexpr int TOTAL = BAR + 256 + 1024;    // barriers + TMEM slot + alignment slack
+};
+
+PD_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// Byte offset of (row, 16-byte chunk) of a 128B-swizzled tile (the TMA / UMMA SW128 pattern).
+PD_DEVICE uint32_t sw128(int row, int chunk) { return row * 128 + ((chunk ^ (row & 7)) << 4); }
+
+__global__ void __launch_bounds__(FWD_THREADS, 2)
+    k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ out,
+                  float* __restrict__ lse, int S, int H, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + FwdSmem::Q;
+  uint8_t* sK = smem + FwdSmem::K;
+  uint8_t* sV = smem + FwdSmem::V;
+  uint8_t* sP = smem + FwdSmem::P;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + FwdSmem::BAR);
+  uint64_t* full_q = bar + 0;
+  uint64_t* full_k = bar + 1;
+  uint64_t* full_v = bar + 2;
+  uint64_t* empty_k = bar + 3;
+  uint64_t* empty_v = bar + 4;
+  uint64_t* s_full = bar + 5;
+  uint64_t* p_ready = bar + 6;
+  uint64_t* o_done = bar + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+
+  const int n_qt = S / TQ;
+  const int qt = n_qt - 1 - (int)blockIdx.x;  // heaviest (longest causal row) tiles first
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int D = H * HDIM;
+  const int n_kt = qt + 1;
+  const int row0 = b * S;  // token row of this sequence in qkv
+  const int warp = warp_id();
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    mbar_init(full_q, 1);
+    mbar_init(full_k, 1);
+    mbar_init(full_v, 1);
+    mbar_init(empty_k, 1);
+    mbar_init(empty_v, 1);
+    mbar_init(s_full, 1);
+    mbar_init(p_ready, 4);
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+    fence_proxy_async_smem();
+  }
+  if (warp == 1) tmem_alloc<256, 1>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tO = tmem + 128;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (elect_one()) {
+      mbar_arrive_expect_tx(full_q, TILE_BYTES);
+      tma_load_2d(sQ, &tm_qkv, full_q, h * HDIM, row0 + qt * TQ);
+      for (int j = 0; j < n_kt; ++j) {
+        mbar_wait(empty_k, (j & 1) ^ 1);
+        mbar_arrive_expect_tx(full_k, TILE_BYTES);
+        tma_load_2d(sK, &tm_qkv, full_k, D + h * HDIM, row0 + j * TK);
+        mbar_wait(empty_v, (j & 1) ^ 1);
+        mbar_arrive_expect_tx(full_v, TILE_BYTES);
+        tma_load_2d(sV, &tm_qkv, full_v, 2 * D + h * HDIM, row0 + j * TK);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(TQ, TK, false, false);
+      constexpr uint32_t idesc_o = make_idesc_bf16(TQ, HDIM, false, true);
+      const uint32_t q_addr = smem_u32(sQ), k_addr = smem_u32(sK), v_addr = smem_u32(sV), p_addr = smem_u32(sP);
+      auto issue_s = [&]() {
+#pragma unroll
+        for (int k = 0; k < HDIM / 16; ++k)
+          umma_bf16(tS, make_sw128_desc(q_addr + k * 32, 16, 1024), make_sw128_desc(k_addr + k * 32, 16, 1024),
+                    idesc_s, k != 0);
+        umma_commit(s_full);
+        umma_commit(empty_k);
+      };
+      mbar_wait(full_q, 0);
+      mbar_wait(full_k, 0);
+      tc_fence_after();
+      issue_s();
+      for (int j = 0; j < n_kt; ++j) {
+        mbar_wait(p_ready, j & 1);  // S_j consumed, P_j in smem, O rescaled
+        tc_fence_after();
+        if (j + 1 < n_kt) {
+          mbar_wait(full_k, (j + 1) & 1);
+          tc_fence_after();
+          issue_s();
+        }
+        mbar_wait(full_v, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < TK / 16; ++k) {
+          // A = P (K-major over keys, 64-key atoms 16 KB apart); B = V (MN-major, +16 key rows = 2 KB)
+          const uint64_t ad = make_sw128_desc(p_addr + (k >> 2) * TILE_BYTES + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = make_sw128_desc(v_addr + k * 2048, 8192, 1024);
+          umma_bf16(tO, ad, bd, idesc_o, (j | k) != 0);
+        }
+        umma_commit(o_done);
+        umma_commit(empty_v);
+      }
+    }
+  } else {
+    // ---------------- softmax: thread = query row (TMEM lane 32*(warp%4) + lane)
+    const int quad = warp & 3;
+    const int r = 32 * quad + lane_id();
+    const int q = qt * TQ + r;  // query position in the sequence
+    const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kt; ++j) {
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      const bool diag = j == qt;
+      // pass 1: row max of this tile
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < TK / 32; ++c) {
+        float v[32];
+        tmem_ld_32x32b_x32(tS + lane_base + c * 32, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int key = j * TK + c * 32 + i;
+          const float sv = (diag && key > q) ? -INFINITY : v[i] * scale_log2;
+          mx = fmaxf(mx, sv);
+        }
+      }
+      const float m_new = fmaxf(m, mx);
+      const float alpha = m == -INFINITY ? 0.f : exp2f(m - m_new);
+      if (j > 0) mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} finished: O final for j-1, P free
+      tc_fence_after();
+      // rescale the O row when the running max moved (warp-uniform decision)
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+        for (int c = 0; c < HDIM / 32; ++c) {
+          float o[32];
+          tmem_ld_32x32b_x32(tO + lane_base + c * 32, o);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] *= alpha;
+          tmem_st_32x32b_x32(tO + lane_base + c * 32, o);
+        }
+      }
+      // pass 2: P = exp2(s - m_new) -> bf16 -> smem (K-major SW128, two 64-key atoms)
+      float rs = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < TK / 32; ++c) {
+        float v[32];
+        tmem_ld_32x32b_x32(tS + lane_base + c * 32, v);
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const int key = j * TK + c * 32 + i;
+          const float s0 = (diag && key > q) ? -INFINITY : v[i] * scale_log2;
+          const float s1 = (diag && key + 1 > q) ? -INFINITY : v[i + 1] * scale_log2;
+          const float p0 = exp2f(s0 - m_new), p1 = exp2f(s1 - m_new);
+          rs += p0 + p1;
+          pk[i / 2] = pack_bf16x2(p0, p1);
+        }
+        uint8_t* atom = sP + (c >> 1) * TILE_BYTES;
+        const int chunk0 = (c & 1) * 4;  // 32 keys = four 16-byte chunks of the 128-byte row
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          *reinterpret_cast<uint4*>(atom + sw128(r, chunk0 + u)) =
+              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+      }
+      l = l * alpha + rs;
+      m = m_new;
+      fence_proxy_async_shared();  // P (generic-proxy stores) -> visible to the tensor core
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(p_ready);
+    }
+    mbar_wait(o_done, (n_kt - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = out + ((int64_t)row0 + q) * D + h * HDIM;
+#pragma unroll
+    for (int c = 0; c < HDIM / 32; ++c) {
+      float o[32];
+      tmem_ld_32x32b_x32(tO + lane_base + c * 32, o);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] *= inv;
+      store32_bf16(orow, 0, 0, c * 32, o);
+    }
+    lse[((int64_t)b * H + h) * S + q] = m + log2f(l);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<256, 1>(tmem);
+  }
+}
+
+// ================================================================ backward
+// One CTA per (128-key tile, head, sequence), looping over the query tiles at or after the
+// diagonal.  TMEM columns: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ [384,448).
+//   MMA warp:   S^T = K Q^T, dP^T = V dO^T (M = keys, N = queries, K = 64)
+//               dV += P^T dO, dK += dS^T Q  (M = keys, N = 64, K = queries)
+//               dQ  = dS K                  (M = queries, N = 64, K = keys; A = dS^T read MN-major)
+//   warps 2-5:  thread = TMEM lane: P^T = exp2(S^T*scale - lse), dS^T = P^T (dP^T - D) -> bf16
+//               into shared memory (K-major over queries), and the previous tile's dQ rows out
+//               of TMEM into the fp32 dq_acc with 16-byte vector atomics.
+constexpr int BWD_THREADS = 192;
+struct BwdSmem {
+  static constexpr int K = 0;
+  static constexpr int V = K + TILE_BYTES;
+  static constexpr int Q = V + TILE_BYTES;            // [2] stages
+  static constexpr int DO = Q + 2 * TILE_BYTES;       // [2] stages
+  static constexpr int P = DO + 2 * TILE_BYTES;       // P^T: two K-major atoms over queries
+  static constexpr int DS = P + 2 * TILE_BYTES;       // dS^T
+  static constexpr int LD = DS + 2 * TILE_BYTES;      // lse/D: [2 parity][2][128] floats
+  static constexpr int DQ = LD + 2 * 2 * 128 * 4;     // dQ staging [128][64] fp32 for the TMA reduce-add
+  static constexpr int BAR = DQ + 128 * 64 * 4;
+  static constexpr int TOTAL = BAR + 256 + 1024;
+};
+
+PD_DEVICE void named_sync_128() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__global__ void __launch_bounds__(BWD_THREADS, 1)
+    k_attn_bwd_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                  const __grid_constant__ CUtensorMap tm_dq,
+                  const float* __restrict__ lse, const float* __restrict__ Dv, __nv_bfloat16* __restrict__ dqkv,
+                  float* __restrict__ dq_acc, int S, int H, float scale_log2, float scale) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem + BwdSmem::K;
+  uint8_t* sV = smem + BwdSmem::V;
+  uint8_t* sQ = smem + BwdSmem::Q;
+  uint8_t* sdO = smem + BwdSmem::DO;
+  uint8_t* sP = smem + BwdSmem::P;
+  uint8_t* sdS = smem + BwdSmem::DS;
+  float* sLD = reinterpret_cast<float*>(smem + BwdSmem::LD);
+  float* sDQ = reinterpret_cast<float*>(smem + BwdSmem::DQ);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BwdSmem::BAR);
+  uint64_t* full_kv = bar + 0;
+  uint64_t* full_qdo = bar + 1;   // [2]
+  uint64_t* empty_qdo = bar + 3;  // [2]
+  uint64_t* sdp_full = bar + 5;
+  uint64_t* pds_ready = bar + 6;
+  uint64_t* dq_full = bar + 7;
+  uint64_t* dq_free = bar + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+
+  const int n_t = S / TK;
+  const int kt = (int)blockIdx.x;  // key tile; tile 0 has the most query tiles and starts first
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int D = H * HDIM;
+  const int row0 = b * S;
+  const int N = n_t - kt;  // query tiles kt .. n_t-1
+  const int warp = warp_id();
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_do);
+    mbar_init(full_kv, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&full_qdo[i], 1); mbar_init(&empty_qdo[i], 1); }
+    mbar_init(sdp_full, 1);
+    mbar_init(pds_ready, 4);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_free, 4);
+    fence_barrier_init();
+    fence_proxy_async_smem();
+  }
+  if (warp == 1) tmem_alloc<512, 1>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tP = tmem + 128, tdV = tmem + 256, tdK = tmem + 320, tdQ = tmem + 384;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_arrive_expect_tx(full_kv, 2 * TILE_BYTES);
+      tma_load_2d(sK, &tm_qkv, full_kv, D + h * HDIM, row0 + kt * TK);
+      tma_load_2d(sV, &tm_qkv, full_kv, 2 * D + h * HDIM, row0 + kt * TK);
+      for (int n = 0; n < N; ++n) {
+        const int st = n & 1, qt = kt + n;
+        mbar_wait(&empty_qdo[st], ((n >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full_qdo[st], 2 * TILE_BYTES);
+        tma_load_2d(sQ + st * TILE_BYTES, &tm_qkv, &full_qdo[st], h * HDIM, row0 + qt * TQ);
+        tma_load_2d(sdO + st * TILE_BYTES, &tm_do, &full_qdo[st], h * HDIM, row0 + qt * TQ);
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc_sq = make_idesc_bf16(TK, TQ, false, false);      // S^T, dP^T
+      constexpr uint32_t idesc_kv = make_idesc_bf16(TK, HDIM, false, true);     // dV, dK
+      constexpr uint32_t idesc_q = make_idesc_bf16(TQ, HDIM, true, true);       // dQ (A = dS^T MN-major)
+      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), p_addr = smem_u32(sP), ds_addr = smem_u32(sdS);
+      mbar_wait(full_kv, 0);
+      for (int n = 0; n < N; ++n) {
+        const int st = n & 1;
+        const uint32_t q_addr = smem_u32(sQ + st * TILE_BYTES), do_addr = smem_u32(sdO + st * TILE_BYTES);
+        mbar_wait(&full_qdo[st], (n >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < HDIM / 16; ++k) {
+          umma_bf16(tS, make_sw128_desc(k_addr + k * 32, 16, 1024), make_sw128_desc(q_addr + k * 32, 16, 1024),
+                    idesc_sq, k != 0);
+          umma_bf16(tP, make_sw128_desc(v_addr + k * 32, 16, 1024), make_sw128_desc(do_addr + k * 32, 16, 1024),
+                    idesc_sq, k != 0);
+        }
+        umma_commit(sdp_full);
+        mbar_wait(pds_ready, n & 1);
+        if (n > 0) mbar_wait(dq_free, (n - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < TQ / 16; ++k) {
+          const uint32_t a_off = (k >> 2) * TILE_BYTES + (k & 3) * 32;  // K-major over queries
+          umma_bf16(tdV, make_sw128_desc(p_addr + a_off, 16, 1024), make_sw128_desc(do_addr + k * 2048, 8192, 1024),
+                    idesc_kv, (n | k) != 0);
+          umma_bf16(tdK, make_sw128_desc(ds_addr + a_off, 16, 1024), make_sw128_desc(q_addr + k * 2048, 8192, 1024),
+                    idesc_kv, (n | k) != 0);
+        }
+#pragma unroll
+        for (int k = 0; k < TK / 16; ++k)  // K = keys: dS^T rows (+2 KB per 16), query atoms 16 KB apart
+          umma_bf16(tdQ, make_sw128_desc(ds_addr + k * 2048, TILE_BYTES, 1024),
+                    make_sw128_desc(k_addr + k * 2048, 8192, 1024), idesc_q, k != 0);
+        umma_commit(dq_full);
+        umma_commit(&empty_qdo[st]);
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    const int r = 32 * quad + lane_id();      // TMEM lane: key row (S^T, dP^T, dK, dV) / query row (dQ)
+    const int key = kt * TK + r;
+    const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
+    const int t = threadIdx.x - 64;           // 0..127 within the compute warps
+    // dQ rows of a query tile: TMEM -> staging smem (row r, 16-byte chunks in a per-thread rotated
+    // order against bank conflicts) -> one TMA reduce-add of the 128 x 64 fp32 box into dq_acc.
+    auto flush_dq = [&](int qt) {
+      uint32_t v0[32], v1[32];
+      tmem_ld_32x32b_x32_nowait(tdQ + lane_base, v0);
+      tmem_ld_32x32b_x32_nowait(tdQ + lane_base + 32, v1);
+      tmem_wait_ld();
+      if (t == 0) bulk_wait_read0();  // the previous reduce has finished reading the staging
+      named_sync_128();
+      // two [128][32] fp32 halves, 128B-swizzled (chunk c of row r at c ^ (r & 7)): conflict-free
+      uint8_t* st0 = reinterpret_cast<uint8_t*>(sDQ);
+      uint8_t* st1 = st0 + 128 * 128;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        *reinterpret_cast<uint4*>(st0 + sw128(r, c)) = make_uint4(v0[4 * c], v0[4 * c + 1], v0[4 * c + 2], v0[4 * c + 3]);
+        *reinterpret_cast<uint4*>(st1 + sw128(r, c)) = make_uint4(v1[4 * c], v1[4 * c + 1], v1[4 * c + 2], v1[4 * c + 3]);
+      }
+      fence_proxy_async_shared();
+      named_sync_128();
+      if (t == 0) {
+        tma_reduce_add_2d(&tm_dq, st0, h * HDIM, row0 + qt * TQ);
+        tma_reduce_add_2d(&tm_dq, st1, h * HDIM + 32, row0 + qt * TQ);
+        bulk_commit();
+      }
+    };
+    for (int n = 0; n < N; ++n) {
+      const int qt = kt + n;
+      const int par = n & 1;
+      float* sL = sLD + par * 256;
+      float* sDd = sL + 128;
+      sL[t] = lse[((int64_t)b * H + h) * S + qt * TQ + t];
+      sDd[t] = Dv[((int64_t)b * H + h) * S + qt * TQ + t];
+      mbar_wait(sdp_full, n & 1);
+      tc_fence_after();
+      if (n > 0) {  // MMAs of n-1 are done: their dQ is ready and P^T / dS^T smem are free
+        mbar_wait(dq_full, (n - 1) & 1);
+        tc_fence_after();
+        flush_dq(qt - 1);
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(dq_free);
+      }
+      named_sync_128();  // lse / D of this query tile are in shared memory
+      const bool diag = n == 0;
+#pragma unroll 1
+      for (int c = 0; c < TQ / 32; ++c) {
+        uint32_t svr[32], dpr[32];
+        tmem_ld_32x32b_x32_nowait(tS + lane_base + c * 32, svr);
+        tmem_ld_32x32b_x32_nowait(tP + lane_base + c * 32, dpr);
+        tmem_wait_ld();
+        const float* sv = reinterpret_cast<const float*>(svr);
+        const float* dp = reinterpret_cast<const float*>(dpr);
+        uint32_t pk[16], dk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float pp[2], dd[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int ql = c * 32 + i + e;
+            const int q = qt * TQ + ql;
+            float p = exp2f(sv[i + e] * scale_log2 - sL[ql]);
+            if (diag && q < key) p = 0.f;
+            pp[e] = p;
+            dd[e] = p * (dp[i + e] - sDd[ql]);
+          }
+          pk[i / 2] = pack_bf16x2(pp[0], pp[1]);
+          dk[i / 2] = pack_bf16x2(dd[0], dd[1]);
+        }
+        const int atom = (c >> 1) * TILE_BYTES;
+        const int chunk0 = (c & 1) * 4;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          *reinterpret_cast<uint4*>(sP + atom + sw128(r, chunk0 + u)) =
+              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          *reinterpret_cast<uint4*>(sdS + atom + sw128(r, chunk0 + u)) =
+              make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+        }
+      }
+      fence_proxy_async_shared();
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(pds_ready);
+    }
+    mbar_wait(dq_full, (N - 1) & 1);
+    tc_fence_after();
+    flush_dq(kt + N - 1);
+    if (t == 0) bulk_wait_all0();  // the last reduce-add has completed before the CTA exits
+    // dK (scaled) and dV rows of this thread's key into the k / v slices of dqkv
+    __nv_bfloat16* row = dqkv + ((int64_t)row0 + key) * 3 * D;
+#pragma unroll
+    for (int c = 0; c < HDIM / 32; ++c) {
+      float v[32];
+      tmem_ld_32x32b_x32(tdK + lane_base + c * 32, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] *= scale;
+      store32_bf16(row + D + h * HDIM, 0, 0, c * 32, v);
+      tmem_ld_32x32b_x32(tdV + lane_base + c * 32, v);
+      store32_bf16(row + 2 * D + h * HDIM, 0, 0, c * 32, v);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512, 1>(tmem);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D map over a row-major bf16 [rows, cols] matrix, 64 x 128 boxes, 128B swizzle.
+int map_rows(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols) {
+  auto fn = encode_tiled();
+  if (!fn) return set_error(PD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : set_error(PD_ERR_CUDA, "attention tensor map (%d)", (int)r);
+}
+
+}  // namespace
+
+int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int S, int H, cudaStream_t st) {
+  if (S % TQ || B < 1 || H < 1) return set_error(PD_ERR_INVALID, "attention: seq %% 128 == 0 required");
+  CUtensorMap tm;
+  const int rc = map_rows(&tm, qkv, (int64_t)B * S, 3ll * H * HDIM);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem::TOTAL) != cudaSuccess)
+      return set_error(PD_ERR_CUDA, "attention fwd: shared memory attribute");
+    attr = true;
+  }
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)HDIM);
+  k_attn_fwd_tc<<<dim3(S / TQ, H, B), FWD_THREADS, FwdSmem::TOTAL, st>>>(tm, static_cast<__nv_bfloat16*>(out), lse,
+                                                                         S, H, scale_log2);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "attention fwd: %s", cudaGetErrorString(e));
+}
+
+int attn_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* Dv, float* dq_acc, void* dqkv, int B,
+                int S, int H, cudaStream_t st) {
+  if (S % TQ || B < 1 || H < 1) return set_error(PD_ERR_INVALID, "attention: seq %% 128 == 0 required");
+  CUtensorMap tq, tdo, tdq;
+  int rc = map_rows(&tq, qkv, (int64_t)B * S, 3ll * H * HDIM);
+  if (rc) return rc;
+  rc = map_rows(&tdo, dout, (int64_t)B * S, (int64_t)H * HDIM);
+  if (rc) return rc;
+  {
+    auto fn = encode_tiled();
+    cuuint64_t dims[2] = {(cuuint64_t)H * HDIM, (cuuint64_t)B * S};
+    cuuint64_t strides[1] = {(cuuint64_t)H * HDIM * 4};
+    cuuint32_t box[2] = {32, 128};
+    cuuint32_t es[2] = {1, 1};
+    if (fn(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq_acc, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+      return set_error(PD_ERR_CUDA, "attention bwd: dQ tensor map");
+  }
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_attn_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem::TOTAL) != cudaSuccess)
+      return set_error(PD_ERR_CUDA, "attention bwd: shared memory attribute");
+    attr = true;
+  }
+  const float scale = 1.0f / sqrtf((float)HDIM);
+  k_attn_bwd_tc<<<dim3(S / TK, H, B), BWD_THREADS, BwdSmem::TOTAL, st>>>(
+      tq, tdo, tdq, lse, Dv, static_cast<__nv_bfloat16*>(dqkv), dq_acc, S, H, scale * 1.4426950408889634f, scale);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "attention bwd: %s", cudaGetErrorString(e));
+}
+
+}  // namespace pd

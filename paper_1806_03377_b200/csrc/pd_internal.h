@@ -37,6 +37,9 @@ int softmax_ce(const float* logits, int64_t ldz, const int* labels, int B, int V
                cudaStream_t st);
 
 int attn_fwd(const void* qkv, void* out, float* lse, int B, int S, int H, cudaStream_t st);
+int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int S, int H, cudaStream_t st);
+int attn_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* Dv, float* dq_acc, void* dqkv, int B,
+                int S, int H, cudaStream_t st);
 int attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, float* Dv, float* dq_acc,
              void* dqkv, int B, int S, int H, cudaStream_t st);
 int ln_fwd(const void* x, const float* gb, void* y, float* mean, float* rstd, int64_t T, int D, cudaStream_t st);

@@ -813,7 +813,7 @@ int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc) {
       const bool tkind = y.kind == PD_LAYER_EMBED || y.kind == PD_LAYER_BLOCK || y.kind == PD_LAYER_HEAD;
       if (tkind) {
         if (d.rep > 1) return set_error(PD_ERR_INVALID, "worker %d: transformer stages are not replicated", d.worker);
-        if (y.h < 64 || y.h % 64) return set_error(PD_ERR_INVALID, "worker %d layer %d: seq %% 64", d.worker, l);
+        if (y.h < 128 || y.h % 128) return set_error(PD_ERR_INVALID, "worker %d layer %d: seq %% 128", d.worker, l);
         if (y.kind == PD_LAYER_BLOCK && (y.w * 64 != y.c_in || y.ffn < 1))
           return set_error(PD_ERR_INVALID, "worker %d layer %d: d = 64 * heads required", d.worker, l);
         if (y.kind == PD_LAYER_HEAD && (y.vocab < 1 || y.vocab > y.c_out || !d.is_last || !d.logits))

@@ -274,8 +274,8 @@ class GPTSpec:
             raise ValidationError("head dim must be 64 (d == 64 * heads)")
         if self.d % 256 or self.d > 2048:
             raise ValidationError("d must be a multiple of 256 and <= 2048 (LayerNorm kernel)")
-        if self.seq % 64:
-            raise ValidationError("seq must be a multiple of 64 (attention tiles)")
+        if self.seq % 128:
+            raise ValidationError("seq must be a multiple of 128 (attention tiles)")
         if self.ffn % 8:
             raise ValidationError("ffn must be a multiple of 8")
 

@@ -32,7 +32,7 @@ def _ref_attn(qkv, B, S, H):
     return F.scaled_dot_product_attention(q, k, v, is_causal=True)
 
 
-@pytest.mark.parametrize("B,S,H", [(1, 64, 1), (2, 128, 2), (2, 256, 4), (1, 1024, 16)])
+@pytest.mark.parametrize("B,S,H", [(1, 128, 1), (2, 128, 2), (2, 384, 4), (1, 1024, 16)])
 def test_attention_fwd_bwd(B, S, H):
     d = 64 * H
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -160,7 +160,7 @@ def test_gelu_resid_epilogues():
 
 
 def tiny_gpt(**kw):
-    base = dict(vocab=250, d=256, heads=4, layers=2, seq=64, batch=2, lr=2e-3, n_blocks=3, seed=0)
+    base = dict(vocab=250, d=256, heads=4, layers=2, seq=128, batch=2, lr=2e-3, n_blocks=3, seed=0)
     base.update(kw)
     return pd.GPTSpec(**base)
 
