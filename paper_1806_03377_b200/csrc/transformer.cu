@@ -213,35 +213,59 @@ __global__ void __launch_bounds__(256) k_embed_bwd(const int* __restrict__ tok, 
 }
 
 // Softmax cross-entropy over the first V of Vp fp32 logit columns; columns >= V get dz = 0.
+// One block per row, two passes over the row: an online (max, sum-exp) pass with 16-byte loads,
+// then the gradient pass (softmax - onehot) / rows written as bf16.
+__device__ __forceinline__ void online_merge(float& m, float& s, float m2, float s2) {
+  const float mx = fmaxf(m, m2);
+  s = (m == -INFINITY ? 0.f : s * __expf(m - mx)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mx));
+  m = mx;
+}
+
 __global__ void __launch_bounds__(512) k_softmax_ce_v(const float* __restrict__ z, int64_t ldz,
                                                       const int* __restrict__ labels, int V, int Vp, float inv_n,
                                                       __nv_bfloat16* __restrict__ dz, int64_t ldd,
                                                       float* __restrict__ loss) {
-  __shared__ float sh[32];
+  __shared__ float shm[32], shs[32];
   const int64_t r = blockIdx.x;
   const float* row = z + r * ldz;
   const int nw = blockDim.x >> 5;
-  float m = -INFINITY;
-  for (int j = threadIdx.x; j < V; j += blockDim.x) m = fmaxf(m, row[j]);
-  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+  const int V4 = V / 4;
+  float m = -INFINITY, s = 0.f;
+  for (int j = threadIdx.x; j < V4; j += blockDim.x) {
+    const float4 x = reinterpret_cast<const float4*>(row)[j];
+    const float mx = fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w));
+    if (mx > m) {
+      s = (m == -INFINITY ? 0.f : s * __expf(m - mx));
+      m = mx;
+    }
+    s += __expf(x.x - m) + __expf(x.y - m) + __expf(x.z - m) + __expf(x.w - m);
+  }
+  for (int j = V4 * 4 + threadIdx.x; j < V; j += blockDim.x) online_merge(m, s, row[j], 1.f);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) online_merge(m, s, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, s, o));
+  if ((threadIdx.x & 31) == 0) {
+    shm[threadIdx.x >> 5] = m;
+    shs[threadIdx.x >> 5] = s;
+  }
   __syncthreads();
-  m = sh[0];
-  for (int w = 1; w < nw; ++w) m = fmaxf(m, sh[w]);
-  __syncthreads();
-  float s = 0.f;
-  for (int j = threadIdx.x; j < V; j += blockDim.x) s += __expf(row[j] - m);
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
-  __syncthreads();
-  s = 0.f;
-  for (int w = 0; w < nw; ++w) s += sh[w];
+  m = shm[0];
+  s = shs[0];
+  for (int w = 1; w < nw; ++w) online_merge(m, s, shm[w], shs[w]);
   const int lab = labels[r];
   const float inv_s = 1.f / s;
   __nv_bfloat16* drow = dz + r * ldd;
-  for (int j = threadIdx.x; j < Vp; j += blockDim.x) {
-    const float p = j < V ? __expf(row[j] - m) * inv_s : 0.f;
-    drow[j] = __float2bfloat16_rn((p - (j == lab ? 1.f : 0.f)) * inv_n);
+  const int Vp4 = Vp / 4;
+  for (int j = threadIdx.x; j < Vp4; j += blockDim.x) {
+    const float4 x = reinterpret_cast<const float4*>(row)[j];
+    const float xv[4] = {x.x, x.y, x.z, x.w};
+    float g[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int c = 4 * j + e;
+      const float p = c < V ? __expf(xv[e] - m) * inv_s : 0.f;
+      g[e] = (p - (c == lab ? 1.f : 0.f)) * inv_n;
+    }
+    *reinterpret_cast<uint2*>(drow + 4 * j) = make_uint2(pack_bf16x2(g[0], g[1]), pack_bf16x2(g[2], g[3]));
   }
   if (threadIdx.x == 0) atomicAdd(loss, inv_n * (m + __logf(s) - row[lab]));
 }
@@ -310,7 +334,8 @@ int embed_bwd(const int* tok, const void* dx, float* gte, float* gpe, int64_t T,
 
 int softmax_ce_v(const float* logits, int64_t ldz, const int* labels, int64_t rows, int V, int Vp, void* dz,
                  int64_t ldd, float* loss, cudaStream_t st) {
-  if (rows < 1 || V < 1 || Vp < V) return set_error(PD_ERR_INVALID, "softmax_ce: bad shape");
+  if (rows < 1 || V < 1 || Vp < V || Vp % 4 || ldz % 4 || ldd % 4)
+    return set_error(PD_ERR_INVALID, "softmax_ce: bad shape (Vp and row pitches must be multiples of 4)");
   k_softmax_ce_v<<<(unsigned)rows, 512, 0, st>>>(logits, ldz, labels, V, Vp, 1.f / (float)rows,
                                                  static_cast<__nv_bfloat16*>(dz), ldd, loss);
   return status("softmax_ce_v");
