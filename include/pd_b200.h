@@ -308,6 +308,9 @@ int pd_rt_records(pd_runtime* rt, pd_record* out, int cap, int* n_out);
 /* serial=1: every hosted stage issues on one stream in program order (single-GPU mode;
  * the per-item dependencies are then satisfied by stream order). */
 int pd_rt_set_serial(pd_runtime* rt, int on);
+/* graph=1: single-process programs are captured into a CUDA graph on the next run and
+ * replayed afterwards (runs with tracing, kernel timing or cross-process flags launch directly). */
+int pd_rt_set_graph(pd_runtime* rt, int on);
 /* Per-kernel CUDA-event timing on the launching stage stream (resets the counters).
  * stats: n_classes (<= 8) classes x {launches, total ms, algorithmic flops}; classes are
  * 0 forward GEMM, 1 dgrad GEMM, 2 wgrad(+SGD) GEMM, 3 attention, 4 LayerNorm, 5 loss,

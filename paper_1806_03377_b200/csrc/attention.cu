@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "pd_internal.h"
+#include "ptx.cuh"
 
 namespace pd {
 
@@ -25,6 +26,7 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 __global__ void __launch_bounds__(256) k_attn_bwd_pre(const __nv_bfloat16* __restrict__ o,
                                                       const __nv_bfloat16* __restrict__ dout, float* __restrict__ Dv,
                                                       float* __restrict__ dq_acc, int Bsz, int S, int H) {
+  griddep_wait();
   const int D = H * HD;
   const int64_t rows = (int64_t)Bsz * S * H;  // one (token, head) per 8 threads
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -57,6 +59,7 @@ __global__ void __launch_bounds__(256) k_attn_bwd_pre(const __nv_bfloat16* __res
 
 __global__ void __launch_bounds__(256) k_attn_dq_cast(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv,
                                                       int64_t T, int D, float scale) {
+  griddep_wait();
   const int64_t n4 = T * D / 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 v = reinterpret_cast<const float4*>(dq_acc)[i];
@@ -85,7 +88,7 @@ int attn_bwd(const void* qkv, const void* out, const void* dout, const float* ls
   if (S % 128 || B < 1 || H < 1) return set_error(PD_ERR_INVALID, "attention: S %% 128 == 0 required");
   const float scale = 1.0f / sqrtf((float)HD);
   const int64_t rows = (int64_t)B * S * H;
-  k_attn_bwd_pre<<<(unsigned)((rows * 8 + 255) / 256), 256, 0, st>>>(
+  launch_pdl(k_attn_bwd_pre, dim3((unsigned)((rows * 8 + 255) / 256)), dim3(256), 0, st, 
       static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), Dv, dq_acc, B, S, H);
   int rc = status("attn_bwd_pre");
   if (rc) return rc;
@@ -94,7 +97,7 @@ int attn_bwd(const void* qkv, const void* out, const void* dout, const float* ls
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  k_attn_dq_cast<<<sms * 8, 256, 0, st>>>(dq_acc, static_cast<__nv_bfloat16*>(dqkv), (int64_t)B * S, H * HD, scale);
+  launch_pdl(k_attn_dq_cast, dim3(sms * 8), dim3(256), 0, st, dq_acc, static_cast<__nv_bfloat16*>(dqkv), (int64_t)B * S, H * HD, scale);
   return status("attn_dq_cast");
 }
 

@@ -60,6 +60,7 @@ PD_DEVICE uint32_t sw128(int row, int chunk) { return row * 128 + ((chunk ^ (row
 __global__ void __launch_bounds__(FWD_THREADS, 2)
     k_attn_fwd_tc(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ out,
                   float* __restrict__ lse, int S, int H, float scale_log2) {
+  griddep_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem + FwdSmem::Q;
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                   const __grid_constant__ CUtensorMap tm_dq,
                   const float* __restrict__ lse, const float* __restrict__ Dv, __nv_bfloat16* __restrict__ dqkv,
                   float* __restrict__ dq_acc, int S, int H, float scale_log2, float scale) {
+  griddep_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem + BwdSmem::K;
@@ -533,7 +535,7 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int S, int H, cud
     attr = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)HDIM);
-  k_attn_fwd_tc<<<dim3(S / TQ, H, B), FWD_THREADS, FwdSmem::TOTAL, st>>>(tm, static_cast<__nv_bfloat16*>(out), lse,
+  launch_pdl(k_attn_fwd_tc, dim3(S / TQ, H, B), dim3(FWD_THREADS), FwdSmem::TOTAL, st, tm, static_cast<__nv_bfloat16*>(out), lse,
                                                                          S, H, scale_log2);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "attention fwd: %s", cudaGetErrorString(e));
@@ -565,7 +567,7 @@ int attn_bwd_tc(const void* qkv, const void* dout, const float* lse, const float
     attr = true;
   }
   const float scale = 1.0f / sqrtf((float)HDIM);
-  k_attn_bwd_tc<<<dim3(S / TK, H, B), BWD_THREADS, BwdSmem::TOTAL, st>>>(
+  launch_pdl(k_attn_bwd_tc, dim3(S / TK, H, B), dim3(BWD_THREADS), BwdSmem::TOTAL, st, 
       tq, tdo, tdq, lse, Dv, static_cast<__nv_bfloat16*>(dqkv), dq_acc, S, H, scale * 1.4426950408889634f, scale);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "attention bwd: %s", cudaGetErrorString(e));

@@ -134,6 +134,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();    // operands / epilogue inputs may come from the previous kernel on the stream
+  griddep_launch();  // the next kernel may start its prologue as our CTAs retire
 
   if (warp == 0) {
     // ---------------- TMA producer (every CTA loads its own halves)
@@ -646,13 +648,15 @@ static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tw, M, N, K, ep, cv);
   if (e != cudaSuccess) return set_error(PD_ERR_CUDA, "tcgen05 gemm launch: %s", cudaGetErrorString(e));
   return 0;

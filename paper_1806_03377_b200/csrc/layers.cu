@@ -40,6 +40,7 @@ int grid_for(int64_t work, int threads) {
 // maximum wins; arg[n,p,q,c] = dh*2+dw.  8 channels (16 bytes) per thread.
 __global__ void __launch_bounds__(256) k_maxpool_fwd(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
                                                      uint8_t* __restrict__ arg, int n, int H, int W, int C) {
+  griddep_wait();
   const int Ho = H / 2, Wo = W / 2, C8 = C / 8;
   const int64_t total = (int64_t)n * Ho * Wo * C8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(256) k_maxpool_fwd(const __nv_bfloat16* __rest
 // dx[window position k] = (arg == k) ? dy : 0  (every input element written exactly once)
 __global__ void __launch_bounds__(256) k_maxpool_bwd(const __nv_bfloat16* __restrict__ dy, const uint8_t* __restrict__ arg,
                                                      __nv_bfloat16* __restrict__ dx, int n, int H, int W, int C) {
+  griddep_wait();
   const int Ho = H / 2, Wo = W / 2, C8 = C / 8;
   const int64_t total = (int64_t)n * Ho * Wo * C8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(256) k_maxpool_bwd(const __nv_bfloat16* __rest
 int maxpool_fwd(const void* x, void* y, uint8_t* arg, int n, int H, int W, int C, cudaStream_t st) {
   if (C % 8 || H % 2 || W % 2) return set_error(PD_ERR_INVALID, "maxpool: C %% 8 and even H, W required");
   const int64_t total = (int64_t)n * (H / 2) * (W / 2) * (C / 8);
-  k_maxpool_fwd<<<grid_for(total, 256), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x),
+  launch_pdl(k_maxpool_fwd, dim3(grid_for(total, 256)), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(x),
                                                       static_cast<__nv_bfloat16*>(y), arg, n, H, W, C);
   return launch_status("maxpool_fwd");
 }
@@ -112,7 +114,7 @@ int maxpool_fwd(const void* x, void* y, uint8_t* arg, int n, int H, int W, int C
 int maxpool_bwd(const void* dy, const uint8_t* arg, void* dx, int n, int H, int W, int C, cudaStream_t st) {
   if (C % 8 || H % 2 || W % 2) return set_error(PD_ERR_INVALID, "maxpool: C %% 8 and even H, W required");
   const int64_t total = (int64_t)n * (H / 2) * (W / 2) * (C / 8);
-  k_maxpool_bwd<<<grid_for(total, 256), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(dy), arg,
+  launch_pdl(k_maxpool_bwd, dim3(grid_for(total, 256)), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(dy), arg,
                                                       static_cast<__nv_bfloat16*>(dx), n, H, W, C);
   return launch_status("maxpool_bwd");
 }
@@ -125,6 +127,7 @@ int maxpool_bwd(const void* dy, const uint8_t* arg, void* dx, int n, int H, int 
 // with eight 16-byte stores (the output stream is what bounds this kernel).
 __global__ void __launch_bounds__(256) k_im2col3(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ cols,
                                                  int n, int H, int W, int C, int kpad) {
+  griddep_wait();
   const int64_t pixels = (int64_t)n * H * W;
   for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < pixels;
        pix += (int64_t)gridDim.x * blockDim.x) {
@@ -152,7 +155,7 @@ __global__ void __launch_bounds__(256) k_im2col3(const __nv_bfloat16* __restrict
 int im2col3(const void* x, void* cols, int n, int H, int W, int C, int kpad, cudaStream_t st) {
   if (9 * C > kpad || kpad != 64) return set_error(PD_ERR_INVALID, "im2col: kpad must be 64 and >= 9*C (%d)", kpad);
   const int64_t total = (int64_t)n * H * W;
-  k_im2col3<<<grid_for(total, 256), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x),
+  launch_pdl(k_im2col3, dim3(grid_for(total, 256)), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(x),
                                                   static_cast<__nv_bfloat16*>(cols), n, H, W, C, kpad);
   return launch_status("im2col3");
 }
@@ -183,6 +186,7 @@ __device__ __forceinline__ void finish_update(const float* part, int S, int C, f
 __global__ void __launch_bounds__(CS_THREADS) k_colsum_part(const __nv_bfloat16* __restrict__ x, int64_t rows, int C,
                                                             int64_t rows_per, float* __restrict__ part, int* counter,
                                                             float* grad, float* master, float* out, float lr) {
+  griddep_wait();
   extern __shared__ float red[];  // narrow rows: [CS_THREADS / (C/8)][C]
   __shared__ bool last;
   const int C8 = C / 8;
@@ -250,6 +254,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_reduce_sgd(const float* __restrict__ part, int S, int64_t stride, int64_t n,
                                                     float* __restrict__ grad, float* __restrict__ master,
                                                     T* __restrict__ out, float lr) {
+  griddep_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float g = 0.f;
     for (int s = 0; s < S; ++s) g += part[s * stride + i];
@@ -269,9 +274,9 @@ int reduce_sgd(int out_dtype, const float* part, int S, int64_t stride, int64_t 
   if (!grad && (!master || !out)) return set_error(PD_ERR_INVALID, "reduce_sgd: need grad or master+out");
   const int g = grid_for(n, 256);
   if (out_dtype == PD_BF16)
-    k_reduce_sgd<__nv_bfloat16><<<g, 256, 0, st>>>(part, S, stride, n, grad, master, static_cast<__nv_bfloat16*>(out), lr);
+    launch_pdl(k_reduce_sgd<__nv_bfloat16>, dim3(g), dim3(256), 0, st, part, S, stride, n, grad, master, static_cast<__nv_bfloat16*>(out), lr);
   else
-    k_reduce_sgd<float><<<g, 256, 0, st>>>(part, S, stride, n, grad, master, static_cast<float*>(out), lr);
+    launch_pdl(k_reduce_sgd<float>, dim3(g), dim3(256), 0, st, part, S, stride, n, grad, master, static_cast<float*>(out), lr);
   return launch_status("reduce_sgd");
 }
 
@@ -292,7 +297,7 @@ int bias_grad_tall(const void* dz, int64_t rows, int C, float* part, float* grad
   const int64_t per = (rows + blocks - 1) / blocks;
   const int lanes = CS_THREADS / (C / 8);
   const size_t smem = C / 8 > CS_THREADS / 2 ? 0 : (size_t)(lanes > 0 ? lanes : 1) * C * sizeof(float);
-  k_colsum_part<<<blocks, CS_THREADS, smem, st>>>(static_cast<const __nv_bfloat16*>(dz), rows, C, per, part, counter,
+  launch_pdl(k_colsum_part, dim3(blocks), dim3(CS_THREADS), smem, st, static_cast<const __nv_bfloat16*>(dz), rows, C, per, part, counter,
                                                   grad, master, out, lr);
   int rc = launch_status("colsum_part");
   if (rc || counter) return rc;

@@ -63,6 +63,24 @@ int cast_f32(int dtype, const float* src, void* out, int64_t n, cudaStream_t st)
 int flag_signal(int* flag, int value, cudaStream_t st);
 int flag_wait(const int* flag, int value, int* err_word, cudaStream_t st);
 
+// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while its
+// stream predecessor drains; it must call griddep_wait() (ptx.cuh) before reading earlier results.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 inline EpiArgs to_epi(const pd_epilogue& e) {
   EpiArgs a{};
   a.out = e.out; a.ldo = e.ldo; a.bias = e.bias; a.relu = e.relu; a.mask = e.mask; a.ldm = e.ldm;

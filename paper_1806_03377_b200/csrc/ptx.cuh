@@ -125,6 +125,15 @@ PD_DEVICE void bulk_wait_all0() { asm volatile("cp.async.bulk.wait_group 0;" :::
 // Generic-proxy shared-memory writes -> visible to the async proxy (TMA store reads).
 PD_DEVICE void fence_proxy_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// A kernel launched with cudaLaunchAttributeProgrammaticStreamSerialization may start (and run
+// its prologue: barrier init, TMEM alloc, descriptor prefetch) while its stream predecessor is
+// draining; griddep_wait() blocks until the predecessor has completed and its writes are visible,
+// so it must precede every read of data the predecessor produced.  griddep_launch() lets this
+// kernel's own successor start early.
+PD_DEVICE void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+PD_DEVICE void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- clusters (CTA pairs)
 PD_DEVICE uint32_t cluster_ctarank() {
   uint32_t r;

@@ -129,6 +129,13 @@ struct pd_runtime {
   // kernel accounting: launches of our kernels, and optional per-GEMM event timing by class
   int64_t launches = 0;
   bool serial = false;             // all hosted workers on one stream (single-GPU timing mode)
+  // CUDA graph of one whole run (single-process programs): captured on the first eligible run,
+  // replayed afterwards so the host enqueues one graph instead of thousands of kernels.
+  bool graph_mode = false;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaStream_t graph_stream = nullptr;
+  int64_t graph_launches = 0;
   cudaStream_t shared = nullptr;
   // end-of-run drain: (worker, peer ack flag, final occupant) of every outbox slot in another
   // process, so the next run cannot overwrite a slot the peer still reads
@@ -139,6 +146,13 @@ struct pd_runtime {
   std::vector<KT> kt;
   size_t kt_used = 0;
 };
+
+static void drop_graph(pd_runtime* rt) {
+  if (rt->graph_exec) cudaGraphExecDestroy(rt->graph_exec);
+  if (rt->graph) cudaGraphDestroy(rt->graph);
+  rt->graph_exec = nullptr;
+  rt->graph = nullptr;
+}
 
 namespace {
 
@@ -911,6 +925,7 @@ int pd_rt_load_program(pd_runtime* rt, const int32_t* items, int n_items) {
         if (!rt->views.count(S.d.first_worker + r))
           return set_error(PD_ERR_INVALID, "item %d: no view of replica worker %d", i, S.d.first_worker + r);
   }
+  drop_graph(rt);
   rt->items.assign(items, items + (size_t)n_items * PD_ITEM_WIDTH);
   // drain list: final occupant of every remote outbox slot
   rt->drain.clear();
@@ -939,10 +954,50 @@ int pd_rt_load_program(pd_runtime* rt, const int32_t* items, int n_items) {
   return 0;
 }
 
+static int run_body(pd_runtime* rt, cudaStream_t main, int trace);
+
+// Graph replay is valid when the run has no cross-process flags (whose values carry the run
+// epoch), no tracing and no per-kernel timing: then every run enqueues exactly the same work.
+static bool graph_eligible(pd_runtime* rt, int trace) {
+  if (!rt->graph_mode || trace || rt->ktiming || !rt->drain.empty()) return false;
+  for (const auto& kv : rt->stages)
+    if (kv.second.d.remote_prev || kv.second.d.remote_next) return false;
+  for (const auto& kv : rt->views)
+    if (kv.second.v.remote) return false;
+  return true;
+}
+
 int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
   if (!rt) return set_error(PD_ERR_INVALID, "pd_rt_run: null runtime");
   cudaStream_t main = static_cast<cudaStream_t>(stream);
   PD_CHECK(cudaSetDevice(rt->device));
+  if (!graph_eligible(rt, trace)) return run_body(rt, main, trace);
+  if (!rt->graph_exec) {
+    // capture on a private stream (the caller's may be the legacy default stream, which cannot
+    // be captured); the instantiated graph is then launched into the caller's stream
+    if (!rt->graph_stream) PD_CHECK(cudaStreamCreateWithFlags(&rt->graph_stream, cudaStreamNonBlocking));
+    const int64_t before = rt->launches;
+    PD_CHECK(cudaStreamBeginCapture(rt->graph_stream, cudaStreamCaptureModeRelaxed));
+    const int rc = run_body(rt, rt->graph_stream, 0);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(rt->graph_stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return set_error(PD_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    rt->graph = g;
+    PD_CHECK(cudaGraphInstantiate(&rt->graph_exec, g, 0));
+    rt->graph_launches = rt->launches - before;
+    rt->launches = before;
+  }
+  PD_CHECK(cudaGraphLaunch(rt->graph_exec, main));
+  rt->launches += rt->graph_launches;
+  rt->traced = false;
+  return 0;
+}
+
+static int run_body(pd_runtime* rt, cudaStream_t main, int trace) {
   rt->epoch += 1;
   rt->traced = trace != 0;
   PD_CHECK(cudaEventRecord(rt->ev0, main));
@@ -1026,9 +1081,17 @@ int pd_rt_records(pd_runtime* rt, pd_record* out, int cap, int* n_out) {
   return 0;
 }
 
+int pd_rt_set_graph(pd_runtime* rt, int on) {
+  if (!rt) return set_error(PD_ERR_INVALID, "pd_rt_set_graph: null runtime");
+  rt->graph_mode = on != 0;
+  if (!on) drop_graph(rt);
+  return 0;
+}
+
 int pd_rt_set_serial(pd_runtime* rt, int on) {
   if (!rt) return set_error(PD_ERR_INVALID, "pd_rt_set_serial: null runtime");
   PD_CHECK(cudaSetDevice(rt->device));
+  if ((on != 0) != rt->serial) drop_graph(rt);
   if (on && !rt->shared) PD_CHECK(cudaStreamCreateWithFlags(&rt->shared, cudaStreamNonBlocking));
   rt->serial = on != 0;
   return 0;
@@ -1067,6 +1130,8 @@ int pd_rt_launch_count(pd_runtime* rt, int64_t* out) {
 int pd_rt_destroy(pd_runtime* rt) {
   if (!rt) return 0;
   cudaSetDevice(rt->device);
+  drop_graph(rt);
+  if (rt->graph_stream) cudaStreamDestroy(rt->graph_stream);
   for (auto& kv : rt->stages) {
     cudaStreamSynchronize(kv.second.stream);
     cudaStreamDestroy(kv.second.stream);

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include "pd_internal.h"
+#include "ptx.cuh"
 
 namespace pd {
 
@@ -46,6 +47,7 @@ template <int NV>
 __global__ void __launch_bounds__(LN_WARPS * 32) k_ln_fwd(const __nv_bfloat16* __restrict__ x, const float* __restrict__ gb,
                                                           __nv_bfloat16* __restrict__ y, float* __restrict__ mean,
                                                           float* __restrict__ rstd, int64_t T, int D, float eps) {
+  griddep_wait();
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * (int64_t)LN_WARPS + (threadIdx.x >> 5);
   if (row >= T) return;
@@ -97,6 +99,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32) k_ln_bwd(const __nv_bfloat16* _
                                                           __nv_bfloat16* __restrict__ dx, float* __restrict__ part,
                                                           int64_t T, int D, int64_t rows_per_block, int* counter,
                                                           float* master, float* mout, float lr) {
+  griddep_wait();
   extern __shared__ float red[];  // [LN_WARPS][2*D]
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -179,6 +182,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32) k_ln_bwd(const __nv_bfloat16* _
 __global__ void __launch_bounds__(256) k_embed_fwd(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ wte,
                                                    const __nv_bfloat16* __restrict__ wpe, __nv_bfloat16* __restrict__ x,
                                                    int64_t T, int S, int D) {
+  griddep_wait();
   const int D8 = D / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T * D8; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = i / D8;
@@ -225,6 +229,7 @@ __global__ void __launch_bounds__(512) k_softmax_ce_v(const float* __restrict__ 
                                                       const int* __restrict__ labels, int V, int Vp, float inv_n,
                                                       __nv_bfloat16* __restrict__ dz, int64_t ldd,
                                                       float* __restrict__ loss) {
+  griddep_wait();
   __shared__ float shm[32], shs[32];
   const int64_t r = blockIdx.x;
   const float* row = z + r * ldz;
@@ -278,10 +283,10 @@ int ln_fwd(const void* x, const float* gb, void* y, float* mean, float* rstd, in
   auto X = static_cast<const __nv_bfloat16*>(x);
   auto Y = static_cast<__nv_bfloat16*>(y);
   switch (D / 256) {
-    case 1: k_ln_fwd<1><<<g, LN_WARPS * 32, 0, st>>>(X, gb, Y, mean, rstd, T, D, 1e-5f); break;
-    case 2: k_ln_fwd<2><<<g, LN_WARPS * 32, 0, st>>>(X, gb, Y, mean, rstd, T, D, 1e-5f); break;
-    case 4: k_ln_fwd<4><<<g, LN_WARPS * 32, 0, st>>>(X, gb, Y, mean, rstd, T, D, 1e-5f); break;
-    case 8: k_ln_fwd<8><<<g, LN_WARPS * 32, 0, st>>>(X, gb, Y, mean, rstd, T, D, 1e-5f); break;
+    case 1: launch_pdl(k_ln_fwd<1>, dim3(g), dim3(LN_WARPS * 32), 0, st, X, gb, Y, mean, rstd, T, D, 1e-5f); break;
+    case 2: launch_pdl(k_ln_fwd<2>, dim3(g), dim3(LN_WARPS * 32), 0, st, X, gb, Y, mean, rstd, T, D, 1e-5f); break;
+    case 4: launch_pdl(k_ln_fwd<4>, dim3(g), dim3(LN_WARPS * 32), 0, st, X, gb, Y, mean, rstd, T, D, 1e-5f); break;
+    case 8: launch_pdl(k_ln_fwd<8>, dim3(g), dim3(LN_WARPS * 32), 0, st, X, gb, Y, mean, rstd, T, D, 1e-5f); break;
     default: return set_error(PD_ERR_INVALID, "layernorm: D/256 must be 1, 2, 4 or 8");
   }
   return status("ln_fwd");
@@ -304,7 +309,7 @@ int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, 
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return set_error(PD_ERR_CUDA, "ln_bwd: shared memory attribute");
-    kern<<<blocks, LN_WARPS * 32, smem, st>>>(static_cast<const __nv_bfloat16*>(dy),
+    launch_pdl(kern, dim3(blocks), dim3(LN_WARPS * 32), smem, st, static_cast<const __nv_bfloat16*>(dy),
                                               static_cast<const __nv_bfloat16*>(x), mean, rstd, gb,
                                               static_cast<const __nv_bfloat16*>(dres), static_cast<__nv_bfloat16*>(dx),
                                               part, T, D, per, counter, master, out, lr);
@@ -321,7 +326,7 @@ int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, 
 
 int embed_fwd(const int* tok, const void* wte, const void* wpe, void* x, int64_t T, int S, int D, cudaStream_t st) {
   if (D % 8) return set_error(PD_ERR_INVALID, "embedding: D %% 8 == 0");
-  k_embed_fwd<<<sms() * 8, 256, 0, st>>>(tok, static_cast<const __nv_bfloat16*>(wte),
+  launch_pdl(k_embed_fwd, dim3(sms() * 8), dim3(256), 0, st, tok, static_cast<const __nv_bfloat16*>(wte),
                                         static_cast<const __nv_bfloat16*>(wpe), static_cast<__nv_bfloat16*>(x), T, S, D);
   return status("embed_fwd");
 }
@@ -336,7 +341,7 @@ int softmax_ce_v(const float* logits, int64_t ldz, const int* labels, int64_t ro
                  int64_t ldd, float* loss, cudaStream_t st) {
   if (rows < 1 || V < 1 || Vp < V || Vp % 4 || ldz % 4 || ldd % 4)
     return set_error(PD_ERR_INVALID, "softmax_ce: bad shape (Vp and row pitches must be multiples of 4)");
-  k_softmax_ce_v<<<(unsigned)rows, 512, 0, st>>>(logits, ldz, labels, V, Vp, 1.f / (float)rows,
+  launch_pdl(k_softmax_ce_v, dim3((unsigned)rows), dim3(512), 0, st, logits, ldz, labels, V, Vp, 1.f / (float)rows,
                                                  static_cast<__nv_bfloat16*>(dz), ldd, loss);
   return status("softmax_ce_v");
 }

@@ -111,6 +111,8 @@ class Executor:
         self._exchange()
         self._build_runtime()
         self.runs = 0
+        if self.world == 1 and os.environ.get("PD_GRAPHS", "1") != "0":
+            self.set_graph(True)
 
     # ------------------------------------------------------------------ setup
     KINDS = {"linear": nat.PD_LAYER_LINEAR, "conv": nat.PD_LAYER_CONV3, "embed": nat.PD_LAYER_EMBED,
@@ -478,6 +480,10 @@ class Executor:
             for l, (W, bias) in enumerate(zip(b.tensors["w_master"], b.tensors["b_master"])):
                 out[st.first_layer + l] = (W.cpu().numpy().astype(np.float64), bias.cpu().numpy().astype(np.float64))
         return out
+
+    def set_graph(self, on: bool) -> None:
+        """Replay single-process runs from a captured CUDA graph (the first eligible run captures)."""
+        nat.check(nat.lib().pd_rt_set_graph(self._rt, int(on)), "pd_rt_set_graph")
 
     def set_serial(self, on: bool) -> None:
         """Issue every hosted stage on one stream in program order (single-GPU timing mode)."""
