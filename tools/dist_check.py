@@ -20,13 +20,25 @@ def main():
     torch.distributed.init_process_group(backend)
     rank = torch.distributed.get_rank()
     reps = [int(x) for x in os.environ.get("PD_REPS", "1-1-1-1").split("-")]  # replication per stage
+    model = os.environ.get("PD_MODEL", "mlp")
     n_stages = len(reps)
     K = 20
-    stages = tuple(pd.Stage(2 * s + 1, 2 * s + 2, r) for s, r in enumerate(reps))
+    if model == "conv":  # VGG-style: conv stack (layers 1-3) and classifier (4-5), PD_REPS = "r0-r1"
+        bounds = [(1, 3), (4, 5)]
+        layers = (pd.LayerDef("conv", 64), pd.LayerDef("conv", 64, pool=True), pd.LayerDef("conv", 128, pool=True),
+                  pd.LayerDef("linear", 32), pd.LayerDef("linear", 16))
+        spec = pd.ConvNetSpec(image=(8, 8, 3), layers=layers, batch=16, lr=1e-3, n_blocks=4, seed=0)
+    elif model == "gpt":  # GPT-2-style: embedding + block | block + head
+        bounds = [(1, 2), (3, 4)]
+        spec = pd.GPTSpec(vocab=250, d=256, heads=4, layers=2, seq=128, batch=2, lr=2e-3, n_blocks=3, seed=0)
+    else:
+        bounds = [(2 * s + 1, 2 * s + 2) for s in range(n_stages)]
+        spec = pd.mlp(256, 2 * n_stages, batch=128, dtype="bf16", lr=2e-3, n_blocks=4, seed=3)
+    K = K - K % max(reps)
+    stages = tuple(pd.Stage(a, b, r) for (a, b), r in zip(bounds, reps))
     used = sum(reps)
     plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=pd.noam_for(used, reps[0]), machines_used=used)
     cfg = pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=K)
-    spec = pd.mlp(256, 2 * n_stages, batch=128, dtype="bf16", lr=2e-3, n_blocks=4, seed=3)
     ex = pd.Executor(cfg, model=spec)
     runs = []
     for r in range(3):  # repeated runs exercise the epoch-tagged flags and the end-of-run drain
@@ -35,19 +47,28 @@ def main():
         torch.cuda.synchronize()
         runs.append(ex.result())
     if rank == 0:
-        from oracle.pipeline_oracle import mlp_train
-
-        X, T = pd.make_data(spec)
+        X, T = pd.make_data_any(spec)
         v = lambda s, mb, d: runs[0].ledger.version_used(s, mb, pd.Direction(d))  # noqa: E731
-        bounds = [(st.first_layer, st.last_layer) for st in stages]
-        P = pd.init_params(spec)
+        P = pd.init_params_any(spec)
         worst = 0.0
         for res in runs:
-            want, P = mlp_train(P, X, T, spec.lr, bounds, v, K, emulate="bf16", reps=reps)
+            if model == "conv":
+                from oracle.convnet_oracle import convnet_train
+
+                want, P = convnet_train(spec.geoms(), P, X, T, spec.lr, bounds, v, K, reps=reps)
+            elif model == "gpt":
+                from oracle.gpt_oracle import gpt_train
+
+                want, P = gpt_train(spec, P, X, T, spec.lr, bounds, v, K)
+            else:
+                from oracle.pipeline_oracle import mlp_train
+
+                want, P = mlp_train(P, X, T, spec.lr, bounds, v, K, emulate="bf16", reps=reps)
             got = np.array(res.losses[:K])
             worst = max(worst, float(np.max(np.abs(got - want) / np.abs(want))))
         rep = runs[-1].report
         print(json.dumps({"ok": bool(worst <= 3e-2), "max_rel_loss_err": worst, "world": ex.world, "reps": reps,
+                          "model": model,
                           "device_of_worker": runs[-1].extras["device_of_worker"],
                           "bubble": runs[-1].extras["bubble_fraction"],
                           "steady_minibatches_per_s": rep.steady_throughput if rep else None}), flush=True)
