@@ -260,6 +260,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint64_t* bars = epi_bar + 2 * e;
     const int lane = lane_id();
     uint32_t bar_phase[2] = {0, 0};
+    // the master stream (read once, written once) must not evict the L2-resident operands
+    const uint64_t stream_pol = l2_policy_evict_first();
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = unit; u < work; u += units) {
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         bulk_wait_read0();  // previous tile's stores have finished reading both buffers
         for (int i = 0; i < 2 && i < nck; ++i) {
           mbar_arrive_expect_tx(&bars[i], 4096);
-          tma_load_2d(buf0 + i * 4096, &tmW, &bars[i], n0 + (c_begin + i) * 32, row0);
+          tma_load_2d_hint(buf0 + i * 4096, &tmW, &bars[i], n0 + (c_begin + i) * 32, row0, stream_pol);
         }
       }
       mbar_wait(&tmem_full[acc], acc_phase);
@@ -317,12 +319,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         fence_proxy_async_shared();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&tmW, buf0 + b * 4096, col0, row0);  // TMA clips rows/cols outside [M, N)
+          tma_store_2d_hint(&tmW, buf0 + b * 4096, col0, row0, stream_pol);  // TMA clips rows/cols outside [M, N)
           bulk_commit();
           if (i + 2 < nck) {
             bulk_wait_read0();  // this buffer's store has read the smem block
             mbar_arrive_expect_tx(&bars[b], 4096);
-            tma_load_2d(buf0 + b * 4096, &tmW, &bars[b], n0 + (c + 2) * 32, row0);
+            tma_load_2d_hint(buf0 + b * 4096, &tmW, &bars[b], n0 + (c + 2) * 32, row0, stream_pol);
           }
         }
         __syncwarp();
@@ -695,6 +697,13 @@ static int launch_bn(const void* A, int64_t lda, const void* B, int64_t ldb, int
     // narrow outputs (the im2col'ed first convolution, c_out = 64): a 256-wide tile would be 3/4 padding
     if (N <= 64) return launch_tc<1, 64, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
     if (N <= 128) return launch_tc<1, 128, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
+  }
+  if constexpr (KIND == EPI_SGD && B_MN) {
+    // wgrad + SGD on small weight matrices: 256 x 128 pair tiles double the tile count (e.g. a
+    // 1024 x 1024 weight: 32 instead of 16 pair tiles); large ones keep 256-wide tiles, whose
+    // operand traffic per flop is lower (measured: 8192^2 0.27 ms vs 0.31 ms with 128-wide tiles)
+    const long units256 = (long)((M + 255) / 256) * ((N + 255) / 256);
+    if (M > TC_BM && units256 <= 16) return launch_tc<2, 128, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
   }
   int cg, bn;
   pick_cfg(M, N, B_MN, &cg, &bn);
