@@ -60,7 +60,7 @@ struct TcCfg {
   // GRADF32: per warp a padded 32x33 transpose block.
   static constexpr int STG_BYTES = KIND == EPI_SGD ? TC_EPI_WARPS * 2 * 4096
                                  : (KIND == EPI_GRADF32 ? TC_EPI_WARPS * TC_STG_FLOATS * 4 : 0);
-  static constexpr int PIPE_BUDGET = 200 * 1024 - STG_BYTES;
+  static constexpr int PIPE_BUDGET = 227 * 1024 - 2048 - STG_BYTES;  // all of the 227 KB opt-in smem
   static constexpr int STAGES = PIPE_BUDGET / STAGE_BYTES > 8 ? 8 : PIPE_BUDGET / STAGE_BYTES;
   static constexpr int TMEM_COLS = 512;
   static constexpr int BAR_BYTES = 1024;  // mbarriers + TMEM slot, keeps the epilogue region 1 KB aligned
@@ -113,8 +113,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // the fp32 master read-modify-write, so co-resident tiles walk along the rows (n fastest) and
   // HBM sees long contiguous row runs instead of 1 KB pieces 32 KB apart.
   constexpr bool kNFast = transposed_epilogue(KIND);
-  auto tile_m = [&](int t) { return kNFast ? t / num_n : t % num_m; };
-  auto tile_n = [&](int t) { return kNFast ? t % num_n : t / num_m; };
+  // SGD: grouped rasterisation - bands of kGroup tile rows walked column by column, so the
+  // co-resident tiles touch ~kGroup A blocks and ~units/kGroup B blocks (a compact operand
+  // working set that survives the streamed master traffic in L2)
+  constexpr int kGroup = KIND == EPI_SGD ? 8 : 0;
+  auto tile_m = [&](int t) {
+    if constexpr (kGroup > 0) {
+      const int band = t / (kGroup * num_n), in = t - band * kGroup * num_n;
+      const int rows = num_m - band * kGroup < kGroup ? num_m - band * kGroup : kGroup;
+      return band * kGroup + in % rows;
+    }
+    return kNFast ? t / num_n : t % num_m;
+  };
+  auto tile_n = [&](int t) {
+    if constexpr (kGroup > 0) {
+      const int band = t / (kGroup * num_n), in = t - band * kGroup * num_n;
+      const int rows = num_m - band * kGroup < kGroup ? num_m - band * kGroup : kGroup;
+      return in / rows;
+    }
+    return kNFast ? t % num_n : t / num_m;
+  };
 
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch_desc(&tmA);
