@@ -317,6 +317,11 @@ int pd_rt_set_graph(pd_runtime* rt, int on);
  * 6 update/reduction (bias sums, split-K / allreduce + SGD), 7 other (pool, im2col, embedding, cast). */
 int pd_rt_kernel_timing(pd_runtime* rt, int on);
 int pd_rt_kernel_stats(pd_runtime* rt, double* out, int n_classes);
+/* Per-layer timing (the layer profiler): %globaltimer stamps around every layer's forward and
+ * backward on the stage stream, into the caller's device buffer ts[2*cap] (NULL: off); works in
+ * graph replay.  stats = average ms per pass, out[2*l] forward, out[2*l+1] backward. */
+int pd_rt_layer_timing(pd_runtime* rt, uint64_t* ts, int cap);
+int pd_rt_layer_stats(pd_runtime* rt, int worker, int n_layers, double* out);
 /* Kernels of this library launched by the runtime since creation. */
 int pd_rt_launch_count(pd_runtime* rt, int64_t* out);
 int pd_rt_destroy(pd_runtime* rt);

@@ -84,5 +84,5 @@ from .profiles import (  # noqa: F401
     stage_time,
     weight_sync_time,
 )
-from .profiler import profile_mlp  # noqa: F401
+from .profiler import profile_mlp, profile_model  # noqa: F401
 from .program import Program, compile_program, resolve_versions  # noqa: F401

@@ -27,7 +27,7 @@ EXPORTED = (
     "pd_abi_version", "pd_last_error", "pd_device_sm_count", "pd_gemm", "pd_bias_sgd", "pd_sgd_update", "pd_cast", "pd_allreduce_sgd", "pd_bias_grad",
     "pd_flag_signal", "pd_flag_wait", "pd_copy", "pd_ipc_get_handle", "pd_ipc_open", "pd_ipc_close",
     "pd_enable_peer_access", "pd_rt_create", "pd_rt_add_stage", "pd_rt_add_view", "pd_rt_load_program", "pd_rt_run",
-    "pd_rt_records", "pd_rt_set_serial", "pd_rt_set_graph", "pd_rt_kernel_timing", "pd_rt_kernel_stats", "pd_rt_launch_count", "pd_rt_destroy",
+    "pd_rt_records", "pd_rt_set_serial", "pd_rt_set_graph", "pd_rt_layer_timing", "pd_rt_layer_stats", "pd_rt_kernel_timing", "pd_rt_kernel_stats", "pd_rt_launch_count", "pd_rt_destroy",
     "pd_conv3x3", "pd_splitk_plan", "pd_maxpool2", "pd_maxpool2_bwd", "pd_im2col3", "pd_reduce_sgd",
     "pd_colsum_blocks", "pd_bias_grad_tall", "pd_softmax_ce", "pd_memcpy_async", "pd_layer_scratch_floats",
     "pd_layer_save_bytes", "pd_layer_work_bytes", "pd_attention_fwd", "pd_attention_bwd", "pd_layernorm_fwd",
@@ -125,6 +125,8 @@ def lib() -> ctypes.CDLL:
         L.pd_rt_kernel_timing.argtypes = [c_void_p, c_int]
         L.pd_rt_set_serial.argtypes = [c_void_p, c_int]
         L.pd_rt_set_graph.argtypes = [c_void_p, c_int]
+        L.pd_rt_layer_timing.argtypes = [c_void_p, c_void_p, c_int]
+        L.pd_rt_layer_stats.argtypes = [c_void_p, c_int, c_int, POINTER(c_double)]
         L.pd_rt_kernel_stats.argtypes = [c_void_p, POINTER(c_double), c_int]
         L.pd_rt_launch_count.argtypes = [c_void_p, POINTER(c_int64)]
         L.pd_device_sm_count.argtypes = [c_int, POINTER(c_int)]

@@ -223,6 +223,18 @@ __global__ void k_flag_wait(const int* flag, int v, int* err) {
   }
 }
 
+__global__ void k_timestamp(uint64_t* p) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *p = t;
+}
+
+int timestamp(uint64_t* p, cudaStream_t st) {
+  k_timestamp<<<1, 1, 0, st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "timestamp: %s", cudaGetErrorString(e));
+}
+
 int flag_signal(int* flag, int value, cudaStream_t st) {
   k_flag_signal<<<1, 1, 0, st>>>(flag, value);
   cudaError_t e = cudaGetLastError();

@@ -161,6 +161,10 @@ int im2col3(const void* x, void* cols, int n, int H, int W, int C, int kpad, cud
 }
 
 // ---------------------------------------------------------------- column sums (bias gradients)
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
 // Block b sums rows [b*rows_per, ...) of a [rows, C] bf16 matrix into part[b][C] (fp32); narrow
 // rows: each thread owns 8 columns (one 16-byte vector) and a strided set of rows; wide rows
 // (C/8 > 128): each thread owns column groups and walks the block's rows.  With a counter, the
@@ -206,9 +210,14 @@ __global__ void __launch_bounds__(CS_THREADS) k_colsum_part(const __nv_bfloat16*
           acc[2 * j + 1] += b;
         }
       }
-      float4* dst = reinterpret_cast<float4*>(part + (int64_t)blockIdx.x * C + cg * 8);
-      dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      if (counter) {  // fused mode: accumulate straight into the zeroed part[0..C)
+        red_add_v4(part + cg * 8, acc[0], acc[1], acc[2], acc[3]);
+        red_add_v4(part + cg * 8 + 4, acc[4], acc[5], acc[6], acc[7]);
+      } else {
+        float4* dst = reinterpret_cast<float4*>(part + (int64_t)blockIdx.x * C + cg * 8);
+        dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      }
     }
   } else {
     const int lanes = CS_THREADS / C8;  // row lanes per block
@@ -233,7 +242,8 @@ __global__ void __launch_bounds__(CS_THREADS) k_colsum_part(const __nv_bfloat16*
     for (int c = threadIdx.x; c < C; c += CS_THREADS) {
       float s = 0.f;
       for (int l = 0; l < lanes; ++l) s += red[l * C + c];
-      part[(int64_t)blockIdx.x * C + c] = s;
+      if (counter) atomicAdd(part + c, s);
+      else part[(int64_t)blockIdx.x * C + c] = s;
     }
   }
   if (!counter) return;
@@ -243,7 +253,7 @@ __global__ void __launch_bounds__(CS_THREADS) k_colsum_part(const __nv_bfloat16*
   __syncthreads();
   if (!last) return;
   __threadfence();
-  finish_update(part, gridDim.x, C, grad, master, out, lr);
+  finish_update(part, 1, C, grad, master, out, lr);  // part[0..C) holds the column sums
   if (threadIdx.x == 0) *counter = 0;
 }
 
@@ -297,6 +307,10 @@ int bias_grad_tall(const void* dz, int64_t rows, int C, float* part, float* grad
   const int64_t per = (rows + blocks - 1) / blocks;
   const int lanes = CS_THREADS / (C / 8);
   const size_t smem = C / 8 > CS_THREADS / 2 ? 0 : (size_t)(lanes > 0 ? lanes : 1) * C * sizeof(float);
+  if (counter) {
+    cudaError_t e = cudaMemsetAsync(part, 0, sizeof(float) * C, st);
+    if (e != cudaSuccess) return set_error(PD_ERR_CUDA, "colsum accumulator: %s", cudaGetErrorString(e));
+  }
   launch_pdl(k_colsum_part, dim3(blocks), dim3(CS_THREADS), smem, st, static_cast<const __nv_bfloat16*>(dz), rows, C, per, part, counter,
                                                   grad, master, out, lr);
   int rc = launch_status("colsum_part");

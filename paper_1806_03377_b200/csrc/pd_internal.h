@@ -61,6 +61,7 @@ int allreduce_sgd(int dtype, const float* const* grads, int n_rep, float* master
 int bias_grad(int dtype, const void* dz, int rows, int cols, int64_t ld, float* out, cudaStream_t st);
 int cast_f32(int dtype, const float* src, void* out, int64_t n, cudaStream_t st);
 int flag_signal(int* flag, int value, cudaStream_t st);
+int timestamp(uint64_t* p, cudaStream_t st);  // *p = %globaltimer (ns) when the stream reaches it
 int flag_wait(const int* flag, int value, int* err_word, cudaStream_t st);
 
 // Launch with programmatic stream serialization (PDL): the kernel may be scheduled while its

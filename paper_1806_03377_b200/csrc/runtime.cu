@@ -141,6 +141,12 @@ struct pd_runtime {
   // process, so the next run cannot overwrite a slot the peer still reads
   struct Drain { int worker; int* flag; int mb; };
   std::vector<Drain> drain;
+  bool ltiming = false;  // per-layer fwd / bwd %globaltimer stamps (the layer profiler)
+  struct LT { int worker, layer, dir; };
+  std::vector<LT> lt;
+  size_t lt_used = 0;
+  uint64_t* ts = nullptr;  // caller-owned device buffer [2 * ts_cap]
+  int ts_cap = 0;
   bool ktiming = false;
   struct KT { int cls; double flops; cudaEvent_t a, b; };
   std::vector<KT> kt;
@@ -247,6 +253,26 @@ int signal_flag(pd_runtime* rt, Stage& S, int* flag, int value) {
   return 0;
 }
 
+// %globaltimer stamps around one layer's pass (fwd dir 0 / bwd dir 1) while layer timing is on:
+// tiny kernels on the stage stream, so they also work inside a replayed CUDA graph (the host
+// enqueue rate then never starves the timed kernels).  The end stamp is written when the object
+// leaves scope (end of the layer's loop iteration).
+struct LayerTimer {
+  cudaStream_t st = nullptr;
+  uint64_t* end = nullptr;
+  LayerTimer(pd_runtime* rt, int worker, int layer, int dir, cudaStream_t stream) : st(stream) {
+    if (!rt->ltiming || (int)rt->lt_used >= rt->ts_cap) return;
+    const size_t i = rt->lt_used++;
+    if (i == rt->lt.size()) rt->lt.push_back({});
+    rt->lt[i] = {worker, layer, dir};
+    timestamp(rt->ts + 2 * i, stream);
+    end = rt->ts + 2 * i + 1;
+  }
+  ~LayerTimer() {
+    if (end) timestamp(end, st);
+  }
+};
+
 int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
   cudaStream_t ST = stream_of(rt, S);
   const pd_stage_desc& d = S.d;
@@ -254,6 +280,7 @@ int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
   const int wslot = it[PD_IT_WSLOT], act = it[PD_IT_ACT], mb = it[PD_IT_MB];
   const void* x = d.is_first ? S.act_in[it[PD_IT_BLOCK]] : S.act_in[it[PD_IT_XSLOT]];
   for (int l = 0; l < L; ++l) {
+    LayerTimer ltimer(rt, S.d.worker, l, 0, ST);
     const int K = (int)S.dims[l], N = (int)S.dims[l + 1];
     EpiArgs ep{};
     ep.bias = S.b_ring[(size_t)l * d.ring_depth + wslot];
@@ -294,6 +321,7 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
   }
   const void* dz = d.is_last ? S.dz_last[act] : S.grad_in[it[PD_IT_GSLOT]];
   for (int l = L - 1; l >= 0; --l) {
+    LayerTimer ltimer(rt, S.d.worker, l, 1, ST);
     const int Kin = (int)S.dims[l], Nout = (int)S.dims[l + 1];
     const void* X = (l == 0) ? (d.is_first ? S.act_in[it[PD_IT_BLOCK]] : S.act_in[it[PD_IT_XSLOT]])
                              : S.act[(size_t)(l - 1) * d.act_depth + act];
@@ -585,6 +613,7 @@ int run_forward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
   const int wslot = it[PD_IT_WSLOT], act = it[PD_IT_ACT], mb = it[PD_IT_MB];
   const void* x = d.is_first ? S.act_in[it[PD_IT_BLOCK]] : S.act_in[it[PD_IT_XSLOT]];
   for (int l = 0; l < L; ++l) {
+    LayerTimer ltimer(rt, S.d.worker, l, 0, ST);
     const Layer& Y = S.layers[l];
     const pd_layer& y = Y.d;
     const bool last = l == L - 1;
@@ -664,6 +693,7 @@ int run_backward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
   const void* dz = d.is_last ? S.dz_last[act] : S.grad_in[it[PD_IT_GSLOT]];
   auto other_tmp = [&](const void* p) { return p == d.tmp[0] ? d.tmp[1] : d.tmp[0]; };
   for (int l = L - 1; l >= 0; --l) {
+    LayerTimer ltimer(rt, S.d.worker, l, 1, ST);
     const Layer& Y = S.layers[l];
     const pd_layer& y = Y.d;
     const void* X = (l == 0) ? (d.is_first ? S.act_in[it[PD_IT_BLOCK]] : S.act_in[it[PD_IT_XSLOT]])
@@ -977,6 +1007,7 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
     // be captured); the instantiated graph is then launched into the caller's stream
     if (!rt->graph_stream) PD_CHECK(cudaStreamCreateWithFlags(&rt->graph_stream, cudaStreamNonBlocking));
     const int64_t before = rt->launches;
+    rt->lt_used = 0;  // layer-timing events captured into the graph are re-recorded by every replay
     PD_CHECK(cudaStreamBeginCapture(rt->graph_stream, cudaStreamCaptureModeRelaxed));
     const int rc = run_body(rt, rt->graph_stream, 0);
     cudaGraph_t g = nullptr;
@@ -1118,6 +1149,34 @@ int pd_rt_kernel_stats(pd_runtime* rt, double* out9, int n_classes) {
     out9[3 * k.cls + 1] += ms;
     out9[3 * k.cls + 2] += k.flops;
   }
+  return 0;
+}
+
+int pd_rt_layer_timing(pd_runtime* rt, uint64_t* ts, int cap) {
+  if (!rt) return set_error(PD_ERR_INVALID, "pd_rt_layer_timing: null runtime");
+  rt->ltiming = ts != nullptr && cap > 0;
+  rt->ts = ts;
+  rt->ts_cap = rt->ltiming ? cap : 0;
+  rt->lt_used = 0;
+  drop_graph(rt);  // the next run (re)captures with or without the stamps
+  return 0;
+}
+
+int pd_rt_layer_stats(pd_runtime* rt, int worker, int n_layers, double* out) {
+  if (!rt || !out || n_layers < 1) return set_error(PD_ERR_INVALID, "pd_rt_layer_stats: bad argument");
+  std::vector<double> cnt(2 * n_layers, 0.0);
+  for (int i = 0; i < 2 * n_layers; ++i) out[i] = 0.0;
+  PD_CHECK(cudaSetDevice(rt->device));
+  std::vector<uint64_t> h(2 * rt->lt_used);
+  if (!h.empty()) PD_CHECK(cudaMemcpy(h.data(), rt->ts, h.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < rt->lt_used; ++i) {
+    const auto& x = rt->lt[i];
+    if (x.worker != worker || x.layer < 0 || x.layer >= n_layers) continue;
+    out[2 * x.layer + x.dir] += (double)(h[2 * i + 1] - h[2 * i]) * 1e-6;  // ns -> ms
+    cnt[2 * x.layer + x.dir] += 1.0;
+  }
+  for (int i = 0; i < 2 * n_layers; ++i)
+    if (cnt[i] > 0) out[i] /= cnt[i];
   return 0;
 }
 

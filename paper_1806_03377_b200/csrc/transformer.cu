@@ -159,7 +159,8 @@ __global__ void __launch_bounds__(LN_WARPS * 32) k_ln_bwd(const __nv_bfloat16* _
     float s = 0.f;
 #pragma unroll
     for (int w = 0; w < LN_WARPS; ++w) s += red[w * 2 * D + c];
-    part[blockIdx.x * 2 * (int64_t)D + c] = s;
+    if (counter) atomicAdd(part + c, s);  // fused mode: part[0..2D) is a zeroed accumulator
+    else part[blockIdx.x * 2 * (int64_t)D + c] = s;
   }
   if (!counter) return;
   __threadfence();
@@ -168,9 +169,8 @@ __global__ void __launch_bounds__(LN_WARPS * 32) k_ln_bwd(const __nv_bfloat16* _
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int c = threadIdx.x; c < 2 * D; c += LN_WARPS * 32) {  // fixed block order
-    float g = 0.f;
-    for (int b = 0; b < (int)gridDim.x; ++b) g += __ldcg(part + (int64_t)b * 2 * D + c);
+  for (int c = threadIdx.x; c < 2 * D; c += LN_WARPS * 32) {
+    const float g = __ldcg(part + c);
     const float w = master[c] - lr * g;
     master[c] = w;
     mout[c] = w;
@@ -305,6 +305,10 @@ int ln_bwd(const void* dy, const void* x, const float* mean, const float* rstd, 
   const int blocks = ln_bwd_blocks(T);
   const int64_t per = (T + blocks - 1) / blocks;
   const size_t smem = (size_t)LN_WARPS * 2 * D * sizeof(float);
+  if (counter) {
+    cudaError_t e = cudaMemsetAsync(part, 0, sizeof(float) * 2 * D, st);
+    if (e != cudaSuccess) return set_error(PD_ERR_CUDA, "ln_bwd accumulator: %s", cudaGetErrorString(e));
+  }
   auto launch = [&](auto kern) -> int {
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)

@@ -13,8 +13,10 @@ round-trips through ``save_profile`` into the reference's JSON format, so either
 
 from __future__ import annotations
 
+import ctypes
+
 from . import _native as nat
-from .models import MLPSpec
+from .models import ConvNetSpec, GPTSpec, MLPSpec
 from .profiles import LayerProfile, ModelProfile
 
 
@@ -66,3 +68,65 @@ def profile_mlp(spec: MLPSpec, repeats: int = 10, warmup: int = 3, device=None) 
             times.append(a.elapsed_time(b) / repeats * 1e-3)
         layers.append(LayerProfile(l, f"linear{l}_{din}x{dout}", times[0], times[1], B * dout, din * dout + dout))
     return ModelProfile(layers=tuple(layers), minibatch_size=B)
+
+
+def _layer_names(spec) -> list[str]:
+    if isinstance(spec, MLPSpec):
+        return [f"linear{l}_{a}x{b}" for l, (a, b) in enumerate(zip(spec.widths[:-1], spec.widths[1:]), start=1)]
+    names = []
+    for l, g in enumerate(spec.geoms(), start=1):
+        if g.kind == "conv":
+            names.append(f"conv{l}_{g.h}x{g.w}x{g.c_in}-{g.c_out}" + ("_pool" if g.pool else ""))
+        elif g.kind == "linear":
+            names.append(f"fc{l}_{g.c_in}x{g.c_out}")
+        else:
+            names.append(f"{g.kind}{l}")
+    return names
+
+
+def profile_model(spec, minibatches: int = 12, steps: int = 2, device=None) -> ModelProfile:
+    """Measured per-layer profile of any executor model (MLP, ConvNet, GPT) as a reference-format
+    ``ModelProfile``: the whole model runs as ONE stage through the executor's own kernel chains
+    (so conv pools, attention, LayerNorm, losses and the fused updates are all included) with
+    per-layer CUDA events on the stage stream; fwd_time / bwd_time are the averages over
+    ``steps`` runs of ``minibatches`` minibatches.  activation_elems = batch x the layer's output
+    features (the message a stage boundary after this layer would carry), param_elems = its
+    weights + biases.  Feed it to ``solve`` to partition on B200 measurements."""
+    import torch
+
+    from .executor import Executor
+    from .ledger import SimConfig
+    from .plans import Plan, Stage
+
+    L = spec.num_layers
+    plan = Plan(stages=(Stage(1, L, 1),), bottleneck_time=1.0, noam=1, machines_used=1)
+    cfg = SimConfig(plan=plan, mode="weight_stashing", num_minibatches=max(11, minibatches))
+    ex = Executor(cfg, model=spec, device=device)
+    try:
+        ex.set_serial(True)
+        ex.set_graph(True)  # replayed as a CUDA graph: no host launch gaps inside the timed layers
+        ex.step()  # warm-up (tensor maps, attributes, caches)
+        torch.cuda.synchronize(ex.device)
+        lib = nat.lib()
+        cap = 2 * L * cfg.num_minibatches + 16  # stamps of one run (a replay rewrites the same slots)
+        ts = torch.zeros(2 * cap, dtype=torch.int64, device=ex.device)
+        nat.check(lib.pd_rt_layer_timing(ex._rt, ts.data_ptr(), cap), "pd_rt_layer_timing")
+        for _ in range(steps + 1):  # the first run captures the graph (with the stamp kernels)
+            ex.step()
+        torch.cuda.synchronize(ex.device)
+        buf = (ctypes.c_double * (2 * L))()
+        nat.check(lib.pd_rt_layer_stats(ex._rt, 0, L, buf), "pd_rt_layer_stats")
+        nat.check(lib.pd_rt_layer_timing(ex._rt, None, 0), "pd_rt_layer_timing")
+    finally:
+        ex.close()
+    names = _layer_names(spec)
+    if isinstance(spec, MLPSpec):
+        outs = list(spec.widths[1:])
+        params = [a * b + b for a, b in zip(spec.widths[:-1], spec.widths[1:])]
+    else:
+        geo = spec.geoms()
+        outs = [g.out_features for g in geo]
+        params = [g.w_numel + g.b_numel for g in geo]
+    layers = tuple(LayerProfile(l + 1, names[l], buf[2 * l] * 1e-3, buf[2 * l + 1] * 1e-3, spec.batch * outs[l],
+                                params[l]) for l in range(L))
+    return ModelProfile(layers=layers, minibatch_size=spec.batch)

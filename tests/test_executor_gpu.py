@@ -172,3 +172,26 @@ def test_profile_plan_run_loop(tmp_path):
     K = max(plan.noam + 10, 2 * plan.noam + plan.num_stages + 2)
     res = pd.run(pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=K), ctx, model=spec)
     assert np.all(np.isfinite(res.losses[:K])) and res.report.steady_throughput > 0
+
+
+@pytest.mark.parametrize("which", ["vgg", "gpt"])
+def test_profile_model_then_solve(which, tmp_path):
+    """Measured per-layer profile of a conv net / transformer (one stage, layer events) ->
+    reference JSON -> solve() -> a runnable plan."""
+    if which == "vgg":
+        layers = (pd.LayerDef("conv", 64), pd.LayerDef("conv", 64, pool=True), pd.LayerDef("conv", 128, pool=True),
+                  pd.LayerDef("linear", 64), pd.LayerDef("linear", 16))
+        spec = pd.ConvNetSpec(image=(32, 32, 3), layers=layers, batch=32, lr=1e-3, n_blocks=2, seed=0)
+    else:
+        spec = pd.GPTSpec(vocab=250, d=256, heads=4, layers=3, seq=128, batch=2, lr=1e-3, n_blocks=2, seed=0)
+    prof = pd.profile_model(spec, minibatches=11, steps=1)
+    assert prof.num_layers == spec.num_layers
+    assert all(l.fwd_time > 0 and l.bwd_time > 0 for l in prof.layers)
+    path = tmp_path / "profile.json"
+    pd.save_profile(prof, path)
+    ctx = pd.build_context(pd.load_profile(path), pd.HardwareSpec(2, 770e9, 2))
+    plan = pd.solve(ctx, max_replication=1)
+    assert plan.num_layers == spec.num_layers
+    K = max(plan.noam + 10, 2 * plan.noam + plan.num_stages + 2)
+    res = pd.run(pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=K), ctx, model=spec)
+    assert np.all(np.isfinite(res.losses[:K]))
