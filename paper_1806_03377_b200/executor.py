@@ -481,6 +481,48 @@ class Executor:
                 out[st.first_layer + l] = (W.cpu().numpy().astype(np.float64), bias.cpu().numpy().astype(np.float64))
         return out
 
+    # ------------------------------------------------------------------ checkpoints
+    def save_checkpoint(self, directory) -> list[str]:
+        """Per-stage weight checkpoint, written by each process for the workers it hosts without
+        any global coordination: one .npz per worker with the fp32 master
+        weights and biases of its layers and the number of completed runs."""
+        import pathlib
+
+        torch = _torch()
+        torch.cuda.synchronize(self.device)
+        out = pathlib.Path(directory)
+        out.mkdir(parents=True, exist_ok=True)
+        paths = []
+        for b in self.bufs.values():
+            arrays = {}
+            for l, (W, bias) in enumerate(zip(b.tensors["w_master"], b.tensors["b_master"])):
+                arrays[f"W{l}"] = W.cpu().numpy()
+                arrays[f"b{l}"] = bias.cpu().numpy()
+            path = out / f"stage{b.stage:02d}_worker{b.wid:02d}.npz"
+            np.savez(path, runs=np.int64(self.runs), **arrays)
+            paths.append(str(path))
+        return paths
+
+    def load_checkpoint(self, directory) -> None:
+        """Restore the hosted workers' master weights from ``save_checkpoint`` files (the next run
+        refreshes version 0 of every ring from them)."""
+        import pathlib
+
+        torch = _torch()
+        src = pathlib.Path(directory)
+        for b in self.bufs.values():
+            path = src / f"stage{b.stage:02d}_worker{b.wid:02d}.npz"
+            if not path.exists():
+                raise ValidationError(f"no checkpoint for worker {b.wid} (stage {b.stage}) in {src}")
+            data = np.load(path)
+            for l, (W, bias) in enumerate(zip(b.tensors["w_master"], b.tensors["b_master"])):
+                w, bb = data[f"W{l}"], data[f"b{l}"]
+                if w.shape != tuple(W.shape) or bb.shape != tuple(bias.shape):
+                    raise ValidationError(f"checkpoint {path.name}: layer {l} shape mismatch")
+                W.copy_(torch.from_numpy(w).to(W.device))
+                bias.copy_(torch.from_numpy(bb).to(bias.device))
+        torch.cuda.synchronize(self.device)
+
     def set_graph(self, on: bool) -> None:
         """Replay single-process runs from a captured CUDA graph (the first eligible run captures)."""
         nat.check(nat.lib().pd_rt_set_graph(self._rt, int(on)), "pd_rt_set_graph")
