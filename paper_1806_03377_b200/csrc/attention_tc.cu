@@ -54,6 +54,13 @@ PD_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const float (&v)[32]) {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// 2^x on the SFU (ex2.approx, flush-to-zero): x <= 0 here, so no range handling is needed.
+PD_DEVICE float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Byte offset of (row, 16-byte chunk) of a 128B-swizzled tile (the TMA / UMMA SW128 pattern).
 PD_DEVICE uint32_t sw128(int row, int chunk) { return row * 128 + ((chunk ^ (row & 7)) << 4); }
 
@@ -170,21 +177,24 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
       mbar_wait(s_full, j & 1);
       tc_fence_after();
       const bool diag = j == qt;
-      // pass 1: row max of this tile
-      float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < TK / 32; ++c) {
-        float v[32];
-        tmem_ld_32x32b_x32(tS + lane_base + c * 32, v);
+      // the whole S row in registers (four loads, one wait): max, then exp2 from the same values
+      uint32_t sr[TK];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int key = j * TK + c * 32 + i;
-          const float sv = (diag && key > q) ? -INFINITY : v[i] * scale_log2;
-          mx = fmaxf(mx, sv);
-        }
+      for (int c = 0; c < TK / 32; ++c)
+        tmem_ld_32x32b_x32_nowait(tS + lane_base + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32 * c));
+      tmem_wait_ld();
+      float* sv = reinterpret_cast<float*>(sr);
+      if (diag) {  // causal mask, diagonal tile only: keys j*TK + i > q
+        const int lim = q - j * TK;
+#pragma unroll
+        for (int i = 0; i < TK; ++i)
+          if (i > lim) sv[i] = -INFINITY;
       }
-      const float m_new = fmaxf(m, mx);
-      const float alpha = m == -INFINITY ? 0.f : exp2f(m - m_new);
+      float mx = sv[0];
+#pragma unroll
+      for (int i = 1; i < TK; ++i) mx = fmaxf(mx, sv[i]);
+      const float m_new = fmaxf(m, mx * scale_log2);  // scale > 0: max commutes with it
+      const float alpha = m == -INFINITY ? 0.f : fast_exp2(m - m_new);
       if (j > 0) mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} finished: O final for j-1, P free
       tc_fence_after();
       // rescale the O row when the running max moved (warp-uniform decision)
@@ -198,19 +208,16 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
           tmem_st_32x32b_x32(tO + lane_base + c * 32, o);
         }
       }
-      // pass 2: P = exp2(s - m_new) -> bf16 -> smem (K-major SW128, two 64-key atoms)
+      // P = exp2(s*scale - m_new) -> bf16 -> smem (K-major SW128, two 64-key atoms)
       float rs = 0.f;
-#pragma unroll 1
+      const float neg = -m_new;
+#pragma unroll
       for (int c = 0; c < TK / 32; ++c) {
-        float v[32];
-        tmem_ld_32x32b_x32(tS + lane_base + c * 32, v);
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          const int key = j * TK + c * 32 + i;
-          const float s0 = (diag && key > q) ? -INFINITY : v[i] * scale_log2;
-          const float s1 = (diag && key + 1 > q) ? -INFINITY : v[i + 1] * scale_log2;
-          const float p0 = exp2f(s0 - m_new), p1 = exp2f(s1 - m_new);
+          const float p0 = fast_exp2(fmaf(sv[32 * c + i], scale_log2, neg));
+          const float p1 = fast_exp2(fmaf(sv[32 * c + i + 1], scale_log2, neg));
           rs += p0 + p1;
           pk[i / 2] = pack_bf16x2(p0, p1);
         }
@@ -439,20 +446,24 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         const float* sv = reinterpret_cast<const float*>(svr);
         const float* dp = reinterpret_cast<const float*>(dpr);
         uint32_t pk[16], dk[16];
+        const float4* L4 = reinterpret_cast<const float4*>(sL + c * 32);
+        const float4* D4 = reinterpret_cast<const float4*>(sDd + c * 32);
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          float pp[2], dd[2];
+        for (int i = 0; i < 32; i += 4) {
+          const float4 lv = L4[i / 4], dv = D4[i / 4];
+          const float ls[4] = {lv.x, lv.y, lv.z, lv.w}, ds[4] = {dv.x, dv.y, dv.z, dv.w};
+          float pp[4], dd[4];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int ql = c * 32 + i + e;
-            const int q = qt * TQ + ql;
-            float p = exp2f(sv[i + e] * scale_log2 - sL[ql]);
-            if (diag && q < key) p = 0.f;
+          for (int e = 0; e < 4; ++e) {
+            float p = fast_exp2(fmaf(sv[i + e], scale_log2, -ls[e]));
+            if (diag && qt * TQ + c * 32 + i + e < key) p = 0.f;
             pp[e] = p;
-            dd[e] = p * (dp[i + e] - sDd[ql]);
+            dd[e] = p * (dp[i + e] - ds[e]);
           }
           pk[i / 2] = pack_bf16x2(pp[0], pp[1]);
+          pk[i / 2 + 1] = pack_bf16x2(pp[2], pp[3]);
           dk[i / 2] = pack_bf16x2(dd[0], dd[1]);
+          dk[i / 2 + 1] = pack_bf16x2(dd[2], dd[3]);
         }
         const int atom = (c >> 1) * TILE_BYTES;
         const int chunk0 = (c & 1) * 4;
