@@ -45,14 +45,17 @@ PD_DEVICE void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
 PD_DEVICE void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// The suspend-time hint lets the waiting warp sleep until the phase completes (or the hint
+// expires) instead of spinning: waiting producer / MMA warps then stop stealing issue slots from
+// the epilogue / softmax warps that share their SM sub-partition.
 PD_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)
       : "memory");
 }
 
