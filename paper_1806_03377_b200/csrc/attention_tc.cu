@@ -177,22 +177,20 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
       mbar_wait(s_full, j & 1);
       tc_fence_after();
       const bool diag = j == qt;
-      // the whole S row in registers (four loads, one wait): max, then exp2 from the same values
-      uint32_t sr[TK];
+      // two passes over the S row in TMEM, 64 columns (two loads, one wait) at a time, so the
+      // softmax warps stay within the register budget of two CTAs per SM
+      const int lim = diag ? q - j * TK : TK;  // causal: keys j*TK + i > q are masked
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int h2 = 0; h2 < 2; ++h2) {
+        uint32_t sr[64];
+        tmem_ld_32x32b_x32_nowait(tS + lane_base + h2 * 64, *reinterpret_cast<uint32_t(*)[32]>(sr));
+        tmem_ld_32x32b_x32_nowait(tS + lane_base + h2 * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+        tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < TK / 32; ++c)
-        tmem_ld_32x32b_x32_nowait(tS + lane_base + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32 * c));
-      tmem_wait_ld();
-      float* sv = reinterpret_cast<float*>(sr);
-      if (diag) {  // causal mask, diagonal tile only: keys j*TK + i > q
-        const int lim = q - j * TK;
-#pragma unroll
-        for (int i = 0; i < TK; ++i)
-          if (i > lim) sv[i] = -INFINITY;
+        for (int i = 0; i < 64; ++i)
+          if (h2 * 64 + i <= lim) mx = fmaxf(mx, __uint_as_float(sr[i]));
       }
-      float mx = sv[0];
-#pragma unroll
-      for (int i = 1; i < TK; ++i) mx = fmaxf(mx, sv[i]);
       const float m_new = fmaxf(m, mx * scale_log2);  // scale > 0: max commutes with it
       const float alpha = m == -INFINITY ? 0.f : fast_exp2(m - m_new);
       if (j > 0) mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} finished: O final for j-1, P free
@@ -208,24 +206,29 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
           tmem_st_32x32b_x32(tO + lane_base + c * 32, o);
         }
       }
-      // P = exp2(s*scale - m_new) -> bf16 -> smem (K-major SW128, two 64-key atoms)
+      // P = exp2(s*scale - m_new) -> bf16 -> smem (K-major SW128; 64-key atom h2)
       float rs = 0.f;
       const float neg = -m_new;
+#pragma unroll 1
+      for (int h2 = 0; h2 < 2; ++h2) {
+        uint32_t sr[64];
+        tmem_ld_32x32b_x32_nowait(tS + lane_base + h2 * 64, *reinterpret_cast<uint32_t(*)[32]>(sr));
+        tmem_ld_32x32b_x32_nowait(tS + lane_base + h2 * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+        tmem_wait_ld();
+        uint32_t pk[32];
 #pragma unroll
-      for (int c = 0; c < TK / 32; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float p0 = fast_exp2(fmaf(sv[32 * c + i], scale_log2, neg));
-          const float p1 = fast_exp2(fmaf(sv[32 * c + i + 1], scale_log2, neg));
+        for (int i = 0; i < 64; i += 2) {
+          float p0 = fast_exp2(fmaf(__uint_as_float(sr[i]), scale_log2, neg));
+          float p1 = fast_exp2(fmaf(__uint_as_float(sr[i + 1]), scale_log2, neg));
+          if (h2 * 64 + i > lim) p0 = 0.f;
+          if (h2 * 64 + i + 1 > lim) p1 = 0.f;
           rs += p0 + p1;
           pk[i / 2] = pack_bf16x2(p0, p1);
         }
-        uint8_t* atom = sP + (c >> 1) * TILE_BYTES;
-        const int chunk0 = (c & 1) * 4;  // 32 keys = four 16-byte chunks of the 128-byte row
+        uint8_t* atom = sP + h2 * TILE_BYTES;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          *reinterpret_cast<uint4*>(atom + sw128(r, chunk0 + u)) =
+        for (int u = 0; u < 8; ++u)
+          *reinterpret_cast<uint4*>(atom + sw128(r, u)) =
               make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
       }
       l = l * alpha + rs;
