@@ -346,9 +346,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       for (int n = 0; n < N; ++n) {
         const int st = n & 1, qt = kt + n;
         mbar_wait(&empty_qdo[st], ((n >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&full_qdo[st], 2 * TILE_BYTES);
+        mbar_arrive_expect_tx(&full_qdo[st], 2 * TILE_BYTES + 2 * TQ * 4);
         tma_load_2d(sQ + st * TILE_BYTES, &tm_qkv, &full_qdo[st], h * HDIM, row0 + qt * TQ);
         tma_load_2d(sdO + st * TILE_BYTES, &tm_do, &full_qdo[st], h * HDIM, row0 + qt * TQ);
+        // this query tile's log-sum-exp and D rows ride along with Q / dO (stage buffers)
+        const int64_t lrow = ((int64_t)b * H + h) * S + qt * TQ;
+        bulk_load_1d(sLD + st * 256, lse + lrow, TQ * 4, &full_qdo[st]);
+        bulk_load_1d(sLD + st * 256 + 128, Dv + lrow, TQ * 4, &full_qdo[st]);
       }
     }
   } else if (warp == 1) {
@@ -423,14 +427,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     };
     for (int n = 0; n < N; ++n) {
       const int qt = kt + n;
-      const int par = n & 1;
-      float* sL = sLD + par * 256;
-      float* sDd = sL + 128;
-      sL[t] = lse[((int64_t)b * H + h) * S + qt * TQ + t];
-      sDd[t] = Dv[((int64_t)b * H + h) * S + qt * TQ + t];
-      mbar_wait(sdp_full, n & 1);
-      tc_fence_after();
-      if (n > 0) {  // MMAs of n-1 are done: their dQ is ready and P^T / dS^T smem are free
+      const int par = n & 1;  // stage of this query tile's Q / dO / lse / D buffers
+      const float* sL = sLD + par * 256;
+      const float* sDd = sL + 128;
+      if (n > 0) {  // MMAs of n-1 are done: flush their dQ while S^T / dP^T of n run on the tensor core
         mbar_wait(dq_full, (n - 1) & 1);
         tc_fence_after();
         flush_dq(qt - 1);
@@ -438,7 +438,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(dq_free);
       }
-      named_sync_128();  // lse / D of this query tile are in shared memory
+      mbar_wait(sdp_full, n & 1);  // implies the stage's TMA (incl. lse / D) has landed
+      tc_fence_after();
       const bool diag = n == 0;
 #pragma unroll 1
       for (int c = 0; c < TQ / 32; ++c) {

@@ -72,6 +72,14 @@ PD_DEVICE void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar
       : "memory");
 }
 
+// 1-D bulk copy global -> shared (size multiple of 16 B), completion counted on `bar`.
+PD_DEVICE void bulk_load_1d(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // 4-D im2col bulk tensor load (NHWC activation, implicit-GEMM convolution): `pixelsPerColumn`
 // consecutive output pixels starting at the bounding-box coordinate (w, h, n), each reading the
 // channelsPerPixel channels from c at input position (w + ow, h + oh); halo pixels outside the
