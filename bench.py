@@ -374,6 +374,19 @@ def run_ours(args, rank, world):
     ex.step(stream=stream)
     torch.cuda.synchronize()
     kstats = ex.kernel_stats()
+    # per-stage tensor-core utilisation: the stage's GEMM FLOPs over the stage's serial kernel time
+    peaks_, _ = load_peaks()
+    peak_ = float(peaks_.get("bf16_tflops_sustained", peaks_.get("bf16_tflops")))
+    stage_util = {}
+    for w in sorted(b.wid for b in ex.bufs.values()):
+        ks = ex.kernel_stats(w)
+        busy = sum(v["total_ms"] for v in ks.values())
+        fl = sum(v["total_flops"] for k, v in ks.items() if k in ("fwd", "dgrad", "wgrad_sgd"))
+        gemm_ms = sum(v["total_ms"] for k, v in ks.items() if k in ("fwd", "dgrad", "wgrad_sgd"))
+        if busy > 0:
+            stage_util[str(w)] = {"tc_util_busy": round(fl / (busy * 1e-3) / 1e12 / peak_, 3),
+                                  "tc_util_gemm": round(fl / (gemm_ms * 1e-3) / 1e12 / peak_, 3) if gemm_ms else None,
+                                  "busy_ms": round(busy, 2)}
     ex.kernel_timing(False)
     ex.set_serial(args.serial == "on")
     samples = args.steps * args.minibatches * args.batch
@@ -459,6 +472,9 @@ def run_ours(args, rank, world):
         "clocks": clocks.summary(),
         "gemm_classes": per_class,
         "kernel_time_ms_serial_step": kernel_time,
+        "stage_tc_util": stage_util,
+        "stage_tc_util_definition": "per worker: GEMM algorithmic FLOPs / serial kernel time / measured sustained "
+                                    "bf16 peak (tc_util_busy over all its kernels, tc_util_gemm over its GEMMs only)",
         "model_tflops": value * flops_per_sample / 1e12,
         "model_frac_of_sustained_peak": value * flops_per_sample / 1e12 / peak / world,
         "bubble_fraction": res.extras.get("bubble_fraction"),

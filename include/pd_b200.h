@@ -316,7 +316,7 @@ int pd_rt_set_graph(pd_runtime* rt, int on);
  * 0 forward GEMM, 1 dgrad GEMM, 2 wgrad(+SGD) GEMM, 3 attention, 4 LayerNorm, 5 loss,
  * 6 update/reduction (bias sums, split-K / allreduce + SGD), 7 other (pool, im2col, embedding, cast). */
 int pd_rt_kernel_timing(pd_runtime* rt, int on);
-int pd_rt_kernel_stats(pd_runtime* rt, double* out, int n_classes);
+int pd_rt_kernel_stats(pd_runtime* rt, int worker, double* out, int n_classes);  /* worker -1: all */
 /* Per-layer timing (the layer profiler): %globaltimer stamps around every layer's forward and
  * backward on the stage stream, into the caller's device buffer ts[2*cap] (NULL: off); works in
  * graph replay.  stats = average ms per pass, out[2*l] forward, out[2*l+1] backward. */

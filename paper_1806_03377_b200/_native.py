@@ -127,7 +127,7 @@ def lib() -> ctypes.CDLL:
         L.pd_rt_set_graph.argtypes = [c_void_p, c_int]
         L.pd_rt_layer_timing.argtypes = [c_void_p, c_void_p, c_int]
         L.pd_rt_layer_stats.argtypes = [c_void_p, c_int, c_int, POINTER(c_double)]
-        L.pd_rt_kernel_stats.argtypes = [c_void_p, POINTER(c_double), c_int]
+        L.pd_rt_kernel_stats.argtypes = [c_void_p, c_int, POINTER(c_double), c_int]
         L.pd_rt_launch_count.argtypes = [c_void_p, POINTER(c_int64)]
         L.pd_device_sm_count.argtypes = [c_int, POINTER(c_int)]
         L.pd_conv3x3.argtypes = [c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, POINTER(Epilogue),

@@ -148,7 +148,8 @@ struct pd_runtime {
   uint64_t* ts = nullptr;  // caller-owned device buffer [2 * ts_cap]
   int ts_cap = 0;
   bool ktiming = false;
-  struct KT { int cls; double flops; cudaEvent_t a, b; };
+  struct KT { int cls; int worker; double flops; cudaEvent_t a, b; };
+  int cur_worker = -1;  // worker of the item being enqueued (per-stage kernel statistics)
   std::vector<KT> kt;
   size_t kt_used = 0;
 };
@@ -193,6 +194,7 @@ int timed_gemm(pd_runtime* rt, int cls, int dtype, const void* A, int a_mn, int6
     }
     slot = &rt->kt[rt->kt_used++];
     slot->cls = cls;
+    slot->worker = rt->cur_worker;
     slot->flops = 2.0 * (double)M * (double)N * (double)K;
     PD_CHECK(cudaEventRecord(slot->a, st));
   }
@@ -234,6 +236,7 @@ int timed_call(pd_runtime* rt, int cls, cudaStream_t st, Fn&& fn) {
     }
     slot = &rt->kt[rt->kt_used++];
     slot->cls = cls;
+    slot->worker = rt->cur_worker;
     slot->flops = 0.0;
     PD_CHECK(cudaEventRecord(slot->a, st));
   }
@@ -377,6 +380,7 @@ int timed_conv(pd_runtime* rt, int cls, int pass, const void* act, const void* o
     }
     slot = &rt->kt[rt->kt_used++];
     slot->cls = cls;
+    slot->worker = rt->cur_worker;
     slot->flops = 2.0 * (double)n * h * w * 9.0 * cin * cout;
     PD_CHECK(cudaEventRecord(slot->a, st));
   }
@@ -1057,6 +1061,7 @@ static int run_body(pd_runtime* rt, cudaStream_t main, int trace) {
     cudaStream_t ST = stream_of(rt, S);
     const int op = it[PD_IT_OP], mb = it[PD_IT_MB];
     const bool fwd = op == 0;
+    rt->cur_worker = it[PD_IT_WORKER];
     const int dep = it[PD_IT_DEP], war = it[PD_IT_WAR];
     if (dep >= 0) PD_CHECK(cudaStreamWaitEvent(ST, rt->ev_end[dep], 0));
     if (war >= 0) PD_CHECK(cudaStreamWaitEvent(ST, rt->ev_end[war], 0));
@@ -1135,7 +1140,7 @@ int pd_rt_kernel_timing(pd_runtime* rt, int on) {
   return 0;
 }
 
-int pd_rt_kernel_stats(pd_runtime* rt, double* out9, int n_classes) {
+int pd_rt_kernel_stats(pd_runtime* rt, int worker, double* out9, int n_classes) {
   if (!rt || !out9 || n_classes < 1) return set_error(PD_ERR_INVALID, "pd_rt_kernel_stats: null argument");
   for (int i = 0; i < 3 * n_classes; ++i) out9[i] = 0.0;
   PD_CHECK(cudaSetDevice(rt->device));
@@ -1144,7 +1149,7 @@ int pd_rt_kernel_stats(pd_runtime* rt, double* out9, int n_classes) {
     float ms = 0.f;
     PD_CHECK(cudaEventSynchronize(k.b));
     PD_CHECK(cudaEventElapsedTime(&ms, k.a, k.b));
-    if (k.cls >= n_classes) continue;
+    if (k.cls >= n_classes || (worker >= 0 && k.worker != worker)) continue;
     out9[3 * k.cls + 0] += 1.0;
     out9[3 * k.cls + 1] += ms;
     out9[3 * k.cls + 2] += k.flops;

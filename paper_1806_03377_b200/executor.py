@@ -537,17 +537,19 @@ class Executor:
 
     KERNEL_CLASSES = ("fwd", "dgrad", "wgrad_sgd", "attention", "layernorm", "loss", "update", "other")
 
-    def kernel_stats(self) -> dict:
+    def kernel_stats(self, worker: int = -1) -> dict:
         """{class: launches, avg ms, algorithmic flops per launch, total ms} per kernel class
-        (GEMM passes fwd / dgrad / wgrad_sgd, then attention, layernorm, loss, update, other)."""
+        (GEMM passes fwd / dgrad / wgrad_sgd, then attention, layernorm, loss, update, other),
+        over all hosted workers or one (``worker``)."""
         n = len(self.KERNEL_CLASSES)
         buf = (ctypes.c_double * (3 * n))()
-        nat.check(nat.lib().pd_rt_kernel_stats(self._rt, buf, n), "pd_rt_kernel_stats")
+        nat.check(nat.lib().pd_rt_kernel_stats(self._rt, worker, buf, n), "pd_rt_kernel_stats")
         out = {}
         for i, name in enumerate(self.KERNEL_CLASSES):
             n, ms, fl = buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]
             if n:
-                out[name] = {"launches": int(n), "avg_ms": ms / n, "flops_per_launch": fl / n, "total_ms": ms}
+                out[name] = {"launches": int(n), "avg_ms": ms / n, "flops_per_launch": fl / n, "total_ms": ms,
+                             "total_flops": fl}
         return out
 
     def launch_count(self) -> int:
