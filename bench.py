@@ -271,10 +271,29 @@ def cpu_sample_gpt(args, seconds=12.0, max_minibatches=1):
                       f"(fwd+bwd+SGD, torch-CPU fp32 autograd oracle) in {el:.1f} s"}
 
 
+def _all_host_threads():
+    """Use every host core for the CPU arms even under torchrun (which exports OMP_NUM_THREADS=1)."""
+    n = os.cpu_count() or 1
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(limits=n)
+    except Exception:
+        pass
+    try:
+        import torch
+
+        torch.set_num_threads(n)
+    except Exception:
+        pass
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
     import numpy as np  # noqa: F401
+
+    _all_host_threads()
 
     cfg = workload(args)
     vgg = args.workload == "vgg"
@@ -484,6 +503,7 @@ def run_ours(args, rank, world):
         "steady_minibatches_per_s": rep.steady_throughput if rep else None,
     }
     if not args.no_cpu_baseline and world == 1:
+        _all_host_threads()
         out["cpu_baseline"] = (cpu_sample_vgg(args) if args.workload == "vgg" else
                                cpu_sample_gpt(args) if args.workload == "gpt" else cpu_sample(args))
     ex.close()
