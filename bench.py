@@ -274,6 +274,8 @@ def cpu_sample_gpt(args, seconds=12.0, max_minibatches=1):
 def _all_host_threads():
     """Use every host core for the CPU arms even under torchrun (which exports OMP_NUM_THREADS=1)."""
     n = os.cpu_count() or 1
+    import numpy  # noqa: F401  (load its BLAS before setting the pool size)
+
     try:
         from threadpoolctl import threadpool_limits
 
