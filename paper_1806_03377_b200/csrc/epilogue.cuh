@@ -40,6 +40,8 @@ struct EpiArgs {
   int64_t ldw;
   float lr;             // SGD
   void* aux;            // GELU: pre-activation output (activation dtype, ld = ldo)
+  int accumulate;       // GRADF32: red.add into out (zeroed by the caller) instead of storing;
+                        // split-K partials then all land in one buffer (runtime-internal)
 };
 
 // GPT-2's tanh GELU and its derivative.

@@ -420,7 +420,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               const float bcol = ep.bias ? ep.bias[col] : 0.f;
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
-                if (i < rows) *po = stg[i * 33 + lane] + bcol;
+                if (i < rows) {
+                  if (ep.accumulate) atomicAdd(po, stg[i * 33 + lane] + bcol);
+                  else *po = stg[i * 33 + lane] + bcol;
+                }
                 po += ep.ldo;
               }
             }
@@ -803,7 +806,7 @@ static int conv_launch(int pass, const void* act, const void* other, int n, int 
   if (kind != EPI_GRADF32) return set_error(PD_ERR_INVALID, "conv wgrad: GRADF32 epilogue only");
   const int M = pass == PD_CONV_WGRAD ? 9 * cin : cin;
   splitk_plan(M, cout, pix, &cv.splits, &cv.kb_per);
-  cv.split_stride = (int64_t)M * ep.ldo;
+  cv.split_stride = ep.accumulate ? 0 : (int64_t)M * ep.ldo;  // accumulate: every split adds into one buffer
   if (pass == PD_CONV_WGRAD) {
     cv.C = cin;
     return launch_tc<1, BN, true, true, EPI_GRADF32, SRC_CONV_WGRAD>(act, cin, other, cout, M, cout, pix, ep, st, cv);

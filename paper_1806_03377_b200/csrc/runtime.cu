@@ -765,13 +765,15 @@ int run_backward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
       EpiArgs ep{};
       ep.out = d.part;
       ep.ldo = y.c_out;
+      ep.accumulate = 1;  // splits red.add into one zeroed fp32 gradient (no partial round trip)
+      PD_CHECK(cudaMemsetAsync(d.part, 0, sizeof(float) * (size_t)M * y.c_out, ST));
       if (y.im2col)
         PD_TRY(timed_conv(rt, KC_WGRAD, PD_GEMM_WGRAD_SPLITK, Y.cols[act], dy, B, y.h, y.w, 64, y.c_out, EPI_GRADF32,
                           ep, ST));
       else
         PD_TRY(timed_conv(rt, KC_WGRAD, PD_CONV_WGRAD, X, dy, B, y.h, y.w, y.c_in, y.c_out, EPI_GRADF32, ep, ST));
       const int64_t n = (int64_t)M * y.c_out;
-      PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return reduce_sgd(d.dtype, d.part, splits, n, n, gW, S.w_master[l], ring_new, d.lr, ST); }));
+      PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return reduce_sgd(d.dtype, d.part, 1, n, n, gW, S.w_master[l], ring_new, d.lr, ST); }));
       PD_TRY(bias_grad_tall(dy, pix, y.c_out, d.part, gb, S.b_master[l], bring_new, d.lr, ST, d.sync));
       rt->launches += 3;
     }
