@@ -5,6 +5,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 
 #include "pd_internal.h"
 #include "ptx.cuh"
@@ -12,6 +13,19 @@
 namespace pd {
 
 static thread_local char g_err[1024] = {0};
+
+// Programmatic dependent launch is opt-in (PD_PDL=1): with several stage streams replayed from
+// one CUDA graph it measured slower (GPT-2: 290 vs 294 seq/s) and one run in five hung, so the
+// default launches fully serialized kernels.  The kernels keep their griddepcontrol.wait, which
+// returns at once for a normally launched grid.
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PD_PDL");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
 
 int set_error(int code, const char* fmt, ...) {
   va_list ap;

@@ -66,6 +66,9 @@ int flag_wait(const int* flag, int value, int* err_word, cudaStream_t st);
 
 // Launch with programmatic stream serialization (PDL): the kernel may be scheduled while its
 // stream predecessor drains; it must call griddep_wait() (ptx.cuh) before reading earlier results.
+// PD_PDL=1 in the environment enables programmatic dependent launch (default off, kernels.cu).
+bool pdl_enabled();
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {
@@ -78,7 +81,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   a[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = a;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
