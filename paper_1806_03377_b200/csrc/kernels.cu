@@ -66,8 +66,63 @@ __global__ void __launch_bounds__(512)
   }
 }
 
+// bf16 with cols % 64 == 0: block = 64 columns; 8 lanes x 16 B cover a row segment, 64 row lanes,
+// four independent 16-byte loads in flight per thread (a [2048 x 8192] gradient: 128 blocks).
+__global__ void __launch_bounds__(512)
+    k_bias_sgd_v(const __nv_bfloat16* __restrict__ dz, int rows, int64_t ld, float* __restrict__ bm,
+                 float* __restrict__ bo, float lr) {
+  __shared__ float part[64][65];
+  const int cl = threadIdx.x & 7, rl = threadIdx.x >> 3;  // column lane (8 cols), row lane (0..63)
+  const int64_t c0 = blockIdx.x * 64 + cl * 8;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int r = rl;
+  for (; r + 192 < rows; r += 256) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const uint4*>(dz + (int64_t)(r + 64 * u) * ld + c0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float a, b;
+        unpack_bf16x2(w[j], a, b);
+        acc[2 * j] += a;
+        acc[2 * j + 1] += b;
+      }
+    }
+  }
+  for (; r < rows; r += 64) {
+    const uint4 v = *reinterpret_cast<const uint4*>(dz + (int64_t)r * ld + c0);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float a, b;
+      unpack_bf16x2(w[j], a, b);
+      acc[2 * j] += a;
+      acc[2 * j + 1] += b;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) part[rl][cl * 8 + j] = acc[j];
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    float t = 0.f;
+    for (int g = 0; g < 64; ++g) t += part[g][threadIdx.x];
+    const int64_t c = blockIdx.x * 64 + threadIdx.x;
+    const float b = bm[c] - lr * t;
+    bm[c] = b;
+    bo[c] = b;
+  }
+}
+
 int bias_sgd(int dtype, const void* dz, int rows, int cols, int64_t ld, float* b_master, float* b_out, float lr,
              cudaStream_t st) {
+  if (dtype == PD_BF16 && cols % 64 == 0 && ld % 8 == 0 && (reinterpret_cast<uintptr_t>(dz) & 15) == 0) {
+    k_bias_sgd_v<<<cols / 64, 512, 0, st>>>(static_cast<const __nv_bfloat16*>(dz), rows, ld, b_master, b_out, lr);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "bias_sgd: %s", cudaGetErrorString(e));
+  }
   dim3 grid((cols + 31) / 32);
   if (dtype == PD_BF16)
     k_bias_sgd<__nv_bfloat16><<<grid, 512, 0, st>>>(static_cast<const __nv_bfloat16*>(dz), rows, cols, ld,
