@@ -201,7 +201,8 @@ typedef struct pd_stage_desc {
   float* logits;            /* PD_LOSS_CE: fp32 [batch, classes] */
   float* part;              /* fp32 scratch for split-K partials and column-sum blocks (size from
                                pd_layer_scratch_floats) */
-  int* sync;                /* 16 zeroed int32: self-resetting counters of single-launch reductions */
+  int* sync;                /* 16 zeroed int32: self-resetting counters of single-launch reductions ([0])
+                               and of the fused hand-off GEMMs ([8] forward, [9] backward) */
 } pd_stage_desc;
 
 enum pd_layer_kind { PD_LAYER_LINEAR = 0, PD_LAYER_CONV3 = 1, PD_LAYER_EMBED = 2, PD_LAYER_BLOCK = 3, PD_LAYER_HEAD = 4 };

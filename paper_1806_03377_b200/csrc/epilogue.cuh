@@ -42,6 +42,12 @@ struct EpiArgs {
   void* aux;            // GELU: pre-activation output (activation dtype, ld = ldo)
   int accumulate;       // GRADF32: red.add into out (zeroed by the caller) instead of storing;
                         // split-K partials then all land in one buffer (runtime-internal)
+  // Fused cross-process hand-off (runtime-internal, tcgen05 path): when sig_flag is set, every
+  // CTA fences its epilogue stores at system scope and bumps sig_counter; the last CTA resets the
+  // counter and st.release.sys's sig_value into sig_flag (the receiver's inbox flag).
+  int* sig_flag;
+  int sig_value;
+  int* sig_counter;
 };
 
 // GPT-2's tanh GELU and its derivative.

@@ -490,11 +490,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (lane_id() == 0 && lsum != 0.f) atomicAdd(ep.loss, 0.5f * ep.scale * lsum);
     }
   }
+  if (ep.sig_flag) __threadfence_system();  // this thread's payload stores, before the CTA's arrival
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::TMEM_COLS, CG>(tmem_base);
+  }
+  if (ep.sig_flag && threadIdx.x == 0) {
+    // fused hand-off: the last CTA to finish publishes the payload to the peer's inbox flag
+    __threadfence_system();
+    if (atomicAdd(ep.sig_counter, 1) == (int)gridDim.x - 1) {
+      *ep.sig_counter = 0;
+      __threadfence();
+      st_release_sys(ep.sig_flag, ep.sig_value);
+    }
   }
 }
 
@@ -871,6 +881,7 @@ static int simt(const void* A, int a_mn, int64_t lda, const void* B, int b_mn, i
 int gemm_simt(int dtype, const void* A, int a_mn, int64_t lda, const void* B, int b_mn, int64_t ldb, int M, int N,
               int K, int kind, const EpiArgs& ep, cudaStream_t st) {
   if (M <= 0 || N <= 0 || K <= 0) return set_error(PD_ERR_INVALID, "gemm: empty shape %dx%dx%d", M, N, K);
+  if (ep.sig_flag) return set_error(PD_ERR_INVALID, "gemm: fused hand-off needs the tcgen05 path");
   if (dtype == PD_F32) return simt<float>(A, a_mn, lda, B, b_mn, ldb, M, N, K, kind, ep, st);
   if (dtype == PD_BF16) return simt<__nv_bfloat16>(A, a_mn, lda, B, b_mn, ldb, M, N, K, kind, ep, st);
   return set_error(PD_ERR_INVALID, "unknown dtype %d", dtype);

@@ -11,6 +11,7 @@
 // the fused allreduce+SGD kernel) writes the committed version into its slot (simulator.py:315).
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <vector>
@@ -102,6 +103,7 @@ struct Stage {
   std::vector<const float*> target;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_done = nullptr;
+  bool fused_signal = false;  // this item's hand-off flag was released by the producing GEMM
 };
 
 struct View {
@@ -276,6 +278,26 @@ struct LayerTimer {
   }
 };
 
+// Compute + hand-off fusion: the GEMM whose epilogue stores a stage's payload into a remote
+// inbox also releases the receiver's inbox flag from its last CTA (EpiArgs::sig_flag), so no
+// separate signal kernel trails the GEMM and the receiver can start as soon as the stores land.
+// tcgen05 (bf16) path only; PD_FUSED_HANDOFF=0 falls back to the stand-alone signal kernel.
+bool fused_handoff_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PD_FUSED_HANDOFF");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+void fuse_handoff(pd_runtime* rt, Stage& S, EpiArgs& ep, int* flag, int mb, int counter) {
+  if (!flag || S.d.dtype != PD_BF16 || !S.d.sync || !fused_handoff_enabled()) return;
+  ep.sig_flag = flag;
+  ep.sig_value = flag_val(rt->epoch, mb);
+  ep.sig_counter = S.d.sync + counter;
+  S.fused_signal = true;
+}
+
 int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
   cudaStream_t ST = stream_of(rt, S);
   const pd_stage_desc& d = S.d;
@@ -301,8 +323,10 @@ int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.loss = d.loss + mb;
     } else {
       // the epilogue stores straight into the next stage's inbox slot (peer-mapped if remote)
-      ep.out = rt->views.at(it[PD_IT_DST]).act_in[it[PD_IT_OUT]];
+      const View& V = rt->views.at(it[PD_IT_DST]);
+      ep.out = V.act_in[it[PD_IT_OUT]];
       ep.relu = d.relu_last;
+      fuse_handoff(rt, S, ep, V.v.remote ? V.v.act_ready + it[PD_IT_OUT] : nullptr, it[PD_IT_MB], 8);
     }
     const void* W = S.w_ring[(size_t)l * d.ring_depth + wslot];
     PD_TRY(timed_gemm(rt, KC_FWD, d.dtype, x, 0, K, W, 0, K, B, N, K, kind, ep, ST));
@@ -339,6 +363,10 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.ldo = Kin;
       ep.mask = X;
       ep.ldm = Kin;
+      if (l == 0) {
+        const View& V = rt->views.at(it[PD_IT_DST]);
+        fuse_handoff(rt, S, ep, V.v.remote ? V.v.grad_ready + it[PD_IT_OUT] : nullptr, it[PD_IT_MB], 9);
+      }
       PD_TRY(timed_gemm(rt, KC_DGRAD, d.dtype, dz, 0, Nout, Wst, 1, Kin, B, Kin, Nout, EPI_MASK, ep, ST));
     }
     if (replicated) {
@@ -1076,13 +1104,14 @@ static int run_body(pd_runtime* rt, cudaStream_t main, int trace) {
     }
     if (rt->traced) PD_CHECK(cudaEventRecord(rt->ev_start[i], ST));
     const bool layered = !S.layers.empty();
+    S.fused_signal = false;
     if (op == 0) PD_TRY(layered ? run_forward_layers(rt, S, it) : run_forward(rt, S, it));
     else if (op == 1) PD_TRY(layered ? run_backward_layers(rt, S, it) : run_backward(rt, S, it));
     else PD_TRY(run_reduce(rt, S, it));
     // cross-process hand-off: publish the payload the epilogue stored into the peer inbox
     if ((op == 0 && !S.d.is_last) || (op == 1 && !S.d.is_first)) {
       const View& V = rt->views.at(it[PD_IT_DST]);
-      if (V.v.remote) PD_TRY(signal_flag(rt, S, (fwd ? V.v.act_ready : V.v.grad_ready) + it[PD_IT_OUT], mb));
+      if (V.v.remote && !S.fused_signal) PD_TRY(signal_flag(rt, S, (fwd ? V.v.act_ready : V.v.grad_ready) + it[PD_IT_OUT], mb));
     }
     if (op == 1) {  // my inbox slots are free again: tell producers in other processes
       if (!S.d.is_first && S.d.remote_prev) PD_TRY(signal_flag(rt, S, S.d.act_ack + it[PD_IT_XSLOT], mb));
