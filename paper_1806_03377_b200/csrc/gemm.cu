@@ -36,7 +36,11 @@ namespace pd {
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;           // 64 bf16 = 128 B = one swizzle row
 constexpr int TC_EPI_WARPS = 8;     // two warps per TMEM lane quadrant, each owning half the columns
-constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;  // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2.. epilogue
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
+#ifndef PD_SGD_BUF
+#define PD_SGD_BUF 1
+#endif
+constexpr int TC_SGD_BUF = PD_SGD_BUF;  // fp32 master blocks in flight per SGD epilogue warp  // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2.. epilogue
 constexpr int TC_ACC_STRIDE = 256;  // TMEM columns between the two accumulator buffers
 
 // fp32-output epilogues (SGD update of the fp32 master, raw fp32 gradient) stage each warp's
@@ -56,9 +60,11 @@ struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
   static constexpr int B_BYTES = BNL * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  // SGD: per epilogue warp two TMA-fed 32x32 fp32 master blocks (4 KB each, 128B-swizzled);
+  // SGD: per epilogue warp TC_SGD_BUF TMA-fed 32x32 fp32 master blocks (4 KB each, 128B-swizzled;
+  // one is best: 2048x8192x8192 wgrad+SGD 246 / 252 / 271 / 294 us with 1 / 2 / 3 / 4, as the
+  // smem is worth more as operand stages: 6 / 5 / 4 / 3);
   // GRADF32: per warp a padded 32x33 transpose block.
-  static constexpr int STG_BYTES = KIND == EPI_SGD ? TC_EPI_WARPS * 2 * 4096
+  static constexpr int STG_BYTES = KIND == EPI_SGD ? TC_EPI_WARPS * TC_SGD_BUF * 4096
                                  : (KIND == EPI_GRADF32 ? TC_EPI_WARPS * TC_STG_FLOATS * 4 : 0);
   static constexpr int PIPE_BUDGET = 227 * 1024 - 2048 - STG_BYTES;  // all of the 227 KB opt-in smem
   static constexpr int STAGES = PIPE_BUDGET / STAGE_BYTES > 8 ? 8 : PIPE_BUDGET / STAGE_BYTES;
@@ -66,7 +72,9 @@ struct TcCfg {
   static constexpr int BAR_BYTES = 1024;  // mbarriers + TMEM slot, keeps the epilogue region 1 KB aligned
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + BAR_BYTES + STG_BYTES;
   static_assert(BN % 32 == 0 && BN % (16 * CG) == 0 && BN <= 256, "BN");
-  static_assert(!B_MN || B_ROWS % 64 == 0, "MN-major B needs whole 64-wide atoms per CTA");
+  // MN-major B is staged as whole 64-wide swizzle atoms; a partial last atom (BN=224: 112 rows per
+  // CTA = 64 + 48) is loaded in full and the MMA reads only its first B_ROWS % 64 columns
+  static_assert(!B_MN || B_ROWS % 16 == 0, "MN-major B rows per CTA");
 };
 
 template <int CG, int BN, bool A_MN, bool B_MN, int KIND, int SRC = SRC_2D>
@@ -143,7 +151,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], CG); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tmem_full[a], 1); mbar_init(&tmem_empty[a], CG * TC_EPI_WARPS); }
     if constexpr (KIND == EPI_SGD)
-      for (int i = 0; i < 2 * TC_EPI_WARPS; ++i) mbar_init(&epi_bar[i], 1);
+      for (int i = 0; i < TC_SGD_BUF * TC_EPI_WARPS; ++i) mbar_init(&epi_bar[i], 1);
     fence_barrier_init();
     fence_proxy_async_smem();
   }
@@ -264,8 +272,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if constexpr (KIND == EPI_SGD) {
     // ---------------- wgrad + SGD epilogue.  Each warp owns 32 accumulator rows (its TMEM lane
     // quadrant) and half of the tile's 32-column chunks.  The fp32 master block of a chunk
-    // (32x32, 4 KB) is TMA-loaded into a 128B-swizzled smem buffer ahead of use (double
-    // buffered, issued before the tile's accumulator is ready), updated in place
+    // (32x32, 4 KB) is TMA-loaded into a 128B-swizzled smem buffer ahead of use (TC_SGD_BUF
+    // deep, the first issued before the tile's accumulator is ready), updated in place
     // (w = m - lr*acc), TMA-stored back, and the bf16 version copy is written from registers.
     // HBM sees only bulk, fully coalesced master traffic.
     const int q = warp & 3;
@@ -274,10 +282,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int c_begin = half ? (NC + 1) / 2 : 0;
     const int c_end = half ? NC : (NC + 1) / 2;
     const int e = warp - 2;
-    uint8_t* buf0 = epi_smem + e * 2 * 4096;
-    uint64_t* bars = epi_bar + 2 * e;
+    uint8_t* buf0 = epi_smem + e * TC_SGD_BUF * 4096;
+    uint64_t* bars = epi_bar + TC_SGD_BUF * e;
     const int lane = lane_id();
-    uint32_t bar_phase[2] = {0, 0};
+    uint32_t bar_phase = 0;  // bit b: parity of buffer b's next load
     // the master stream (read once, written once) must not evict the L2-resident operands
     const uint64_t stream_pol = l2_policy_evict_first();
     int acc = 0;
@@ -291,7 +299,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // prefetch the first two master blocks of this tile while its MMAs are still running
       if (lane == 0) {
         bulk_wait_read0();  // previous tile's stores have finished reading both buffers
-        for (int i = 0; i < 2 && i < nck; ++i) {
+        for (int i = 0; i < TC_SGD_BUF && i < nck; ++i) {
           mbar_arrive_expect_tx(&bars[i], 4096);
           tma_load_2d_hint(buf0 + i * 4096, &tmW, &bars[i], n0 + (c_begin + i) * 32, row0, stream_pol);
         }
@@ -300,11 +308,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_after();
 #pragma unroll 1
       for (int i = 0; i < nck; ++i) {
-        const int c = c_begin + i, b = i & 1;
+        const int c = c_begin + i, b = i % TC_SGD_BUF;
         float v[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * TC_ACC_STRIDE + c * 32, v);
-        mbar_wait(&bars[b], bar_phase[b]);
-        bar_phase[b] ^= 1;
+        mbar_wait(&bars[b], (bar_phase >> b) & 1);
+        bar_phase ^= 1u << b;
         // row `lane` of the block: 16-byte chunk j sits at position j ^ (lane & 7) (SWIZZLE_128B)
         float4* row = reinterpret_cast<float4*>(buf0 + b * 4096 + lane * 128);
         uint32_t packed[16];
@@ -325,7 +333,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + r * ep.ldo + col0);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
-              o[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+              st_stream_v4(o + j, make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]),
+                           stream_pol);  // the version copy is next read many kernels later
           } else {
             for (int j = 0; j < 32 && col0 + j < N; ++j) {
               float a, bb;
@@ -339,10 +348,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (lane == 0) {
           tma_store_2d_hint(&tmW, buf0 + b * 4096, col0, row0, stream_pol);  // TMA clips rows/cols outside [M, N)
           bulk_commit();
-          if (i + 2 < nck) {
+          if (i + TC_SGD_BUF < nck) {
             bulk_wait_read0();  // this buffer's store has read the smem block
             mbar_arrive_expect_tx(&bars[b], 4096);
-            tma_load_2d_hint(buf0 + b * 4096, &tmW, &bars[b], n0 + (c + 2) * 32, row0, stream_pol);
+            tma_load_2d_hint(buf0 + b * 4096, &tmW, &bars[b], n0 + (c + TC_SGD_BUF) * 32, row0, stream_pol);
           }
         }
         __syncwarp();
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(&tmem_empty[acc], 0); else mbar_arrive(&tmem_empty[acc]);
+        if constexpr (CG == 2) mbar_arrive_cluster_relaxed(&tmem_empty[acc], 0); else mbar_arrive(&tmem_empty[acc]);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
@@ -436,7 +445,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(&tmem_empty[acc], 0); else mbar_arrive(&tmem_empty[acc]);
+        if constexpr (CG == 2) mbar_arrive_cluster_relaxed(&tmem_empty[acc], 0); else mbar_arrive(&tmem_empty[acc]);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
@@ -480,7 +489,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(&tmem_empty[acc], 0); else mbar_arrive(&tmem_empty[acc]);
+        if constexpr (CG == 2) mbar_arrive_cluster_relaxed(&tmem_empty[acc], 0); else mbar_arrive(&tmem_empty[acc]);
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
@@ -712,7 +721,6 @@ static void pick_cfg(int M, int N, bool b_mn, int* cg, int* bn) {
     if (g_force_cg && c != g_force_cg) continue;
     if (c == 2 && M <= TC_BM) continue;  // a single 128-row tile gains nothing from a pair
     for (int b : {256, 224}) {
-      if (b_mn && b != 256) continue;  // MN-major B is staged in whole 64-wide atoms
       const long units = (long)((M + TC_BM * c - 1) / (TC_BM * c)) * ((N + b - 1) / b);
       const long slots = sms / c;
       const long cost = ((units + slots - 1) / slots) * b * (c == 2 ? 2 : 1) * 100 / (c == 2 ? 205 : 100);
@@ -739,14 +747,10 @@ static int launch_bn(const void* A, int64_t lda, const void* B, int64_t ldb, int
   int cg, bn;
   pick_cfg(M, N, B_MN, &cg, &bn);
   if (cg == 2) {
-    if (bn == 224) {
-      if constexpr (!B_MN) return launch_tc<2, 224, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
-    }
+    if (bn == 224) return launch_tc<2, 224, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
     return launch_tc<2, 256, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
   }
-  if (bn == 224) {
-    if constexpr (!B_MN) return launch_tc<1, 224, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
-  }
+  if (bn == 224) return launch_tc<1, 224, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
   return launch_tc<1, 256, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
 }
 
