@@ -61,6 +61,65 @@ PD_DEVICE float fast_exp2(float x) {
   return y;
 }
 
+constexpr float RESCALE_LOG2 = 8.f;  // forward: rescale O only when the running max grows by > 2^8
+
+// Row max over 64 S values (raw scores); MASK: only columns base+i <= lim count.  The unmasked form
+// keeps four independent chains (3-input FMNMX).
+template <bool MASK>
+PD_DEVICE float row_max64(const uint32_t (&sr)[64], int base, int lim, float mx) {
+  if constexpr (MASK) {
+#pragma unroll
+    for (int i = 0; i < 64; ++i)
+      if (base + i <= lim) mx = fmaxf(mx, __uint_as_float(sr[i]));
+    return mx;
+  } else {
+    float a = mx, b = -INFINITY, c = -INFINITY, d = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < 64; i += 8) {
+      a = fmaxf(a, fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])));
+      b = fmaxf(b, fmaxf(__uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3])));
+      c = fmaxf(c, fmaxf(__uint_as_float(sr[i + 4]), __uint_as_float(sr[i + 5])));
+      d = fmaxf(d, fmaxf(__uint_as_float(sr[i + 6]), __uint_as_float(sr[i + 7])));
+    }
+    return fmaxf(fmaxf(a, b), fmaxf(c, d));
+  }
+}
+
+// p = exp2(s*scale + neg) for 64 scores -> 32 packed bf16 pairs; returns the fp32 sum.  The
+// unmasked form computes s*scale + neg two at a time (FFMA2) and sums with FADD2.
+template <bool MASK>
+PD_DEVICE float exp_pack64(const uint32_t (&sr)[64], int base, int lim, float scale, float neg, uint32_t (&pk)[32]) {
+  if constexpr (MASK) {
+    float rs = 0.f;
+#pragma unroll
+    for (int i = 0; i < 64; i += 2) {
+      float p0 = fast_exp2(fmaf(__uint_as_float(sr[i]), scale, neg));
+      float p1 = fast_exp2(fmaf(__uint_as_float(sr[i + 1]), scale, neg));
+      if (base + i > lim) p0 = 0.f;
+      if (base + i + 1 > lim) p1 = 0.f;
+      rs += p0 + p1;
+      pk[i / 2] = pack_bf16x2(p0, p1);
+    }
+    return rs;
+  } else {
+    const float2 sc = make_float2(scale, scale), ng = make_float2(neg, neg);
+    float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;
+#pragma unroll
+    for (int i = 0; i < 64; i += 4) {
+      const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])), sc, ng);
+      const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3])), sc, ng);
+      const float2 p0 = make_float2(fast_exp2(x0.x), fast_exp2(x0.y));
+      const float2 p1 = make_float2(fast_exp2(x1.x), fast_exp2(x1.y));
+      acc0 = __fadd2_rn(acc0, p0);
+      acc1 = __fadd2_rn(acc1, p1);
+      pk[i / 2] = pack_bf16x2(p0.x, p0.y);
+      pk[i / 2 + 1] = pack_bf16x2(p1.x, p1.y);
+    }
+    const float2 t = __fadd2_rn(acc0, acc1);
+    return t.x + t.y;
+  }
+}
+
 // Byte offset of (row, 16-byte chunk) of a 128B-swizzled tile (the TMA / UMMA SW128 pattern).
 PD_DEVICE uint32_t sw128(int row, int chunk) { return row * 128 + ((chunk ^ (row & 7)) << 4); }
 
@@ -178,8 +237,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
       tc_fence_after();
       const bool diag = j == qt;
       // two passes over the S row in TMEM, 64 columns (two loads, one wait) at a time, so the
-      // softmax warps stay within the register budget of two CTAs per SM
-      const int lim = diag ? q - j * TK : TK;  // causal: keys j*TK + i > q are masked
+      // softmax warps stay within the register budget of two CTAs per SM.  Only the diagonal tile
+      // carries the causal mask (keys j*TK + i > q); the others run the unmasked, packed path.
+      const int lim = diag ? q - j * TK : TK;
       float mx = -INFINITY;
 #pragma unroll 1
       for (int h2 = 0; h2 < 2; ++h2) {
@@ -187,16 +247,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
         tmem_ld_32x32b_x32_nowait(tS + lane_base + h2 * 64, *reinterpret_cast<uint32_t(*)[32]>(sr));
         tmem_ld_32x32b_x32_nowait(tS + lane_base + h2 * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
         tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 64; ++i)
-          if (h2 * 64 + i <= lim) mx = fmaxf(mx, __uint_as_float(sr[i]));
+        mx = diag ? row_max64<true>(sr, h2 * 64, lim, mx) : row_max64<false>(sr, 0, 0, mx);
       }
       const float m_new = fmaxf(m, mx * scale_log2);  // scale > 0: max commutes with it
-      const float alpha = m == -INFINITY ? 0.f : fast_exp2(m - m_new);
       if (j > 0) mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} finished: O final for j-1, P free
       tc_fence_after();
-      // rescale the O row when the running max moved (warp-uniform decision)
-      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+      // Lazy rescaling: keep the stale running max (exponents up to 2^RESCALE_LOG2, exact in fp32
+      // and bf16 range) unless some row of the warp moved by more than that; then the warp
+      // rescales its O rows in TMEM and l.  m only has to be consistent between O, l and lse.
+      if (j == 0) {
+        m = m_new;
+      } else if (__any_sync(0xffffffffu, m_new > m + RESCALE_LOG2)) {
+        const float alpha = fast_exp2(m - m_new);
 #pragma unroll
         for (int c = 0; c < HDIM / 32; ++c) {
           float o[32];
@@ -205,10 +267,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
           for (int i = 0; i < 32; ++i) o[i] *= alpha;
           tmem_st_32x32b_x32(tO + lane_base + c * 32, o);
         }
+        l *= alpha;
+        m = m_new;
       }
-      // P = exp2(s*scale - m_new) -> bf16 -> smem (K-major SW128; 64-key atom h2)
+      // P = exp2(s*scale - m) -> bf16 -> smem (K-major SW128; 64-key atom h2)
       float rs = 0.f;
-      const float neg = -m_new;
+      const float neg = -m;
 #pragma unroll 1
       for (int h2 = 0; h2 < 2; ++h2) {
         uint32_t sr[64];
@@ -216,23 +280,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
         tmem_ld_32x32b_x32_nowait(tS + lane_base + h2 * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
         tmem_wait_ld();
         uint32_t pk[32];
-#pragma unroll
-        for (int i = 0; i < 64; i += 2) {
-          float p0 = fast_exp2(fmaf(__uint_as_float(sr[i]), scale_log2, neg));
-          float p1 = fast_exp2(fmaf(__uint_as_float(sr[i + 1]), scale_log2, neg));
-          if (h2 * 64 + i > lim) p0 = 0.f;
-          if (h2 * 64 + i + 1 > lim) p1 = 0.f;
-          rs += p0 + p1;
-          pk[i / 2] = pack_bf16x2(p0, p1);
-        }
+        rs += diag ? exp_pack64<true>(sr, h2 * 64, lim, scale_log2, neg, pk)
+                   : exp_pack64<false>(sr, 0, 0, scale_log2, neg, pk);
         uint8_t* atom = sP + h2 * TILE_BYTES;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           *reinterpret_cast<uint4*>(atom + sw128(r, u)) =
               make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
       }
-      l = l * alpha + rs;
-      m = m_new;
+      l += rs;
       fence_proxy_async_shared();  // P (generic-proxy stores) -> visible to the tensor core
       tc_fence_before();
       __syncwarp();
@@ -270,6 +326,40 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
 //               into shared memory (K-major over queries), and the previous tile's dQ rows out
 //               of TMEM into the fp32 dq_acc with 16-byte vector atomics.
 constexpr int BWD_THREADS = 192;
+
+// One 32-query chunk of a key row: P^T = exp2(S^T*scale - lse), dS^T = P^T (dP^T - D) -> bf16 pairs.
+// nlse holds -lse.  MASK (diagonal tile only): queries q0+i < key are causal-masked.  The unmasked
+// form runs two elements per FFMA2 / FMUL2.
+template <bool MASK>
+PD_DEVICE void bwd_chunk32(const uint32_t (&svr)[32], const uint32_t (&dpr)[32], const float* nlse, const float* Dd,
+                           int q0, int key, float scale, uint32_t (&pk)[16], uint32_t (&dk)[16]) {
+  const float* sv = reinterpret_cast<const float*>(svr);
+  const float* dp = reinterpret_cast<const float*>(dpr);
+  const float4* L4 = reinterpret_cast<const float4*>(nlse);
+  const float4* D4 = reinterpret_cast<const float4*>(Dd);
+  const float2 sc = make_float2(scale, scale), m1 = make_float2(-1.f, -1.f);
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) {
+    const float4 lv = L4[i / 4], dv = D4[i / 4];
+    const float2 x0 = __ffma2_rn(make_float2(sv[i], sv[i + 1]), sc, make_float2(lv.x, lv.y));
+    const float2 x1 = __ffma2_rn(make_float2(sv[i + 2], sv[i + 3]), sc, make_float2(lv.z, lv.w));
+    float2 p0 = make_float2(fast_exp2(x0.x), fast_exp2(x0.y));
+    float2 p1 = make_float2(fast_exp2(x1.x), fast_exp2(x1.y));
+    if constexpr (MASK) {
+      if (q0 + i < key) p0.x = 0.f;
+      if (q0 + i + 1 < key) p0.y = 0.f;
+      if (q0 + i + 2 < key) p1.x = 0.f;
+      if (q0 + i + 3 < key) p1.y = 0.f;
+    }
+    const float2 t0 = __ffma2_rn(make_float2(dv.x, dv.y), m1, make_float2(dp[i], dp[i + 1]));  // dP - D
+    const float2 t1 = __ffma2_rn(make_float2(dv.z, dv.w), m1, make_float2(dp[i + 2], dp[i + 3]));
+    const float2 d0 = __fmul2_rn(p0, t0), d1 = __fmul2_rn(p1, t1);
+    pk[i / 2] = pack_bf16x2(p0.x, p0.y);
+    pk[i / 2 + 1] = pack_bf16x2(p1.x, p1.y);
+    dk[i / 2] = pack_bf16x2(d0.x, d0.y);
+    dk[i / 2 + 1] = pack_bf16x2(d1.x, d1.y);
+  }
+}
 struct BwdSmem {
   static constexpr int K = 0;
   static constexpr int V = K + TILE_BYTES;
@@ -301,6 +391,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint8_t* sdS = smem + BwdSmem::DS;
   float* sLD = reinterpret_cast<float*>(smem + BwdSmem::LD);
   float* sDQ = reinterpret_cast<float*>(smem + BwdSmem::DQ);
+  float* sLn = sLD;  // written once per tile by the compute warps (lse -> -lse)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BwdSmem::BAR);
   uint64_t* full_kv = bar + 0;
   uint64_t* full_qdo = bar + 1;   // [2]
@@ -428,7 +519,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     for (int n = 0; n < N; ++n) {
       const int qt = kt + n;
       const int par = n & 1;  // stage of this query tile's Q / dO / lse / D buffers
-      const float* sL = sLD + par * 256;
+      const float* sL = sLD + par * 256;  // -lse after the in-place negation below
       const float* sDd = sL + 128;
       if (n > 0) {  // MMAs of n-1 are done: flush their dQ while S^T / dP^T of n run on the tensor core
         mbar_wait(dq_full, (n - 1) & 1);
@@ -440,6 +531,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       }
       mbar_wait(sdp_full, n & 1);  // implies the stage's TMA (incl. lse / D) has landed
       tc_fence_after();
+      // negate this tile's lse once in smem (thread t: entry t) so the exponent is one FFMA2
+      sLn[par * 256 + t] = -sLn[par * 256 + t];
+      named_sync_128();
       const bool diag = n == 0;
 #pragma unroll 1
       for (int c = 0; c < TQ / 32; ++c) {
@@ -447,28 +541,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         tmem_ld_32x32b_x32_nowait(tS + lane_base + c * 32, svr);
         tmem_ld_32x32b_x32_nowait(tP + lane_base + c * 32, dpr);
         tmem_wait_ld();
-        const float* sv = reinterpret_cast<const float*>(svr);
-        const float* dp = reinterpret_cast<const float*>(dpr);
         uint32_t pk[16], dk[16];
-        const float4* L4 = reinterpret_cast<const float4*>(sL + c * 32);
-        const float4* D4 = reinterpret_cast<const float4*>(sDd + c * 32);
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 lv = L4[i / 4], dv = D4[i / 4];
-          const float ls[4] = {lv.x, lv.y, lv.z, lv.w}, ds[4] = {dv.x, dv.y, dv.z, dv.w};
-          float pp[4], dd[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float p = fast_exp2(fmaf(sv[i + e], scale_log2, -ls[e]));
-            if (diag && qt * TQ + c * 32 + i + e < key) p = 0.f;
-            pp[e] = p;
-            dd[e] = p * (dp[i + e] - ds[e]);
-          }
-          pk[i / 2] = pack_bf16x2(pp[0], pp[1]);
-          pk[i / 2 + 1] = pack_bf16x2(pp[2], pp[3]);
-          dk[i / 2] = pack_bf16x2(dd[0], dd[1]);
-          dk[i / 2 + 1] = pack_bf16x2(dd[2], dd[3]);
-        }
+        if (diag) bwd_chunk32<true>(svr, dpr, sL + c * 32, sDd + c * 32, qt * TQ + c * 32, key, scale_log2, pk, dk);
+        else bwd_chunk32<false>(svr, dpr, sL + c * 32, sDd + c * 32, 0, 0, scale_log2, pk, dk);
         const int atom = (c >> 1) * TILE_BYTES;
         const int chunk0 = (c & 1) * 4;
 #pragma unroll
