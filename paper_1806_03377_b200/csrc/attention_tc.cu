@@ -322,10 +322,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
 //   MMA warp:   S^T = K Q^T, dP^T = V dO^T (M = keys, N = queries, K = 64)
 //               dV += P^T dO, dK += dS^T Q  (M = keys, N = 64, K = queries)
 //               dQ  = dS K                  (M = queries, N = 64, K = keys; A = dS^T read MN-major)
-//   warps 2-5:  thread = TMEM lane: P^T = exp2(S^T*scale - lse), dS^T = P^T (dP^T - D) -> bf16
+//   warps 2-9:  thread = TMEM lane, two warps per lane quadrant splitting the 128 query columns (and
+//               the 64 dQ / dK / dV columns) so two compute warps per SM sub-partition hide each
+//               other's latency: P^T = exp2(S^T*scale - lse), dS^T = P^T (dP^T - D) -> bf16
 //               into shared memory (K-major over queries), and the previous tile's dQ rows out
 //               of TMEM into the fp32 dq_acc with 16-byte vector atomics.
-constexpr int BWD_THREADS = 192;
+constexpr int BWD_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 compute (two per TMEM lane quadrant)
 
 // One 32-query chunk of a key row: P^T = exp2(S^T*scale - lse), dS^T = P^T (dP^T - D) -> bf16 pairs.
 // nlse holds -lse.  MASK (diagonal tile only): queries q0+i < key are causal-masked.  The unmasked
@@ -373,7 +375,7 @@ struct BwdSmem {
   static constexpr int TOTAL = BAR + 256 + 1024;
 };
 
-PD_DEVICE void named_sync_128() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+PD_DEVICE void named_sync_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }  // the 8 compute warps
 
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     k_attn_bwd_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
@@ -399,7 +401,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint64_t* sdp_full = bar + 5;
   uint64_t* pds_ready = bar + 6;
   uint64_t* dq_full = bar + 7;
-  uint64_t* dq_free = bar + 8;
+  uint64_t* sdp_free = bar + 8;  // compute warps have read S^T / dP^T of the current tile
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
 
   const int n_t = S / TK;
@@ -416,9 +418,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     mbar_init(full_kv, 1);
     for (int i = 0; i < 2; ++i) { mbar_init(&full_qdo[i], 1); mbar_init(&empty_qdo[i], 1); }
     mbar_init(sdp_full, 1);
-    mbar_init(pds_ready, 4);
+    mbar_init(pds_ready, 8);
     mbar_init(dq_full, 1);
-    mbar_init(dq_free, 4);
+    mbar_init(sdp_free, 8);
     fence_barrier_init();
     fence_proxy_async_smem();
   }
@@ -452,8 +454,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       constexpr uint32_t idesc_kv = make_idesc_bf16(TK, HDIM, false, true);     // dV, dK
       constexpr uint32_t idesc_q = make_idesc_bf16(TQ, HDIM, true, true);       // dQ (A = dS^T MN-major)
       const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), p_addr = smem_u32(sP), ds_addr = smem_u32(sdS);
-      mbar_wait(full_kv, 0);
-      for (int n = 0; n < N; ++n) {
+      // S^T / dP^T of tile n+1 are issued as soon as the compute warps have read tile n's (sdp_free),
+      // so they run under the compute warps' dQ flush and P / dS stores; dV / dK / dQ of tile n
+      // then run under the compute warps' exp / dS math of tile n+1.
+      auto issue_sdp = [&](int n) {
         const int st = n & 1;
         const uint32_t q_addr = smem_u32(sQ + st * TILE_BYTES), do_addr = smem_u32(sdO + st * TILE_BYTES);
         mbar_wait(&full_qdo[st], (n >> 1) & 1);
@@ -466,8 +470,15 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
                     idesc_sq, k != 0);
         }
         umma_commit(sdp_full);
-        mbar_wait(pds_ready, n & 1);
-        if (n > 0) mbar_wait(dq_free, (n - 1) & 1);
+      };
+      mbar_wait(full_kv, 0);
+      issue_sdp(0);
+      for (int n = 0; n < N; ++n) {
+        const int st = n & 1;
+        const uint32_t q_addr = smem_u32(sQ + st * TILE_BYTES), do_addr = smem_u32(sdO + st * TILE_BYTES);
+        mbar_wait(sdp_free, n & 1);  // S^T / dP^T of n are in the compute warps' registers
+        if (n + 1 < N) issue_sdp(n + 1);
+        mbar_wait(pds_ready, n & 1);  // P^T / dS^T of n in smem, dQ of n-1 flushed out of TMEM
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < TQ / 16; ++k) {
@@ -487,32 +498,31 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     }
   } else {
     const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;         // warps 2-5: query columns 0..63, warps 6-9: 64..127
     const int r = 32 * quad + lane_id();      // TMEM lane: key row (S^T, dP^T, dK, dV) / query row (dQ)
     const int key = kt * TK + r;
     const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
-    const int t = threadIdx.x - 64;           // 0..127 within the compute warps
+    const int t = threadIdx.x - 64;           // 0..255 within the compute warps
     // dQ rows of a query tile: TMEM -> staging smem (row r, 16-byte chunks in a per-thread rotated
     // order against bank conflicts) -> one TMA reduce-add of the 128 x 64 fp32 box into dq_acc.
     auto flush_dq = [&](int qt) {
-      uint32_t v0[32], v1[32];
-      tmem_ld_32x32b_x32_nowait(tdQ + lane_base, v0);
-      tmem_ld_32x32b_x32_nowait(tdQ + lane_base + 32, v1);
+      // this warp's 32 dQ columns (half) of its 32 rows
+      uint32_t v0[32];
+      tmem_ld_32x32b_x32_nowait(tdQ + lane_base + half * 32, v0);
       tmem_wait_ld();
       if (t == 0) bulk_wait_read0();  // the previous reduce has finished reading the staging
-      named_sync_128();
+      named_sync_compute();
       // two [128][32] fp32 halves, 128B-swizzled (chunk c of row r at c ^ (r & 7)): conflict-free
       uint8_t* st0 = reinterpret_cast<uint8_t*>(sDQ);
-      uint8_t* st1 = st0 + 128 * 128;
+      uint8_t* sth = st0 + half * 128 * 128;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        *reinterpret_cast<uint4*>(st0 + sw128(r, c)) = make_uint4(v0[4 * c], v0[4 * c + 1], v0[4 * c + 2], v0[4 * c + 3]);
-        *reinterpret_cast<uint4*>(st1 + sw128(r, c)) = make_uint4(v1[4 * c], v1[4 * c + 1], v1[4 * c + 2], v1[4 * c + 3]);
-      }
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<uint4*>(sth + sw128(r, c)) = make_uint4(v0[4 * c], v0[4 * c + 1], v0[4 * c + 2], v0[4 * c + 3]);
       fence_proxy_async_shared();
-      named_sync_128();
+      named_sync_compute();
       if (t == 0) {
         tma_reduce_add_2d(&tm_dq, st0, h * HDIM, row0 + qt * TQ);
-        tma_reduce_add_2d(&tm_dq, st1, h * HDIM + 32, row0 + qt * TQ);
+        tma_reduce_add_2d(&tm_dq, st0 + 128 * 128, h * HDIM + 32, row0 + qt * TQ);
         bulk_commit();
       }
     };
@@ -521,37 +531,42 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const int par = n & 1;  // stage of this query tile's Q / dO / lse / D buffers
       const float* sL = sLD + par * 256;  // -lse after the in-place negation below
       const float* sDd = sL + 128;
-      if (n > 0) {  // MMAs of n-1 are done: flush their dQ while S^T / dP^T of n run on the tensor core
-        mbar_wait(dq_full, (n - 1) & 1);
-        tc_fence_after();
-        flush_dq(qt - 1);
-        tc_fence_before();
-        __syncwarp();
-        if (lane_id() == 0) mbar_arrive(dq_free);
-      }
       mbar_wait(sdp_full, n & 1);  // implies the stage's TMA (incl. lse / D) has landed
       tc_fence_after();
       // negate this tile's lse once in smem (thread t: entry t) so the exponent is one FFMA2
-      sLn[par * 256 + t] = -sLn[par * 256 + t];
-      named_sync_128();
+      if (t < TQ) sLn[par * 256 + t] = -sLn[par * 256 + t];
+      named_sync_compute();
       const bool diag = n == 0;
-#pragma unroll 1
-      for (int c = 0; c < TQ / 32; ++c) {
+      uint32_t pk[2][16], dk[2][16];
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {  // this warp's two 32-query chunks
+        const int c = 2 * half + cc;
         uint32_t svr[32], dpr[32];
         tmem_ld_32x32b_x32_nowait(tS + lane_base + c * 32, svr);
         tmem_ld_32x32b_x32_nowait(tP + lane_base + c * 32, dpr);
         tmem_wait_ld();
-        uint32_t pk[16], dk[16];
-        if (diag) bwd_chunk32<true>(svr, dpr, sL + c * 32, sDd + c * 32, qt * TQ + c * 32, key, scale_log2, pk, dk);
-        else bwd_chunk32<false>(svr, dpr, sL + c * 32, sDd + c * 32, 0, 0, scale_log2, pk, dk);
+        if (diag) bwd_chunk32<true>(svr, dpr, sL + c * 32, sDd + c * 32, qt * TQ + c * 32, key, scale_log2, pk[cc], dk[cc]);
+        else bwd_chunk32<false>(svr, dpr, sL + c * 32, sDd + c * 32, 0, 0, scale_log2, pk[cc], dk[cc]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(sdp_free);  // the tensor core may overwrite S^T / dP^T now
+      if (n > 0) {  // dV / dK / dQ of n-1 are done: P / dS smem is free, flush dQ of n-1
+        mbar_wait(dq_full, (n - 1) & 1);
+        tc_fence_after();
+        flush_dq(qt - 1);
+      }
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c = 2 * half + cc;
         const int atom = (c >> 1) * TILE_BYTES;
         const int chunk0 = (c & 1) * 4;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           *reinterpret_cast<uint4*>(sP + atom + sw128(r, chunk0 + u)) =
-              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+              make_uint4(pk[cc][4 * u], pk[cc][4 * u + 1], pk[cc][4 * u + 2], pk[cc][4 * u + 3]);
           *reinterpret_cast<uint4*>(sdS + atom + sw128(r, chunk0 + u)) =
-              make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+              make_uint4(dk[cc][4 * u], dk[cc][4 * u + 1], dk[cc][4 * u + 2], dk[cc][4 * u + 3]);
         }
       }
       fence_proxy_async_shared();
@@ -565,8 +580,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     if (t == 0) bulk_wait_all0();  // the last reduce-add has completed before the CTA exits
     // dK (scaled) and dV rows of this thread's key into the k / v slices of dqkv
     __nv_bfloat16* row = dqkv + ((int64_t)row0 + key) * 3 * D;
-#pragma unroll
-    for (int c = 0; c < HDIM / 32; ++c) {
+    {
+      const int c = half;  // this warp's 32 of the 64 head dims
       float v[32];
       tmem_ld_32x32b_x32(tdK + lane_base + c * 32, v);
 #pragma unroll
