@@ -42,6 +42,14 @@ struct FwdSmem {
   static constexpr int TOTAL = BAR + 256 + 1024;    // barriers + TMEM slot + alignment slack
 };
 
+PD_DEVICE void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+PD_DEVICE void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 PD_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const float (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -318,15 +326,19 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
 
 // ================================================================ backward
 // One CTA per (128-key tile, head, sequence), looping over the query tiles at or after the
-// diagonal.  TMEM columns: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ [384,448).
+// diagonal.  TMEM columns: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ [384,448),
+// P^T (bf16 pairs) [448,512).
 //   MMA warp:   S^T = K Q^T, dP^T = V dO^T (M = keys, N = queries, K = 64)
 //               dV += P^T dO, dK += dS^T Q  (M = keys, N = 64, K = queries)
 //               dQ  = dS K                  (M = queries, N = 64, K = keys; A = dS^T read MN-major)
 //   warps 2-9:  thread = TMEM lane, two warps per lane quadrant splitting the 128 query columns (and
 //               the 64 dQ / dK / dV columns) so two compute warps per SM sub-partition hide each
-//               other's latency: P^T = exp2(S^T*scale - lse), dS^T = P^T (dP^T - D) -> bf16
-//               into shared memory (K-major over queries), and the previous tile's dQ rows out
-//               of TMEM into the fp32 dq_acc with 16-byte vector atomics.
+//               other's latency: P^T = exp2(S^T*scale - lse) -> bf16 into TMEM cols [448,512)
+//               (the A operand of dV += P^T dO, read straight from TMEM), dS^T = P^T (dP^T - D)
+//               -> bf16 into shared memory (K-major over queries; A of dK, MN-major A of dQ), and
+//               the previous tile's dQ out of TMEM into the fp32 dq_acc by TMA reduce-add.
+//   Q / dO / lse / D stream through a 3-stage ring; S^T / dP^T of tile n+1 are issued once the
+//   compute warps hold tile n in registers (sdp_free).
 constexpr int BWD_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 compute (two per TMEM lane quadrant)
 
 // One 32-query chunk of a key row: P^T = exp2(S^T*scale - lse), dS^T = P^T (dP^T - D) -> bf16 pairs.
@@ -362,15 +374,15 @@ PD_DEVICE void bwd_chunk32(const uint32_t (&svr)[32], const uint32_t (&dpr)[32],
     dk[i / 2 + 1] = pack_bf16x2(d1.x, d1.y);
   }
 }
+constexpr int BWD_STAGES = 3;  // Q / dO / lse / D ring: tile n+1's loads start while n-1's MMAs drain
 struct BwdSmem {
   static constexpr int K = 0;
   static constexpr int V = K + TILE_BYTES;
-  static constexpr int Q = V + TILE_BYTES;            // [2] stages
-  static constexpr int DO = Q + 2 * TILE_BYTES;       // [2] stages
-  static constexpr int P = DO + 2 * TILE_BYTES;       // P^T: two K-major atoms over queries
-  static constexpr int DS = P + 2 * TILE_BYTES;       // dS^T
-  static constexpr int LD = DS + 2 * TILE_BYTES;      // lse/D: [2 parity][2][128] floats
-  static constexpr int DQ = LD + 2 * 2 * 128 * 4;     // dQ staging [128][64] fp32 for the TMA reduce-add
+  static constexpr int Q = V + TILE_BYTES;                      // [BWD_STAGES]
+  static constexpr int DO = Q + BWD_STAGES * TILE_BYTES;        // [BWD_STAGES]
+  static constexpr int DS = DO + BWD_STAGES * TILE_BYTES;       // dS^T: two K-major atoms over queries
+  static constexpr int LD = DS + 2 * TILE_BYTES;                // lse/D: [stage][2][128] floats
+  static constexpr int DQ = LD + BWD_STAGES * 2 * 128 * 4;      // dQ staging [128][64] fp32 (TMA reduce-add)
   static constexpr int BAR = DQ + 128 * 64 * 4;
   static constexpr int TOTAL = BAR + 256 + 1024;
 };
@@ -389,20 +401,19 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint8_t* sV = smem + BwdSmem::V;
   uint8_t* sQ = smem + BwdSmem::Q;
   uint8_t* sdO = smem + BwdSmem::DO;
-  uint8_t* sP = smem + BwdSmem::P;
   uint8_t* sdS = smem + BwdSmem::DS;
   float* sLD = reinterpret_cast<float*>(smem + BwdSmem::LD);
   float* sDQ = reinterpret_cast<float*>(smem + BwdSmem::DQ);
   float* sLn = sLD;  // written once per tile by the compute warps (lse -> -lse)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BwdSmem::BAR);
   uint64_t* full_kv = bar + 0;
-  uint64_t* full_qdo = bar + 1;   // [2]
-  uint64_t* empty_qdo = bar + 3;  // [2]
-  uint64_t* sdp_full = bar + 5;
-  uint64_t* pds_ready = bar + 6;
-  uint64_t* dq_full = bar + 7;
-  uint64_t* sdp_free = bar + 8;  // compute warps have read S^T / dP^T of the current tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+  uint64_t* full_qdo = bar + 1;                // [BWD_STAGES]
+  uint64_t* empty_qdo = full_qdo + BWD_STAGES;  // [BWD_STAGES]
+  uint64_t* sdp_full = empty_qdo + BWD_STAGES;
+  uint64_t* pds_ready = sdp_full + 1;
+  uint64_t* dq_full = sdp_full + 2;
+  uint64_t* sdp_free = sdp_full + 3;  // compute warps have read S^T / dP^T of the current tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sdp_full + 4);
 
   const int n_t = S / TK;
   const int kt = (int)blockIdx.x;  // key tile; tile 0 has the most query tiles and starts first
@@ -416,7 +427,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     tma_prefetch_desc(&tm_qkv);
     tma_prefetch_desc(&tm_do);
     mbar_init(full_kv, 1);
-    for (int i = 0; i < 2; ++i) { mbar_init(&full_qdo[i], 1); mbar_init(&empty_qdo[i], 1); }
+    for (int i = 0; i < BWD_STAGES; ++i) { mbar_init(&full_qdo[i], 1); mbar_init(&empty_qdo[i], 1); }
     mbar_init(sdp_full, 1);
     mbar_init(pds_ready, 8);
     mbar_init(dq_full, 1);
@@ -430,6 +441,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS = tmem, tP = tmem + 128, tdV = tmem + 256, tdK = tmem + 320, tdQ = tmem + 384;
+  const uint32_t tPt = tmem + 448;  // P^T as bf16 pairs (64 columns), the A operand of dV
 
   if (warp == 0) {
     if (elect_one()) {
@@ -437,8 +449,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       tma_load_2d(sK, &tm_qkv, full_kv, D + h * HDIM, row0 + kt * TK);
       tma_load_2d(sV, &tm_qkv, full_kv, 2 * D + h * HDIM, row0 + kt * TK);
       for (int n = 0; n < N; ++n) {
-        const int st = n & 1, qt = kt + n;
-        mbar_wait(&empty_qdo[st], ((n >> 1) & 1) ^ 1);
+        const int st = n % BWD_STAGES, qt = kt + n;
+        mbar_wait(&empty_qdo[st], ((n / BWD_STAGES) & 1) ^ 1);
         mbar_arrive_expect_tx(&full_qdo[st], 2 * TILE_BYTES + 2 * TQ * 4);
         tma_load_2d(sQ + st * TILE_BYTES, &tm_qkv, &full_qdo[st], h * HDIM, row0 + qt * TQ);
         tma_load_2d(sdO + st * TILE_BYTES, &tm_do, &full_qdo[st], h * HDIM, row0 + qt * TQ);
@@ -453,14 +465,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       constexpr uint32_t idesc_sq = make_idesc_bf16(TK, TQ, false, false);      // S^T, dP^T
       constexpr uint32_t idesc_kv = make_idesc_bf16(TK, HDIM, false, true);     // dV, dK
       constexpr uint32_t idesc_q = make_idesc_bf16(TQ, HDIM, true, true);       // dQ (A = dS^T MN-major)
-      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), p_addr = smem_u32(sP), ds_addr = smem_u32(sdS);
+      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), ds_addr = smem_u32(sdS);
       // S^T / dP^T of tile n+1 are issued as soon as the compute warps have read tile n's (sdp_free),
       // so they run under the compute warps' dQ flush and P / dS stores; dV / dK / dQ of tile n
       // then run under the compute warps' exp / dS math of tile n+1.
       auto issue_sdp = [&](int n) {
-        const int st = n & 1;
+        const int st = n % BWD_STAGES;
         const uint32_t q_addr = smem_u32(sQ + st * TILE_BYTES), do_addr = smem_u32(sdO + st * TILE_BYTES);
-        mbar_wait(&full_qdo[st], (n >> 1) & 1);
+        mbar_wait(&full_qdo[st], (n / BWD_STAGES) & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < HDIM / 16; ++k) {
@@ -474,7 +486,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       mbar_wait(full_kv, 0);
       issue_sdp(0);
       for (int n = 0; n < N; ++n) {
-        const int st = n & 1;
+        const int st = n % BWD_STAGES;
         const uint32_t q_addr = smem_u32(sQ + st * TILE_BYTES), do_addr = smem_u32(sdO + st * TILE_BYTES);
         mbar_wait(sdp_free, n & 1);  // S^T / dP^T of n are in the compute warps' registers
         if (n + 1 < N) issue_sdp(n + 1);
@@ -483,8 +495,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < TQ / 16; ++k) {
           const uint32_t a_off = (k >> 2) * TILE_BYTES + (k & 3) * 32;  // K-major over queries
-          umma_bf16(tdV, make_sw128_desc(p_addr + a_off, 16, 1024), make_sw128_desc(do_addr + k * 2048, 8192, 1024),
-                    idesc_kv, (n | k) != 0);
+          // dV += P^T dO with P^T in TMEM (8 columns = 16 bf16 queries per step)
+          umma_bf16_ts(tdV, tPt + k * 8, make_sw128_desc(do_addr + k * 2048, 8192, 1024), idesc_kv, (n | k) != 0);
           umma_bf16(tdK, make_sw128_desc(ds_addr + a_off, 16, 1024), make_sw128_desc(q_addr + k * 2048, 8192, 1024),
                     idesc_kv, (n | k) != 0);
         }
@@ -528,7 +540,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     };
     for (int n = 0; n < N; ++n) {
       const int qt = kt + n;
-      const int par = n & 1;  // stage of this query tile's Q / dO / lse / D buffers
+      const int par = n % BWD_STAGES;  // stage of this query tile's Q / dO / lse / D buffers
       const float* sL = sLD + par * 256;  // -lse after the in-place negation below
       const float* sDd = sL + 128;
       mbar_wait(sdp_full, n & 1);  // implies the stage's TMA (incl. lse / D) has landed
@@ -562,13 +574,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         const int atom = (c >> 1) * TILE_BYTES;
         const int chunk0 = (c & 1) * 4;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          *reinterpret_cast<uint4*>(sP + atom + sw128(r, chunk0 + u)) =
-              make_uint4(pk[cc][4 * u], pk[cc][4 * u + 1], pk[cc][4 * u + 2], pk[cc][4 * u + 3]);
+        for (int u = 0; u < 4; ++u)
           *reinterpret_cast<uint4*>(sdS + atom + sw128(r, chunk0 + u)) =
               make_uint4(dk[cc][4 * u], dk[cc][4 * u + 1], dk[cc][4 * u + 2], dk[cc][4 * u + 3]);
-        }
+        tmem_st_32x32b_x16(tPt + lane_base + c * 16, pk[cc]);
       }
+      tmem_wait_st();
       fence_proxy_async_shared();
       tc_fence_before();
       __syncwarp();
