@@ -22,7 +22,8 @@ namespace pd {
 //   EPI_RESID  : out = acc + bias + mask                        (projection + residual stream)
 enum EpiKind : int {
   EPI_STORE = 0, EPI_LOSS = 1, EPI_MASK = 2, EPI_SGD = 3, EPI_GRADF32 = 4,
-  EPI_GELU = 5, EPI_GELU_BWD = 6, EPI_RESID = 7
+  EPI_GELU = 5, EPI_GELU_BWD = 6, EPI_RESID = 7,
+  EPI_SGD_STREAM = 8  // internal: EPI_SGD for short K on the tcgen05 path (deeper master prefetch)
 };
 
 struct EpiArgs {

@@ -36,16 +36,19 @@ namespace pd {
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;           // 64 bf16 = 128 B = one swizzle row
 constexpr int TC_EPI_WARPS = 8;     // two warps per TMEM lane quadrant, each owning half the columns
-constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
-#ifndef PD_SGD_BUF
-#define PD_SGD_BUF 1
-#endif
-constexpr int TC_SGD_BUF = PD_SGD_BUF;  // fp32 master blocks in flight per SGD epilogue warp  // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2.. epilogue
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;  // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2.. epilogue
+// wgrad + SGD comes in two flavours: EPI_SGD (long K: MMA-bound, one fp32 master block in flight
+// per epilogue warp so the smem goes to operand stages) and EPI_SGD_STREAM (K <= 256, e.g. the
+// VGG classifier at batch 32: the master read-modify-write is the whole kernel, four blocks in
+// flight per warp = a whole tile's master prefetched while its MMAs run).
+__host__ __device__ constexpr bool is_sgd(int kind) { return kind == EPI_SGD || kind == EPI_SGD_STREAM; }
+__host__ __device__ constexpr int sgd_bufs(int kind) { return kind == EPI_SGD_STREAM ? 4 : 1; }
+constexpr int SGD_STREAM_MAX_K = 256;
 constexpr int TC_ACC_STRIDE = 256;  // TMEM columns between the two accumulator buffers
 
 // fp32-output epilogues (SGD update of the fp32 master, raw fp32 gradient) stage each warp's
 // 32x32 accumulator block through shared memory so global traffic is row-contiguous per warp.
-__host__ __device__ constexpr bool transposed_epilogue(int kind) { return kind == EPI_SGD || kind == EPI_GRADF32; }
+__host__ __device__ constexpr bool transposed_epilogue(int kind) { return is_sgd(kind) || kind == EPI_GRADF32; }
 constexpr int TC_STG_FLOATS = 32 * 33;  // per epilogue warp, padded against bank conflicts
 
 // CG = CTA group: 1 -> one SM computes a 128 x BN tile; 2 -> a CTA pair (cluster of 2) computes
@@ -60,11 +63,11 @@ struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;
   static constexpr int B_BYTES = BNL * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  // SGD: per epilogue warp TC_SGD_BUF TMA-fed 32x32 fp32 master blocks (4 KB each, 128B-swizzled;
-  // one is best: 2048x8192x8192 wgrad+SGD 246 / 252 / 271 / 294 us with 1 / 2 / 3 / 4, as the
-  // smem is worth more as operand stages: 6 / 5 / 4 / 3);
+  // SGD: per epilogue warp sgd_bufs(KIND) TMA-fed 32x32 fp32 master blocks (4 KB each, 128B-
+  // swizzled).  Long K wants one (2048x8192x8192 wgrad+SGD 246 / 252 / 271 / 294 us with 1 / 2 / 3
+  // / 4: the smem is worth more as operand stages, 6 / 5 / 4 / 3); short K wants four (see is_sgd);
   // GRADF32: per warp a padded 32x33 transpose block.
-  static constexpr int STG_BYTES = KIND == EPI_SGD ? TC_EPI_WARPS * TC_SGD_BUF * 4096
+  static constexpr int STG_BYTES = is_sgd(KIND) ? TC_EPI_WARPS * sgd_bufs(KIND) * 4096
                                  : (KIND == EPI_GRADF32 ? TC_EPI_WARPS * TC_STG_FLOATS * 4 : 0);
   static constexpr int PIPE_BUDGET = 227 * 1024 - 2048 - STG_BYTES;  // all of the 227 KB opt-in smem
   static constexpr int STAGES = PIPE_BUDGET / STAGE_BYTES > 8 ? 8 : PIPE_BUDGET / STAGE_BYTES;
@@ -77,7 +80,7 @@ struct TcCfg {
   static_assert(!B_MN || B_ROWS % 16 == 0, "MN-major B rows per CTA");
 };
 
-template <int CG, int BN, bool A_MN, bool B_MN, int KIND, int SRC = SRC_2D>
+template <int CG, int BN, bool A_MN, bool B_MN, int KIND, int SRC = SRC_2D, bool SIG = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmW, int M, int N, int K, EpiArgs ep, ConvArgs cv) {
@@ -124,7 +127,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // SGD: grouped rasterisation - bands of kGroup tile rows walked column by column, so the
   // co-resident tiles touch ~kGroup A blocks and ~units/kGroup B blocks (a compact operand
   // working set that survives the streamed master traffic in L2)
-  constexpr int kGroup = KIND == EPI_SGD ? 8 : 0;
+  constexpr int kGroup = is_sgd(KIND) ? 8 : 0;
+  constexpr int NBUF = sgd_bufs(KIND);  // SGD: fp32 master blocks in flight per epilogue warp
   auto tile_m = [&](int t) {
     if constexpr (kGroup > 0) {
       const int band = t / (kGroup * num_n), in = t - band * kGroup * num_n;
@@ -145,13 +149,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if constexpr (KIND == EPI_SGD) tma_prefetch_desc(&tmW);
+    if constexpr (is_sgd(KIND)) tma_prefetch_desc(&tmW);
     // full: leader's arrive.expect_tx (+ the peer's remote arrive for a pair); empty: one MMA commit;
     // tmem_empty: one arrival per epilogue warp of every CTA of the unit
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], CG); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tmem_full[a], 1); mbar_init(&tmem_empty[a], CG * TC_EPI_WARPS); }
-    if constexpr (KIND == EPI_SGD)
-      for (int i = 0; i < TC_SGD_BUF * TC_EPI_WARPS; ++i) mbar_init(&epi_bar[i], 1);
+    if constexpr (is_sgd(KIND))
+      for (int i = 0; i < NBUF * TC_EPI_WARPS; ++i) mbar_init(&epi_bar[i], 1);
     fence_barrier_init();
     fence_proxy_async_smem();
   }
@@ -269,10 +273,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (acc == 0) acc_phase ^= 1;
       }
     }
-  } else if constexpr (KIND == EPI_SGD) {
+  } else if constexpr (is_sgd(KIND)) {
     // ---------------- wgrad + SGD epilogue.  Each warp owns 32 accumulator rows (its TMEM lane
     // quadrant) and half of the tile's 32-column chunks.  The fp32 master block of a chunk
-    // (32x32, 4 KB) is TMA-loaded into a 128B-swizzled smem buffer ahead of use (TC_SGD_BUF
+    // (32x32, 4 KB) is TMA-loaded into a 128B-swizzled smem buffer ahead of use (NBUF
     // deep, the first issued before the tile's accumulator is ready), updated in place
     // (w = m - lr*acc), TMA-stored back, and the bf16 version copy is written from registers.
     // HBM sees only bulk, fully coalesced master traffic.
@@ -282,8 +286,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int c_begin = half ? (NC + 1) / 2 : 0;
     const int c_end = half ? NC : (NC + 1) / 2;
     const int e = warp - 2;
-    uint8_t* buf0 = epi_smem + e * TC_SGD_BUF * 4096;
-    uint64_t* bars = epi_bar + TC_SGD_BUF * e;
+    uint8_t* buf0 = epi_smem + e * NBUF * 4096;
+    uint64_t* bars = epi_bar + NBUF * e;
     const int lane = lane_id();
     uint32_t bar_phase = 0;  // bit b: parity of buffer b's next load
     // the master stream (read once, written once) must not evict the L2-resident operands
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // prefetch the first two master blocks of this tile while its MMAs are still running
       if (lane == 0) {
         bulk_wait_read0();  // previous tile's stores have finished reading both buffers
-        for (int i = 0; i < TC_SGD_BUF && i < nck; ++i) {
+        for (int i = 0; i < NBUF && i < nck; ++i) {
           mbar_arrive_expect_tx(&bars[i], 4096);
           tma_load_2d_hint(buf0 + i * 4096, &tmW, &bars[i], n0 + (c_begin + i) * 32, row0, stream_pol);
         }
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_after();
 #pragma unroll 1
       for (int i = 0; i < nck; ++i) {
-        const int c = c_begin + i, b = i % TC_SGD_BUF;
+        const int c = c_begin + i, b = i % NBUF;
         float v[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * TC_ACC_STRIDE + c * 32, v);
         mbar_wait(&bars[b], (bar_phase >> b) & 1);
@@ -348,10 +352,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (lane == 0) {
           tma_store_2d_hint(&tmW, buf0 + b * 4096, col0, row0, stream_pol);  // TMA clips rows/cols outside [M, N)
           bulk_commit();
-          if (i + TC_SGD_BUF < nck) {
+          if (i + NBUF < nck) {
             bulk_wait_read0();  // this buffer's store has read the smem block
             mbar_arrive_expect_tx(&bars[b], 4096);
-            tma_load_2d_hint(buf0 + b * 4096, &tmW, &bars[b], n0 + (c + TC_SGD_BUF) * 32, row0, stream_pol);
+            tma_load_2d_hint(buf0 + b * 4096, &tmW, &bars[b], n0 + (c + NBUF) * 32, row0, stream_pol);
           }
         }
         __syncwarp();
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const bool okA = colA < N, okB = two && colB < N;
         const int rows = M - row0 < 32 ? (int)(M - row0) : 32;
         float mA[32], mB[32];
-        if constexpr (KIND == EPI_SGD) {
+        if constexpr (is_sgd(KIND)) {
           const float* pa = ep.master + row0 * ep.ldw + colA;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
@@ -410,7 +414,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = v[j];
           __syncwarp();
           if (col_ok) {
-            if constexpr (KIND == EPI_SGD) {
+            if constexpr (is_sgd(KIND)) {
               float* pm = ep.master + row0 * ep.ldw + col;
               __nv_bfloat16* po = static_cast<__nv_bfloat16*>(ep.out) + row0 * ep.ldo + col;
 #pragma unroll
@@ -499,14 +503,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (lane_id() == 0 && lsum != 0.f) atomicAdd(ep.loss, 0.5f * ep.scale * lsum);
     }
   }
-  if (ep.sig_flag) __threadfence_system();  // this thread's payload stores, before the CTA's arrival
+  // SIG (a compile-time variant, so kernels without a hand-off carry none of this code: a runtime
+  // branch here measurably slowed the red.add-heavy split-K wgrad epilogues)
+  if constexpr (SIG) __threadfence_system();  // this thread's payload stores, before the CTA's arrival
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::TMEM_COLS, CG>(tmem_base);
   }
-  if (ep.sig_flag && threadIdx.x == 0) {
+  if (SIG && threadIdx.x == 0) {
     // fused hand-off: the last CTA to finish publishes the payload to the peer's inbox flag
     __threadfence_system();
     if (atomicAdd(ep.sig_counter, 1) == (int)gridDim.x - 1) {
@@ -669,18 +675,28 @@ static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int
   if (rc) return rc;
   CUtensorMap tw;
   memset(&tw, 0, sizeof(tw));
-  if (KIND == EPI_SGD) {
+  if (is_sgd(KIND)) {
     if ((ep.ldw % 4) || (reinterpret_cast<uintptr_t>(ep.master) % 16))
       return set_error(PD_ERR_INVALID, "gemm: SGD master must be 16-byte aligned with ld %% 4 == 0");
     rc = make_map(&tw, ep.master, (uint64_t)N, (uint64_t)M, ep.ldw, 32, 32, true);
     if (rc) return rc;
   }
-  auto kern = k_gemm_tc<CG, BN, A_MN, B_MN, KIND, SRC>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
+  auto kern = k_gemm_tc<CG, BN, A_MN, B_MN, KIND, SRC, false>;
+  static bool attr_set[2] = {false, false};  // per instantiation (plain / hand-off variant)
+  int var = 0;
+  if (ep.sig_flag) {
+    // the fused hand-off exists for the payload-producing epilogues only (MLP forward / dgrad)
+    if constexpr ((KIND == EPI_STORE || KIND == EPI_MASK) && SRC == SRC_2D) {
+      kern = k_gemm_tc<CG, BN, A_MN, B_MN, KIND, SRC, true>;
+      var = 1;
+    } else {
+      return set_error(PD_ERR_INVALID, "gemm: fused hand-off is not available for epilogue kind %d", KIND);
+    }
+  }
+  if (!attr_set[var]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
       return set_error(PD_ERR_CUDA, "cudaFuncSetAttribute(smem=%d) failed", C::SMEM_BYTES);
-    attr_set = true;
+    attr_set[var] = true;
   }
   const int units = ((M + TC_BM * CG - 1) / (TC_BM * CG)) * ((N + BN - 1) / BN) * cv.splits;
   const int max_units = num_sms() / CG;
@@ -740,7 +756,7 @@ static int launch_bn(const void* A, int64_t lda, const void* B, int64_t ldb, int
     if (N <= 64) return launch_tc<1, 64, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
     if (N <= 128) return launch_tc<1, 128, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
   }
-  if constexpr (KIND == EPI_SGD && B_MN) {
+  if constexpr (is_sgd(KIND) && B_MN) {
     // wgrad + SGD on small weight matrices: 256 x 128 pair tiles double the tile count (e.g. a
     // 1024 x 1024 weight: 32 instead of 16 pair tiles); large ones keep 256-wide tiles, whose
     // operand traffic per flop is lower (measured: 8192^2 0.27 ms vs 0.31 ms with 128-wide tiles)
@@ -768,7 +784,10 @@ static int dispatch_kind(int kind, const void* A, int64_t lda, const void* B, in
     case EPI_STORE: return launch_bn<A_MN, B_MN, EPI_STORE>(A, lda, B, ldb, M, N, K, ep, st);
     case EPI_LOSS: return launch_bn<A_MN, B_MN, EPI_LOSS>(A, lda, B, ldb, M, N, K, ep, st);
     case EPI_MASK: return launch_bn<A_MN, B_MN, EPI_MASK>(A, lda, B, ldb, M, N, K, ep, st);
-    case EPI_SGD: return launch_bn<A_MN, B_MN, EPI_SGD>(A, lda, B, ldb, M, N, K, ep, st);
+    case EPI_SGD:
+      if constexpr (A_MN && B_MN)
+        if (K <= SGD_STREAM_MAX_K) return launch_bn<A_MN, B_MN, EPI_SGD_STREAM>(A, lda, B, ldb, M, N, K, ep, st);
+      return launch_bn<A_MN, B_MN, EPI_SGD>(A, lda, B, ldb, M, N, K, ep, st);
     case EPI_GRADF32: return launch_bn<A_MN, B_MN, EPI_GRADF32>(A, lda, B, ldb, M, N, K, ep, st);
     case EPI_GELU:
       if constexpr (!A_MN && !B_MN) return launch_bn<A_MN, B_MN, EPI_GELU>(A, lda, B, ldb, M, N, K, ep, st);
