@@ -125,9 +125,13 @@ int maxpool_bwd(const void* dy, const uint8_t* arg, void* dx, int n, int H, int 
 // 64-channel im2col TMA box; every other layer reads im2col tiles straight from the activation.
 // One thread per output pixel: gathers its 9*C inputs (C <= 7) and writes the 128-byte cols row
 // with eight 16-byte stores (the output stream is what bounds this kernel).
+// CC > 0: channel count known at compile time (VGG's RGB input, C = 3), so the 27 taps unroll and
+// the packed row stays in registers; CC = 0: runtime C (the packing index is dynamic).
+template <int CC>
 __global__ void __launch_bounds__(256) k_im2col3(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ cols,
-                                                 int n, int H, int W, int C, int kpad) {
+                                                 int n, int H, int W, int C_rt, int kpad) {
   griddep_wait();
+  const int C = CC > 0 ? CC : C_rt;
   const int64_t pixels = (int64_t)n * H * W;
   for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < pixels;
        pix += (int64_t)gridDim.x * blockDim.x) {
@@ -136,14 +140,24 @@ __global__ void __launch_bounds__(256) k_im2col3(const __nv_bfloat16* __restrict
     uint32_t w[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) w[i] = 0;
-    int k = 0;
+#pragma unroll
     for (int tap = 0; tap < 9; ++tap) {
       const int hh = p + tap / 3 - 1, ww = q + tap % 3 - 1;
       const bool ok = hh >= 0 && hh < H && ww >= 0 && ww < W;
       const __nv_bfloat16* src = x + ((b * H + hh) * W + ww) * C;
-      for (int c = 0; c < C; ++c, ++k) {
-        const uint16_t v = ok ? __bfloat16_as_ushort(src[c]) : (uint16_t)0;
-        w[k >> 1] |= (uint32_t)v << ((k & 1) * 16);
+      if constexpr (CC > 0) {
+#pragma unroll
+        for (int c = 0; c < CC; ++c) {
+          const int k = tap * CC + c;
+          const uint16_t v = ok ? __bfloat16_as_ushort(src[c]) : (uint16_t)0;
+          w[k >> 1] |= (uint32_t)v << ((k & 1) * 16);
+        }
+      } else {
+        for (int c = 0; c < C; ++c) {
+          const int k = tap * C + c;
+          const uint16_t v = ok ? __bfloat16_as_ushort(src[c]) : (uint16_t)0;
+          w[k >> 1] |= (uint32_t)v << ((k & 1) * 16);
+        }
       }
     }
     uint4* dst = reinterpret_cast<uint4*>(cols + pix * kpad);
@@ -155,8 +169,12 @@ __global__ void __launch_bounds__(256) k_im2col3(const __nv_bfloat16* __restrict
 int im2col3(const void* x, void* cols, int n, int H, int W, int C, int kpad, cudaStream_t st) {
   if (9 * C > kpad || kpad != 64) return set_error(PD_ERR_INVALID, "im2col: kpad must be 64 and >= 9*C (%d)", kpad);
   const int64_t total = (int64_t)n * H * W;
-  launch_pdl(k_im2col3, dim3(grid_for(total, 256)), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(x),
-                                                  static_cast<__nv_bfloat16*>(cols), n, H, W, C, kpad);
+  if (C == 3)
+    launch_pdl(k_im2col3<3>, dim3(grid_for(total, 256)), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(x),
+               static_cast<__nv_bfloat16*>(cols), n, H, W, C, kpad);
+  else
+    launch_pdl(k_im2col3<0>, dim3(grid_for(total, 256)), dim3(256), 0, st, static_cast<const __nv_bfloat16*>(x),
+               static_cast<__nv_bfloat16*>(cols), n, H, W, C, kpad);
   return launch_status("im2col3");
 }
 
