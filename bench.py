@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--stages", type=int, default=8)
     p.add_argument("--mode", default="weight_stashing")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-only", action="store_true",
+                   help="internal: run only the CPU baseline sample and print it (child process)")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--serial", choices=["on", "off"], default="off",
                    help="timed region: issue all hosted stages on one stream (on) or one stream per stage (off); "
@@ -290,6 +292,34 @@ def _all_host_threads():
         pass
 
 
+def _phase(msg):
+    """Progress marker on stderr (stdout carries only the JSON line)."""
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
+def _cpu_sample_for(args):
+    return (cpu_sample_vgg(args) if args.workload == "vgg" else
+            cpu_sample_gpt(args) if args.workload == "gpt" else cpu_sample(args))
+
+
+def cpu_baseline_isolated(args, timeout=300):
+    """The CPU baseline sample in a child process (all host threads, no CUDA context): a stuck or
+    slow CPU library cannot hold back the bench line; on failure the baseline is reported as such."""
+    env = dict(os.environ, OMP_NUM_THREADS=str(os.cpu_count() or 1))
+    for k in ("RANK", "LOCAL_RANK", "WORLD_SIZE", "LOCAL_WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    cmd = [sys.executable, os.path.abspath(__file__)] + [a for a in sys.argv[1:]] + ["--cpu-sample-only"]
+    try:
+        out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout)
+        lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+        if out.returncode == 0 and lines:
+            return json.loads(lines[-1])
+        why = f"child exited {out.returncode}: {out.stderr.strip()[-200:]}"
+    except subprocess.TimeoutExpired:
+        why = f"timed out after {timeout} s"
+    return {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port", "sample": why}
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
@@ -367,9 +397,11 @@ def run_ours(args, rank, world):
             dist.barrier()
 
     stream = torch.cuda.current_stream()
+    _phase("warmup")
     for _ in range(args.warmup):
         ex.step(stream=stream)
     torch.cuda.synchronize()
+    _phase("timed region")
     # ---------------- timed region (device events, max over ranks)
     launches0 = ex.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -389,6 +421,7 @@ def run_ours(args, rank, world):
         ms = float(t.item())
     launches = ex.launch_count() - launches0
     # ---------------- roofline pass: one serial step with per-GEMM CUDA events on the launching stream
+    _phase("serial roofline pass")
     barrier()
     ex.set_serial(True)
     ex.kernel_timing(True)
@@ -413,6 +446,7 @@ def run_ours(args, rank, world):
     samples = args.steps * args.minibatches * args.batch
     value = samples / (ms * 1e-3)
     # ---------------- traced step: bubble / utilisation with the reference's window rule
+    _phase("traced step + e2e")
     barrier()
     torch.cuda.synchronize()
     ex.step(stream=stream, trace=True)
@@ -505,10 +539,10 @@ def run_ours(args, rank, world):
         "steady_minibatches_per_s": rep.steady_throughput if rep else None,
     }
     if not args.no_cpu_baseline and world == 1:
-        _all_host_threads()
-        out["cpu_baseline"] = (cpu_sample_vgg(args) if args.workload == "vgg" else
-                               cpu_sample_gpt(args) if args.workload == "gpt" else cpu_sample(args))
+        _phase("cpu baseline (child process)")
+        out["cpu_baseline"] = cpu_baseline_isolated(args)
     ex.close()
+    _phase("done")
     print(json.dumps(out), flush=True)
 
 
@@ -528,6 +562,10 @@ def apply_workload_defaults(args):
 
 def main():
     args = apply_workload_defaults(parse())
+    if args.cpu_sample_only:
+        _all_host_threads()
+        print(json.dumps(_cpu_sample_for(args)), flush=True)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":

@@ -205,6 +205,34 @@ __device__ __forceinline__ void finish_update(const float* part, int S, int C, f
   }
 }
 
+// acc[0..8) += the 8 bf16 of v
+__device__ __forceinline__ void acc_bf16x8(float (&acc)[8], const uint4 v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float a, b;
+    unpack_bf16x2(w[j], a, b);
+    acc[2 * j] += a;
+    acc[2 * j + 1] += b;
+  }
+}
+
+// Sum rows r, r+step, ... < r1 of column group cg (8 bf16) into acc, four 16-byte loads in flight.
+__device__ __forceinline__ void colsum_rows(const __nv_bfloat16* __restrict__ x, int C, int cg, int64_t r, int64_t r1,
+                                            int64_t step, float (&acc)[8]) {
+  for (; r + 3 * step < r1; r += 4 * step) {
+    const uint4 v0 = *reinterpret_cast<const uint4*>(x + r * C + cg * 8);
+    const uint4 v1 = *reinterpret_cast<const uint4*>(x + (r + step) * C + cg * 8);
+    const uint4 v2 = *reinterpret_cast<const uint4*>(x + (r + 2 * step) * C + cg * 8);
+    const uint4 v3 = *reinterpret_cast<const uint4*>(x + (r + 3 * step) * C + cg * 8);
+    acc_bf16x8(acc, v0);
+    acc_bf16x8(acc, v1);
+    acc_bf16x8(acc, v2);
+    acc_bf16x8(acc, v3);
+  }
+  for (; r < r1; r += step) acc_bf16x8(acc, *reinterpret_cast<const uint4*>(x + r * C + cg * 8));
+}
+
 __global__ void __launch_bounds__(CS_THREADS) k_colsum_part(const __nv_bfloat16* __restrict__ x, int64_t rows, int C,
                                                             int64_t rows_per, float* __restrict__ part, int* counter,
                                                             float* grad, float* master, float* out, float lr) {
@@ -217,17 +245,7 @@ __global__ void __launch_bounds__(CS_THREADS) k_colsum_part(const __nv_bfloat16*
   if (C8 > CS_THREADS / 2) {
     for (int cg = threadIdx.x; cg < C8; cg += CS_THREADS) {
       float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int64_t r = r0; r < r1; ++r) {
-        const uint4 v = *reinterpret_cast<const uint4*>(x + r * C + cg * 8);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float a, b;
-          unpack_bf16x2(w[j], a, b);
-          acc[2 * j] += a;
-          acc[2 * j + 1] += b;
-        }
-      }
+      colsum_rows(x, C, cg, r0, r1, 1, acc);
       if (counter) {  // fused mode: accumulate straight into the zeroed part[0..C)
         red_add_v4(part + cg * 8, acc[0], acc[1], acc[2], acc[3]);
         red_add_v4(part + cg * 8 + 4, acc[4], acc[5], acc[6], acc[7]);
@@ -241,18 +259,7 @@ __global__ void __launch_bounds__(CS_THREADS) k_colsum_part(const __nv_bfloat16*
     const int lanes = CS_THREADS / C8;  // row lanes per block
     const int cg = threadIdx.x % C8, rl = threadIdx.x / C8;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (rl < lanes)
-      for (int64_t r = r0 + rl; r < r1; r += lanes) {
-        const uint4 v = *reinterpret_cast<const uint4*>(x + r * C + cg * 8);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float a, b;
-          unpack_bf16x2(w[j], a, b);
-          acc[2 * j] += a;
-          acc[2 * j + 1] += b;
-        }
-      }
+    if (rl < lanes) colsum_rows(x, C, cg, r0 + rl, r1, lanes, acc);
     if (rl < lanes)
 #pragma unroll
       for (int j = 0; j < 8; ++j) red[rl * C + cg * 8 + j] = acc[j];
