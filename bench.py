@@ -16,6 +16,7 @@ explicit L2 flush is needed between steps.
 from __future__ import annotations
 
 import argparse
+import faulthandler
 import json
 import os
 import statistics
@@ -562,6 +563,9 @@ def apply_workload_defaults(args):
 
 def main():
     args = apply_workload_defaults(parse())
+    # a stuck run prints every thread's Python stack on stderr (the device side traps on its own:
+    # mbarrier waits give up after 20 s, flag waits after 10 s)
+    faulthandler.dump_traceback_later(float(os.environ.get("PD_BENCH_WATCHDOG_S", "600")), exit=False)
     if args.cpu_sample_only:
         _all_host_threads()
         print(json.dumps(_cpu_sample_for(args)), flush=True)

@@ -3,6 +3,7 @@
 // (shared-memory matrix descriptor, instruction descriptor for kind::f16).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -48,15 +49,34 @@ PD_DEVICE void mbar_arrive(uint64_t* bar) {
 // The suspend-time hint lets the waiting warp sleep until the phase completes (or the hint
 // expires) instead of spinning: waiting producer / MMA warps then stop stealing issue slots from
 // the epilogue / softmax warps that share their SM sub-partition.
-PD_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t addr = smem_u32(bar);
+PD_DEVICE bool mbar_try(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
-      "r"(parity), "r"(0x989680)
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(0x989680)
       : "memory");
+  return ok != 0;
+}
+// Cold path of a wait that has not completed for 20 s: a protocol bug, not slowness.  Report the
+// barrier and stop the kernel (the host sees a launch failure) instead of hanging the GPU.
+static __device__ __noinline__ void mbar_timeout(uint32_t addr, uint32_t parity) {
+  printf("pd: mbarrier wait timed out (smem 0x%x, parity %u) block (%d,%d,%d) thread %d\n", addr, parity, blockIdx.x,
+         blockIdx.y, blockIdx.z, threadIdx.x);
+  __trap();
+}
+PD_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try(addr, parity)) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (!mbar_try(addr, parity)) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20ull * 1000 * 1000 * 1000) mbar_timeout(addr, parity);
+  }
 }
 
 // ---------------------------------------------------------------- TMA
