@@ -43,6 +43,16 @@ __device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&v)[8]) {
 }
 
 // y = (x - mean) * rstd * gamma + beta ; gamma/beta = gb[0:D], gb[D:2D] (fp32)
+// o[j] = o[j] * gamma[j] + beta[j] for 8 consecutive columns (two 16-byte loads each)
+__device__ __forceinline__ void ln_affine8(const float* __restrict__ g, const float* __restrict__ b, float (&o)[8]) {
+  const float4 g0 = reinterpret_cast<const float4*>(g)[0], g1 = reinterpret_cast<const float4*>(g)[1];
+  const float4 b0 = reinterpret_cast<const float4*>(b)[0], b1 = reinterpret_cast<const float4*>(b)[1];
+  const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+  const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o[j] = fmaf(o[j], gg[j], bb[j]);
+}
+
 template <int NV>
 __global__ void __launch_bounds__(LN_WARPS * 32) k_ln_fwd(const __nv_bfloat16* __restrict__ x, const float* __restrict__ gb,
                                                           __nv_bfloat16* __restrict__ y, float* __restrict__ mean,
@@ -80,7 +90,8 @@ __global__ void __launch_bounds__(LN_WARPS * 32) k_ln_fwd(const __nv_bfloat16* _
       const int c = i * 256 + lane * 8;
       float o[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mu) * rs * gb[c + j] + gb[D + c + j];
+      for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mu) * rs;
+      ln_affine8(gb + c, gb + D + c, o);
       store8(y + row * D + c, o);
     }
   if (lane == 0) {
@@ -123,9 +134,12 @@ __global__ void __launch_bounds__(LN_WARPS * 32) k_ln_bwd(const __nv_bfloat16* _
         load8(dy + row * D + c, dv);
         load8(x + row * D + c, xv);
 #pragma unroll
+        const float4 ga = reinterpret_cast<const float4*>(gb + c)[0], gc = reinterpret_cast<const float4*>(gb + c)[1];
+        const float gm[8] = {ga.x, ga.y, ga.z, ga.w, gc.x, gc.y, gc.z, gc.w};
+#pragma unroll
         for (int j = 0; j < 8; ++j) {
           xh[i][j] = (xv[j] - mu) * rs;
-          g[i][j] = dv[j] * gb[c + j];
+          g[i][j] = dv[j] * gm[j];
           s1 += g[i][j];
           s2 += g[i][j] * xh[i][j];
           pg[i][j] += dv[j] * xh[i][j];
