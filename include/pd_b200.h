@@ -306,6 +306,23 @@ int pd_rt_load_program(pd_runtime* rt, const int32_t* items, int n_items);
  * trace=1 records per-item device timestamps (pd_rt_records). */
 int pd_rt_run(pd_runtime* rt, void* stream, int trace);
 int pd_rt_records(pd_runtime* rt, pd_record* out, int cap, int* n_out);
+/* Device pass records of traced runs (replaces the reference's ledger.record at pass start,
+ * simulator.py:256-264, and its trace, :266-282, with what the device observed).
+ * rec: caller-owned device int64 [(1 + cap) * PD_REC_WIDTH]; row 0 holds the run's start
+ * %globaltimer (ns, comparable across the GPUs of a node), row 1 + i the record of program
+ * item i: PD_REC_T0 / PD_REC_T1 %globaltimer at the pass's start / end, PD_REC_VER0 / PD_REC_VER1
+ * the version tag of the weight ring slot the pass reads at its start / end, PD_REC_BYTES payload
+ * bytes stored into another process's inbox (counted by the storing kernel), PD_REC_COMMIT the
+ * version the pass committed (-1: none).  tags: caller-owned device int32 [64 * hosted workers],
+ * the version held by each ring slot (written in stream order after the committing kernels).
+ * NULL rec switches the records off. */
+#define PD_REC_WIDTH 8
+enum pd_rec_field { PD_REC_T0 = 0, PD_REC_T1 = 1, PD_REC_VER0 = 2, PD_REC_VER1 = 3, PD_REC_BYTES = 4,
+                    PD_REC_COMMIT = 5 };
+int pd_rt_set_records(pd_runtime* rt, int64_t* rec, int cap, int32_t* tags);
+/* The (cg, bn) tile configuration the tcgen05 GEMM dispatch picks for a problem: cg 1 = one CTA
+ * per 128 x bn tile, 2 = a CTA pair per 256 x bn tile (tests pin the bench's instantiations). */
+int pd_gemm_pick(int M, int N, int K, int a_mn, int b_mn, int kind, int* cg, int* bn);
 /* serial=1: every hosted stage issues on one stream in program order (single-GPU mode;
  * the per-item dependencies are then satisfied by stream order). */
 int pd_rt_set_serial(pd_runtime* rt, int on);

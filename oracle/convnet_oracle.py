@@ -27,17 +27,25 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .pipeline_oracle import bf16_round
 
 F = torch.nn.functional
 
 
 def _q_t(x: torch.Tensor) -> torch.Tensor:
-    return torch.from_numpy(bf16_round(x.numpy()))
+    """Round to bf16 through fp32 (nearest-even both times), as pipeline_oracle.bf16_round does."""
+    return x.float().bfloat16().to(x.dtype)
+
+
+def _as_t(a, dtype, device) -> torch.Tensor:
+    """numpy array or torch tensor -> torch tensor of dtype on device (the oracle may run on a GPU
+    as the checker of full-size configurations; its arithmetic is the same)."""
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=dtype)
+    return torch.from_numpy(np.asarray(a, np.float64)).to(device=device, dtype=dtype)
 
 
 def _f32_t(x: torch.Tensor) -> torch.Tensor:
-    return x.float().double()
+    return x.float().to(x.dtype)
 
 
 def _oihw(Wt: torch.Tensor, cin: int, cout: int) -> torch.Tensor:
@@ -54,7 +62,7 @@ def _pool_fwd(y: torch.Tensor):
 
 def _pool_bwd(dz: torch.Tensor, arg: torch.Tensor):
     n, ho, wo, c = dz.shape
-    out = torch.zeros(n, ho, wo, c, 4, dtype=dz.dtype)
+    out = torch.zeros(n, ho, wo, c, 4, dtype=dz.dtype, device=dz.device)
     out.scatter_(-1, arg.unsqueeze(-1), dz.unsqueeze(-1))
     return out.reshape(n, ho, wo, c, 2, 2).permute(0, 1, 4, 2, 5, 3).reshape(n, 2 * ho, 2 * wo, c)
 
@@ -95,7 +103,7 @@ def _backward(geoms, weights, saved, dz, q):
             dy = _pool_bwd(d, arg) if g.pool else d
             dW = torch.nn.grad.conv2d_weight(xin.permute(0, 3, 1, 2), (g.c_out, g.c_in, 3, 3), dy.permute(0, 3, 1, 2),
                                              padding=1)
-            gWt = torch.zeros(g.w_shape, dtype=dW.dtype)
+            gWt = torch.zeros(g.w_shape, dtype=dW.dtype, device=dW.device)
             gWt[: 9 * g.c_in] = dW.permute(2, 3, 1, 0).reshape(9 * g.c_in, g.c_out)
             grads[l] = (gWt, dy.reshape(-1, g.c_out).sum(0))
             if l > 0:
@@ -111,13 +119,14 @@ def _backward(geoms, weights, saved, dz, q):
 
 @torch.no_grad()
 def convnet_train(geoms, params, X, labels, lr, stage_bounds, versions, K, emulate: str | None = "bf16", reps=None,
-                  dtype=torch.float64):
+                  dtype=torch.float64, device=None):
     """Delayed-SGD pipeline training of a conv net (see module docstring).
 
     geoms: per-layer geometry objects (kind, h, w, c_in, c_out, pool, relu, w_shape);
-    params: [(W, b)] fp64 numpy per layer; X [n_blocks, B, H, W, C]; labels [n_blocks, B].
-    dtype: arithmetic type (float64 for parity; float32 for the timed CPU baseline, no emulation).
-    Returns (losses[K], final params list of numpy (W, b)).
+    params: [(W, b)] per layer, numpy or torch; X [n_blocks, B, H, W, C]; labels [n_blocks, B].
+    dtype: arithmetic type (float64 for parity; float32 for the timed CPU baseline, or on a GPU for
+    full-size checks with TF32 off).  device: torch device of the arithmetic (default CPU).
+    Returns (losses[K], final params list of (W, b)): numpy fp64 on the CPU, torch tensors on a device.
     """
     q = _q_t if emulate == "bf16" else (lambda a: a)
     master = _f32_t if emulate == "bf16" else (lambda a: a)
@@ -127,8 +136,7 @@ def convnet_train(geoms, params, X, labels, lr, stage_bounds, versions, K, emula
     for s, (a, b) in enumerate(stage_bounds):
         for l in range(a, b + 1):
             layer_stage[l - 1] = s
-    archives = [{0: [(master(torch.from_numpy(np.asarray(params[l - 1][0], np.float64)).to(dtype)),
-                      master(torch.from_numpy(np.asarray(params[l - 1][1], np.float64)).to(dtype)))
+    archives = [{0: [(master(_as_t(params[l - 1][0], dtype, device)), master(_as_t(params[l - 1][1], dtype, device)))
                      for l in range(a, b + 1)]}
                 for (a, b) in stage_bounds]
     latest_v = [0] * n
@@ -136,8 +144,9 @@ def convnet_train(geoms, params, X, labels, lr, stage_bounds, versions, K, emula
     losses, round_acc = [], {}
     for mb in range(1, K + 1):
         blk = (mb - 1) % X.shape[0]
-        x = torch.from_numpy(np.asarray(X[blk], np.float64)).to(dtype)
-        y = torch.from_numpy(np.asarray(labels[blk], np.int64))
+        x = _as_t(X[blk], dtype, device)
+        y = labels[blk].to(device=device, dtype=torch.int64) if isinstance(labels, torch.Tensor) else \
+            torch.from_numpy(np.asarray(labels[blk], np.int64)).to(device)
         B = x.shape[0]
         fv = [versions(s, mb, "forward") for s in range(n)]
         bv = [versions(s, mb, "backward") for s in range(n)]
@@ -145,11 +154,12 @@ def convnet_train(geoms, params, X, labels, lr, stage_bounds, versions, K, emula
             raise ValueError("convnet_train supports forward version == backward version only")
         weights = [archives[layer_stage[l]][fv[layer_stage[l]]][l - first[layer_stage[l]]] for l in range(len(geoms))]
         logits, saved = _forward(geoms, weights, x, q)
-        logits = logits.float().double() if emulate == "bf16" else logits  # fp32 logits on the device
+        logits = logits.float().to(logits.dtype) if emulate == "bf16" else logits  # fp32 logits on the device
         lse = torch.logsumexp(logits, dim=1)
-        losses.append(float((lse - logits[torch.arange(B), y]).mean()))
+        rows = torch.arange(B, device=logits.device)
+        losses.append(float((lse - logits[rows, y]).mean()))
         p = torch.softmax(logits, dim=1)
-        p[torch.arange(B), y] -= 1.0
+        p[rows, y] -= 1.0
         dz = q(p / B)
         grads = _backward(geoms, weights, saved, dz, q)
         for s, (a, b) in enumerate(stage_bounds):
@@ -170,5 +180,8 @@ def convnet_train(geoms, params, X, labels, lr, stage_bounds, versions, K, emula
             latest_v[s] = mb
     final = []
     for s in range(n):
-        final.extend((W.double().numpy(), b.double().numpy()) for W, b in archives[s][latest_v[s]])
+        if device is not None:
+            final.extend(archives[s][latest_v[s]])
+        else:
+            final.extend((W.double().numpy(), b.double().numpy()) for W, b in archives[s][latest_v[s]])
     return np.array(losses), final

@@ -31,7 +31,7 @@ F = torch.nn.functional
 
 
 def _bf16(x: torch.Tensor) -> torch.Tensor:
-    return x.float().bfloat16().double()
+    return x.float().bfloat16().to(x.dtype)
 
 
 class _Q(torch.autograd.Function):
@@ -85,8 +85,8 @@ def _forward_loss(spec, weights, tok, lab, emulate):
     (We, _), blocks, (Wh, bh) = weights[0], weights[1:-1], weights[-1]
     We_q = QF(We)
     wte, wpe = We_q[:Vp], We_q[Vp:Vp + S]
-    x = Q(wte[tok] + wpe[torch.arange(S)].unsqueeze(0))  # [B, S, d]
-    causal = torch.triu(torch.ones(S, S, dtype=torch.bool), diagonal=1)
+    x = Q(wte[tok] + wpe[torch.arange(S, device=tok.device)].unsqueeze(0))  # [B, S, d]
+    causal = torch.triu(torch.ones(S, S, dtype=torch.bool, device=tok.device), diagonal=1)
     for W, b in blocks:
         Wq = QF(W).reshape(-1)
         Wqkv = Wq[: 3 * d * d].view(3 * d, d)
@@ -122,39 +122,51 @@ class _QFP32(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x):
-        return x.float().double()
+        return x.float().to(x.dtype)
 
     @staticmethod
     def backward(ctx, g):
         return g
 
 
+def _as_t(a, dtype, device):
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=dtype).clone()
+    return torch.from_numpy(np.asarray(a)).to(device=device, dtype=dtype).clone()
+
+
+def _as_i(a, device):
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=torch.int64)
+    return torch.from_numpy(np.asarray(a, np.int64)).to(device)
+
+
 def gpt_train(spec, params, X, labels, lr, stage_bounds, versions, K, emulate: str | None = "bf16",
-              dtype=torch.float64):
+              dtype=torch.float64, device=None):
     """Delayed-SGD pipeline training of a GPTSpec model (see module docstring).
 
-    params: [(W, b)] numpy per profile layer (device layout); X, labels: [n_blocks, B, S] ints.
-    dtype: arithmetic type (float64 for parity; float32 for the timed CPU baseline, no emulation).
-    Returns (losses[K], final params list of numpy (W, b)).
+    params: [(W, b)] per profile layer (device layout), numpy or torch; X, labels: [n_blocks, B, S] ints.
+    dtype: arithmetic type (float64 for parity; float32 for the timed CPU baseline, or on a GPU for
+    full-size checks with TF32 off).  device: torch device of the arithmetic (default CPU).
+    Returns (losses[K], final params list of (W, b)): numpy fp64 on the CPU, torch tensors on a device.
     """
     emul = emulate == "bf16"
-    master = (lambda a: a.float().double()) if emul else (lambda a: a)
+    master = (lambda a: a.float().to(a.dtype)) if emul else (lambda a: a)
     n = len(stage_bounds)
     layer_stage = {}
     for s, (a, b) in enumerate(stage_bounds):
         for l in range(a, b + 1):
             layer_stage[l - 1] = s
     first = [a - 1 for a, _ in stage_bounds]
-    archives = [{0: [(master(torch.from_numpy(np.asarray(params[l - 1][0])).to(dtype).clone()),
-                      master(torch.from_numpy(np.asarray(params[l - 1][1])).to(dtype).clone()))
+    archives = [{0: [(master(_as_t(params[l - 1][0], dtype, device)), master(_as_t(params[l - 1][1], dtype, device)))
                      for l in range(a, b + 1)]} for (a, b) in stage_bounds]
     latest_v = [0] * n
     losses = []
     L = len(params)
     for mb in range(1, K + 1):
         blk = (mb - 1) % X.shape[0]
-        tok = torch.from_numpy(np.asarray(X[blk], np.int64))
-        lab = torch.from_numpy(np.asarray(labels[blk], np.int64))
+        tok = _as_i(X[blk], device)
+        lab = _as_i(labels[blk], device)
         fv = [versions(s, mb, "forward") for s in range(n)]
         if fv != [versions(s, mb, "backward") for s in range(n)]:
             raise ValueError("gpt_train supports forward version == backward version only")
@@ -179,5 +191,8 @@ def gpt_train(spec, params, X, labels, lr, stage_bounds, versions, K, emulate: s
             latest_v[s] = mb
     final = []
     for s in range(n):
-        final.extend((W.double().numpy(), b.double().numpy()) for W, b in archives[s][latest_v[s]])
+        if device is not None:
+            final.extend(archives[s][latest_v[s]])
+        else:
+            final.extend((W.double().numpy(), b.double().numpy()) for W, b in archives[s][latest_v[s]])
     return np.array(losses), final

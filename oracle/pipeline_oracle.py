@@ -194,3 +194,79 @@ def mlp_train(params, X, T, lr, stage_bounds, versions, K, emulate: str | None =
     for s in range(n):
         final.extend(archives[s][latest_v[s]])
     return np.array(losses), final
+
+
+def mlp_train_torch(params, X, T, lr, stage_bounds, versions, K, emulate: str | None = "bf16", device=None,
+                    prune: bool = True):
+    """``mlp_train``'s rule with torch fp32 arithmetic on ``device`` (the checker of full-size
+    configurations, e.g. the 8 x 2-layer MLP-8192 at minibatch 2048, which numpy cannot run in
+    seconds).  Same forward / backward versions, bf16 rounding points (fp32 -> bf16 nearest-even,
+    as ``bf16_round``), fp32 master update onto the latest weights, in-order commits.  TF32 must be
+    off (torch's default for matmul); straight pipelines only.
+
+    params: [(W [out,in], b [out])] torch or numpy; X [n_blocks,B,d0]; T [n_blocks,B,dL].
+    Returns (losses[K] numpy, final [(W, b)] fp32 torch tensors on ``device``).
+    """
+    import torch
+
+    def t32(a):
+        return (a if isinstance(a, torch.Tensor) else torch.from_numpy(np.asarray(a))).to(device=device,
+                                                                                       dtype=torch.float32)
+
+    q = (lambda a: a.bfloat16().float()) if emulate == "bf16" else (lambda a: a)
+    n = len(stage_bounds)
+    L = len(params)
+    layer_stage = {l - 1: s for s, (a, b) in enumerate(stage_bounds) for l in range(a, b + 1)}
+    first = [a - 1 for a, _ in stage_bounds]
+    archives = [{0: [(t32(params[l - 1][0]).clone(), t32(params[l - 1][1]).clone()) for l in range(a, b + 1)]}
+                for (a, b) in stage_bounds]
+    last_reader = [dict() for _ in range(n)]
+    for mb in range(1, K + 1):
+        for s in range(n):
+            for d in ("forward", "backward"):
+                v = versions(s, mb, d)
+                last_reader[s][v] = max(last_reader[s].get(v, 0), mb)
+    latest_v = [0] * n
+    losses = []
+    with torch.no_grad():
+        for mb in range(1, K + 1):
+            blk = (mb - 1) % X.shape[0]
+            x, t = t32(X[blk]), t32(T[blk])
+            B = x.shape[0]
+            fv = [versions(s, mb, "forward") for s in range(n)]
+            bv = [versions(s, mb, "backward") for s in range(n)]
+            h = q(x)
+            inputs = []
+            z = None
+            for l in range(L):
+                s = layer_stage[l]
+                W, b = archives[s][fv[s]][l - first[s]]
+                inputs.append(h)
+                z = h @ q(W).T + b
+                if l < L - 1:
+                    h = q(torch.relu(z))
+            d = z - t
+            losses.append(0.5 / B * float((d.double() * d.double()).sum()))
+            dz = q(d / B)
+            grads = [None] * L
+            for l in range(L - 1, -1, -1):
+                s = layer_stage[l]
+                Xl = inputs[l]
+                grads[l] = (dz.T @ Xl, dz.sum(0))
+                if l > 0:
+                    Wb, _ = archives[s][bv[s]][l - first[s]]
+                    dz = q((dz @ q(Wb)) * (Xl > 0))
+            inputs = None
+            for s, (a, b) in enumerate(stage_bounds):
+                latest = archives[s][latest_v[s]]
+                archives[s][mb] = [(W - lr * grads[l][0], bias - lr * grads[l][1])
+                                   for (W, bias), l in zip(latest, range(a - 1, b))]
+                latest_v[s] = mb
+                if prune:
+                    for v in [v for v in archives[s] if v != mb and last_reader[s].get(v, 0) <= mb]:
+                        del archives[s][v]
+            grads = None
+    final = []
+    for s in range(n):
+        final.extend(archives[s][latest_v[s]])
+    return np.array(losses), final

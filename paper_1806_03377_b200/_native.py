@@ -27,13 +27,16 @@ EXPORTED = (
     "pd_abi_version", "pd_last_error", "pd_device_sm_count", "pd_gemm", "pd_bias_sgd", "pd_sgd_update", "pd_cast", "pd_allreduce_sgd", "pd_bias_grad",
     "pd_flag_signal", "pd_flag_wait", "pd_copy", "pd_ipc_get_handle", "pd_ipc_open", "pd_ipc_close",
     "pd_enable_peer_access", "pd_rt_create", "pd_rt_add_stage", "pd_rt_add_view", "pd_rt_load_program", "pd_rt_run",
-    "pd_rt_records", "pd_rt_set_serial", "pd_rt_set_graph", "pd_rt_layer_timing", "pd_rt_layer_stats", "pd_rt_kernel_timing", "pd_rt_kernel_stats", "pd_rt_launch_count", "pd_rt_destroy",
+    "pd_rt_records", "pd_rt_set_records", "pd_gemm_pick", "pd_rt_set_serial", "pd_rt_set_graph", "pd_rt_layer_timing", "pd_rt_layer_stats", "pd_rt_kernel_timing", "pd_rt_kernel_stats", "pd_rt_launch_count", "pd_rt_destroy",
     "pd_conv3x3", "pd_splitk_plan", "pd_maxpool2", "pd_maxpool2_bwd", "pd_im2col3", "pd_reduce_sgd",
     "pd_colsum_blocks", "pd_bias_grad_tall", "pd_softmax_ce", "pd_memcpy_async", "pd_layer_scratch_floats",
     "pd_layer_save_bytes", "pd_layer_work_bytes", "pd_attention_fwd", "pd_attention_bwd", "pd_layernorm_fwd",
     "pd_layernorm_bwd_blocks", "pd_layernorm_bwd", "pd_embedding_fwd", "pd_embedding_bwd", "pd_softmax_ce_vocab",
 )
 PD_CONV_FWD, PD_CONV_DGRAD, PD_CONV_WGRAD, PD_GEMM_WGRAD_SPLITK = range(4)
+# device pass records (pd_rt_set_records)
+REC_WIDTH = 8
+REC_T0, REC_T1, REC_VER0, REC_VER1, REC_BYTES, REC_COMMIT = range(6)
 
 
 class Epilogue(Structure):
@@ -121,6 +124,8 @@ def lib() -> ctypes.CDLL:
         L.pd_rt_load_program.argtypes = [c_void_p, POINTER(c_int32), c_int]
         L.pd_rt_run.argtypes = [c_void_p, c_void_p, c_int]
         L.pd_rt_records.argtypes = [c_void_p, POINTER(Record), c_int, POINTER(c_int)]
+        L.pd_rt_set_records.argtypes = [c_void_p, c_void_p, c_int, c_void_p]
+        L.pd_gemm_pick.argtypes = [c_int, c_int, c_int, c_int, c_int, c_int, POINTER(c_int), POINTER(c_int)]
         L.pd_rt_destroy.argtypes = [c_void_p]
         L.pd_rt_kernel_timing.argtypes = [c_void_p, c_int]
         L.pd_rt_set_serial.argtypes = [c_void_p, c_int]
@@ -209,6 +214,13 @@ def gemm(A, a_mn: bool, B, b_mn: bool, M: int, N: int, K: int, *, kind: int = EP
                   ldw=ldw if ldw is not None else (master.stride(0) if master is not None else 0), lr=lr)
     check(lib().pd_gemm(dtype_code(A.dtype), ptr(A), int(a_mn), lda, ptr(B), int(b_mn), ldb, M, N, K,
                         ctypes.byref(ep), stream_ptr(stream)), "pd_gemm")
+
+
+def gemm_pick(M: int, N: int, K: int, a_mn: bool, b_mn: bool, kind: int) -> tuple[int, int]:
+    """(CTA group, tile width) the tcgen05 dispatch picks for this problem (gemm.cu choose_cfg)."""
+    cg, bn = c_int(0), c_int(0)
+    check(lib().pd_gemm_pick(M, N, K, int(a_mn), int(b_mn), kind, ctypes.byref(cg), ctypes.byref(bn)), "pd_gemm_pick")
+    return int(cg.value), int(bn.value)
 
 
 def bias_sgd(dz, rows: int, cols: int, b_master, b_out, lr: float, stream=None) -> None:

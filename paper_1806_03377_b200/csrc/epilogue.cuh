@@ -49,6 +49,7 @@ struct EpiArgs {
   int* sig_flag;
   int sig_value;
   int* sig_counter;
+  unsigned long long* sig_bytes;  // nullable: payload bytes stored by the hand-off GEMM (traced runs)
 };
 
 // GPT-2's tanh GELU and its derivative.

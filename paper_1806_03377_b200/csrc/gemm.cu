@@ -464,6 +464,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     float lsum = 0.f;
+    uint32_t stored = 0;  // SIG: payload bytes this lane stored into the peer inbox
     for (int u = unit; u < work; u += units) {
       const int t = u % tiles;
       const int m0 = tile_m(t) * UM + TC_BM * cta;
@@ -483,9 +484,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (row_ok) {
           if (c0 + 32 <= N) {
             lsum += apply_chunk<KIND>(ep, r, c0, v, cur);
+            if constexpr (SIG) stored += 32 * sizeof(__nv_bfloat16);
           } else {
             for (int j = 0; j < 32; ++j)
-              if (c0 + j < N) lsum += epi_elem<KIND, __nv_bfloat16>(ep, r, c0 + j, v[j]);
+              if (c0 + j < N) {
+                lsum += epi_elem<KIND, __nv_bfloat16>(ep, r, c0 + j, v[j]);
+                if constexpr (SIG) stored += sizeof(__nv_bfloat16);
+              }
           }
         }
         cur = nxt;
@@ -501,6 +506,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if constexpr (KIND == EPI_LOSS) {
       lsum = warp_sum(lsum);
       if (lane_id() == 0 && lsum != 0.f) atomicAdd(ep.loss, 0.5f * ep.scale * lsum);
+    }
+    if constexpr (SIG) {
+      stored = __reduce_add_sync(0xffffffffu, stored);
+      if (lane_id() == 0 && ep.sig_bytes && stored) atomicAdd(ep.sig_bytes, (unsigned long long)stored);
     }
   }
   // SIG (a compile-time variant, so kernels without a hand-off carry none of this code: a runtime
@@ -748,23 +757,36 @@ static void pick_cfg(int M, int N, bool b_mn, int* cg, int* bn) {
   }
 }
 
-template <bool A_MN, bool B_MN, int KIND>
-static int launch_bn(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
-                     cudaStream_t st) {
-  if constexpr (!A_MN && B_MN && KIND == EPI_STORE) {
+// The tile configuration of one problem (also reported by pd_gemm_pick for the tests).
+static void choose_cfg(int M, int N, bool a_mn, bool b_mn, int kind, int* cg, int* bn) {
+  if (!a_mn && b_mn && kind == EPI_STORE && N <= 128) {
     // narrow outputs (the im2col'ed first convolution, c_out = 64): a 256-wide tile would be 3/4 padding
-    if (N <= 64) return launch_tc<1, 64, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
-    if (N <= 128) return launch_tc<1, 128, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
+    *cg = 1;
+    *bn = N <= 64 ? 64 : 128;
+    return;
   }
-  if constexpr (is_sgd(KIND) && B_MN) {
+  if (is_sgd(kind) && b_mn) {
     // wgrad + SGD on small weight matrices: 256 x 128 pair tiles double the tile count (e.g. a
     // 1024 x 1024 weight: 32 instead of 16 pair tiles); large ones keep 256-wide tiles, whose
     // operand traffic per flop is lower (measured: 8192^2 0.27 ms vs 0.31 ms with 128-wide tiles)
     const long units256 = (long)((M + 255) / 256) * ((N + 255) / 256);
-    if (M > TC_BM && units256 <= 16) return launch_tc<2, 128, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
+    if (M > TC_BM && units256 <= 16) {
+      *cg = 2;
+      *bn = 128;
+      return;
+    }
   }
+  pick_cfg(M, N, b_mn, cg, bn);
+}
+
+template <bool A_MN, bool B_MN, int KIND>
+static int launch_bn(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
+                     cudaStream_t st) {
   int cg, bn;
-  pick_cfg(M, N, B_MN, &cg, &bn);
+  choose_cfg(M, N, A_MN, B_MN, KIND, &cg, &bn);
+  if constexpr (!A_MN && B_MN && KIND == EPI_STORE) {
+    if (bn == 64) return launch_tc<1, 64, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
+  }
   if (cg == 2) {
     if (bn == 224) return launch_tc<2, 224, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
     if (bn == 192) return launch_tc<2, 192, A_MN, B_MN, KIND>(A, lda, B, ldb, M, N, K, ep, st);
@@ -918,3 +940,9 @@ int gemm_simt(int dtype, const void* A, int a_mn, int64_t lda, const void* B, in
 }
 
 }  // namespace pd
+
+extern "C" int pd_gemm_pick(int M, int N, int K, int a_mn, int b_mn, int kind, int* cg, int* bn) {
+  if (!cg || !bn || M <= 0 || N <= 0 || K <= 0) return pd::set_error(PD_ERR_INVALID, "pd_gemm_pick: bad argument");
+  pd::choose_cfg(M, N, a_mn != 0, b_mn != 0, kind, cg, bn);
+  return 0;
+}

@@ -277,11 +277,12 @@ __global__ void k_flag_signal(int* flag, int v) {
 }
 
 // Bounded spin: ~10 s at %globaltimer resolution, then report through err_word so the host
-// raises SimulationError instead of hanging the GPU.
+// raises SimulationError instead of hanging the GPU.  Flag values grow monotonically modulo 2^32
+// (epoch * 65536 + minibatch, runtime.cu flag_val), so "reached" is a wrap-safe signed difference.
 __global__ void k_flag_wait(const int* flag, int v, int* err) {
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  while (ld_acquire_sys(const_cast<volatile int*>(flag)) < v) {
+  while (flag_before(ld_acquire_sys(const_cast<volatile int*>(flag)), v)) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (t - t0 > 10ull * 1000 * 1000 * 1000) {
@@ -296,6 +297,53 @@ __global__ void k_timestamp(uint64_t* p) {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   *p = t;
+}
+
+// Device pass records (traced runs): each program item gets two one-thread kernels on its
+// worker's stream, bracketing the item's kernels.  Record layout (int64 x PD_REC_WIDTH):
+//   [0] %globaltimer at the start, [1] at the end (ns);
+//   [2] version tag of the weight ring slot the pass reads (wslot) when it starts,
+//   [3] the same tag when it ends (differs only if the slot was overwritten under the pass);
+//   [4] payload bytes stored into another process's inbox (counted by the storing kernel),
+//   [5] version committed (tag written into slot wnew), -1 if none.
+// Ring-slot tags are written only here, in stream order after the committing kernels, so a tag
+// names the version the slot holds for every later kernel of the same worker.
+__global__ void k_rec_begin(int64_t* rec, const int* tag) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  rec[0] = (int64_t)t;
+  rec[2] = tag ? *tag : -1;
+  rec[4] = 0;
+  rec[5] = -1;
+}
+__global__ void k_rec_end(int64_t* rec, const int* tag, int* commit_tag, int commit_v, int64_t host_bytes) {
+  rec[3] = tag ? *tag : -1;
+  if (commit_tag) {
+    *commit_tag = commit_v;
+    rec[5] = commit_v;
+  }
+  if (host_bytes) rec[4] += host_bytes;
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  rec[1] = (int64_t)t;
+}
+int rec_begin(int64_t* rec, const int* tag, cudaStream_t st) {
+  k_rec_begin<<<1, 1, 0, st>>>(rec, tag);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "rec_begin: %s", cudaGetErrorString(e));
+}
+int rec_end(int64_t* rec, const int* tag, int* commit_tag, int commit_v, int64_t host_bytes, cudaStream_t st) {
+  k_rec_end<<<1, 1, 0, st>>>(rec, tag, commit_tag, commit_v, host_bytes);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "rec_end: %s", cudaGetErrorString(e));
+}
+__global__ void k_set_tags(int* tags, int n, int slot, int v) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) tags[i] = i == slot ? v : -1;
+}
+int set_tags(int* tags, int n, int slot, int v, cudaStream_t st) {
+  k_set_tags<<<1, 64, 0, st>>>(tags, n, slot, v);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "set_tags: %s", cudaGetErrorString(e));
 }
 
 int timestamp(uint64_t* p, cudaStream_t st) {

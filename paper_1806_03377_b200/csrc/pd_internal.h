@@ -62,6 +62,9 @@ int bias_grad(int dtype, const void* dz, int rows, int cols, int64_t ld, float* 
 int cast_f32(int dtype, const float* src, void* out, int64_t n, cudaStream_t st);
 int flag_signal(int* flag, int value, cudaStream_t st);
 int timestamp(uint64_t* p, cudaStream_t st);  // *p = %globaltimer (ns) when the stream reaches it
+int rec_begin(int64_t* rec, const int* tag, cudaStream_t st);
+int rec_end(int64_t* rec, const int* tag, int* commit_tag, int commit_v, int64_t host_bytes, cudaStream_t st);
+int set_tags(int* tags, int n, int slot, int v, cudaStream_t st);  // tags[slot] = v, others -1
 int flag_wait(const int* flag, int value, int* err_word, cudaStream_t st);
 
 // Launch with programmatic stream serialization (PDL): the kernel may be scheduled while its

@@ -364,5 +364,7 @@ PD_DEVICE int ld_acquire_sys(volatile int* p) {
   asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Wrap-safe "flag value a has not yet reached target b" (values advance modulo 2^32).
+PD_DEVICE bool flag_before(int a, int b) { return (int)((uint32_t)a - (uint32_t)b) < 0; }
 
 }  // namespace pd

@@ -103,7 +103,12 @@ struct Stage {
   std::vector<const float*> target;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_done = nullptr;
-  bool fused_signal = false;  // this item's hand-off flag was released by the producing GEMM
+  bool fused_signal = false;
+  int tag_index = 0;           // this worker's 64-slot block in rt->tags
+  int64_t out_bytes = 0;       // forward payload per minibatch (the next stage's input)
+  int64_t in_bytes = 0;        // backward payload per minibatch (the previous stage's output gradient)
+  bool replicas_local = true;  // rep > 1: every replica of this stage is hosted by this process
+  int last_round = 0;          // rep > 1: final allreduce round of the loaded program  // this item's hand-off flag was released by the producing GEMM
 };
 
 struct View {
@@ -149,6 +154,12 @@ struct pd_runtime {
   size_t lt_used = 0;
   uint64_t* ts = nullptr;  // caller-owned device buffer [2 * ts_cap]
   int ts_cap = 0;
+  // device pass records (traced runs, pd_rt_set_records): caller-owned int64 [PD_REC_WIDTH x
+  // (1 + items)] (row 0: run-start %globaltimer) and int32 ring-slot version tags [64 per worker]
+  int64_t* rec = nullptr;
+  int rec_cap = 0;
+  int* tags = nullptr;
+  int64_t* cur_rec = nullptr;  // record of the item being enqueued (traced runs)
   bool ktiming = false;
   struct KT { int cls; int worker; double flops; cudaEvent_t a, b; };
   int cur_worker = -1;  // worker of the item being enqueued (per-stage kernel statistics)
@@ -176,7 +187,9 @@ namespace {
     if (rc_) return rc_;   \
   } while (0)
 
-inline int flag_val(int epoch, int v) { return epoch * 65536 + v; }
+// Flag value of minibatch / round v in run `epoch`: monotone modulo 2^32 (waits compare with a
+// wrap-safe signed difference, ptx.cuh flag_before); v < 65536 is enforced by the host.
+inline int flag_val(int epoch, int v) { return (int)((uint32_t)epoch * 65536u + (uint32_t)v); }
 
 // Kernel-time classes (pd_rt_kernel_stats): the three GEMM passes, then the non-GEMM kernels.
 enum { KC_FWD = 0, KC_DGRAD = 1, KC_WGRAD = 2, KC_ATTN = 3, KC_NORM = 4, KC_LOSS = 5, KC_UPDATE = 6, KC_OTHER = 7,
@@ -295,7 +308,29 @@ void fuse_handoff(pd_runtime* rt, Stage& S, EpiArgs& ep, int* flag, int mb, int 
   ep.sig_flag = flag;
   ep.sig_value = flag_val(rt->epoch, mb);
   ep.sig_counter = S.d.sync + counter;
+  ep.sig_bytes = rt->cur_rec ? reinterpret_cast<unsigned long long*>(rt->cur_rec + 4) : nullptr;
   S.fused_signal = true;
+}
+
+// Replicated stage: before writing round `round`'s parity gradient buffers, every replica's
+// reduction that last read them must be done - round-2 of this run, or (rounds 1 and 2, replicas
+// in other processes) the final rounds of the previous run, whose flag values are smaller.
+// In-process replica sets reset their flags at the start of each run (run_body), so their
+// first two rounds have nothing to wait for.
+int wait_parity_free(pd_runtime* rt, Stage& S, int round) {
+  const pd_stage_desc& d = S.d;
+  if (round >= 3) {
+    for (int r = 0; r < d.rep; ++r)
+      PD_TRY(flag_wait(rt->views.at(d.first_worker + r).v.red_done, flag_val(rt->epoch, round - 2), d.err_word,
+                       stream_of(rt, S)));
+    rt->launches += d.rep;
+  } else if (!S.replicas_local && rt->epoch > 1 && S.last_round > 0) {
+    for (int r = 0; r < d.rep; ++r)
+      PD_TRY(flag_wait(rt->views.at(d.first_worker + r).v.red_done, flag_val(rt->epoch - 1, S.last_round),
+                       d.err_word, stream_of(rt, S)));
+    rt->launches += d.rep;
+  }
+  return 0;
 }
 
 int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
@@ -342,10 +377,7 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
   const int wslot = it[PD_IT_WSLOT], wnew = it[PD_IT_WNEW], act = it[PD_IT_ACT], round = it[PD_IT_ROUND];
   const bool replicated = d.rep > 1;
   const int par = round & 1;
-  if (replicated && round >= 3) {
-    // this round's gradient buffers (parity round % 2) were last read by round-2's reductions
-    for (int r = 0; r < d.rep; ++r) PD_TRY(wait_flag(rt, S, rt->views.at(d.first_worker + r).v.red_done, round - 2));
-  }
+  if (replicated) PD_TRY(wait_parity_free(rt, S, round));
   const void* dz = d.is_last ? S.dz_last[act] : S.grad_in[it[PD_IT_GSLOT]];
   for (int l = L - 1; l >= 0; --l) {
     LayerTimer ltimer(rt, S.d.worker, l, 1, ST);
@@ -718,9 +750,7 @@ int run_backward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
   const int wslot = it[PD_IT_WSLOT], wnew = it[PD_IT_WNEW], act = it[PD_IT_ACT], round = it[PD_IT_ROUND];
   const bool replicated = d.rep > 1;
   const int par = round & 1;
-  if (replicated && round >= 3) {
-    for (int r = 0; r < d.rep; ++r) PD_TRY(wait_flag(rt, S, rt->views.at(d.first_worker + r).v.red_done, round - 2));
-  }
+  if (replicated) PD_TRY(wait_parity_free(rt, S, round));
   const bool update = replicated || wnew >= 0;
   const void* dz = d.is_last ? S.dz_last[act] : S.grad_in[it[PD_IT_GSLOT]];
   auto other_tmp = [&](const void* p) { return p == d.tmp[0] ? d.tmp[1] : d.tmp[0]; };
@@ -925,6 +955,26 @@ int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc) {
       return set_error(PD_ERR_INVALID, "worker %d: cross-entropy needs the logits buffer", d.worker);
   }
   S.d.layers = nullptr;
+  {
+    // hand-off payload per minibatch: the stage's output (forward) and input gradient (backward)
+    const int64_t esz = d.dtype == PD_F32 ? 4 : 2;
+    auto feats = [&](const pd_layer& y, bool out) -> int64_t {
+      if (y.kind == PD_LAYER_CONV3)
+        return out ? (int64_t)(y.pool ? (y.h / 2) * (y.w / 2) : y.h * y.w) * y.c_out : (int64_t)y.h * y.w * y.c_in;
+      if (y.kind == PD_LAYER_LINEAR) return out ? y.c_out : y.c_in;
+      if (y.kind == PD_LAYER_EMBED) return out ? (int64_t)y.h * y.c_out : 0;
+      return (int64_t)y.h * y.c_in;  // BLOCK / HEAD: [seq, d] per sequence
+    };
+    if (S.layers.empty()) {
+      S.out_bytes = (int64_t)d.batch * S.dims[L] * esz;
+      S.in_bytes = (int64_t)d.batch * S.dims[0] * esz;
+    } else {
+      S.out_bytes = (int64_t)d.batch * feats(S.layers.back().d, true) * esz;
+      S.in_bytes = (int64_t)d.batch * feats(S.layers.front().d, false) * esz;
+    }
+  }
+  S.tag_index = (int)rt->stages.size();
+  if (d.ring_depth > 64) return set_error(PD_ERR_INVALID, "worker %d: ring depth %d > 64", d.worker, d.ring_depth);
   S.w_master = copy_arr(d.w_master, L);
   S.b_master = copy_arr(d.b_master, L);
   S.w_ring = copy_arr(d.w_ring, (int64_t)L * d.ring_depth);
@@ -991,6 +1041,18 @@ int pd_rt_load_program(pd_runtime* rt, const int32_t* items, int n_items) {
   }
   drop_graph(rt);
   rt->items.assign(items, items + (size_t)n_items * PD_ITEM_WIDTH);
+  for (auto& kv : rt->stages) {
+    Stage& S = kv.second;
+    S.last_round = 0;
+    S.replicas_local = true;
+    for (int r = 0; r < S.d.rep && S.d.rep > 1; ++r)
+      if (rt->views.at(S.d.first_worker + r).v.remote) S.replicas_local = false;
+  }
+  for (int i = 0; i < n_items; ++i) {
+    const int32_t* it = items + (size_t)i * PD_ITEM_WIDTH;
+    Stage& S = rt->stages.at(it[PD_IT_WORKER]);
+    if (S.d.rep > 1) S.last_round = std::max(S.last_round, (int)it[PD_IT_ROUND]);
+  }
   // drain list: final occupant of every remote outbox slot
   rt->drain.clear();
   std::map<std::pair<int*, int>, std::pair<int, int>> last;  // (ack array, slot) -> (worker, mb)
@@ -1065,6 +1127,18 @@ int pd_rt_run(pd_runtime* rt, void* stream, int trace) {
 static int run_body(pd_runtime* rt, cudaStream_t main, int trace) {
   rt->epoch += 1;
   rt->traced = trace != 0;
+  // In-process replica sets: reset their round flags before any stage stream starts.  A captured
+  // graph bakes this run's epoch into every flag value, so without the reset a replay would find
+  // the previous replay's final values already past every target (and not wait at all).
+  for (auto& kv : rt->stages) {
+    Stage& S = kv.second;
+    if (S.d.rep > 1 && S.replicas_local) {
+      PD_CHECK(cudaMemsetAsync(S.d.red_ready, 0, sizeof(int), main));
+      PD_CHECK(cudaMemsetAsync(S.d.red_done, 0, sizeof(int), main));
+    }
+  }
+  const bool recs = rt->traced && rt->rec;
+  if (recs) PD_TRY(timestamp(reinterpret_cast<uint64_t*>(rt->rec), main));  // before any stage starts
   PD_CHECK(cudaEventRecord(rt->ev0, main));
   int max_mb = 0;
   for (size_t i = 0; i < rt->items.size(); i += PD_ITEM_WIDTH) max_mb = std::max(max_mb, rt->items[i + PD_IT_MB]);
@@ -1081,6 +1155,7 @@ static int run_body(pd_runtime* rt, cudaStream_t main, int trace) {
         PD_CHECK(cudaMemcpyAsync(S.b_ring[(size_t)l * S.d.ring_depth + S.d.init_slot], S.b_master[l],
                                  sizeof(float) * b_numel(S, l), cudaMemcpyDeviceToDevice, ST));
     }
+    if (recs) PD_TRY(set_tags(rt->tags + 64 * S.tag_index, 64, S.d.init_slot, 0, ST));  // slot init_slot = v0
     if (S.d.is_last && S.d.loss)  // losses are indexed by minibatch id
       PD_CHECK(cudaMemsetAsync(S.d.loss, 0, sizeof(float) * (size_t)(max_mb + 1), ST));
   }
@@ -1103,6 +1178,10 @@ static int run_body(pd_runtime* rt, cudaStream_t main, int trace) {
       PD_TRY(wait_flag(rt, S, (fwd ? V.v.act_ack : V.v.grad_ack) + it[PD_IT_OUT], it[PD_IT_AWAIT]));
     }
     if (rt->traced) PD_CHECK(cudaEventRecord(rt->ev_start[i], ST));
+    int* stag = recs ? rt->tags + 64 * S.tag_index : nullptr;
+    const int wslot = it[PD_IT_WSLOT], wnew = it[PD_IT_WNEW];
+    rt->cur_rec = recs ? rt->rec + (size_t)(1 + i) * PD_REC_WIDTH : nullptr;
+    if (recs) PD_TRY(rec_begin(rt->cur_rec, op != 2 && wslot >= 0 ? stag + wslot : nullptr, ST));
     const bool layered = !S.layers.empty();
     S.fused_signal = false;
     if (op == 0) PD_TRY(layered ? run_forward_layers(rt, S, it) : run_forward(rt, S, it));
@@ -1117,6 +1196,19 @@ static int run_body(pd_runtime* rt, cudaStream_t main, int trace) {
       if (!S.d.is_first && S.d.remote_prev) PD_TRY(signal_flag(rt, S, S.d.act_ack + it[PD_IT_XSLOT], mb));
       if (!S.d.is_last && S.d.remote_next) PD_TRY(signal_flag(rt, S, S.d.grad_ack + it[PD_IT_GSLOT], mb));
     }
+    if (recs) {
+      // commit: a backward of an unreplicated stage writes version mb, a replica reduce version
+      // round * rep (simulator.py:315); the tag follows the committing kernels
+      const bool commits = wnew >= 0 && (op == 2 || (op == 1 && S.d.rep == 1));
+      const int commit_v = op == 2 ? it[PD_IT_ROUND] * S.d.rep : mb;
+      int64_t host_bytes = 0;  // stand-alone signal path: the payload the flag publishes
+      if ((op == 0 && !S.d.is_last) || (op == 1 && !S.d.is_first))
+        if (rt->views.at(it[PD_IT_DST]).v.remote && !S.fused_signal) host_bytes = op == 0 ? S.out_bytes : S.in_bytes;
+      PD_TRY(rec_end(rt->cur_rec, op != 2 && wslot >= 0 ? stag + wslot : nullptr, commits ? stag + wnew : nullptr,
+                     commit_v, host_bytes, ST));
+      rt->launches += 2;
+    }
+    rt->cur_rec = nullptr;
     PD_CHECK(cudaEventRecord(rt->ev_end[i], ST));
   }
   for (const auto& dr : rt->drain) PD_TRY(wait_flag(rt, rt->stages[dr.worker], dr.flag, dr.mb));
@@ -1145,6 +1237,17 @@ int pd_rt_records(pd_runtime* rt, pd_record* out, int cap, int* n_out) {
     out[k].t_end_ms = b;
   }
   *n_out = k;
+  return 0;
+}
+
+int pd_rt_set_records(pd_runtime* rt, int64_t* rec, int cap, int32_t* tags) {
+  if (!rt) return set_error(PD_ERR_INVALID, "pd_rt_set_records: null runtime");
+  if (rec && (!tags || cap < (int)(rt->items.size() / PD_ITEM_WIDTH)))
+    return set_error(PD_ERR_INVALID, "pd_rt_set_records: need tags and room for %d items",
+                     (int)(rt->items.size() / PD_ITEM_WIDTH));
+  rt->rec = rec;
+  rt->rec_cap = rec ? cap : 0;
+  rt->tags = rec ? tags : nullptr;
   return 0;
 }
 

@@ -30,7 +30,7 @@ import numpy as np
 
 from . import _native as nat
 from .errors import SimulationError, ValidationError
-from .ledger import Mode, SimConfig, SimResult, TraceEvent, build_report
+from .ledger import Mode, SimConfig, SimResult, TraceEvent, VersionLedger, build_report
 from .models import ConvNetSpec, GPTSpec, MLPSpec, init_params_any, make_data_any
 from .orders import Direction, Schedule, build_schedule, stage_inflight_caps
 from .program import Program, compile_program
@@ -66,6 +66,8 @@ def _validate(cfg: SimConfig, ctx, model: MLPSpec) -> None:
         raise ValidationError(f"plan covers {plan.num_layers} layers, profile has {ctx.num_layers}")
     if plan.num_layers != model.num_layers:
         raise ValidationError(f"plan covers {plan.num_layers} layers, model has {model.num_layers}")
+    if cfg.num_minibatches >= 65536:
+        raise ValidationError("num_minibatches must be below 65536 (device flag values are epoch * 65536 + mb)")
     if any(st.replication > 16 for st in plan.stages):
         raise ValidationError("at most 16 replicas per stage")
     for s, st in enumerate(plan.stages):
@@ -184,7 +186,12 @@ class Executor:
             X, T = make_data_any(m)
         else:
             params = None
-            g = torch.Generator(device=dev).manual_seed(m.seed)
+
+            def gen(key: int):
+                # one stream per global layer (key = layer id) or data tensor (key < 0): every
+                # replica of a stage draws identical weights, and the model does not depend on
+                # which rank hosts which stage
+                return torch.Generator(device=dev).manual_seed(m.seed * 1_000_003 + 1000 + key)
         self.bufs: dict[int, _StageBuf] = {}
         workers = self.program.workers
         for wp in self.hosted:
@@ -207,8 +214,9 @@ class Executor:
                     W = torch.from_numpy(params[gl][0]).float().to(dev)
                     bias = torch.from_numpy(params[gl][1]).float().to(dev)
                 elif geo:
-                    W, bias = self._device_init(geo[l], g, dev, torch, getattr(m, "layers", 0))
+                    W, bias = self._device_init(geo[l], gen(gl), dev, torch, getattr(m, "layers", 0))
                 else:
+                    g = gen(gl)
                     W = torch.randn(*wshape, device=dev, generator=g) * math.sqrt(2.0 / din)
                     bias = torch.randn(nb, device=dev, generator=g) * 0.01
                 t["w_master"].append(W.contiguous())
@@ -220,13 +228,13 @@ class Executor:
                 if params is not None:
                     t["act_in"] = torch.from_numpy(X).to(dev).to(torch.int32).contiguous()
                 else:
-                    t["act_in"] = torch.randint(0, m.vocab, (m.n_blocks, m.batch, m.seq), device=dev, generator=g,
+                    t["act_in"] = torch.randint(0, m.vocab, (m.n_blocks, m.batch, m.seq), device=dev, generator=gen(-1),
                                                 dtype=torch.int32)
             elif wp.stage == 0:
                 if params is not None:
                     t["act_in"] = torch.from_numpy(X.reshape(m.n_blocks, m.batch, -1)).to(dev).to(dt).contiguous()
                 else:
-                    t["act_in"] = torch.randn(m.n_blocks, m.batch, dims[0], device=dev, generator=g).to(dt)
+                    t["act_in"] = torch.randn(m.n_blocks, m.batch, dims[0], device=dev, generator=gen(-1)).to(dt)
             else:
                 t["act_in"] = torch.zeros(b.in_depth, m.batch, dims[0], device=dev, dtype=dt)
             if wp.stage < plan.num_stages - 1:
@@ -238,19 +246,19 @@ class Executor:
                         t["target"] = torch.from_numpy(T).to(dev).to(torch.int32).contiguous()
                     else:
                         t["target"] = torch.randint(0, m.vocab, (m.n_blocks, m.batch, m.seq), device=dev,
-                                                    generator=g, dtype=torch.int32)
+                                                    generator=gen(-2), dtype=torch.int32)
                     t["logits"] = torch.empty(m.tokens, m.vocab_pad, device=dev, dtype=torch.float32)
                 elif self.layered:  # cross-entropy: int32 labels and fp32 logits
                     if params is not None:
                         t["target"] = torch.from_numpy(T).to(dev).to(torch.int32).contiguous()
                     else:
-                        t["target"] = torch.randint(0, m.classes, (m.n_blocks, m.batch), device=dev, generator=g,
+                        t["target"] = torch.randint(0, m.classes, (m.n_blocks, m.batch), device=dev, generator=gen(-2),
                                                     dtype=torch.int32)
                     t["logits"] = torch.empty(m.batch, m.classes, device=dev, dtype=torch.float32)
                 elif params is not None:
                     t["target"] = torch.from_numpy(T).float().to(dev).contiguous()
                 else:
-                    t["target"] = torch.randn(m.n_blocks, m.batch, dims[-1], device=dev, generator=g)
+                    t["target"] = torch.randn(m.n_blocks, m.batch, dims[-1], device=dev, generator=gen(-2))
                 t["loss"] = torch.zeros(self.cfg.num_minibatches + 1, device=dev, dtype=torch.float32)
             tmp_feat = (max(max(x.pre_features for x in geo), max(x.in_features for x in geo)) if geo
                         else max(dims))
@@ -439,6 +447,13 @@ class Executor:
         self._prog = prog
         nat.check(L.pd_rt_load_program(rt, prog.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), prog.shape[0]),
                   "pd_rt_load_program")
+        # device pass records of traced runs: timestamps, the version tag each pass read, bytes
+        # stored into peer inboxes, commits (include/pd_b200.h pd_rt_set_records)
+        torch = _torch()
+        self._rec = torch.zeros((1 + prog.shape[0]) * nat.REC_WIDTH, device=self.device, dtype=torch.int64)
+        self._tags = torch.full((64 * max(1, len(self.bufs)),), -1, device=self.device, dtype=torch.int32)
+        nat.check(L.pd_rt_set_records(rt, self._rec.data_ptr(), prog.shape[0], self._tags.data_ptr()),
+                  "pd_rt_set_records")
 
     # ------------------------------------------------------------------ execution
     def step(self, stream=None, trace: bool = False) -> None:
@@ -568,39 +583,86 @@ class Executor:
             raise SimulationError(f"flag wait timed out (values {err}): a neighbour never delivered")
         return [(r.item, r.t_start_ms, r.t_end_ms) for r in recs[: got.value]]
 
-    def trace(self) -> list[TraceEvent]:
+    def device_records(self) -> tuple[int, list[tuple]]:
+        """(run-start %globaltimer ns, [(program row, t_start ns, t_end ns, version at start, version at
+        end, peer bytes stored, committed version)]) of the last traced run, as the device wrote them."""
+        self.records()  # raises SimulationError if a flag wait timed out
+        rec = self._rec.cpu().numpy().reshape(-1, nat.REC_WIDTH)
+        rows = [(self._prog[i], *[int(x) for x in rec[1 + i, :6]]) for i in range(self._prog.shape[0])]
+        return int(rec[0, 0]), rows
+
+    def trace(self, t0_ns: int | None = None) -> list[TraceEvent]:
+        """Passes of the last traced run in seconds since ``t0_ns`` (default: this rank's run start),
+        with the weight version each pass observed on the device."""
+        start, rows = self.device_records()
+        base = start if t0_ns is None else t0_ns
         evs = []
-        for idx, t0, t1 in self.records():
-            row = self._prog[idx]
+        for row, t0, t1, v0, _v1, _b, _c in rows:
             if row[nat.IT_OP] == 2:  # replica reduction: part of the backward round, not a pass
                 continue
             evs.append(TraceEvent(
-                time_start=t0 * 1e-3, time_end=t1 * 1e-3, worker=int(row[nat.IT_WORKER]),
+                time_start=(t0 - base) * 1e-9, time_end=(t1 - base) * 1e-9, worker=int(row[nat.IT_WORKER]),
                 minibatch=int(row[nat.IT_MB]), stage=int(row[nat.IT_STAGE]),
                 direction=Direction.FORWARD if row[nat.IT_OP] == 0 else Direction.BACKWARD,
-                version_used=int(row[nat.IT_VERSION]),
+                version_used=v0,
             ))
         return evs
 
-    def comm_bytes(self) -> float:
-        """Boundary crossings x message size, counted from the executed program (simulator.py:288)."""
-        m = self.model
+    def device_ledger(self, rows) -> VersionLedger:
+        """The reference's VersionLedger (simulator.py:69-99, recorded at pass start :256-264) rebuilt
+        from the version tags the device passes read; a slot overwritten under a pass (tag at the end
+        differs from the start) is a protocol failure and raises SimulationError."""
         plan = self.cfg.plan
+        led = VersionLedger(n_stages=plan.num_stages, stage_replications=tuple(st.replication for st in plan.stages))
+        for s in range(plan.num_stages):
+            led.latest[s] = 0
+        for row, _t0, _t1, v0, v1, _b, commit in sorted(rows, key=lambda r: r[1]):
+            op, s, mb = int(row[nat.IT_OP]), int(row[nat.IT_STAGE]), int(row[nat.IT_MB])
+            if commit >= 0:
+                led.latest[s] = max(led.latest[s], commit)
+            if op == 2:
+                continue
+            d = Direction.FORWARD if op == 0 else Direction.BACKWARD
+            if v0 < 0 or v0 != v1:
+                raise SimulationError(f"worker {int(row[nat.IT_WORKER])} (stage {s}): ring slot {int(row[nat.IT_WSLOT])} "
+                                      f"held version {v0} at the start of {d.value} of minibatch {mb} and {v1} at its end")
+            led.record(s, mb, d, v0)
+        return led
+
+    def comm_bytes(self) -> float:
+        """The reference's communication count (simulator.py:288 and :320-321) over the executed program:
+        each forward crossing adds the boundary activation bytes, each backward crossing the same bytes,
+        and each backward of a replicated stage (rep - 1) x the stage's weight bytes.  With a
+        CostContext the sizes are the profile's (activation_elems, prefix_W_bytes, hw.bytes_per_elem)
+        exactly as the reference computes them; without one they are the model's own."""
+        m, plan, ctx = self.model, self.cfg.plan, self.ctx
+        n = plan.num_stages
+        if ctx is not None:
+            bpe = ctx.hw.bytes_per_elem
+            act = [ctx.profile.layers[st.last_layer - 1].activation_elems * bpe for st in plan.stages[:-1]]
+            wb = [ctx.prefix_W_bytes[st.last_layer] - ctx.prefix_W_bytes[st.first_layer - 1] for st in plan.stages]
+        else:
+            bpe = m.bytes_per_elem
+            if self.layered:
+                act = [m.batch * self.geoms[st.last_layer - 1].out_features * bpe for st in plan.stages[:-1]]
+                wb = [sum(x.w_numel + x.b_numel for x in self.geoms[st.first_layer - 1: st.last_layer]) * bpe
+                      for st in plan.stages]
+            else:
+                act = [m.batch * m.widths[st.last_layer] * bpe for st in plan.stages[:-1]]
+                wb = [sum(a * b + b for a, b in zip(m.widths[st.first_layer - 1: st.last_layer],
+                                                    m.widths[st.first_layer: st.last_layer + 1])) * bpe
+                      for st in plan.stages]
         total = 0.0
         for row in self._prog:
-            s = int(row[nat.IT_STAGE])
-            if row[nat.IT_OP] == 1 and plan.stages[s].replication > 1:  # one gradient per replica per round
-                if self.layered:
-                    w = sum(x.w_numel for x in self.geoms[plan.stages[s].first_layer - 1: plan.stages[s].last_layer])
-                else:
-                    w = sum(a * b for a, b in zip(m.widths[plan.stages[s].first_layer - 1: plan.stages[s].last_layer],
-                                                  m.widths[plan.stages[s].first_layer: plan.stages[s].last_layer + 1]))
-                total += (plan.stages[s].replication - 1) * w * 4 / plan.stages[s].replication
-            if row[nat.IT_OP] == 0 and s < plan.num_stages - 1:
-                total += m.batch * m.widths[plan.stages[s].last_layer] * m.bytes_per_elem
-            if row[nat.IT_OP] == 1 and s > 0:
-                total += m.batch * m.widths[plan.stages[s].first_layer - 1] * m.bytes_per_elem
-        return total
+            op, s = int(row[nat.IT_OP]), int(row[nat.IT_STAGE])
+            if op == 0 and s < n - 1:
+                total += act[s]
+            if op == 1:
+                if plan.stages[s].replication > 1:
+                    total += (plan.stages[s].replication - 1) * wb[s]
+                if s > 0:
+                    total += act[s - 1]
+        return float(total)
 
     def gpu_utilization(self, trace, rank: int | None = None) -> float:
         """Fraction of the steady window during which GPU `rank` runs at least one pass.
@@ -633,22 +695,38 @@ class Executor:
         torch = _torch()
         torch.cuda.synchronize(self.device)
         traced = getattr(self, "_traced", False)
-        trace = self.trace() if traced else []
+        start, rows = self.device_records() if traced else (0, [])
         losses, weights, comm = self.losses(), self.weights(), self.comm_bytes()
         if self.world > 1:
             parts = [None] * self.world
-            torch.distributed.all_gather_object(parts, (trace, losses, weights, comm), group=self.group)
-            trace = sorted((ev for p in parts for ev in p[0]), key=lambda e: (e.time_start, e.worker))
-            losses = next((p[1] for p in parts if p[1] is not None), None)
-            weights = {k: v for p in parts for k, v in p[2].items()}
-            comm = sum(p[3] for p in parts)
+            torch.distributed.all_gather_object(parts, (start, rows, losses, weights, comm), group=self.group)
+            # one time base for the merged trace: the earliest run start over the ranks (every rank
+            # stamps %globaltimer, a node-wide clock, so the ranks' events line up)
+            start = min(p[0] for p in parts) if traced else 0
+            rows = [r for p in parts for r in p[1]]
+            losses = next((p[2] for p in parts if p[2] is not None), None)
+            weights = {k: v for p in parts for k, v in p[3].items()}
+            comm = parts[0][4]  # the program-wide count is the same on every rank
+        trace, ledger, p2p = [], self.program.ledger, 0
+        if traced:
+            trace = sorted((TraceEvent(time_start=(t0 - start) * 1e-9, time_end=(t1 - start) * 1e-9,
+                                       worker=int(row[nat.IT_WORKER]), minibatch=int(row[nat.IT_MB]),
+                                       stage=int(row[nat.IT_STAGE]),
+                                       direction=Direction.FORWARD if row[nat.IT_OP] == 0 else Direction.BACKWARD,
+                                       version_used=v0)
+                            for row, t0, t1, v0, _v1, _b, _c in rows if row[nat.IT_OP] != 2),
+                           key=lambda e: (e.time_start, e.worker))
+            ledger = self.device_ledger(rows)
+            p2p = sum(b for *_r, b, _c in rows)
         report = build_report(self.cfg, trace, len(self.schedule.workers), comm) if trace else None
         bubble, gpu_util = None, None
         if report is not None:
             gpu_util = sum(self.gpu_utilization(trace, r) for r in range(self.world)) / self.world
             bubble = 1.0 - gpu_util
-        return SimResult(report=report, ledger=self.program.ledger, trace=trace, losses=losses, weights=weights,
+        return SimResult(report=report, ledger=ledger, trace=trace, losses=losses, weights=weights,
                          extras={"bubble_fraction": bubble, "gpu_utilization": gpu_util,
+                                 "ledger_source": "device" if traced else "program",
+                                 "p2p_bytes_measured": p2p if traced else None,
                                  "ring_depths": {b.stage: b.ring_depth for b in self.bufs.values()},
                                  "device_of_worker": list(self.program.device_of),
                                  "device": str(self.device), "runs": self.runs})

@@ -1,0 +1,271 @@
+"""Parity at the configurations the bench runs (BASELINE.json configs[1..3]), kernels and pipelines.
+
+1. The exact tcgen05 instantiations the cfg2 bench step launches, at the bench's layer shapes,
+   against a plain PyTorch fp32 reference (TF32 off):
+     wgrad+SGD  k_gemm_tc<2,256,MN,MN,EPI_SGD>    8192 x 8192 x 2048
+     dgrad      k_gemm_tc<2,224,K,MN,EPI_MASK>    2048 x 8192 x 8192
+     forward    k_gemm_tc<2,224,K,K,EPI_STORE>    2048 x 8192 x 8192
+   pd_gemm_pick pins that these shapes reach those instantiations.
+2. Whole pipelines at full size against the oracle's rule run on the same GPU in torch fp32
+   (oracle/*: mlp_train_torch, convnet_train(device=), gpt_train(device=)), same initial weights
+   and data (read back from the executor before the run), same ledger versions:
+     cfg2  8 stages x 2 layers x 8192, minibatch 2048, 25 minibatches (the steady window's minimum)
+     cfg3  VGG-16 7-1 (conv stack x7 with the round-rule reduce, FC x1), 224x224, minibatch 32, 42 mbs
+     cfg4  GPT-2 medium geometry (d 1024, 16 heads, seq 1024, vocab 50257), 2 blocks + embedding +
+           head on 2 stages, minibatch 8 sequences, 12 minibatches
+
+Tolerances (stated here, per north_star): per-minibatch loss rel <= 2e-3 (MLP), 1e-2 (VGG, GPT);
+training delta of every weight tensor ||dW_dev - dW_ref||_F <= 3e-2 ||dW_ref||_F (biases and
+LayerNorm parameters included); the newest ring slot = bf16(master) bit-exact.  Integer results
+(the device-observed ledger) are exact against the program's resolution.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_1806_03377_b200 as pd  # noqa: E402
+from paper_1806_03377_b200 import _native as nat  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+DELTA_TOL = 3e-2
+
+
+@pytest.fixture(autouse=True)
+def _no_tf32():
+    old = (torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    yield
+    torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32 = old
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ 1. bench instantiations
+def _ops(M, N, K, a_mn, b_mn, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    a = torch.randn((K, M) if a_mn else (M, K), device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn((K, N) if b_mn else (N, K), device="cuda", generator=g).to(torch.bfloat16)
+    A = (a.t() if a_mn else a).float()
+    Bm = (b.t() if b_mn else b).float()
+    return a, b, A @ Bm.t()
+
+
+def test_bench_instantiations_are_pinned():
+    assert nat.gemm_pick(8192, 8192, 2048, True, True, nat.EPI_SGD) == (2, 256)
+    assert nat.gemm_pick(2048, 8192, 8192, False, True, nat.EPI_MASK) == (2, 224)
+    assert nat.gemm_pick(2048, 8192, 8192, False, False, nat.EPI_STORE) == (2, 224)
+    assert nat.gemm_pick(2048, 8192, 8192, False, False, nat.EPI_LOSS) == (2, 224)
+
+
+def test_bench_wgrad_sgd_8192x8192x2048():
+    M, N, K = 8192, 8192, 2048
+    a, b, ref = _ops(M, N, K, True, True, 21)
+    g = torch.Generator(device="cuda").manual_seed(22)
+    master = torch.randn(M, N, device="cuda", generator=g) * 0.01
+    m0 = master.clone()
+    ring = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    lr = 1e-3
+    nat.gemm(a, True, b, True, M, N, K, kind=nat.EPI_SGD, out=ring, master=master, lr=lr)
+    torch.cuda.synchronize()
+    expect = m0 - lr * ref
+    # fp32 accumulation order only: |acc| ~ sqrt(K) ~ 45, fp32 eps * K * |terms| << 1e-3 / lr
+    err = (master - expect).abs().max().item()
+    assert err <= 1e-3 * lr * ref.abs().max().item(), err
+    assert torch.equal(ring, master.to(torch.bfloat16))
+
+
+def test_bench_dgrad_mask_2048x8192x8192():
+    M, N, K = 2048, 8192, 8192
+    a, b, ref = _ops(M, N, K, False, True, 31)
+    mask = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    nat.gemm(a, False, b, True, M, N, K, kind=nat.EPI_MASK, out=out, mask=mask)
+    torch.cuda.synchronize()
+    expect = ref * (mask.float() > 0)
+    # one bf16 rounding of the output (rel 2^-9) + fp32 summation order
+    torch.testing.assert_close(out.float(), expect, atol=1e-3 * ref.abs().max().item(), rtol=4e-3)
+    assert torch.equal(out.float() == 0, (mask.float() <= 0) | (out.float() == 0))
+
+
+def test_bench_forward_store_2048x8192x8192():
+    M, N, K = 2048, 8192, 8192
+    a, b, ref = _ops(M, N, K, False, False, 41)
+    bias = torch.randn(N, device="cuda")
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    nat.gemm(a, False, b, False, M, N, K, kind=nat.EPI_STORE, out=out, bias=bias, relu=True)
+    torch.cuda.synchronize()
+    expect = torch.relu(ref + bias)
+    torch.testing.assert_close(out.float(), expect, atol=1e-3 * ref.abs().max().item(), rtol=4e-3)
+
+
+def test_bn224_partial_atom_dgrad_and_forward():
+    """The 224-wide MN-major B tile (112 rows per CTA = one whole + one partial 64-wide swizzle
+    atom) on a shape whose last column tile is partial: 2048 x 8000 (35 full tiles + 160 columns)."""
+    M, N, K = 2048, 8000, 1024
+    assert nat.gemm_pick(M, N, K, False, True, nat.EPI_MASK)[1] in (224, 192, 256, 128)
+    for b_mn, kind in ((True, nat.EPI_MASK), (False, nat.EPI_STORE)):
+        a, b, ref = _ops(M, N, K, False, b_mn, 51)
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        if kind == nat.EPI_MASK:
+            mask = torch.randn(M, N, device="cuda").to(torch.bfloat16)
+            nat.gemm(a, False, b, b_mn, M, N, K, kind=kind, out=out, mask=mask)
+            expect = ref * (mask.float() > 0)
+        else:
+            nat.gemm(a, False, b, b_mn, M, N, K, kind=kind, out=out)
+            expect = ref
+        torch.cuda.synchronize()
+        torch.testing.assert_close(out.float(), expect, atol=1e-3 * ref.abs().max().item(), rtol=4e-3)
+
+
+def test_bn224_forced_mn_major_partial_atom():
+    """N = 224 exactly with K-major A / MN-major B: one pair tile of 224 columns, 112 B rows per CTA."""
+    M, N, K = 256, 224, 512
+    a, b, ref = _ops(M, N, K, False, True, 61)
+    mask = torch.ones(M, N, device="cuda").to(torch.bfloat16)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    nat.gemm(a, False, b, True, M, N, K, kind=nat.EPI_MASK, out=out, mask=mask)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(out.float(), ref, atol=1e-3 * ref.abs().max().item(), rtol=4e-3)
+
+
+# ------------------------------------------------------------------ 2. full-size pipelines
+def _snapshot(ex):
+    """Initial fp32 master (W, b) per global layer and the resident data / target blocks."""
+    plan = ex.cfg.plan
+    params, X, T = {}, None, None
+    for b in sorted(ex.bufs.values(), key=lambda b: b.wid):
+        st = plan.stages[b.stage]
+        for l, (W, bias) in enumerate(zip(b.tensors["w_master"], b.tensors["b_master"])):
+            params.setdefault(st.first_layer + l, (W.clone(), bias.clone()))
+        if b.stage == 0 and X is None:
+            X = b.tensors["act_in"].clone()
+        if b.stage == plan.num_stages - 1 and T is None:
+            T = b.tensors["target"].clone()
+    return [params[k] for k in sorted(params)], X, T
+
+
+def _masters(ex):
+    plan = ex.cfg.plan
+    out = {}
+    for b in sorted(ex.bufs.values(), key=lambda b: b.wid):
+        st = plan.stages[b.stage]
+        for l, (W, bias) in enumerate(zip(b.tensors["w_master"], b.tensors["b_master"])):
+            out.setdefault(st.first_layer + l, []).append((W, bias))
+    return out
+
+
+def _delta_err(dev, ref, init):
+    d_ref = (ref - init).double()
+    return float(((dev - init).double() - d_ref).norm() / max(float(d_ref.norm()), 1e-30))
+
+
+def _check_weights(ex, params0, final, tol=DELTA_TOL):
+    masters = _masters(ex)
+    worst = 0.0
+    for lid, (W_o, b_o) in enumerate(final, start=1):
+        W0, b0 = params0[lid - 1]
+        reps = masters[lid]
+        for W_d, b_d in reps:  # every replica holds the same weights
+            assert torch.equal(W_d, reps[0][0]) and torch.equal(b_d, reps[0][1]), lid
+        W_d, b_d = reps[0]
+        worst = max(worst, _delta_err(W_d, W_o, W0), _delta_err(b_d, b_o, b0))
+    assert worst <= tol, worst
+    return worst
+
+
+def _check_rings(ex, ledger):
+    """The ring slot holding each stage's newest version is bf16(master) bit for bit."""
+    for b in ex.bufs.values():
+        wp = ex.program.workers[b.wid]
+        slot = wp.ring_slot[ledger.latest[b.stage]]
+        for l, W in enumerate(b.tensors["w_master"]):
+            assert torch.equal(b.tensors["w_ring"][l][slot], W.to(b.tensors["w_ring"][l].dtype)), (b.wid, l)
+            assert torch.equal(b.tensors["b_ring"][l][slot], b.tensors["b_master"][l]), (b.wid, l)
+
+
+def _versions(res):
+    return lambda s, mb, d: res.ledger.version_used(s, mb, pd.Direction(d))  # noqa: E731
+
+
+def _run_traced(ex):
+    ex.step(trace=True)
+    res = ex.result()
+    assert res.extras["ledger_source"] == "device"
+    assert res.ledger.entries == ex.program.ledger.entries  # what the device read == the resolution
+    return res
+
+
+def test_cfg2_mlp8192_full_shape_parity():
+    from oracle.pipeline_oracle import mlp_train_torch
+
+    K = 25  # NOAM + 10 and the reference's steady window (simulator.py:364-375) at 8 x 1
+    stages = tuple(pd.Stage(2 * s + 1, 2 * s + 2, 1) for s in range(8))
+    plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=8, machines_used=8)
+    cfg = pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=K)
+    spec = pd.mlp(8192, 16, batch=2048, dtype="bf16", lr=1e-4, n_blocks=4, seed=0)
+    ex = pd.Executor(cfg, model=spec)
+    try:
+        params0, X, T = _snapshot(ex)
+        res = _run_traced(ex)
+        assert pd.staleness_check(res.ledger, "weight_stashing", 8) == []
+        got = np.array(res.losses[:K])
+        want, final = mlp_train_torch(params0, X, T, spec.lr, [(a.first_layer, a.last_layer) for a in stages],
+                                      _versions(res), K, emulate="bf16", device="cuda")
+        rel = np.max(np.abs(got - want) / np.abs(want))
+        assert np.all(np.isfinite(got)) and rel <= 2e-3, (rel, got[:4], want[:4])
+        worst = _check_weights(ex, params0, final)
+        _check_rings(ex, res.ledger)
+        print(f"cfg2 full shape: loss rel {rel:.2e}, worst weight-delta err {worst:.2e}")
+    finally:
+        ex.close()
+
+
+def test_cfg3_vgg16_7_1_full_shape_parity():
+    from oracle.convnet_oracle import convnet_train
+
+    K = 42  # whole rounds of 7 and the steady window (2*2*7 + 2 + 7 = 37)
+    plan = pd.Plan(stages=(pd.Stage(1, 13, 7), pd.Stage(14, 16, 1)), bottleneck_time=1.0, noam=2, machines_used=8)
+    cfg = pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=K)
+    spec = pd.vgg16(batch=32, lr=1e-3, n_blocks=2, seed=0)
+    ex = pd.Executor(cfg, model=spec)
+    try:
+        params0, X, y = _snapshot(ex)
+        res = _run_traced(ex)
+        got = np.array(res.losses[:K])
+        Ximg = X.reshape(X.shape[0], spec.batch, *spec.image)
+        want, final = convnet_train(spec.geoms(), params0, Ximg, y, spec.lr, [(1, 13), (14, 16)], _versions(res), K,
+                                    reps=[7, 1], dtype=torch.float32, device="cuda")
+        rel = np.max(np.abs(got - want) / np.abs(want))
+        assert np.all(np.isfinite(got)) and rel <= 1e-2, (rel, got[:4], want[:4])
+        worst = _check_weights(ex, params0, final)
+        _check_rings(ex, res.ledger)
+        print(f"VGG-16 7-1 full shape: loss rel {rel:.2e}, worst weight-delta err {worst:.2e}")
+    finally:
+        ex.close()
+
+
+def test_cfg4_gpt2_medium_geometry_parity():
+    from oracle.gpt_oracle import gpt_train
+
+    K = 12
+    spec = pd.GPTSpec(vocab=50257, d=1024, heads=16, layers=2, seq=1024, batch=8, lr=1e-3, n_blocks=2, seed=0)
+    bounds = [(1, 2), (3, 4)]
+    plan = pd.Plan(stages=tuple(pd.Stage(a, b, 1) for a, b in bounds), bottleneck_time=1.0, noam=2, machines_used=2)
+    cfg = pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=K)
+    ex = pd.Executor(cfg, model=spec)
+    try:
+        params0, X, y = _snapshot(ex)
+        res = _run_traced(ex)
+        got = np.array(res.losses[:K])
+        want, final = gpt_train(spec, params0, X, y, spec.lr, bounds, _versions(res), K, dtype=torch.float32,
+                                device="cuda")
+        rel = np.max(np.abs(got - want) / np.abs(want))
+        assert np.all(np.isfinite(got)) and rel <= 1e-2, (rel, got[:4], want[:4])
+        worst = _check_weights(ex, params0, final)
+        _check_rings(ex, res.ledger)
+        print(f"GPT-2 medium geometry: loss rel {rel:.2e}, worst weight-delta err {worst:.2e}")
+    finally:
+        ex.close()
