@@ -195,3 +195,49 @@ def test_profile_model_then_solve(which, tmp_path):
     K = max(plan.noam + 10, 2 * plan.noam + plan.num_stages + 2)
     res = pd.run(pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=K), ctx, model=spec)
     assert np.all(np.isfinite(res.losses[:K]))
+
+
+def test_replicated_graph_replay_multi_step_parity():
+    """2-1 plan on one GPU with CUDA-graph replay (the default at world 1): run 1 traced (direct
+    launch), runs 2-4 untraced (run 2 captures the graph, 3 and 4 replay it).  The replica round
+    flags are reset inside every replay, so each run's reductions wait for the run's own gradients:
+    the losses of every run and the final weights match the oracle chained over the four runs."""
+    stages = (pd.Stage(1, 2, 2), pd.Stage(3, 4, 1))
+    plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=pd.noam_for(3, 2), machines_used=3)
+    cfg = pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=16)
+    spec = pd.mlp(256, 4, batch=128, dtype="bf16", lr=2e-3, n_blocks=4, seed=4)
+    X, T = pd.make_data(spec)
+    params = pd.init_params(spec)
+    ex = pd.Executor(cfg, model=spec)
+    try:
+        for run in range(4):
+            ex.step(trace=(run == 0))
+            res = ex.result()
+            if run == 0:
+                led = res.ledger
+            v = lambda s, mb, d: led.version_used(s, mb, pd.Direction(d))  # noqa: E731
+            want, params = mlp_train(params, X, T, spec.lr, [(1, 2), (3, 4)], v, 16, emulate="bf16", reps=[2, 1])
+            got = np.array(res.losses[:16])
+            assert np.max(np.abs(got - want) / np.abs(want)) <= 2e-2, (run, got[:4], want[:4])
+        assert weight_delta_err(spec, res.weights, params) <= 1e-1
+        # both replicas of stage 0 hold bit-identical masters
+        w = [b for b in ex.bufs.values() if b.stage == 0]
+        assert len(w) == 2
+        for l in range(2):
+            assert torch.equal(w[0].tensors["w_master"][l], w[1].tensors["w_master"][l])
+    finally:
+        ex.close()
+
+
+def test_device_ledger_matches_golden_and_counts_no_peer_bytes():
+    """The ledger returned by run() is rebuilt from the version tags the device passes read
+    (pd_rt_set_records) and equals the reference simulator's golden ledger; in one process no
+    payload crosses a process boundary, so the measured peer bytes are zero."""
+    cfg, _ = straight_cfg(4, 2, 20, "vertical_sync")
+    spec = pd.mlp(256, 8, batch=64, dtype="bf16", lr=1e-3, n_blocks=4, seed=3)
+    res = pd.run(cfg, model=spec)
+    assert res.extras["ledger_source"] == "device"
+    g = load_json("ledgers.json")["straight4_k20"]["vertical_sync"]
+    assert sorted([s, mb, d.value, v] for (s, mb, d), v in res.ledger.entries.items()) == g
+    assert res.extras["p2p_bytes_measured"] == 0
+    assert all(ev.time_end > ev.time_start >= 0 for ev in res.trace)

@@ -67,7 +67,24 @@ def main():
             got = np.array(res.losses[:K])
             worst = max(worst, float(np.max(np.abs(got - want) / np.abs(want))))
         rep = runs[-1].report
-        print(json.dumps({"ok": bool(worst <= 3e-2), "max_rel_loss_err": worst, "world": ex.world, "reps": reps,
+        # the traced run's ledger is rebuilt from the version tags every rank's passes read on the
+        # device; it must equal the program's static resolution exactly
+        ledger_ok = runs[-1].extras["ledger_source"] == "device" and \
+            runs[-1].ledger.entries == ex.program.ledger.entries
+        # payload bytes stored into another process's inbox, counted by the storing kernels, equal
+        # the payloads of the program's cross-process hand-offs
+        out_feat = [spec.batch * spec.widths[st.last_layer] * spec.bytes_per_elem for st in plan.stages]
+        want_bytes = 0
+        for it in ex.program.items:
+            if it["dir"] == "R" or it["dst"] < 0:
+                continue
+            if ex.program.device_of[it["dst"]] == ex.program.device_of[it["worker"]]:
+                continue
+            want_bytes += out_feat[it["stage"]] if it["dir"] is pd.Direction.FORWARD else out_feat[it["stage"] - 1]
+        bytes_ok = runs[-1].extras["p2p_bytes_measured"] == want_bytes
+        print(json.dumps({"ok": bool(worst <= 3e-2 and ledger_ok and bytes_ok), "max_rel_loss_err": worst,
+                          "ledger_ok": ledger_ok, "p2p_bytes_measured": runs[-1].extras["p2p_bytes_measured"],
+                          "p2p_bytes_expected": want_bytes, "world": ex.world, "reps": reps,
                           "model": model,
                           "device_of_worker": runs[-1].extras["device_of_worker"],
                           "bubble": runs[-1].extras["bubble_fraction"],
