@@ -6,9 +6,11 @@ prints ONE JSON line on rank 0.
 Workload (BASELINE.json configs[1]): 8-stage, 16-layer MLP, width 8192, bf16 storage /
 fp32 accumulate, straight pipeline (one stage per GPU at N=8; 8/N stages per GPU below),
 1F1B with weight stashing, minibatch 2048, synthetic data.
-A bench "step" = one execution of the whole 1F1B schedule over K=64 minibatches
-(pipeline fill + steady state + drain), i.e. 64*2048 = 131,072 samples; at 8 GPUs the
-fill/drain bubble of a 64-minibatch schedule is 7/71.
+A bench "step" = one execution of the whole 1F1B schedule over K=256 minibatches
+(pipeline fill + steady state + drain), i.e. 256*2048 = 524,288 samples; at 8 GPUs the
+fill/drain bubble of a 256-minibatch schedule is 7/263 (2.7 %).
+`--gpus N` without torchrun re-launches itself as N ranks (torch.distributed.run, 127.0.0.1);
+under torchrun WORLD_SIZE must equal --gpus.
 The working set (~15 GB of weight versions + activations) is >100x the 126 MB L2, so no
 explicit L2 flush is needed between steps.
 """
@@ -41,7 +43,7 @@ def parse():
                    help="mlp: configs[1] MLP-8192 straight pipeline (headline); vgg: configs[2] VGG-16 7-1; "
                         "gpt: configs[3] GPT-2 medium 8-stage")
     p.add_argument("--batch", type=int, default=2048)
-    p.add_argument("--minibatches", type=int, default=64)
+    p.add_argument("--minibatches", type=int, default=256)
     p.add_argument("--width", type=int, default=8192)
     p.add_argument("--layers", type=int, default=16)
     p.add_argument("--stages", type=int, default=8)
@@ -274,6 +276,64 @@ def cpu_sample_gpt(args, seconds=12.0, max_minibatches=1):
                       f"(fwd+bwd+SGD, torch-CPU fp32 autograd oracle) in {el:.1f} s"}
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def reference_simulator_sample(args, seconds=3.0):
+    """The reference's own CPU path for this configuration: pipesim.run + staleness_check
+    (simulator.py:401-411, 423-466) on the same plan / mode / minibatch count, with the measured
+    B200 layer profile (profiles/layer_profiles, reference JSON format) as its cost context.  Runs
+    the unmodified package installed in baseline/_ref (pip --target, git-ignored); None if absent."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "pipesim")):
+        return {"available": False, "why": "baseline/_ref/pipesim not installed"}
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import pipesim as ps
+
+    prof_name = {"mlp": "mlp8192_profile.json", "vgg": "vgg16_profile.json", "gpt": "gpt2_medium_profile.json"}
+    prof = ps.load_profile(os.path.join(REPO, "profiles", "layer_profiles", prof_name[args.workload]))
+    if args.workload == "vgg":
+        stages = (ps.Stage(1, 13, 7), ps.Stage(14, 16, 1))
+        machines, bpe = 8, 2
+    elif args.workload == "gpt":
+        stages = tuple(ps.Stage(a, b, 1) for a, b in GPT_BOUNDS)
+        machines, bpe = 8, 2
+    else:
+        per = args.layers // args.stages
+        stages = tuple(ps.Stage(s * per + 1, (s + 1) * per, 1) for s in range(args.stages))
+        machines, bpe = args.stages, 2
+    if prof.num_layers != stages[-1].last_layer:
+        return {"available": False, "why": f"profile has {prof.num_layers} layers, plan {stages[-1].last_layer}"}
+    ctx = ps.build_context(prof, ps.HardwareSpec(machines=machines, bandwidth=900e9, bytes_per_elem=bpe))
+    plan = ps.Plan(stages=stages, bottleneck_time=1.0, noam=ps.noam_for(machines, stages[0].replication),
+                   machines_used=machines)
+    cfg = ps.SimConfig(plan=plan, mode=ps.Mode(args.mode), num_minibatches=args.minibatches)
+    runs, t0 = 0, time.perf_counter()
+    while True:
+        res = ps.run(cfg, ctx)
+        if plan.stages[0].replication == 1 and all(st.replication == 1 for st in plan.stages):
+            ps.staleness_check(res.ledger, cfg.mode, plan.num_stages)
+        runs += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return {"available": True, "package": f"pipesim {ps.__version__} (unmodified, baseline/_ref)",
+            "ms_per_run": el / runs * 1e3, "runs": runs, "minibatches_per_run": args.minibatches,
+            "threads": 1, "what": "pipesim.run + staleness_check: the reference's discrete-event simulation of "
+                                  "this schedule (simulated, not trained, minibatches)"}
+
+
 def _all_host_threads():
     """Use every host core for the CPU arms even under torchrun (which exports OMP_NUM_THREADS=1)."""
     n = os.cpu_count() or 1
@@ -398,6 +458,13 @@ def run_ours(args, rank, world):
             dist.barrier()
 
     stream = torch.cuda.current_stream()
+    red_dev = "cuda" if dist is not None and dist.get_backend() == "nccl" else "cpu"
+
+    def reduce(vals, op):
+        t = torch.tensor(vals, device=red_dev, dtype=torch.float64)
+        dist.all_reduce(t, op=op)
+        return [float(x) for x in t.cpu()]
+
     _phase("warmup")
     for _ in range(args.warmup):
         ex.step(stream=stream)
@@ -417,9 +484,7 @@ def run_ours(args, rank, world):
         barrier()
     ms = start.elapsed_time(end)
     if dist is not None:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = reduce([ms], dist.ReduceOp.MAX)[0]
     launches = ex.launch_count() - launches0
     # ---------------- roofline pass: one serial step with per-GEMM CUDA events on the launching stream
     _phase("serial roofline pass")
@@ -482,14 +547,15 @@ def run_ours(args, rank, world):
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     if dist is not None:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = reduce([e2e_ms], dist.ReduceOp.MAX)[0]
     e2e_value = args.e2e_steps * args.minibatches * args.batch / (e2e_ms * 1e-3)
+    gpus_active = 1
     if dist is not None:  # whole-job counts
-        t = torch.tensor([float(h2d), float(d2h), float(launches)], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t)
-        h2d, d2h, launches = int(t[0]), int(t[1]), int(t[2])
+        h2d, d2h, launches = [int(x) for x in reduce([float(h2d), float(d2h), float(launches)], dist.ReduceOp.SUM)]
+        devs = [None] * world
+        dist.all_gather_object(devs, torch.cuda.get_device_properties(dev).uuid if hasattr(
+            torch.cuda.get_device_properties(dev), "uuid") else str(dev))
+        gpus_active = len({str(d) for d in devs})
     if rank != 0:
         ex.close()
         return
@@ -533,13 +599,17 @@ def run_ours(args, rank, world):
                                     "bf16 peak (tc_util_busy over all its kernels, tc_util_gemm over its GEMMs only)",
         "model_tflops": value * flops_per_sample / 1e12,
         "model_frac_of_sustained_peak": value * flops_per_sample / 1e12 / peak / world,
+        "gpus_active": gpus_active,
         "bubble_fraction": res.extras.get("bubble_fraction"),
+        "bubble_fraction_whole_run": res.extras.get("bubble_fraction_whole_run"),
         "bubble_definition": "1 - fraction of the reference's steady window (simulator.py:361-385) in which the GPU "
-                             "runs a pass (union over its hosted stages)",
+                             "runs a pass (union over its hosted stages), mean over GPUs; whole_run: the same over "
+                             "each GPU's first pass start .. last pass end, including pipeline fill and drain",
+        "p2p": p2p_summary(res, args),
         "per_worker_utilization": [round(u, 4) for u in rep.per_worker_utilization] if rep else None,
         "steady_minibatches_per_s": rep.steady_throughput if rep else None,
     }
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline:
         _phase("cpu baseline (child process)")
         out["cpu_baseline"] = cpu_baseline_isolated(args)
     ex.close()
@@ -547,17 +617,43 @@ def run_ours(args, rank, world):
     print(json.dumps(out), flush=True)
 
 
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: run N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1; rank 0's JSON line goes to stdout."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    _phase(f"launching {args.gpus} ranks: {' '.join(cmd[1:6])} ...")
+    return subprocess.run(cmd).returncode
+
+
+def p2p_summary(res, args):
+    """Inter-stage payload bytes stored into other processes' inboxes during the traced step,
+    counted by the storing kernels (pd_rt_set_records), per pipeline boundary, and the average
+    rate over the traced step.  Zero at N=1 (every boundary is on one GPU)."""
+    by = res.extras.get("p2p_bytes_by_boundary") or {}
+    span = max((ev.time_end for ev in res.trace), default=0.0)
+    return {"bytes_traced_step": res.extras.get("p2p_bytes_measured"),
+            "bytes_by_boundary": by,
+            "avg_gbs_by_boundary": {k: (v / span / 1e9 if span else None) for k, v in by.items()},
+            "definition": "boundary s = stages s|s+1, both directions; GB/s averaged over the traced step"}
+
+
 def apply_workload_defaults(args):
     if args.workload == "gpt":
         if "--batch" not in sys.argv:
             args.batch = 8  # sequences of 1024 tokens per minibatch
         if "--minibatches" not in sys.argv:
-            args.minibatches = 32  # >= 25 for the reference's steady window at 8 stages
+            args.minibatches = 128  # fill/drain 7/135 at 8 GPUs; >= 25 for the reference's steady window
     if args.workload == "vgg":
         if "--batch" not in sys.argv:
             args.batch = 32  # PAPER.md:816
         if "--minibatches" not in sys.argv:
-            args.minibatches = 42  # 6 allreduce rounds of 7; >= 37 for the reference's steady window
+            args.minibatches = 126  # 18 allreduce rounds of 7; >= 37 for the reference's steady window
     return args
 
 
@@ -568,10 +664,23 @@ def main():
     faulthandler.dump_traceback_later(float(os.environ.get("PD_BENCH_WATCHDOG_S", "600")), exit=False)
     if args.cpu_sample_only:
         _all_host_threads()
-        print(json.dumps(_cpu_sample_for(args)), flush=True)
+        out = _cpu_sample_for(args)
+        out["cpu_model"] = cpu_model()
+        out["host_cpus"] = os.cpu_count()
+        try:
+            out["reference_simulator"] = reference_simulator_sample(args)
+        except Exception as e:  # the baseline is reported, never fatal
+            out["reference_simulator"] = {"available": False, "why": f"{type(e).__name__}: {e}"}
+        print(json.dumps(out), flush=True)
         return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to report a different GPU count",
+              file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank)
         return
@@ -583,7 +692,6 @@ def main():
         # host plumbing only (IPC handle exchange, barriers, max-over-ranks); the data path is
         # peer stores + flags.  Several ranks per GPU (functional testing) cannot use NCCL.
         torch.distributed.init_process_group("nccl" if ngpu >= world else "gloo")
-    args.gpus = world
     run_ours(args, rank, world)
     if world > 1:
         import torch

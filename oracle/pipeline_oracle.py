@@ -197,7 +197,7 @@ def mlp_train(params, X, T, lr, stage_bounds, versions, K, emulate: str | None =
 
 
 def mlp_train_torch(params, X, T, lr, stage_bounds, versions, K, emulate: str | None = "bf16", device=None,
-                    prune: bool = True):
+                    prune: bool = True, dtype=None):
     """``mlp_train``'s rule with torch fp32 arithmetic on ``device`` (the checker of full-size
     configurations, e.g. the 8 x 2-layer MLP-8192 at minibatch 2048, which numpy cannot run in
     seconds).  Same forward / backward versions, bf16 rounding points (fp32 -> bf16 nearest-even,
@@ -205,15 +205,20 @@ def mlp_train_torch(params, X, T, lr, stage_bounds, versions, K, emulate: str | 
     off (torch's default for matmul); straight pipelines only.
 
     params: [(W [out,in], b [out])] torch or numpy; X [n_blocks,B,d0]; T [n_blocks,B,dL].
-    Returns (losses[K] numpy, final [(W, b)] fp32 torch tensors on ``device``).
+    dtype: arithmetic type (default torch.float32; torch.float64 gives the exact-arithmetic reference
+    against which an fp32 run's own rounding drift can be measured).
+    Returns (losses[K] numpy, final [(W, b)] torch tensors on ``device``).
     """
     import torch
 
-    def t32(a):
-        return (a if isinstance(a, torch.Tensor) else torch.from_numpy(np.asarray(a))).to(device=device,
-                                                                                       dtype=torch.float32)
+    dtype = dtype or torch.float32
 
-    q = (lambda a: a.bfloat16().float()) if emulate == "bf16" else (lambda a: a)
+    def t32(a):
+        return (a if isinstance(a, torch.Tensor) else torch.from_numpy(np.asarray(a))).to(device=device, dtype=dtype)
+
+    # bf16 storage: round through fp32 (nearest-even); fp32 master weights
+    q = (lambda a: a.float().bfloat16().to(dtype)) if emulate == "bf16" else (lambda a: a)
+    mst = (lambda a: a.float().to(dtype)) if emulate == "bf16" else (lambda a: a)
     n = len(stage_bounds)
     L = len(params)
     layer_stage = {l - 1: s for s, (a, b) in enumerate(stage_bounds) for l in range(a, b + 1)}
@@ -259,7 +264,7 @@ def mlp_train_torch(params, X, T, lr, stage_bounds, versions, K, emulate: str | 
             inputs = None
             for s, (a, b) in enumerate(stage_bounds):
                 latest = archives[s][latest_v[s]]
-                archives[s][mb] = [(W - lr * grads[l][0], bias - lr * grads[l][1])
+                archives[s][mb] = [(mst(W - lr * grads[l][0]), mst(bias - lr * grads[l][1]))
                                    for (W, bias), l in zip(latest, range(a - 1, b))]
                 latest_v[s] = mb
                 if prune:

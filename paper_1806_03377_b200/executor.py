@@ -664,18 +664,25 @@ class Executor:
                     total += act[s - 1]
         return float(total)
 
-    def gpu_utilization(self, trace, rank: int | None = None) -> float:
+    def gpu_utilization(self, trace, rank: int | None = None, whole_run: bool = False) -> float:
         """Fraction of the steady window during which GPU `rank` runs at least one pass.
 
         The reference's per-worker utilisation (simulator.py:379-385) is kept in the report;
         with several stages per GPU the device-level bubble is 1 - (union of their busy time).
+        whole_run: over the GPU's own first pass start .. last pass end (fill and drain included).
         """
         from .ledger import steady_window
 
         rank = self.rank if rank is None else rank
-        k1, k2 = steady_window(self.cfg, self.cfg.plan.num_stages, self.cfg.plan.stages[0].replication)
-        done = {ev.minibatch: ev.time_end for ev in trace if ev.stage == 0 and ev.direction is Direction.BACKWARD}
-        t1, t2 = done[k1], done[k2]
+        if whole_run:
+            mine = [ev for ev in trace if self.program.device_of[ev.worker] == rank]
+            if not mine:
+                return 0.0
+            t1, t2 = min(ev.time_start for ev in mine), max(ev.time_end for ev in mine)
+        else:
+            k1, k2 = steady_window(self.cfg, self.cfg.plan.num_stages, self.cfg.plan.stages[0].replication)
+            done = {ev.minibatch: ev.time_end for ev in trace if ev.stage == 0 and ev.direction is Direction.BACKWARD}
+            t1, t2 = done[k1], done[k2]
         iv = sorted((max(ev.time_start, t1), min(ev.time_end, t2)) for ev in trace
                     if self.program.device_of[ev.worker] == rank and ev.time_end > t1 and ev.time_start < t2)
         busy, cur_lo, cur_hi = 0.0, None, None
@@ -707,7 +714,7 @@ class Executor:
             losses = next((p[2] for p in parts if p[2] is not None), None)
             weights = {k: v for p in parts for k, v in p[3].items()}
             comm = parts[0][4]  # the program-wide count is the same on every rank
-        trace, ledger, p2p = [], self.program.ledger, 0
+        trace, ledger, p2p, p2p_by = [], self.program.ledger, 0, {}
         if traced:
             trace = sorted((TraceEvent(time_start=(t0 - start) * 1e-9, time_end=(t1 - start) * 1e-9,
                                        worker=int(row[nat.IT_WORKER]), minibatch=int(row[nat.IT_MB]),
@@ -718,15 +725,23 @@ class Executor:
                            key=lambda e: (e.time_start, e.worker))
             ledger = self.device_ledger(rows)
             p2p = sum(b for *_r, b, _c in rows)
+            for row, *_x, b, _c in rows:
+                if b:
+                    k = int(row[nat.IT_STAGE]) - (0 if row[nat.IT_OP] == 0 else 1)
+                    p2p_by[k] = p2p_by.get(k, 0) + int(b)
         report = build_report(self.cfg, trace, len(self.schedule.workers), comm) if trace else None
-        bubble, gpu_util = None, None
+        bubble, gpu_util, bubble_run = None, None, None
         if report is not None:
             gpu_util = sum(self.gpu_utilization(trace, r) for r in range(self.world)) / self.world
             bubble = 1.0 - gpu_util
+        if trace:
+            bubble_run = 1.0 - sum(self.gpu_utilization(trace, r, whole_run=True) for r in range(self.world)) / self.world
         return SimResult(report=report, ledger=ledger, trace=trace, losses=losses, weights=weights,
                          extras={"bubble_fraction": bubble, "gpu_utilization": gpu_util,
+                                 "bubble_fraction_whole_run": bubble_run,
                                  "ledger_source": "device" if traced else "program",
                                  "p2p_bytes_measured": p2p if traced else None,
+                                 "p2p_bytes_by_boundary": p2p_by if traced else None,
                                  "ring_depths": {b.stage: b.ring_depth for b in self.bufs.values()},
                                  "device_of_worker": list(self.program.device_of),
                                  "device": str(self.device), "runs": self.runs})
