@@ -315,7 +315,7 @@ def reference_simulator_sample(args, seconds=3.0):
         machines, bpe = args.stages, 2
     if prof.num_layers != stages[-1].last_layer:
         return {"available": False, "why": f"profile has {prof.num_layers} layers, plan {stages[-1].last_layer}"}
-    ctx = ps.build_context(prof, ps.HardwareSpec(machines=machines, bandwidth=900e9, bytes_per_elem=bpe))
+    ctx = ps.build_context(prof, ps.HardwareSpec(num_machines=machines, bandwidth=900e9, bytes_per_elem=bpe))
     plan = ps.Plan(stages=stages, bottleneck_time=1.0, noam=ps.noam_for(machines, stages[0].replication),
                    machines_used=machines)
     cfg = ps.SimConfig(plan=plan, mode=ps.Mode(args.mode), num_minibatches=args.minibatches)
@@ -553,8 +553,7 @@ def run_ours(args, rank, world):
     if dist is not None:  # whole-job counts
         h2d, d2h, launches = [int(x) for x in reduce([float(h2d), float(d2h), float(launches)], dist.ReduceOp.SUM)]
         devs = [None] * world
-        dist.all_gather_object(devs, torch.cuda.get_device_properties(dev).uuid if hasattr(
-            torch.cuda.get_device_properties(dev), "uuid") else str(dev))
+        dist.all_gather_object(devs, str(getattr(torch.cuda.get_device_properties(dev), "uuid", dev)))
         gpus_active = len({str(d) for d in devs})
     if rank != 0:
         ex.close()
