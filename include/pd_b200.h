@@ -203,6 +203,16 @@ typedef struct pd_stage_desc {
                                pd_layer_scratch_floats) */
   int* sync;                /* 16 zeroed int32: self-resetting counters of single-launch reductions ([0])
                                and of the fused hand-off GEMMs ([8] forward, [9] backward) */
+  /* Fused bias gradient (bf16 MLP stages with rep 1 and every width % 32 == 0): the GEMM that
+   * writes a layer's output gradient dZ also writes fp32 column-sum partials [ceil(batch/32)][width]
+   * of it, and the layer's wgrad+SGD GEMM applies the bias update from them (no separate bias
+   * pass over dZ).  bpart[l], l < n_layers-1: partials of the inner layers' dZ (from this stage's
+   * dgrad); grad_bpart[grad_depth]: one per gradient-inbox slot (written by the next stage's dgrad,
+   * peer-mapped across processes); dz_bpart[act_depth]: the loss gradient's (last stage). */
+  int fused_bias;
+  float* const* bpart;
+  float* const* grad_bpart;
+  float* const* dz_bpart;
 } pd_stage_desc;
 
 enum pd_layer_kind { PD_LAYER_LINEAR = 0, PD_LAYER_CONV3 = 1, PD_LAYER_EMBED = 2, PD_LAYER_BLOCK = 3, PD_LAYER_HEAD = 4 };
@@ -268,6 +278,8 @@ typedef struct pd_worker_view {
   float* const* red_grad;   /* [n_layers*2] */
   float* const* red_bgrad;  /* [n_layers*2] */
   int* red_ready; int* red_done;
+  int fused_bias;           /* the worker consumes bias partials (pd_stage_desc.fused_bias) */
+  float* const* grad_bpart; /* [grad_depth]: partials of its gradient-inbox slots */
 } pd_worker_view;
 
 /* Program item: PD_ITEM_WIDTH int32 fields, see program.py:compile_program. */

@@ -74,7 +74,8 @@ class StageDesc(Structure):
         ("red_grad", POINTER(c_void_p)), ("red_bgrad", POINTER(c_void_p)), ("red_ready", c_void_p),
         ("red_done", c_void_p), ("err_word", c_void_p),
         ("layers", POINTER(LayerDesc)), ("loss_kind", c_int), ("logits", c_void_p), ("part", c_void_p),
-        ("sync", c_void_p),
+        ("sync", c_void_p), ("fused_bias", c_int), ("bpart", POINTER(c_void_p)), ("grad_bpart", POINTER(c_void_p)),
+        ("dz_bpart", POINTER(c_void_p)),
     ]
 
 
@@ -84,7 +85,7 @@ class WorkerView(Structure):
         ("act_in", POINTER(c_void_p)), ("grad_in", POINTER(c_void_p)),
         ("act_ready", c_void_p), ("act_ack", c_void_p), ("grad_ready", c_void_p), ("grad_ack", c_void_p),
         ("red_grad", POINTER(c_void_p)), ("red_bgrad", POINTER(c_void_p)), ("red_ready", c_void_p),
-        ("red_done", c_void_p),
+        ("red_done", c_void_p), ("fused_bias", c_int), ("grad_bpart", POINTER(c_void_p)),
     ]
 
 

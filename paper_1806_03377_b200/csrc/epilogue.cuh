@@ -50,6 +50,18 @@ struct EpiArgs {
   int sig_value;
   int* sig_counter;
   unsigned long long* sig_bytes;  // nullable: payload bytes stored by the hand-off GEMM (traced runs)
+  // Fused bias gradient (tcgen05 path, runtime-internal).  Producer side (EPI_MASK / EPI_LOSS, the
+  // kernels that write a layer's output gradient dZ): when colsum is set, every epilogue warp also
+  // writes the column sums of its 32 stored (bf16-rounded) rows, colsum[(row / 32) * ldc + col],
+  // one plain store per (row block, column): the partials are complete and deterministic, no
+  // atomics.  Consumer side (EPI_SGD, the wgrad of that layer): bpart = those partials ([nrb][ldc],
+  // summed in row-block order), bmaster -= lr * sum; bring (the new version's bias) = bmaster.
+  float* colsum;
+  int64_t ldc;
+  const float* bpart;
+  int nrb;
+  float* bmaster;
+  float* bring;
 };
 
 // GPT-2's tanh GELU and its derivative.
@@ -281,6 +293,23 @@ __device__ __forceinline__ float apply_chunk(const EpiArgs& ep, int64_t r, int64
     for (int i = 0; i < 8; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
   }
   return lsum;
+}
+
+// Column sums of a warp's 32 x 32 block (lane = row, v[j] = column j): a butterfly transpose-
+// reduction (31 shuffles) that leaves the sum of column `lane` in the return value.
+__device__ __forceinline__ float warp_colsum32(float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 16; k >= 1; k >>= 1) {
+    const bool upper = lane & k;
+#pragma unroll
+    for (int i = 0; i < k; ++i) {
+      const float send = upper ? v[i] : v[i + k];
+      const float keep = upper ? v[i + k] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+    }
+  }
+  return v[0];
 }
 
 __device__ __forceinline__ float warp_sum(float x) {

@@ -300,6 +300,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int n0 = tile_n(t) * BN;
       const int row0 = m0 + 32 * q;
       const int nck = c_end - c_begin;
+      // fused bias SGD (rows of this warp, once per row: the tile of column 0, first half):
+      // b -= lr * sum of the producer's per-row-block column sums, written as the new version
+      if (ep.bpart && tile_n(t) == 0 && half == 0 && row0 + lane < M) {
+        const int64_t rr = row0 + lane;
+        float g = 0.f;
+#pragma unroll 8
+        for (int rb = 0; rb < ep.nrb; ++rb) g += ep.bpart[(int64_t)rb * ep.ldc + rr];
+        const float b = ep.bmaster[rr] - ep.lr * g;
+        ep.bmaster[rr] = b;
+        ep.bring[rr] = b;
+      }
       // prefetch the first two master blocks of this tile while its MMAs are still running
       if (lane == 0) {
         bulk_wait_read0();  // previous tile's stores have finished reading both buffers
@@ -491,6 +502,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 lsum += epi_elem<KIND, __nv_bfloat16>(ep, r, c0 + j, v[j]);
                 if constexpr (SIG) stored += sizeof(__nv_bfloat16);
               }
+          }
+        }
+        if constexpr (KIND == EPI_MASK || KIND == EPI_LOSS) {
+          // fused bias gradient: column sums of the 32 stored rows (bf16-rounded, as the
+          // consumer's stand-alone column sum would read them); the host enables it only for
+          // N % 32 == 0, so every chunk is full
+          if (ep.colsum) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = row_ok ? __bfloat162float(__float2bfloat16_rn(v[j])) : 0.f;
+            const float cs = warp_colsum32(v);
+            const int64_t rb = (m0 + 32 * q) / 32;
+            if (m0 + 32 * q < M) {
+              ep.colsum[rb * ep.ldc + c0 + lane_id()] = cs;
+              if constexpr (SIG) stored += sizeof(float);
+            }
           }
         }
         cur = nxt;

@@ -101,6 +101,7 @@ struct Stage {
   std::vector<float*> w_master, b_master, b_ring, red_grad, red_bgrad;
   std::vector<void*> w_ring, act, act_in, grad_in, dz_last;
   std::vector<const float*> target;
+  std::vector<float*> bpart, grad_bpart, dz_bpart;  // fused bias gradient partials (d.fused_bias)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_done = nullptr;
   bool fused_signal = false;
@@ -114,7 +115,7 @@ struct Stage {
 struct View {
   pd_worker_view v{};
   std::vector<void*> act_in, grad_in;
-  std::vector<float*> red_grad, red_bgrad;
+  std::vector<float*> red_grad, red_bgrad, grad_bpart;
 };
 
 template <typename T>
@@ -356,6 +357,10 @@ int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.ldt = N;
       ep.scale = 1.0f / (float)B;
       ep.loss = d.loss + mb;
+      if (d.fused_bias) {  // dZ's column-sum partials for this layer's fused bias update
+        ep.colsum = S.dz_bpart[act];
+        ep.ldc = N;
+      }
     } else {
       // the epilogue stores straight into the next stage's inbox slot (peer-mapped if remote)
       const View& V = rt->views.at(it[PD_IT_DST]);
@@ -398,6 +403,13 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
       if (l == 0) {
         const View& V = rt->views.at(it[PD_IT_DST]);
         fuse_handoff(rt, S, ep, V.v.remote ? V.v.grad_ready + it[PD_IT_OUT] : nullptr, it[PD_IT_MB], 9);
+        if (V.v.fused_bias) {  // the receiver's bias partials ride along with the gradient
+          ep.colsum = V.grad_bpart[it[PD_IT_OUT]];
+          ep.ldc = Kin;
+        }
+      } else if (d.fused_bias) {
+        ep.colsum = S.bpart[l - 1];
+        ep.ldc = Kin;
       }
       PD_TRY(timed_gemm(rt, KC_DGRAD, d.dtype, dz, 0, Nout, Wst, 1, Kin, B, Kin, Nout, EPI_MASK, ep, ST));
     }
@@ -417,10 +429,20 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.out = S.w_ring[(size_t)l * d.ring_depth + wnew];
       ep.ldo = Kin;
       ep.lr = d.lr;
+      if (d.fused_bias) {
+        // the bias update rides in this GEMM's epilogue, from the dZ producer's column sums
+        ep.bpart = l < L - 1 ? S.bpart[l] : (d.is_last ? S.dz_bpart[act] : S.grad_bpart[it[PD_IT_GSLOT]]);
+        ep.nrb = (B + 31) / 32;
+        ep.ldc = Nout;
+        ep.bmaster = S.b_master[l];
+        ep.bring = S.b_ring[(size_t)l * d.ring_depth + wnew];
+      }
       PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, Nout, X, 1, Kin, Nout, Kin, B, EPI_SGD, ep, ST));
-      PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return bias_sgd(d.dtype, dz, B, Nout, Nout, S.b_master[l], S.b_ring[(size_t)l * d.ring_depth + wnew], d.lr,
-                      ST); }));
-      rt->launches += 1;
+      if (!d.fused_bias) {
+        PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return bias_sgd(d.dtype, dz, B, Nout, Nout, S.b_master[l], S.b_ring[(size_t)l * d.ring_depth + wnew], d.lr,
+                        ST); }));
+        rt->launches += 1;
+      }
     }
     dz = out;
   }
@@ -986,6 +1008,17 @@ int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc) {
     S.dz_last = copy_arr(d.dz_last, d.act_depth);
     S.target = copy_arr(d.target, d.n_data_blocks);
   }
+  if (d.fused_bias) {
+    bool ok = d.dtype == PD_BF16 && d.rep == 1 && !d.layers && (L == 1 || d.bpart) &&
+              (d.is_last ? d.dz_bpart != nullptr : d.grad_bpart != nullptr);
+    for (int l = 0; l <= L && ok; ++l) ok = S.dims[l] % 32 == 0;
+    if (!ok)
+      return set_error(PD_ERR_INVALID, "worker %d: fused bias needs a bf16 MLP stage, rep 1, widths %% 32 == 0 "
+                       "and its partial buffers", d.worker);
+    S.bpart = copy_arr(d.bpart, (int64_t)L - 1);
+    if (d.is_last) S.dz_bpart = copy_arr(d.dz_bpart, d.act_depth);
+    else S.grad_bpart = copy_arr(d.grad_bpart, d.grad_depth);
+  }
   if (d.rep > 1) {
     S.red_grad = copy_arr(d.red_grad, (int64_t)L * 2);
     S.red_bgrad = copy_arr(d.red_bgrad, (int64_t)L * 2);
@@ -1006,6 +1039,10 @@ int pd_rt_add_view(pd_runtime* rt, const pd_worker_view* view) {
   V.grad_in = copy_arr(view->grad_in, view->grad_depth);
   V.red_grad = copy_arr(view->red_grad, (int64_t)view->n_layers * 2);
   V.red_bgrad = copy_arr(view->red_bgrad, (int64_t)view->n_layers * 2);
+  if (view->fused_bias) {
+    if (!view->grad_bpart) return set_error(PD_ERR_INVALID, "view of worker %d: fused bias without partials", view->worker);
+    V.grad_bpart = copy_arr(view->grad_bpart, view->grad_depth);
+  }
   rt->views[view->worker] = std::move(V);
   return 0;
 }

@@ -260,6 +260,14 @@ class Executor:
                 else:
                     t["target"] = torch.randn(m.n_blocks, m.batch, dims[-1], device=dev, generator=gen(-2))
                 t["loss"] = torch.zeros(self.cfg.num_minibatches + 1, device=dev, dtype=torch.float32)
+            if self.fused_bias(wp.stage):  # fp32 column-sum partials [ceil(B/32), width] per consumed dZ
+                nrb = -(-m.batch // 32)
+                f32 = dict(device=dev, dtype=torch.float32)
+                t["bpart"] = [torch.zeros(nrb, dims[l + 1], **f32) for l in range(L - 1)]
+                if wp.stage < plan.num_stages - 1:
+                    t["grad_bpart"] = torch.zeros(b.grad_depth, nrb, dims[-1], **f32)
+                else:
+                    t["dz_bpart"] = torch.zeros(b.act_depth, nrb, dims[-1], **f32)
             tmp_feat = (max(max(x.pre_features for x in geo), max(x.in_features for x in geo)) if geo
                         else max(dims))
             t["tmp"] = [torch.empty(m.batch, tmp_feat, device=dev, dtype=dt) for _ in range(2)]
@@ -291,7 +299,16 @@ class Executor:
                 t["red_flags"] = torch.zeros(2, **i32)
             self.bufs[wp.wid] = b
 
-    EXPORTS = ("act_in", "grad_in", "act_ready", "act_ack", "grad_ready", "grad_ack", "red_flags")
+    EXPORTS = ("act_in", "grad_in", "act_ready", "act_ack", "grad_ready", "grad_ack", "red_flags", "grad_bpart")
+
+    def fused_bias(self, stage: int) -> bool:
+        """Bias gradients fused into the GEMM epilogues (include/pd_b200.h pd_stage_desc.fused_bias):
+        bf16 MLP stages with replication 1 and every width a multiple of 32 (PD_FUSED_BIAS=0: off)."""
+        if self.layered or self.model.dtype != "bf16" or os.environ.get("PD_FUSED_BIAS", "1") == "0":
+            return False
+        st = self.cfg.plan.stages[stage]
+        widths = self.model.widths[st.first_layer - 1: st.last_layer + 1]
+        return st.replication == 1 and all(w % 32 == 0 for w in widths)
 
     def _exchange(self) -> None:
         """Publish CUDA IPC handles of this rank's inboxes, flags and reduction buffers."""
@@ -379,6 +396,9 @@ class Executor:
             if wp.stage < n - 1:
                 v.grad_in = arr(self._addr(wid, "grad_in"))
                 v.grad_ready, v.grad_ack = iptr(self._addr(wid, "grad_ready")), iptr(self._addr(wid, "grad_ack"))
+            if wp.stage < n - 1 and self.fused_bias(wp.stage):
+                v.fused_bias = 1
+                v.grad_bpart = arr(self._addr(wid, "grad_bpart"))
             if st.replication > 1:
                 v.red_grad = arr(self._red_addrs(wid, "red_grad"))
                 v.red_bgrad = arr(self._red_addrs(wid, "red_bgrad"))
@@ -432,6 +452,13 @@ class Executor:
             d.tmp[0], d.tmp[1] = t["tmp"][0].data_ptr(), t["tmp"][1].data_ptr()
             d.err_word = t["err"].data_ptr()
             d.sync = t["sync"].data_ptr()
+            if self.fused_bias(b.stage):
+                d.fused_bias = 1
+                d.bpart = arr([x.data_ptr() for x in t["bpart"]])
+                if is_last:
+                    d.dz_bpart = arr([x.data_ptr() for x in t["dz_bpart"]])
+                else:
+                    d.grad_bpart = arr([x.data_ptr() for x in t["grad_bpart"]])
             if self.layered:
                 descs = (nat.LayerDesc * nl)(*[self._layer_desc(x, t["argmax"][l], t["cols"][l], t["save"][l],
                                                                 t["work"]) for l, x in enumerate(b.geoms)])

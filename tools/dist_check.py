@@ -80,7 +80,12 @@ def main():
                 continue
             if ex.program.device_of[it["dst"]] == ex.program.device_of[it["worker"]]:
                 continue
-            want_bytes += out_feat[it["stage"]] if it["dir"] is pd.Direction.FORWARD else out_feat[it["stage"] - 1]
+            if it["dir"] is pd.Direction.FORWARD:
+                want_bytes += out_feat[it["stage"]]
+            else:
+                want_bytes += out_feat[it["stage"] - 1]
+                if ex.fused_bias(it["stage"] - 1):  # + the receiver's fp32 bias partials [ceil(B/32), width]
+                    want_bytes += -(-spec.batch // 32) * spec.widths[plan.stages[it["stage"] - 1].last_layer] * 4
         bytes_ok = runs[-1].extras["p2p_bytes_measured"] == want_bytes
         print(json.dumps({"ok": bool(worst <= 3e-2 and ledger_ok and bytes_ok), "max_rel_loss_err": worst,
                           "ledger_ok": ledger_ok, "p2p_bytes_measured": runs[-1].extras["p2p_bytes_measured"],
