@@ -1240,7 +1240,11 @@ static int run_body(pd_runtime* rt, cudaStream_t main, int trace) {
       const int commit_v = op == 2 ? it[PD_IT_ROUND] * S.d.rep : mb;
       int64_t host_bytes = 0;  // stand-alone signal path: the payload the flag publishes
       if ((op == 0 && !S.d.is_last) || (op == 1 && !S.d.is_first))
-        if (rt->views.at(it[PD_IT_DST]).v.remote && !S.fused_signal) host_bytes = op == 0 ? S.out_bytes : S.in_bytes;
+        if (rt->views.at(it[PD_IT_DST]).v.remote && !S.fused_signal) {
+          host_bytes = op == 0 ? S.out_bytes : S.in_bytes;
+          if (op == 1 && rt->views.at(it[PD_IT_DST]).v.fused_bias)  // + the receiver's bias partials
+            host_bytes += (int64_t)((S.d.batch + 31) / 32) * S.dims[0] * 4;
+        }
       PD_TRY(rec_end(rt->cur_rec, op != 2 && wslot >= 0 ? stag + wslot : nullptr, commits ? stag + wnew : nullptr,
                      commit_v, host_bytes, ST));
       rt->launches += 2;
