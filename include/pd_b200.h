@@ -213,6 +213,11 @@ typedef struct pd_stage_desc {
   float* const* bpart;
   float* const* grad_bpart;
   float* const* dz_bpart;
+  /* Replicated stages: per-layer round flags of the sharded reduction (runtime.cu
+   * issue_layer_reduce): red_lready[l] = last round whose layer-l gradient is complete here,
+   * red_lupd[l] = last round whose layer-l shard this replica has reduced and applied. */
+  int* red_lready;          /* [n_layers] */
+  int* red_lupd;            /* [n_layers] */
 } pd_stage_desc;
 
 enum pd_layer_kind { PD_LAYER_LINEAR = 0, PD_LAYER_CONV3 = 1, PD_LAYER_EMBED = 2, PD_LAYER_BLOCK = 3, PD_LAYER_HEAD = 4 };
@@ -280,6 +285,10 @@ typedef struct pd_worker_view {
   int* red_ready; int* red_done;
   int fused_bias;           /* the worker consumes bias partials (pd_stage_desc.fused_bias) */
   float* const* grad_bpart; /* [grad_depth]: partials of its gradient-inbox slots */
+  /* replicated stages: the replica's fp32 masters (all-gather source) and per-layer round flags */
+  float* const* w_master;   /* [n_layers] */
+  float* const* b_master;   /* [n_layers] */
+  int* red_lready; int* red_lupd;  /* [n_layers] each */
 } pd_worker_view;
 
 /* Program item: PD_ITEM_WIDTH int32 fields, see program.py:compile_program. */
@@ -329,8 +338,10 @@ int pd_rt_records(pd_runtime* rt, pd_record* out, int cap, int* n_out);
  * the version held by each ring slot (written in stream order after the committing kernels).
  * NULL rec switches the records off. */
 #define PD_REC_WIDTH 8
+/* PD_REC_RED_BYTES: bytes a replicated stage's sharded reduction (issued from this backward) read
+ * from the other replicas' memory, counted by the reduction kernels. */
 enum pd_rec_field { PD_REC_T0 = 0, PD_REC_T1 = 1, PD_REC_VER0 = 2, PD_REC_VER1 = 3, PD_REC_BYTES = 4,
-                    PD_REC_COMMIT = 5 };
+                    PD_REC_COMMIT = 5, PD_REC_RED_BYTES = 6 };
 int pd_rt_set_records(pd_runtime* rt, int64_t* rec, int cap, int32_t* tags);
 /* The (cg, bn) tile configuration the tcgen05 GEMM dispatch picks for a problem: cg 1 = one CTA
  * per 128 x bn tile, 2 = a CTA pair per 256 x bn tile (tests pin the bench's instantiations). */

@@ -36,7 +36,7 @@ EXPORTED = (
 PD_CONV_FWD, PD_CONV_DGRAD, PD_CONV_WGRAD, PD_GEMM_WGRAD_SPLITK = range(4)
 # device pass records (pd_rt_set_records)
 REC_WIDTH = 8
-REC_T0, REC_T1, REC_VER0, REC_VER1, REC_BYTES, REC_COMMIT = range(6)
+REC_T0, REC_T1, REC_VER0, REC_VER1, REC_BYTES, REC_COMMIT, REC_RED_BYTES = range(7)
 
 
 class Epilogue(Structure):
@@ -75,7 +75,7 @@ class StageDesc(Structure):
         ("red_done", c_void_p), ("err_word", c_void_p),
         ("layers", POINTER(LayerDesc)), ("loss_kind", c_int), ("logits", c_void_p), ("part", c_void_p),
         ("sync", c_void_p), ("fused_bias", c_int), ("bpart", POINTER(c_void_p)), ("grad_bpart", POINTER(c_void_p)),
-        ("dz_bpart", POINTER(c_void_p)),
+        ("dz_bpart", POINTER(c_void_p)), ("red_lready", c_void_p), ("red_lupd", c_void_p),
     ]
 
 
@@ -86,6 +86,8 @@ class WorkerView(Structure):
         ("act_ready", c_void_p), ("act_ack", c_void_p), ("grad_ready", c_void_p), ("grad_ack", c_void_p),
         ("red_grad", POINTER(c_void_p)), ("red_bgrad", POINTER(c_void_p)), ("red_ready", c_void_p),
         ("red_done", c_void_p), ("fused_bias", c_int), ("grad_bpart", POINTER(c_void_p)),
+        ("w_master", POINTER(c_void_p)), ("b_master", POINTER(c_void_p)), ("red_lready", c_void_p),
+        ("red_lupd", c_void_p),
     ]
 
 

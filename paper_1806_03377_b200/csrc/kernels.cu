@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <algorithm>
 
 #include "pd_internal.h"
 #include "ptx.cuh"
@@ -203,6 +204,128 @@ int allreduce_sgd(int dtype, const float* const* grads, int n_rep, float* master
   return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "allreduce_sgd: %s", cudaGetErrorString(e));
 }
 
+// ---------------------------------------------------------------- sharded replica reduction
+// A replicated stage's round-k update as reduce-scatter + all-gather over peer memory, issued per
+// layer as soon as every replica's layer gradient exists (runtime.cu issue_layer_reduce), so it
+// runs under the remaining backward.  Replica `self` owns the shard [self*shard, (self+1)*shard):
+//   step 1 (k_shard_rs_sgd): sum the R replicas' fp32 gradients of its shard in replica order
+//          0..R-1, master -= lr * sum, ring (new version) = cast(master);
+//   step 2 (k_shard_ag): copy every other owner's updated master shard, ring = cast.
+// Every element is summed once, by its owner, in a fixed order, so all replicas end bit-identical
+// (the same arithmetic as k_allreduce_sgd, which every replica ran over the whole tensor).
+// Peer traffic per replica and round: (R-1)/R of the gradient in step 1 plus (R-1)/R of the
+// master in step 2 = 2 (R-1)/R x 4 B per parameter (k_allreduce_sgd read (R-1) x 4 B).
+// peer_bytes (nullable) accumulates the bytes each kernel loaded from other replicas' memory.
+__device__ __forceinline__ void add_peer_bytes(unsigned long long* ctr, unsigned long long v) {
+  if (!ctr) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(ctr, v);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_shard_rs_sgd(GradPtrs g, int R, int self, float* __restrict__ m, T* __restrict__ o, int64_t lo, int64_t hi,
+                   float lr, unsigned long long* peer_bytes) {
+  unsigned long long nb = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t lo4 = lo / 4, hi4 = hi / 4;  // lo is a multiple of 4
+  for (int64_t i = lo4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi4; i += stride) {
+    float4 s = reinterpret_cast<const float4*>(g.p[0])[i];
+    for (int r = 1; r < R; ++r) {
+      const float4 t = reinterpret_cast<const float4*>(g.p[r])[i];
+      s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
+    }
+    nb += (unsigned long long)(R - 1) * 16;
+    float4 w = reinterpret_cast<float4*>(m)[i];
+    w.x -= lr * s.x; w.y -= lr * s.y; w.z -= lr * s.z; w.w -= lr * s.w;
+    reinterpret_cast<float4*>(m)[i] = w;
+    o[4 * i] = from_f<T>(w.x); o[4 * i + 1] = from_f<T>(w.y);
+    o[4 * i + 2] = from_f<T>(w.z); o[4 * i + 3] = from_f<T>(w.w);
+  }
+  for (int64_t i = 4 * hi4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += stride) {
+    float s = 0.f;
+    for (int r = 0; r < R; ++r) s += g.p[r][i];
+    nb += (unsigned long long)(R - 1) * 4;
+    const float w = m[i] - lr * s;
+    m[i] = w;
+    o[i] = from_f<T>(w);
+  }
+  add_peer_bytes(peer_bytes, nb);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_shard_ag(GradPtrs masters, int self, float* __restrict__ m, T* __restrict__ o, int64_t n, int64_t shard,
+               unsigned long long* peer_bytes) {
+  unsigned long long nb = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n4 = n / 4;  // shard is a multiple of 4, so a float4 never straddles two owners
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const int q = (int)((4 * i) / shard);
+    if (q == self) continue;
+    const float4 w = reinterpret_cast<const float4*>(masters.p[q])[i];
+    nb += 16;
+    reinterpret_cast<float4*>(m)[i] = w;
+    o[4 * i] = from_f<T>(w.x); o[4 * i + 1] = from_f<T>(w.y);
+    o[4 * i + 2] = from_f<T>(w.z); o[4 * i + 3] = from_f<T>(w.w);
+  }
+  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int q = (int)(i / shard);
+    if (q == self) continue;
+    const float w = masters.p[q][i];
+    nb += 4;
+    m[i] = w;
+    o[i] = from_f<T>(w);
+  }
+  add_peer_bytes(peer_bytes, nb);
+}
+
+int64_t shard_size(int64_t n, int R) { return ((n + R - 1) / R + 3) / 4 * 4; }
+
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+int shard_rs_sgd(int dtype, const float* const* grads, int R, int self, float* master, void* out, int64_t n, float lr,
+                 unsigned long long* peer_bytes, cudaStream_t st) {
+  if (R < 2 || R > PD_MAX_REP || self < 0 || self >= R) return set_error(PD_ERR_INVALID, "shard_rs_sgd: %d/%d", self, R);
+  GradPtrs g{};
+  for (int r = 0; r < R; ++r) g.p[r] = grads[r];
+  const int64_t sh = shard_size(n, R);
+  const int64_t lo = std::min<int64_t>(n, self * sh), hi = std::min<int64_t>(n, lo + sh);
+  if (hi <= lo) return 0;
+  const int grid = (int)std::min<int64_t>((int64_t)sm_count() * 4, ((hi - lo) / 4 + 255) / 256 + 1);
+  if (dtype == PD_BF16)
+    k_shard_rs_sgd<__nv_bfloat16><<<grid, 256, 0, st>>>(g, R, self, master, static_cast<__nv_bfloat16*>(out), lo, hi,
+                                                         lr, peer_bytes);
+  else
+    k_shard_rs_sgd<float><<<grid, 256, 0, st>>>(g, R, self, master, static_cast<float*>(out), lo, hi, lr, peer_bytes);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "shard_rs_sgd: %s", cudaGetErrorString(e));
+}
+
+int shard_ag(int dtype, const float* const* masters, int R, int self, float* master, void* out, int64_t n,
+             unsigned long long* peer_bytes, cudaStream_t st) {
+  if (R < 2 || R > PD_MAX_REP || self < 0 || self >= R) return set_error(PD_ERR_INVALID, "shard_ag: %d/%d", self, R);
+  GradPtrs g{};
+  for (int r = 0; r < R; ++r) g.p[r] = masters[r];
+  const int64_t sh = shard_size(n, R);
+  const int grid = (int)std::min<int64_t>((int64_t)sm_count() * 4, (n / 4 + 255) / 256 + 1);
+  if (dtype == PD_BF16)
+    k_shard_ag<__nv_bfloat16><<<grid, 256, 0, st>>>(g, self, master, static_cast<__nv_bfloat16*>(out), n, sh, peer_bytes);
+  else
+    k_shard_ag<float><<<grid, 256, 0, st>>>(g, self, master, static_cast<float*>(out), n, sh, peer_bytes);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "shard_ag: %s", cudaGetErrorString(e));
+}
+
 template <typename T>
 __global__ void __launch_bounds__(512)
     k_bias_grad(const T* __restrict__ dz, int rows, int cols, int64_t ld, float* __restrict__ out) {
@@ -305,7 +428,8 @@ __global__ void k_timestamp(uint64_t* p) {
 //   [2] version tag of the weight ring slot the pass reads (wslot) when it starts,
 //   [3] the same tag when it ends (differs only if the slot was overwritten under the pass);
 //   [4] payload bytes stored into another process's inbox (counted by the storing kernel),
-//   [5] version committed (tag written into slot wnew), -1 if none.
+//   [5] version committed (tag written into slot wnew), -1 if none;
+//   [6] bytes a replicated stage's sharded reduction read from other replicas (backward items).
 // Ring-slot tags are written only here, in stream order after the committing kernels, so a tag
 // names the version the slot holds for every later kernel of the same worker.
 __global__ void k_rec_begin(int64_t* rec, const int* tag) {
@@ -315,6 +439,7 @@ __global__ void k_rec_begin(int64_t* rec, const int* tag) {
   rec[2] = tag ? *tag : -1;
   rec[4] = 0;
   rec[5] = -1;
+  rec[6] = 0;
 }
 __global__ void k_rec_end(int64_t* rec, const int* tag, int* commit_tag, int commit_v, int64_t host_bytes) {
   rec[3] = tag ? *tag : -1;

@@ -59,6 +59,13 @@ int sgd_update(int dtype, float* master, const float* grad, void* out, int64_t n
 int allreduce_sgd(int dtype, const float* const* grads, int n_rep, float* master, void* out, int64_t n, float lr,
                   cudaStream_t st);
 int bias_grad(int dtype, const void* dz, int rows, int cols, int64_t ld, float* out, cudaStream_t st);
+// Sharded replica reduction (kernels.cu): reduce-scatter + SGD of this replica's shard, then the
+// all-gather of the other owners' updated master shards.  peer_bytes: nullable byte counter.
+int64_t shard_size(int64_t n, int R);
+int shard_rs_sgd(int dtype, const float* const* grads, int R, int self, float* master, void* out, int64_t n, float lr,
+                 unsigned long long* peer_bytes, cudaStream_t st);
+int shard_ag(int dtype, const float* const* masters, int R, int self, float* master, void* out, int64_t n,
+             unsigned long long* peer_bytes, cudaStream_t st);
 int cast_f32(int dtype, const float* src, void* out, int64_t n, cudaStream_t st);
 int flag_signal(int* flag, int value, cudaStream_t st);
 int timestamp(uint64_t* p, cudaStream_t st);  // *p = %globaltimer (ns) when the stream reaches it

@@ -103,6 +103,9 @@ struct Stage {
   std::vector<const float*> target;
   std::vector<float*> bpart, grad_bpart, dz_bpart;  // fused bias gradient partials (d.fused_bias)
   cudaStream_t stream = nullptr;
+  cudaStream_t rstream = nullptr;      // rep > 1: the sharded reduction runs here, under the backward
+  cudaEvent_t ev_red = nullptr;        // rep > 1: this round's reduction finished (joined by REDUCE)
+  std::vector<cudaEvent_t> ev_layer;   // rep > 1: layer l's gradient is complete (fork to rstream)
   cudaEvent_t ev_done = nullptr;
   bool fused_signal = false;
   int tag_index = 0;           // this worker's 64-slot block in rt->tags
@@ -115,7 +118,7 @@ struct Stage {
 struct View {
   pd_worker_view v{};
   std::vector<void*> act_in, grad_in;
-  std::vector<float*> red_grad, red_bgrad, grad_bpart;
+  std::vector<float*> red_grad, red_bgrad, grad_bpart, w_master, b_master;
 };
 
 template <typename T>
@@ -334,6 +337,54 @@ int wait_parity_free(pd_runtime* rt, Stage& S, int round) {
   return 0;
 }
 
+// Sharded reduction of a replicated stage, issued per layer from the backward as
+// soon as this replica's layer-l gradient of round `round` is complete: the stage stream signals
+// red_lready[l] and forks to the reduction stream, which waits for every replica's layer-l
+// gradient, reduce-scatters + applies SGD to the shard this replica owns, signals red_lupd[l],
+// waits for every owner's update and all-gathers the other shards of the new master (and writes
+// the new version into ring slot wnew).  After the stage's last layer (l == 0) it signals red_done
+// and records ev_red, which the round's REDUCE item joins back into the stage stream.  Serial mode
+// (one stream for all workers) cannot overlap replicas, so it keeps the whole-tensor reduction.
+bool sharded_reduce(const pd_runtime* rt, const Stage& S) {
+  return S.d.rep > 1 && !rt->serial && S.rstream && S.d.red_lready && S.d.red_lupd;
+}
+
+int issue_layer_reduce(pd_runtime* rt, Stage& S, int l, int round, int wnew, cudaStream_t ST) {
+  const pd_stage_desc& d = S.d;
+  const int val = flag_val(rt->epoch, round), par = round & 1;
+  if (wnew < 0) return set_error(PD_ERR_INVALID, "worker %d: replicated backward without a commit slot", d.worker);
+  PD_TRY(flag_signal(d.red_lready + l, val, ST));
+  PD_CHECK(cudaEventRecord(S.ev_layer[l], ST));
+  cudaStream_t R = S.rstream;
+  PD_CHECK(cudaStreamWaitEvent(R, S.ev_layer[l], 0));
+  std::vector<const float*> g(d.rep), gb(d.rep), m(d.rep), mb(d.rep);
+  for (int r = 0; r < d.rep; ++r) {
+    const View& V = rt->views.at(d.first_worker + r);
+    PD_TRY(flag_wait(V.v.red_lready + l, val, d.err_word, R));
+    g[r] = V.red_grad[(size_t)l * 2 + par];
+    gb[r] = V.red_bgrad[(size_t)l * 2 + par];
+    m[r] = V.w_master[l];
+    mb[r] = V.b_master[l];
+  }
+  unsigned long long* ctr = rt->cur_rec ? reinterpret_cast<unsigned long long*>(rt->cur_rec + 6) : nullptr;
+  void* ring = S.w_ring[(size_t)l * d.ring_depth + wnew];
+  float* bring = S.b_ring[(size_t)l * d.ring_depth + wnew];
+  const int64_t nw = w_numel(S, l), nb = b_numel(S, l);
+  PD_TRY(shard_rs_sgd(d.dtype, g.data(), d.rep, d.replica, S.w_master[l], ring, nw, d.lr, ctr, R));
+  if (nb > 0) PD_TRY(shard_rs_sgd(PD_F32, gb.data(), d.rep, d.replica, S.b_master[l], bring, nb, d.lr, ctr, R));
+  PD_TRY(flag_signal(d.red_lupd + l, val, R));
+  for (int r = 0; r < d.rep; ++r) PD_TRY(flag_wait(rt->views.at(d.first_worker + r).v.red_lupd + l, val, d.err_word, R));
+  PD_TRY(shard_ag(d.dtype, m.data(), d.rep, d.replica, S.w_master[l], ring, nw, ctr, R));
+  if (nb > 0) PD_TRY(shard_ag(PD_F32, mb.data(), d.rep, d.replica, S.b_master[l], bring, nb, ctr, R));
+  rt->launches += 4 + 2 * d.rep + (nb > 0 ? 2 : 0);
+  if (l == 0) {
+    PD_TRY(flag_signal(d.red_done, val, R));
+    PD_CHECK(cudaEventRecord(S.ev_red, R));
+    rt->launches += 1;
+  }
+  return 0;
+}
+
 int run_forward(pd_runtime* rt, Stage& S, const int32_t* it) {
   cudaStream_t ST = stream_of(rt, S);
   const pd_stage_desc& d = S.d;
@@ -421,6 +472,7 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
       PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, Nout, X, 1, Kin, Nout, Kin, B, EPI_GRADF32, ep, ST));
       PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return bias_grad(d.dtype, dz, B, Nout, Nout, S.red_bgrad[(size_t)l * 2 + par], ST); }));
       rt->launches += 1;
+      if (sharded_reduce(rt, S)) PD_TRY(issue_layer_reduce(rt, S, l, round, wnew, ST));
     } else if (wnew >= 0) {
       // wgrad + SGD onto the latest weights, written as version mb into ring slot wnew
       EpiArgs ep{};
@@ -446,7 +498,7 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
     }
     dz = out;
   }
-  if (replicated) PD_TRY(signal_flag(rt, S, d.red_ready, round));
+  if (replicated && !sharded_reduce(rt, S)) PD_TRY(signal_flag(rt, S, d.red_ready, round));
   return 0;
 }
 
@@ -812,6 +864,7 @@ int run_backward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
         PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, y.c_out, X, 1, y.c_in, y.c_out, y.c_in, B, EPI_GRADF32, ep, ST));
         PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return bias_grad(d.dtype, dz, B, y.c_out, y.c_out, gb, ST); }));
         rt->launches += 1;
+        if (sharded_reduce(rt, S)) PD_TRY(issue_layer_reduce(rt, S, l, round, wnew, ST));  // after its dgrad
       } else if (update) {
         EpiArgs ep{};
         ep.master = S.w_master[l];
@@ -867,9 +920,11 @@ int run_backward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
       ep.ldm = y.c_in;
       PD_TRY(timed_conv(rt, KC_DGRAD, PD_CONV_DGRAD, dy, Wst, B, y.h, y.w, y.c_in, y.c_out, EPI_MASK, ep, ST));
     }
+    // the layer's new version may overwrite ring slot wnew only after this layer's dgrad read wslot
+    if (replicated && sharded_reduce(rt, S)) PD_TRY(issue_layer_reduce(rt, S, l, round, wnew, ST));
     dz = dst;
   }
-  if (replicated) PD_TRY(signal_flag(rt, S, d.red_ready, round));
+  if (replicated && !sharded_reduce(rt, S)) PD_TRY(signal_flag(rt, S, d.red_ready, round));
   return 0;
 }
 
@@ -879,6 +934,10 @@ int run_reduce(pd_runtime* rt, Stage& S, const int32_t* it) {
   cudaStream_t ST = stream_of(rt, S);
   const pd_stage_desc& d = S.d;
   const int round = it[PD_IT_ROUND], wnew = it[PD_IT_WNEW], par = round & 1;
+  if (sharded_reduce(rt, S)) {  // issued per layer from the backward; join it back here
+    PD_CHECK(cudaStreamWaitEvent(ST, S.ev_red, 0));
+    return 0;
+  }
   for (int r = 0; r < d.rep; ++r) PD_TRY(wait_flag(rt, S, rt->views.at(d.first_worker + r).v.red_ready, round));
   std::vector<const float*> g(d.rep), gb(d.rep);
   for (int l = 0; l < d.n_layers; ++l) {
@@ -1027,6 +1086,12 @@ int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc) {
   PD_CHECK(cudaSetDevice(rt->device));
   PD_CHECK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
   PD_CHECK(cudaEventCreateWithFlags(&S.ev_done, cudaEventDisableTiming));
+  if (d.rep > 1 && d.red_lready && d.red_lupd) {
+    PD_CHECK(cudaStreamCreateWithFlags(&S.rstream, cudaStreamNonBlocking));
+    PD_CHECK(cudaEventCreateWithFlags(&S.ev_red, cudaEventDisableTiming));
+    S.ev_layer.assign(L, nullptr);
+    for (int l = 0; l < L; ++l) PD_CHECK(cudaEventCreateWithFlags(&S.ev_layer[l], cudaEventDisableTiming));
+  }
   rt->stages.emplace(d.worker, std::move(S));
   return 0;
 }
@@ -1039,6 +1104,10 @@ int pd_rt_add_view(pd_runtime* rt, const pd_worker_view* view) {
   V.grad_in = copy_arr(view->grad_in, view->grad_depth);
   V.red_grad = copy_arr(view->red_grad, (int64_t)view->n_layers * 2);
   V.red_bgrad = copy_arr(view->red_bgrad, (int64_t)view->n_layers * 2);
+  if (view->w_master) {
+    V.w_master = copy_arr(view->w_master, view->n_layers);
+    V.b_master = copy_arr(view->b_master, view->n_layers);
+  }
   if (view->fused_bias) {
     if (!view->grad_bpart) return set_error(PD_ERR_INVALID, "view of worker %d: fused bias without partials", view->worker);
     V.grad_bpart = copy_arr(view->grad_bpart, view->grad_depth);
@@ -1172,6 +1241,8 @@ static int run_body(pd_runtime* rt, cudaStream_t main, int trace) {
     if (S.d.rep > 1 && S.replicas_local) {
       PD_CHECK(cudaMemsetAsync(S.d.red_ready, 0, sizeof(int), main));
       PD_CHECK(cudaMemsetAsync(S.d.red_done, 0, sizeof(int), main));
+      if (S.d.red_lready) PD_CHECK(cudaMemsetAsync(S.d.red_lready, 0, sizeof(int) * S.d.n_layers, main));
+      if (S.d.red_lupd) PD_CHECK(cudaMemsetAsync(S.d.red_lupd, 0, sizeof(int) * S.d.n_layers, main));
     }
   }
   const bool recs = rt->traced && rt->rec;
@@ -1375,6 +1446,12 @@ int pd_rt_destroy(pd_runtime* rt) {
     cudaStreamSynchronize(kv.second.stream);
     cudaStreamDestroy(kv.second.stream);
     cudaEventDestroy(kv.second.ev_done);
+    if (kv.second.rstream) {
+      cudaStreamSynchronize(kv.second.rstream);
+      cudaStreamDestroy(kv.second.rstream);
+      cudaEventDestroy(kv.second.ev_red);
+      for (auto e : kv.second.ev_layer) cudaEventDestroy(e);
+    }
   }
   for (auto e : rt->ev_start) cudaEventDestroy(e);
   for (auto e : rt->ev_end) cudaEventDestroy(e);

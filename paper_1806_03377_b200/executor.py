@@ -297,6 +297,7 @@ class Executor:
                 t["red_bgrad"] = [[torch.zeros(t["b_master"][l].numel(), device=dev) for _ in range(2)]
                                   for l in range(L)]
                 t["red_flags"] = torch.zeros(2, **i32)
+                t["red_lflags"] = torch.zeros(2, L, **i32)  # per-layer ready / updated rounds
             self.bufs[wp.wid] = b
 
     EXPORTS = ("act_in", "grad_in", "act_ready", "act_ack", "grad_ready", "grad_ack", "red_flags", "grad_bpart")
@@ -333,6 +334,9 @@ class Executor:
             if "red_grad" in b.tensors:
                 ent["red_grad"] = [[export(g) for g in pair] for pair in b.tensors["red_grad"]]
                 ent["red_bgrad"] = [[export(g) for g in pair] for pair in b.tensors["red_bgrad"]]
+                ent["w_master"] = [export(w) for w in b.tensors["w_master"]]
+                ent["b_master"] = [export(x) for x in b.tensors["b_master"]]
+                ent["red_lflags"] = export(b.tensors["red_lflags"])
             mine[b.wid] = ent
         gathered = [None] * self.world
         torch.distributed.all_gather_object(gathered, mine, group=self.group)
@@ -354,6 +358,12 @@ class Executor:
         h, off, slot, count = ent
         base = nat.ipc_import(h, off)
         return [base + k * slot for k in range(count)]
+
+    def _list_addrs(self, wid: int, name: str) -> list[int]:
+        """Addresses of worker wid's per-layer tensor list `name` (local or peer-mapped)."""
+        if self.program.device_of[wid] == self.rank:
+            return [x.data_ptr() for x in self.bufs[wid].tensors[name]]
+        return [nat.ipc_import(h, off) for (h, off, _s, _c) in self._remote[wid][name]]
 
     def _red_addrs(self, wid: int, name: str) -> list[int]:
         if self.program.device_of[wid] == self.rank:
@@ -404,6 +414,10 @@ class Executor:
                 v.red_bgrad = arr(self._red_addrs(wid, "red_bgrad"))
                 fl = self._addr(wid, "red_flags")
                 v.red_ready, v.red_done = fl[0], fl[1]
+                v.w_master = arr(self._list_addrs(wid, "w_master"))
+                v.b_master = arr(self._list_addrs(wid, "b_master"))
+                lf = self._addr(wid, "red_lflags")  # rows: ready, updated
+                v.red_lready, v.red_lupd = lf[0], lf[1]
             self._keep.append(v)
             nat.check(L.pd_rt_add_view(rt, ctypes.byref(v)), "pd_rt_add_view")
 
@@ -449,6 +463,7 @@ class Executor:
                 d.red_grad = arr([g.data_ptr() for pair in t["red_grad"] for g in pair])
                 d.red_bgrad = arr([g.data_ptr() for pair in t["red_bgrad"] for g in pair])
                 d.red_ready, d.red_done = t["red_flags"].data_ptr(), t["red_flags"].data_ptr() + 4
+                d.red_lready, d.red_lupd = t["red_lflags"][0].data_ptr(), t["red_lflags"][1].data_ptr()
             d.tmp[0], d.tmp[1] = t["tmp"][0].data_ptr(), t["tmp"][1].data_ptr()
             d.err_word = t["err"].data_ptr()
             d.sync = t["sync"].data_ptr()
@@ -730,10 +745,13 @@ class Executor:
         torch.cuda.synchronize(self.device)
         traced = getattr(self, "_traced", False)
         start, rows = self.device_records() if traced else (0, [])
+        # bytes the replicas' sharded reductions read from each other (counted by the kernels)
+        red = int(self._rec.view(-1, nat.REC_WIDTH)[1:, nat.REC_RED_BYTES].sum().item()) if traced else 0
         losses, weights, comm = self.losses(), self.weights(), self.comm_bytes()
         if self.world > 1:
             parts = [None] * self.world
-            torch.distributed.all_gather_object(parts, (start, rows, losses, weights, comm), group=self.group)
+            torch.distributed.all_gather_object(parts, (start, rows, losses, weights, comm, red), group=self.group)
+            red = sum(p[5] for p in parts)
             # one time base for the merged trace: the earliest run start over the ranks (every rank
             # stamps %globaltimer, a node-wide clock, so the ranks' events line up)
             start = min(p[0] for p in parts) if traced else 0
@@ -769,6 +787,7 @@ class Executor:
                                  "ledger_source": "device" if traced else "program",
                                  "p2p_bytes_measured": p2p if traced else None,
                                  "p2p_bytes_by_boundary": p2p_by if traced else None,
+                                 "replica_reduce_bytes_measured": red if traced else None,
                                  "ring_depths": {b.stage: b.ring_depth for b in self.bufs.values()},
                                  "device_of_worker": list(self.program.device_of),
                                  "device": str(self.device), "runs": self.runs})

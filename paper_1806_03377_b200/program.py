@@ -237,9 +237,10 @@ def compile_program(schedule: Schedule, mode, *, n_blocks: int = 1, world_size: 
                         rec["out"] = jd % dst.grad_depth
                         if jd >= dst.grad_depth:
                             rec["war"] = ("B", s - 1, dst.mine[jd - dst.grad_depth])
-                if rep == 1:
-                    rec["wnew"] = commit_slot
-                else:
+                # the commit slot: written by this backward (rep 1) or by the round's sharded
+                # reduction, which the backward issues layer by layer (rep > 1)
+                rec["wnew"] = commit_slot
+                if rep > 1:
                     # replicated stage (round rule): the backward only produces this
                     # replica's gradient; a REDUCE item sums all replicas' round-k gradients and commits
                     rec["round"] = rounds

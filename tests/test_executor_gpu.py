@@ -149,6 +149,12 @@ def test_replicated_stage_round_rule_parity(serial):
     # both replicas hold the same weights; compare replica 0's (worker 0) with the oracle
     assert weight_delta_err(spec, res.weights, final) <= 1e-1
     assert res.report is not None and res.report.steady_throughput > 0
+    if not serial:
+        # sharded reduction: per round, every replica reads (R-1)/R of the gradient (reduce-scatter)
+        # and (R-1)/R of the master (all-gather) from the others: 8 (R-1) bytes per parameter in total
+        R, rounds = 2, 16 // 2
+        n = sum(a * b + b for a, b in zip(spec.widths[0:2], spec.widths[1:3]))
+        assert res.extras["replica_reduce_bytes_measured"] == rounds * 8 * (R - 1) * n
 
 
 def test_replicated_requires_whole_rounds():

@@ -142,7 +142,11 @@ def test_replicated_program_has_reduce_rounds():
     red = arr[arr[:, 0] == 2]
     bwd0 = arr[(arr[:, 0] == 1) & (arr[:, 1] == 0)]
     assert len(red) == len(bwd0) == 16  # one reduce per replica backward
-    assert all(r[18] >= 1 for r in red) and all(b[6] == -1 for b in bwd0)  # commit happens in the reduce
+    # the backward carries its round's commit slot (the sharded reduction it issues writes it); the
+    # version is committed (tagged) when the round's reduce item joins the reduction
+    assert all(r[18] >= 1 for r in red)
+    by_round = {(int(r[3]), int(r[18])): int(r[6]) for r in red}
+    assert all(int(b[6]) == by_round[(int(b[3]), int(b[18]))] for b in bwd0)
     # every reduce is issued after both replicas' backwards of its round
     pos = {(int(r[0]), int(r[3]), int(r[18])): i for i, r in enumerate(arr) if r[18] > 0}
     for (op, w, k), i in pos.items():

@@ -24,7 +24,8 @@ def f(row, name):
 
 
 def enqueue(world, rank, prog, epoch):
-    """Per-worker op queues for one rank, mirroring pd_rt_run (receiver-owned flags)."""
+    """Per-worker op queues for one rank, mirroring pd_rt_run (receiver-owned flags); a replicated
+    worker also has its reduction-stream queue (worker, "R")."""
     queues = {}
     val = lambda mb: epoch * 65536 + mb  # noqa: E731
     last = {}
@@ -47,10 +48,25 @@ def enqueue(world, rank, prog, epoch):
         if op == 1 and rep > 1 and k >= 3:
             for r in range(rep):
                 q.append(("wait", ("red_done", world.first[s] + r), val(k - 2)))
-        if op == 2:
-            for r in range(rep):
-                q.append(("wait", ("red_ready", world.first[s] + r), val(k)))
+        if op == 2:  # the reduce item joins the round's reduction stream (runtime.cu run_reduce)
+            q.append(("event", ("red", w, k)))
         q.append(("exec", row))
+        if op == 1 and rep > 1:
+            # sharded reduction, per layer in backward order (runtime.cu issue_layer_reduce): the
+            # stage stream signals layer l ready and forks; the reduction stream waits for every
+            # replica's layer l, reduce-scatters its shard, signals, waits for every owner, gathers
+            rq = queues.setdefault((w, "R"), [])
+            for l in range(world.layers[s] - 1, -1, -1):
+                q.append(("set", ("lready", w, l), val(k)))
+                q.append(("record", ("lev", w, l, k)))
+                rq.append(("event", ("lev", w, l, k)))
+                rq += [("wait", ("lready", world.first[s] + r, l), val(k)) for r in range(rep)]
+                rq.append(("rs", w, s, l, k))
+                rq.append(("set", ("lupd", w, l), val(k)))
+                rq += [("wait", ("lupd", world.first[s] + r, l), val(k)) for r in range(rep)]
+                rq.append(("ag", w, s, l, k))
+            rq.append(("set", ("red_done", w), val(k)))
+            rq.append(("record", ("red", w, k)))
         q.append(("record", (rank, i)))
         q.append(("signals", row, epoch))
         if op in (0, 1) and f(row, "out") >= 0:
@@ -67,6 +83,9 @@ class World:
         self.prog = pd.compile_program(pd.build_schedule(plan, K), mode, world_size=world)
         self.world = world
         self.first = [sum(self.reps[:s]) for s in range(self.n)]
+        self.layers = [st.last_layer - st.first_layer + 1 for st in plan.stages]
+        self.grads = {}   # (worker, layer, parity) -> round whose gradient the buffer holds
+        self.shards = {}  # (stage, layer, owner) -> last round applied by the owner
         self.flags = {}
         self.slots = {}  # (kind, receiver worker, slot) -> [occupant mb, consumed?]
         self.events = set()
@@ -104,6 +123,17 @@ class World:
         kind = op[0]
         if kind == "record":
             self.events.add(op[1])
+        elif kind == "set":
+            self.flags[op[1]] = op[2]
+        elif kind == "rs":  # owner w reads every replica's layer-l gradient of round k
+            _, w, s, l, k = op
+            for r in range(self.reps[s]):
+                assert self.grads.get((self.first[s] + r, l, k % 2)) == k, ("reduced a stale gradient", w, l, k)
+            self.shards[(s, l, w)] = k
+        elif kind == "ag":  # w gathers every owner's round-k shard
+            _, w, s, l, k = op
+            for r in range(self.reps[s]):
+                assert self.shards.get((s, l, self.first[s] + r)) == k, ("gathered a wrong shard", w, l, k)
         elif kind == "exec":
             row = op[1]
             w, s, mb, o = f(row, "worker"), f(row, "stage"), f(row, "mb"), f(row, "op")
@@ -128,6 +158,9 @@ class World:
                     k = ("grad", f(row, "dst"), f(row, "out"))
                     assert k not in self.slots or self.slots[k][1], ("gradient inbox overwritten", k, mb)
                     self.slots[k] = [mb, False]
+                if self.reps[s] > 1:  # this replica's round-k gradients land in the parity buffers
+                    for l in range(self.layers[s]):
+                        self.grads[(w, l, f(row, "round") % 2)] = f(row, "round")
         elif kind == "signals":
             row, epoch = op[1], op[2]
             w, s, mb, o = f(row, "worker"), f(row, "stage"), f(row, "mb"), f(row, "op")
@@ -141,10 +174,7 @@ class World:
                     self.flags[("act_ack", w, f(row, "x"))] = v
                 if s < self.n - 1:
                     self.flags[("grad_ack", w, f(row, "g"))] = v
-                if self.reps[s] > 1:
-                    self.flags[("red_ready", w)] = epoch * 65536 + f(row, "round")
-            if o == 2:
-                self.flags[("red_done", w)] = epoch * 65536 + f(row, "round")
+
 
 
 @pytest.mark.parametrize("n,world,K", [(4, 2, 20), (8, 2, 25), (8, 4, 25), (8, 8, 25), (3, 2, 16), (4, 4, 14)])
