@@ -338,10 +338,10 @@ int pd_rt_records(pd_runtime* rt, pd_record* out, int cap, int* n_out);
  * the version held by each ring slot (written in stream order after the committing kernels).
  * NULL rec switches the records off. */
 #define PD_REC_WIDTH 8
-/* PD_REC_RED_BYTES: bytes a replicated stage's sharded reduction (issued from this backward) read
- * from the other replicas' memory, counted by the reduction kernels. */
+/* Row 0: [0] run-start %globaltimer, [1] bytes the replicated stages' sharded reductions read from
+ * other replicas' memory during the run (counted by the reduction kernels). */
 enum pd_rec_field { PD_REC_T0 = 0, PD_REC_T1 = 1, PD_REC_VER0 = 2, PD_REC_VER1 = 3, PD_REC_BYTES = 4,
-                    PD_REC_COMMIT = 5, PD_REC_RED_BYTES = 6 };
+                    PD_REC_COMMIT = 5 };
 int pd_rt_set_records(pd_runtime* rt, int64_t* rec, int cap, int32_t* tags);
 /* The (cg, bn) tile configuration the tcgen05 GEMM dispatch picks for a problem: cg 1 = one CTA
  * per 128 x bn tile, 2 = a CTA pair per 256 x bn tile (tests pin the bench's instantiations). */

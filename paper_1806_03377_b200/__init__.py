@@ -8,6 +8,13 @@ weight-version ring, peer-store inboxes) instead of simulating it.
 
 __version__ = "0.1.0"
 
+import os as _os
+
+# Every hosted worker issues on its own stream (plus a reduction stream per replicated worker):
+# give them their own hardware work queues when this process creates its CUDA context (the default
+# of 8 folds more streams onto shared queues, serialising independent stages).
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 from .errors import (  # noqa: F401
     ConsistencyError,
     NativeError,

@@ -36,7 +36,7 @@ EXPORTED = (
 PD_CONV_FWD, PD_CONV_DGRAD, PD_CONV_WGRAD, PD_GEMM_WGRAD_SPLITK = range(4)
 # device pass records (pd_rt_set_records)
 REC_WIDTH = 8
-REC_T0, REC_T1, REC_VER0, REC_VER1, REC_BYTES, REC_COMMIT, REC_RED_BYTES = range(7)
+REC_T0, REC_T1, REC_VER0, REC_VER1, REC_BYTES, REC_COMMIT = range(6)
 
 
 class Epilogue(Structure):

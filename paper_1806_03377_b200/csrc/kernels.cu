@@ -428,8 +428,7 @@ __global__ void k_timestamp(uint64_t* p) {
 //   [2] version tag of the weight ring slot the pass reads (wslot) when it starts,
 //   [3] the same tag when it ends (differs only if the slot was overwritten under the pass);
 //   [4] payload bytes stored into another process's inbox (counted by the storing kernel),
-//   [5] version committed (tag written into slot wnew), -1 if none;
-//   [6] bytes a replicated stage's sharded reduction read from other replicas (backward items).
+//   [5] version committed (tag written into slot wnew), -1 if none.
 // Ring-slot tags are written only here, in stream order after the committing kernels, so a tag
 // names the version the slot holds for every later kernel of the same worker.
 __global__ void k_rec_begin(int64_t* rec, const int* tag) {
@@ -439,7 +438,6 @@ __global__ void k_rec_begin(int64_t* rec, const int* tag) {
   rec[2] = tag ? *tag : -1;
   rec[4] = 0;
   rec[5] = -1;
-  rec[6] = 0;
 }
 __global__ void k_rec_end(int64_t* rec, const int* tag, int* commit_tag, int commit_v, int64_t host_bytes) {
   rec[3] = tag ? *tag : -1;

@@ -106,6 +106,8 @@ struct Stage {
   cudaStream_t rstream = nullptr;      // rep > 1: the sharded reduction runs here, under the backward
   cudaEvent_t ev_red = nullptr;        // rep > 1: this round's reduction finished (joined by REDUCE)
   std::vector<cudaEvent_t> ev_layer;   // rep > 1: layer l's gradient is complete (fork to rstream)
+  std::vector<cudaEvent_t> ev_upd;     // rep > 1: this replica's layer-l shard is reduced and applied
+  int issued_round = 0;                // rep > 1: last round whose reduction has been enqueued
   cudaEvent_t ev_done = nullptr;
   bool fused_signal = false;
   int tag_index = 0;           // this worker's 64-slot block in rt->tags
@@ -337,47 +339,102 @@ int wait_parity_free(pd_runtime* rt, Stage& S, int round) {
   return 0;
 }
 
-// Sharded reduction of a replicated stage, issued per layer from the backward as
-// soon as this replica's layer-l gradient of round `round` is complete: the stage stream signals
-// red_lready[l] and forks to the reduction stream, which waits for every replica's layer-l
-// gradient, reduce-scatters + applies SGD to the shard this replica owns, signals red_lupd[l],
-// waits for every owner's update and all-gathers the other shards of the new master (and writes
-// the new version into ring slot wnew).  After the stage's last layer (l == 0) it signals red_done
-// and records ev_red, which the round's REDUCE item joins back into the stage stream.  Serial mode
-// (one stream for all workers) cannot overlap replicas, so it keeps the whole-tensor reduction.
+// Sharded reduction of a replicated stage.  The backward marks each layer's
+// gradient complete (layer_grad_ready: an event, plus the red_lready flag when some replica lives
+// in another process).  The round's first REDUCE item then enqueues, for every replica hosted
+// here, on its reduction stream: per layer (deepest first) wait for every replica's layer-l
+// gradient, reduce-scatter + SGD of the shard it owns (ev_upd / red_lupd), and after all layers
+// the all-gather of the other owners' updated shards; red_done and ev_red close the round, and
+// each replica's REDUCE item joins ev_red into its stage stream.  On the device a layer's
+// reduction starts as soon as the last replica's layer-l gradient exists, under that replica's
+// remaining backward.  It is enqueued only once every replica's backward of the round has been
+// enqueued (the REDUCE items follow all of them in the issue order), so no wait is ever submitted
+// ahead of its producer: in-process waits are events, cross-process waits are flag polls.
+// Serial mode (one stream for all workers) cannot overlap replicas: it keeps the whole-tensor
+// reduction (run_reduce), which computes the same sums in the same order.
+bool sharded_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PD_SHARDED_REDUCE");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
 bool sharded_reduce(const pd_runtime* rt, const Stage& S) {
-  return S.d.rep > 1 && !rt->serial && S.rstream && S.d.red_lready && S.d.red_lupd;
+  return S.d.rep > 1 && !rt->serial && S.rstream && S.d.red_lready && S.d.red_lupd && sharded_enabled();
 }
 
-int issue_layer_reduce(pd_runtime* rt, Stage& S, int l, int round, int wnew, cudaStream_t ST) {
-  const pd_stage_desc& d = S.d;
-  const int val = flag_val(rt->epoch, round), par = round & 1;
-  if (wnew < 0) return set_error(PD_ERR_INVALID, "worker %d: replicated backward without a commit slot", d.worker);
-  PD_TRY(flag_signal(d.red_lready + l, val, ST));
+int layer_grad_ready(pd_runtime* rt, Stage& S, int l, int round, cudaStream_t ST) {
   PD_CHECK(cudaEventRecord(S.ev_layer[l], ST));
-  cudaStream_t R = S.rstream;
-  PD_CHECK(cudaStreamWaitEvent(R, S.ev_layer[l], 0));
-  std::vector<const float*> g(d.rep), gb(d.rep), m(d.rep), mb(d.rep);
-  for (int r = 0; r < d.rep; ++r) {
-    const View& V = rt->views.at(d.first_worker + r);
-    PD_TRY(flag_wait(V.v.red_lready + l, val, d.err_word, R));
-    g[r] = V.red_grad[(size_t)l * 2 + par];
-    gb[r] = V.red_bgrad[(size_t)l * 2 + par];
-    m[r] = V.w_master[l];
-    mb[r] = V.b_master[l];
+  if (!S.replicas_local) {
+    PD_TRY(flag_signal(S.d.red_lready + l, flag_val(rt->epoch, round), ST));
+    rt->launches += 1;
   }
-  unsigned long long* ctr = rt->cur_rec ? reinterpret_cast<unsigned long long*>(rt->cur_rec + 6) : nullptr;
-  void* ring = S.w_ring[(size_t)l * d.ring_depth + wnew];
-  float* bring = S.b_ring[(size_t)l * d.ring_depth + wnew];
-  const int64_t nw = w_numel(S, l), nb = b_numel(S, l);
-  PD_TRY(shard_rs_sgd(d.dtype, g.data(), d.rep, d.replica, S.w_master[l], ring, nw, d.lr, ctr, R));
-  if (nb > 0) PD_TRY(shard_rs_sgd(PD_F32, gb.data(), d.rep, d.replica, S.b_master[l], bring, nb, d.lr, ctr, R));
-  PD_TRY(flag_signal(d.red_lupd + l, val, R));
-  for (int r = 0; r < d.rep; ++r) PD_TRY(flag_wait(rt->views.at(d.first_worker + r).v.red_lupd + l, val, d.err_word, R));
-  PD_TRY(shard_ag(d.dtype, m.data(), d.rep, d.replica, S.w_master[l], ring, nw, ctr, R));
-  if (nb > 0) PD_TRY(shard_ag(PD_F32, mb.data(), d.rep, d.replica, S.b_master[l], bring, nb, ctr, R));
-  rt->launches += 4 + 2 * d.rep + (nb > 0 ? 2 : 0);
-  if (l == 0) {
+  return 0;
+}
+
+int issue_round_reduce(pd_runtime* rt, Stage& S0, int round, int wnew) {
+  const pd_stage_desc& d0 = S0.d;
+  const int val = flag_val(rt->epoch, round), par = round & 1, L = d0.n_layers;
+  std::vector<Stage*> local;
+  for (int r = 0; r < d0.rep; ++r) {
+    auto f = rt->stages.find(d0.first_worker + r);
+    if (f != rt->stages.end()) local.push_back(&f->second);
+  }
+  auto peer_wait = [&](cudaStream_t R, int q, int l, bool upd) -> int {
+    auto f = rt->stages.find(d0.first_worker + q);
+    if (f != rt->stages.end()) {
+      PD_CHECK(cudaStreamWaitEvent(R, upd ? f->second.ev_upd[l] : f->second.ev_layer[l], 0));
+      return 0;
+    }
+    const View& V = rt->views.at(d0.first_worker + q);
+    rt->launches += 1;
+    return flag_wait((upd ? V.v.red_lupd : V.v.red_lready) + l, val, S0.d.err_word, R);
+  };
+  unsigned long long* ctr = rt->traced && rt->rec ? reinterpret_cast<unsigned long long*>(rt->rec + 1) : nullptr;
+  std::vector<const float*> g(d0.rep), gb(d0.rep), m(d0.rep), mb(d0.rep);
+  for (Stage* Sp : local) {  // pass 1: reduce-scatter + SGD of each local replica's own shard
+    Stage& S = *Sp;
+    const pd_stage_desc& d = S.d;
+    S.issued_round = round;
+    cudaStream_t R = S.rstream;
+    for (int l = L - 1; l >= 0; --l) {
+      for (int q = 0; q < d.rep; ++q) {
+        PD_TRY(peer_wait(R, q, l, false));
+        const View& V = rt->views.at(d.first_worker + q);
+        g[q] = V.red_grad[(size_t)l * 2 + par];
+        gb[q] = V.red_bgrad[(size_t)l * 2 + par];
+      }
+      const int64_t nw = w_numel(S, l), nb = b_numel(S, l);
+      PD_TRY(shard_rs_sgd(d.dtype, g.data(), d.rep, d.replica, S.w_master[l], S.w_ring[(size_t)l * d.ring_depth + wnew],
+                          nw, d.lr, ctr, R));
+      if (nb > 0)
+        PD_TRY(shard_rs_sgd(PD_F32, gb.data(), d.rep, d.replica, S.b_master[l], S.b_ring[(size_t)l * d.ring_depth + wnew],
+                            nb, d.lr, ctr, R));
+      PD_CHECK(cudaEventRecord(S.ev_upd[l], R));
+      if (!S.replicas_local) PD_TRY(flag_signal(d.red_lupd + l, val, R));
+      rt->launches += 1 + (nb > 0) + (!S.replicas_local);
+    }
+  }
+  for (Stage* Sp : local) {  // pass 2: all-gather the other owners' updated shards
+    Stage& S = *Sp;
+    const pd_stage_desc& d = S.d;
+    cudaStream_t R = S.rstream;
+    for (int l = L - 1; l >= 0; --l) {
+      for (int q = 0; q < d.rep; ++q) {
+        if (q != d.replica) PD_TRY(peer_wait(R, q, l, true));
+        const View& V = rt->views.at(d.first_worker + q);
+        m[q] = V.w_master[l];
+        mb[q] = V.b_master[l];
+      }
+      const int64_t nw = w_numel(S, l), nb = b_numel(S, l);
+      PD_TRY(shard_ag(d.dtype, m.data(), d.rep, d.replica, S.w_master[l], S.w_ring[(size_t)l * d.ring_depth + wnew], nw,
+                      ctr, R));
+      if (nb > 0)
+        PD_TRY(shard_ag(PD_F32, mb.data(), d.rep, d.replica, S.b_master[l], S.b_ring[(size_t)l * d.ring_depth + wnew], nb,
+                        ctr, R));
+      rt->launches += 1 + (nb > 0);
+    }
     PD_TRY(flag_signal(d.red_done, val, R));
     PD_CHECK(cudaEventRecord(S.ev_red, R));
     rt->launches += 1;
@@ -472,7 +529,7 @@ int run_backward(pd_runtime* rt, Stage& S, const int32_t* it) {
       PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, Nout, X, 1, Kin, Nout, Kin, B, EPI_GRADF32, ep, ST));
       PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return bias_grad(d.dtype, dz, B, Nout, Nout, S.red_bgrad[(size_t)l * 2 + par], ST); }));
       rt->launches += 1;
-      if (sharded_reduce(rt, S)) PD_TRY(issue_layer_reduce(rt, S, l, round, wnew, ST));
+      if (sharded_reduce(rt, S)) PD_TRY(layer_grad_ready(rt, S, l, round, ST));
     } else if (wnew >= 0) {
       // wgrad + SGD onto the latest weights, written as version mb into ring slot wnew
       EpiArgs ep{};
@@ -864,7 +921,7 @@ int run_backward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
         PD_TRY(timed_gemm(rt, KC_WGRAD, d.dtype, dz, 1, y.c_out, X, 1, y.c_in, y.c_out, y.c_in, B, EPI_GRADF32, ep, ST));
         PD_TRY(timed_call(rt, KC_UPDATE, ST, [&]() { return bias_grad(d.dtype, dz, B, y.c_out, y.c_out, gb, ST); }));
         rt->launches += 1;
-        if (sharded_reduce(rt, S)) PD_TRY(issue_layer_reduce(rt, S, l, round, wnew, ST));  // after its dgrad
+        if (sharded_reduce(rt, S)) PD_TRY(layer_grad_ready(rt, S, l, round, ST));  // after its dgrad
       } else if (update) {
         EpiArgs ep{};
         ep.master = S.w_master[l];
@@ -921,7 +978,7 @@ int run_backward_layers(pd_runtime* rt, Stage& S, const int32_t* it) {
       PD_TRY(timed_conv(rt, KC_DGRAD, PD_CONV_DGRAD, dy, Wst, B, y.h, y.w, y.c_in, y.c_out, EPI_MASK, ep, ST));
     }
     // the layer's new version may overwrite ring slot wnew only after this layer's dgrad read wslot
-    if (replicated && sharded_reduce(rt, S)) PD_TRY(issue_layer_reduce(rt, S, l, round, wnew, ST));
+    if (replicated && sharded_reduce(rt, S)) PD_TRY(layer_grad_ready(rt, S, l, round, ST));
     dz = dst;
   }
   if (replicated && !sharded_reduce(rt, S)) PD_TRY(signal_flag(rt, S, d.red_ready, round));
@@ -934,7 +991,8 @@ int run_reduce(pd_runtime* rt, Stage& S, const int32_t* it) {
   cudaStream_t ST = stream_of(rt, S);
   const pd_stage_desc& d = S.d;
   const int round = it[PD_IT_ROUND], wnew = it[PD_IT_WNEW], par = round & 1;
-  if (sharded_reduce(rt, S)) {  // issued per layer from the backward; join it back here
+  if (sharded_reduce(rt, S)) {  // the round's first REDUCE item enqueues it for every local replica
+    if (S.issued_round < round) PD_TRY(issue_round_reduce(rt, S, round, wnew));
     PD_CHECK(cudaStreamWaitEvent(ST, S.ev_red, 0));
     return 0;
   }
@@ -1090,7 +1148,11 @@ int pd_rt_add_stage(pd_runtime* rt, const pd_stage_desc* desc) {
     PD_CHECK(cudaStreamCreateWithFlags(&S.rstream, cudaStreamNonBlocking));
     PD_CHECK(cudaEventCreateWithFlags(&S.ev_red, cudaEventDisableTiming));
     S.ev_layer.assign(L, nullptr);
-    for (int l = 0; l < L; ++l) PD_CHECK(cudaEventCreateWithFlags(&S.ev_layer[l], cudaEventDisableTiming));
+    S.ev_upd.assign(L, nullptr);
+    for (int l = 0; l < L; ++l) {
+      PD_CHECK(cudaEventCreateWithFlags(&S.ev_layer[l], cudaEventDisableTiming));
+      PD_CHECK(cudaEventCreateWithFlags(&S.ev_upd[l], cudaEventDisableTiming));
+    }
   }
   rt->stages.emplace(d.worker, std::move(S));
   return 0;
@@ -1246,7 +1308,11 @@ static int run_body(pd_runtime* rt, cudaStream_t main, int trace) {
     }
   }
   const bool recs = rt->traced && rt->rec;
-  if (recs) PD_TRY(timestamp(reinterpret_cast<uint64_t*>(rt->rec), main));  // before any stage starts
+  if (recs) {
+    PD_CHECK(cudaMemsetAsync(rt->rec + 1, 0, sizeof(int64_t), main));  // sharded-reduction peer bytes
+    PD_TRY(timestamp(reinterpret_cast<uint64_t*>(rt->rec), main));      // before any stage starts
+  }
+  for (auto& kv : rt->stages) kv.second.issued_round = 0;
   PD_CHECK(cudaEventRecord(rt->ev0, main));
   int max_mb = 0;
   for (size_t i = 0; i < rt->items.size(); i += PD_ITEM_WIDTH) max_mb = std::max(max_mb, rt->items[i + PD_IT_MB]);
@@ -1451,6 +1517,7 @@ int pd_rt_destroy(pd_runtime* rt) {
       cudaStreamDestroy(kv.second.rstream);
       cudaEventDestroy(kv.second.ev_red);
       for (auto e : kv.second.ev_layer) cudaEventDestroy(e);
+      for (auto e : kv.second.ev_upd) cudaEventDestroy(e);
     }
   }
   for (auto e : rt->ev_start) cudaEventDestroy(e);

@@ -746,7 +746,7 @@ class Executor:
         traced = getattr(self, "_traced", False)
         start, rows = self.device_records() if traced else (0, [])
         # bytes the replicas' sharded reductions read from each other (counted by the kernels)
-        red = int(self._rec.view(-1, nat.REC_WIDTH)[1:, nat.REC_RED_BYTES].sum().item()) if traced else 0
+        red = int(self._rec[1].item()) if traced else 0  # row 0, field 1 (include/pd_b200.h)
         losses, weights, comm = self.losses(), self.weights(), self.comm_bytes()
         if self.world > 1:
             parts = [None] * self.world
