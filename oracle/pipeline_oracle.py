@@ -197,7 +197,7 @@ def mlp_train(params, X, T, lr, stage_bounds, versions, K, emulate: str | None =
 
 
 def mlp_train_torch(params, X, T, lr, stage_bounds, versions, K, emulate: str | None = "bf16", device=None,
-                    prune: bool = True, dtype=None):
+                    prune: bool = True, dtype=None, ksplit: int = 1):
     """``mlp_train``'s rule with torch fp32 arithmetic on ``device`` (the checker of full-size
     configurations, e.g. the 8 x 2-layer MLP-8192 at minibatch 2048, which numpy cannot run in
     seconds).  Same forward / backward versions, bf16 rounding points (fp32 -> bf16 nearest-even,
@@ -207,9 +207,21 @@ def mlp_train_torch(params, X, T, lr, stage_bounds, versions, K, emulate: str | 
     params: [(W [out,in], b [out])] torch or numpy; X [n_blocks,B,d0]; T [n_blocks,B,dL].
     dtype: arithmetic type (default torch.float32; torch.float64 gives the exact-arithmetic reference
     against which an fp32 run's own rounding drift can be measured).
+    ksplit: every product is summed over ``ksplit`` contiguous K chunks (a different fp32 summation
+    order: the spread of such variants is the rounding-noise floor of fp32-accumulating GEMMs).
     Returns (losses[K] numpy, final [(W, b)] torch tensors on ``device``).
     """
     import torch
+
+    def mm(a, b):
+        if ksplit <= 1:
+            return a @ b
+        kk = a.shape[1]
+        step = (kk + ksplit - 1) // ksplit
+        out = a[:, :step] @ b[:step]
+        for k0 in range(step, kk, step):
+            out = out + a[:, k0:k0 + step] @ b[k0:k0 + step]
+        return out
 
     dtype = dtype or torch.float32
 
@@ -247,7 +259,7 @@ def mlp_train_torch(params, X, T, lr, stage_bounds, versions, K, emulate: str | 
                 s = layer_stage[l]
                 W, b = archives[s][fv[s]][l - first[s]]
                 inputs.append(h)
-                z = h @ q(W).T + b
+                z = mm(h, q(W).T) + b
                 if l < L - 1:
                     h = q(torch.relu(z))
             d = z - t
@@ -257,10 +269,10 @@ def mlp_train_torch(params, X, T, lr, stage_bounds, versions, K, emulate: str | 
             for l in range(L - 1, -1, -1):
                 s = layer_stage[l]
                 Xl = inputs[l]
-                grads[l] = (dz.T @ Xl, dz.sum(0))
+                grads[l] = (mm(dz.T, Xl), dz.sum(0))
                 if l > 0:
                     Wb, _ = archives[s][bv[s]][l - first[s]]
-                    dz = q((dz @ q(Wb)) * (Xl > 0))
+                    dz = q(mm(dz, q(Wb)) * (Xl > 0))
             inputs = None
             for s, (a, b) in enumerate(stage_bounds):
                 latest = archives[s][latest_v[s]]

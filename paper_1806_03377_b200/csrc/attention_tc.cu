@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "epilogue.cuh"
@@ -126,6 +127,34 @@ PD_DEVICE float exp_pack64(const uint32_t (&sr)[64], int base, int lim, float sc
     const float2 t = __fadd2_rn(acc0, acc1);
     return t.x + t.y;
   }
+}
+
+// p = exp2(s*scale + neg) for 32 scores sr[0..31] -> 16 packed bf16 pairs (pk[i] = keys 2i, 2i+1,
+// the column layout of a bf16 A operand in TMEM); returns the fp32 sum.  MASK: only columns
+// base+i <= lim are kept.
+template <bool MASK>
+PD_DEVICE float exp_pack32(const uint32_t* sr, int base, int lim, float scale, float neg, uint32_t (&pk)[16]) {
+  const float2 sc = make_float2(scale, scale), ng = make_float2(neg, neg);
+  float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) {
+    const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])), sc, ng);
+    const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3])), sc, ng);
+    float2 p0 = make_float2(fast_exp2(x0.x), fast_exp2(x0.y));
+    float2 p1 = make_float2(fast_exp2(x1.x), fast_exp2(x1.y));
+    if constexpr (MASK) {
+      if (base + i > lim) p0.x = 0.f;
+      if (base + i + 1 > lim) p0.y = 0.f;
+      if (base + i + 2 > lim) p1.x = 0.f;
+      if (base + i + 3 > lim) p1.y = 0.f;
+    }
+    acc0 = __fadd2_rn(acc0, p0);
+    acc1 = __fadd2_rn(acc1, p1);
+    pk[i / 2] = pack_bf16x2(p0.x, p0.y);
+    pk[i / 2 + 1] = pack_bf16x2(p1.x, p1.y);
+  }
+  const float2 t = __fadd2_rn(acc0, acc1);
+  return t.x + t.y;
 }
 
 // Byte offset of (row, 16-byte chunk) of a 128B-swizzled tile (the TMA / UMMA SW128 pattern).
@@ -298,6 +327,217 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
       }
       l += rs;
       fence_proxy_async_shared();  // P (generic-proxy stores) -> visible to the tensor core
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(p_ready);
+    }
+    mbar_wait(o_done, (n_kt - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = out + ((int64_t)row0 + q) * D + h * HDIM;
+#pragma unroll
+    for (int c = 0; c < HDIM / 32; ++c) {
+      float o[32];
+      tmem_ld_32x32b_x32(tO + lane_base + c * 32, o);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] *= inv;
+      store32_bf16(orow, 0, 0, c * 32, o);
+    }
+    lse[((int64_t)b * H + h) * S + q] = m + log2f(l);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<256, 1>(tmem);
+  }
+}
+
+// ================================================================ forward, S decoupled from P
+// One CTA per (128-query tile, head, sequence), two CTAs per SM, 256 TMEM columns each:
+//   S [0,128) fp32 scores, O [128,192) fp32 output, P [192,256) bf16 probabilities (key pairs).
+// The softmax warps pull the whole S row into registers (four 32-column loads, one wait) and
+// release S at once (s_free), so S_{j+1} = Q K_{j+1}^T runs on the tensor core while they compute
+// exp2 of tile j.  P_j goes to TMEM (tcgen05.st) and O += P_j V_j reads it as the A operand
+// straight from TMEM (the TS form), so P never touches shared memory.  K and V stream through a
+// two-stage ring.  Numerics are those of k_attn_fwd_tc (same max, exp2, lazy rescale, bf16 P).
+constexpr int FWD2_STAGES = 2;
+struct Fwd2Smem {
+  static constexpr int Q = 0;
+  static constexpr int K = Q + TILE_BYTES;                     // [FWD2_STAGES]
+  static constexpr int V = K + FWD2_STAGES * TILE_BYTES;       // [FWD2_STAGES]
+  static constexpr int BAR = V + FWD2_STAGES * TILE_BYTES;
+  static constexpr int TOTAL = BAR + 256 + 1024;
+};
+
+__global__ void __launch_bounds__(FWD_THREADS, 2)
+    k_attn_fwd_tc2(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ out,
+                   float* __restrict__ lse, int S, int H, float scale_log2) {
+  griddep_wait();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + Fwd2Smem::Q;
+  uint8_t* sK = smem + Fwd2Smem::K;
+  uint8_t* sV = smem + Fwd2Smem::V;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Fwd2Smem::BAR);
+  uint64_t* full_q = bar + 0;
+  uint64_t* full_k = bar + 1;                    // [FWD2_STAGES]
+  uint64_t* full_v = full_k + FWD2_STAGES;       // [FWD2_STAGES]
+  uint64_t* empty_k = full_v + FWD2_STAGES;      // [FWD2_STAGES]
+  uint64_t* empty_v = empty_k + FWD2_STAGES;     // [FWD2_STAGES]
+  uint64_t* s_full = empty_v + FWD2_STAGES;
+  uint64_t* s_free = s_full + 1;
+  uint64_t* p_ready = s_full + 2;
+  uint64_t* o_done = s_full + 3;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 4);
+
+  const int n_qt = S / TQ;
+  const int qt = n_qt - 1 - (int)blockIdx.x;  // heaviest (longest causal row) tiles first
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int D = H * HDIM;
+  const int n_kt = qt + 1;
+  const int row0 = b * S;
+  const int warp = warp_id();
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    mbar_init(full_q, 1);
+    for (int i = 0; i < FWD2_STAGES; ++i) {
+      mbar_init(&full_k[i], 1);
+      mbar_init(&full_v[i], 1);
+      mbar_init(&empty_k[i], 1);
+      mbar_init(&empty_v[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 4);
+    mbar_init(p_ready, 4);
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+    fence_proxy_async_smem();
+  }
+  if (warp == 1) tmem_alloc<256, 1>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tO = tmem + 128, tP = tmem + 192;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (elect_one()) {
+      mbar_arrive_expect_tx(full_q, TILE_BYTES);
+      tma_load_2d(sQ, &tm_qkv, full_q, h * HDIM, row0 + qt * TQ);
+      for (int j = 0; j < n_kt; ++j) {
+        const int st = j % FWD2_STAGES;
+        const uint32_t ph = ((j / FWD2_STAGES) & 1) ^ 1;
+        mbar_wait(&empty_k[st], ph);
+        mbar_arrive_expect_tx(&full_k[st], TILE_BYTES);
+        tma_load_2d(sK + st * TILE_BYTES, &tm_qkv, &full_k[st], D + h * HDIM, row0 + j * TK);
+        mbar_wait(&empty_v[st], ph);
+        mbar_arrive_expect_tx(&full_v[st], TILE_BYTES);
+        tma_load_2d(sV + st * TILE_BYTES, &tm_qkv, &full_v[st], 2 * D + h * HDIM, row0 + j * TK);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(TQ, TK, false, false);
+      constexpr uint32_t idesc_o = make_idesc_bf16(TQ, HDIM, false, true);
+      const uint32_t q_addr = smem_u32(sQ);
+      auto issue_s = [&](int j) {
+        const int st = j % FWD2_STAGES;
+        const uint32_t k_addr = smem_u32(sK + st * TILE_BYTES);
+        mbar_wait(&full_k[st], (j / FWD2_STAGES) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < HDIM / 16; ++k)
+          umma_bf16(tS, make_sw128_desc(q_addr + k * 32, 16, 1024), make_sw128_desc(k_addr + k * 32, 16, 1024),
+                    idesc_s, k != 0);
+        umma_commit(s_full);
+        umma_commit(&empty_k[st]);
+      };
+      mbar_wait(full_q, 0);
+      issue_s(0);
+      for (int j = 0; j < n_kt; ++j) {
+        const int st = j % FWD2_STAGES;
+        mbar_wait(s_free, j & 1);  // S_j is in the softmax warps' registers
+        tc_fence_after();
+        if (j + 1 < n_kt) issue_s(j + 1);
+        mbar_wait(p_ready, j & 1);  // P_j in TMEM, O rescaled
+        mbar_wait(&full_v[st], (j / FWD2_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sV + st * TILE_BYTES);
+#pragma unroll
+        for (int k = 0; k < TK / 16; ++k)  // A = P from TMEM (8 columns = 16 keys), B = V (MN-major)
+          umma_bf16_ts(tO, tP + k * 8, make_sw128_desc(v_addr + k * 2048, 8192, 1024), idesc_o, (j | k) != 0);
+        umma_commit(o_done);
+        umma_commit(&empty_v[st]);
+      }
+    }
+  } else {
+    // ---------------- softmax: thread = query row (TMEM lane 32*(warp%4) + lane)
+    const int quad = warp & 3;
+    const int r = 32 * quad + lane_id();
+    const int q = qt * TQ + r;
+    const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kt; ++j) {
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      uint32_t sr[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        tmem_ld_32x32b_x32_nowait(tS + lane_base + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32 * c));
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(s_free);  // the tensor core may write S_{j+1} now
+      const bool diag = j == qt;
+      const int lim = diag ? q - j * TK : TK;
+      float mx;
+      if (diag) {
+        mx = row_max64<true>(*reinterpret_cast<const uint32_t(*)[64]>(sr), 0, lim, -INFINITY);
+        mx = row_max64<true>(*reinterpret_cast<const uint32_t(*)[64]>(sr + 64), 64, lim, mx);
+      } else {
+        mx = row_max64<false>(*reinterpret_cast<const uint32_t(*)[64]>(sr), 0, 0, -INFINITY);
+        mx = row_max64<false>(*reinterpret_cast<const uint32_t(*)[64]>(sr + 64), 0, 0, mx);
+      }
+      const float m_new = fmaxf(m, mx * scale_log2);
+      if (j > 0) mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} done: O final for j-1, P free
+      tc_fence_after();
+      if (j == 0) {
+        m = m_new;
+      } else if (__any_sync(0xffffffffu, m_new > m + RESCALE_LOG2)) {
+        const float alpha = fast_exp2(m - m_new);
+#pragma unroll
+        for (int c = 0; c < HDIM / 16; ++c) {
+          uint32_t o[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(o[6]), "=r"(o[7]),
+                "=r"(o[8]), "=r"(o[9]), "=r"(o[10]), "=r"(o[11]), "=r"(o[12]), "=r"(o[13]), "=r"(o[14]), "=r"(o[15])
+              : "r"(tO + lane_base + c * 16)
+              : "memory");
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st_32x32b_x16(tO + lane_base + c * 16, o);
+        }
+        tmem_wait_st();
+        l *= alpha;
+        m = m_new;
+      }
+      float rs = 0.f;
+      const float neg = -m;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+        rs += diag ? exp_pack32<true>(sr + 32 * c, 32 * c, lim, scale_log2, neg, pk)
+                   : exp_pack32<false>(sr + 32 * c, 0, 0, scale_log2, neg, pk);
+        tmem_st_32x32b_x16(tP + lane_base + c * 16, pk);
+      }
+      l += rs;
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(p_ready);
@@ -644,15 +884,25 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int S, int H, cud
   CUtensorMap tm;
   const int rc = map_rows(&tm, qkv, (int64_t)B * S, 3ll * H * HDIM);
   if (rc) return rc;
+  static int v1 = -1;  // PD_ATTN_FWD_V1=1: the round-1 kernel (P through shared memory), for A/B runs
+  if (v1 < 0) {
+    const char* e = getenv("PD_ATTN_FWD_V1");
+    v1 = e && atoi(e) ? 1 : 0;
+  }
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(k_attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem::TOTAL) != cudaSuccess)
+    if (cudaFuncSetAttribute(k_attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem::TOTAL) != cudaSuccess ||
+        cudaFuncSetAttribute(k_attn_fwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Smem::TOTAL) != cudaSuccess)
       return set_error(PD_ERR_CUDA, "attention fwd: shared memory attribute");
     attr = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)HDIM);
-  launch_pdl(k_attn_fwd_tc, dim3(S / TQ, H, B), dim3(FWD_THREADS), FwdSmem::TOTAL, st, tm, static_cast<__nv_bfloat16*>(out), lse,
-                                                                         S, H, scale_log2);
+  if (v1)
+    launch_pdl(k_attn_fwd_tc, dim3(S / TQ, H, B), dim3(FWD_THREADS), FwdSmem::TOTAL, st, tm,
+               static_cast<__nv_bfloat16*>(out), lse, S, H, scale_log2);
+  else
+    launch_pdl(k_attn_fwd_tc2, dim3(S / TQ, H, B), dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm,
+               static_cast<__nv_bfloat16*>(out), lse, S, H, scale_log2);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "attention fwd: %s", cudaGetErrorString(e));
 }

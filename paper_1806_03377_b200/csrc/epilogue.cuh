@@ -62,6 +62,7 @@ struct EpiArgs {
   int nrb;
   float* bmaster;
   float* bring;
+  int group;            // SGD rasterisation band height in tiles (set by the launcher; 0 = default 8)
 };
 
 // GPT-2's tanh GELU and its derivative.

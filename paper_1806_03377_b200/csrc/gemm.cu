@@ -127,10 +127,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // SGD: grouped rasterisation - bands of kGroup tile rows walked column by column, so the
   // co-resident tiles touch ~kGroup A blocks and ~units/kGroup B blocks (a compact operand
   // working set that survives the streamed master traffic in L2)
-  constexpr int kGroup = is_sgd(KIND) ? 8 : 0;
+  constexpr bool kGrouped = is_sgd(KIND);
+  const int kGroup = kGrouped ? (ep.group > 0 ? ep.group : 8) : 0;
   constexpr int NBUF = sgd_bufs(KIND);  // SGD: fp32 master blocks in flight per epilogue warp
   auto tile_m = [&](int t) {
-    if constexpr (kGroup > 0) {
+    if constexpr (kGrouped) {
       const int band = t / (kGroup * num_n), in = t - band * kGroup * num_n;
       const int rows = num_m - band * kGroup < kGroup ? num_m - band * kGroup : kGroup;
       return band * kGroup + in % rows;
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     return kNFast ? t / num_n : t % num_m;
   };
   auto tile_n = [&](int t) {
-    if constexpr (kGroup > 0) {
+    if constexpr (kGrouped) {
       const int band = t / (kGroup * num_n), in = t - band * kGroup * num_n;
       const int rows = num_m - band * kGroup < kGroup ? num_m - band * kGroup : kGroup;
       return in / rows;
@@ -507,8 +508,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if constexpr (KIND == EPI_MASK || KIND == EPI_LOSS) {
           // fused bias gradient: column sums of the 32 stored rows (bf16-rounded, as the
           // consumer's stand-alone column sum would read them); the host enables it only for
-          // N % 32 == 0, so every chunk is full
-          if (ep.colsum) {
+          // N % 32 == 0, so a chunk is either full or (the tail of a last, partial tile) wholly
+          // past N, where it must not write: c0 + lane would land in the next row block's columns
+          if (ep.colsum && c0 < N) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = row_ok ? __bfloat162float(__float2bfloat16_rn(v[j])) : 0.f;
             const float cs = warp_colsum32(v);
@@ -716,6 +718,15 @@ static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int
     rc = make_map(&tw, ep.master, (uint64_t)N, (uint64_t)M, ep.ldw, 32, 32, true);
     if (rc) return rc;
   }
+  EpiArgs epl = ep;
+  if constexpr (is_sgd(KIND)) {
+    static int group = -1;  // PD_SGD_GROUP: tile rows per rasterisation band (A/B experiments)
+    if (group < 0) {
+      const char* e = getenv("PD_SGD_GROUP");
+      group = e ? atoi(e) : 8;
+    }
+    epl.group = group;
+  }
   auto kern = k_gemm_tc<CG, BN, A_MN, B_MN, KIND, SRC, false>;
   static bool attr_set[2] = {false, false};  // per instantiation (plain / hand-off variant)
   int var = 0;
@@ -750,7 +761,7 @@ static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tw, M, N, K, ep, cv);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tw, M, N, K, epl, cv);
   if (e != cudaSuccess) return set_error(PD_ERR_CUDA, "tcgen05 gemm launch: %s", cudaGetErrorString(e));
   return 0;
 }
