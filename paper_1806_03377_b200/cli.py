@@ -1,4 +1,4 @@
-"""Command line: ``python -m paper_1806_03377_b200 {profile,plan,simulate}``.
+"""Command line: ``python -m paper_1806_03377_b200 {profile,plan,simulate,compare}``.
 
 Mirrors the reference CLI (pipesim/cli.py:264-358) for the hot path, with the B200 executor as
 the backend of ``simulate``: same positional arguments, options, artefact
@@ -175,6 +175,78 @@ def cmd_simulate(args) -> int:
     return EXIT_OK
 
 
+def _regime_minibatches(plan, k: int) -> int:
+    """Smallest K' >= k that is a whole number of rounds of every replicated stage (the round rule)."""
+    from math import lcm
+
+    step = 1
+    for st in plan.stages:
+        step = lcm(step, st.replication)
+    return -(-k // step) * step
+
+
+def cmd_compare(args) -> int:
+    """The reference's regime comparison (cli.py:211-261: single machine, model parallel, data
+    parallel, straight pipeline, full plan) with every regime EXECUTED on the B200 runtime instead
+    of simulated: each plan runs through the executor (its workers spread over this job's ranks; at
+    one GPU all of them share it) and the measured steady throughput is reported next to the
+    planner's analytic 1 / bottleneck_time.  Speed-ups are relative to the measured single-machine
+    run, as in the reference."""
+    import torch
+
+    from .executor import Executor
+    from .ledger import Mode, SimConfig
+    from .plans import Plan, Stage, solve
+    from .profiles import HardwareSpec, build_context, load_profile, stage_time
+
+    profile = load_profile(args.profile)
+    machines = args.machines
+    ctx = build_context(profile, HardwareSpec(machines, args.bandwidth, args.bytes_per_elem))
+    n = profile.num_layers
+    spec = parse_model(args.model, lr=args.lr, seed=args.seed)
+    if getattr(spec, "num_layers", n) != n:
+        raise ValidationError(f"model has {spec.num_layers} layers but profile has {n}")
+
+    def single_stage(m: int) -> Plan:
+        return Plan(stages=(Stage(1, n, m),), bottleneck_time=stage_time(ctx, 1, n, m), noam=1, machines_used=m)
+
+    straight = solve(ctx, machines=min(machines, n), max_replication=1)
+    regimes = [("single_machine", single_stage(1), None), ("model_parallel", straight, 1),
+               ("data_parallel", single_stage(machines), None), ("straight_pipeline", straight, None),
+               ("full_plan", solve(ctx, machines=machines), None)]
+    rows = []
+    for name, plan, inflight in regimes:
+        k = _regime_minibatches(plan, args.minibatches)
+        cfg = SimConfig(plan=plan, mode=Mode.WEIGHT_STASHING, num_minibatches=k, max_inflight=inflight)
+        ex = Executor(cfg, ctx, model=spec)
+        try:
+            for _ in range(max(0, args.steps - 1)):
+                ex.step()
+            ex.step(trace=True)
+            res = ex.result()
+        finally:
+            ex.close()
+            torch.cuda.empty_cache()
+        rows.append({"regime": name, "config": plan.config_string, "minibatches": k,
+                     "max_inflight": cfg.effective_inflight, "throughput": res.report.steady_throughput,
+                     "samples_per_s": res.report.steady_throughput * spec.batch,
+                     "predicted_throughput": 1.0 / plan.bottleneck_time,
+                     "bubble_fraction": res.extras.get("bubble_fraction")})
+    base = rows[0]["throughput"]
+    world = int(__import__("os").environ.get("WORLD_SIZE", "1"))
+    print(f"{'regime':<18} {'config':<12} {'throughput/s':>14} {'speedup':>9} {'predicted/s':>12}")
+    for r in rows:
+        r["speedup"] = r["throughput"] / base
+        print(f"{r['regime']:<18} {r['config']:<12} {r['throughput']:>14.6f} {r['speedup']:>8.2f}x "
+              f"{r['predicted_throughput']:>12.6f}")
+    out = _out_dir(args)
+    _write_json(out / "compare.json", _manifest("compare", args), {
+        "machines": machines, "n_gpus": world, "regimes": rows,
+        "note": "measured on the B200 runtime; with fewer GPUs than workers, workers share GPUs"})
+    print(f"compare_file: {out / 'compare.json'}")
+    return EXIT_OK
+
+
 def build_parser() -> argparse.ArgumentParser:
     parser = _Parser(prog="python -m paper_1806_03377_b200", description="B200 pipeline-parallel training runtime")
     parser.add_argument("--version", action="version", version=f"paper_1806_03377_b200 {__version__}")
@@ -217,6 +289,19 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--out-dir", default=".")
     p.set_defaults(func=cmd_simulate)
+
+    p = sub.add_parser("compare", help="execute the reference's five training regimes on the B200 runtime")
+    p.add_argument("profile")
+    p.add_argument("--model", required=True)
+    p.add_argument("--machines", type=int, required=True)
+    p.add_argument("--bandwidth", type=float, default=770e9)
+    p.add_argument("--bytes-per-elem", type=int, default=2)
+    p.add_argument("--minibatches", type=int, default=32)
+    p.add_argument("--lr", type=float, default=None)
+    p.add_argument("--steps", type=int, default=2, help="schedule executions per regime (the last one is traced)")
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--out-dir", default=".")
+    p.set_defaults(func=cmd_compare)
     return parser
 
 

@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
                   float* __restrict__ lse, int S, int H, float scale_log2) {
   griddep_wait();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align_1k(smem_raw);
   uint8_t* sQ = smem + FwdSmem::Q;
   uint8_t* sK = smem + FwdSmem::K;
   uint8_t* sV = smem + FwdSmem::V;
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
                    float* __restrict__ lse, int S, int H, float scale_log2) {
   griddep_wait();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align_1k(smem_raw);
   uint8_t* sQ = smem + Fwd2Smem::Q;
   uint8_t* sK = smem + Fwd2Smem::K;
   uint8_t* sV = smem + Fwd2Smem::V;
@@ -392,8 +392,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 4);
 
   const int n_qt = S / TQ;
-  const int qt = n_qt - 1 - (int)blockIdx.x;  // heaviest (longest causal row) tiles first
-  const int h = blockIdx.y, b = blockIdx.z;
+  // grid (H, B, tiles): the tile index varies slowest, so the block scheduler hands out every
+  // (head, sequence)'s longest causal row first and the light diagonal tiles last (LPT order)
+  const int qt = n_qt - 1 - (int)blockIdx.z;
+  const int h = blockIdx.x, b = blockIdx.y;
   const int D = H * HDIM;
   const int n_kt = qt + 1;
   const int row0 = b * S;
@@ -503,12 +505,24 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
         mx = row_max64<false>(*reinterpret_cast<const uint32_t(*)[64]>(sr + 64), 0, 0, mx);
       }
       const float m_new = fmaxf(m, mx * scale_log2);
+      // lazy rescale decision; O itself is rescaled below, once PV_{j-1} has finished with it
+      float alpha = 1.f;
+      const bool rescale = j > 0 && __any_sync(0xffffffffu, m_new > m + RESCALE_LOG2);
+      if (j == 0 || rescale) {
+        alpha = fast_exp2(m - m_new);
+        m = m_new;
+      }
+      // P_j = exp2(s*scale - m) -> packed bf16 pairs in registers (independent of PV_{j-1})
+      float rs = 0.f;
+      const float neg = -m;
+      uint32_t pk[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        rs += diag ? exp_pack32<true>(sr + 32 * c, 32 * c, lim, scale_log2, neg, pk[c])
+                   : exp_pack32<false>(sr + 32 * c, 0, 0, scale_log2, neg, pk[c]);
       if (j > 0) mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} done: O final for j-1, P free
       tc_fence_after();
-      if (j == 0) {
-        m = m_new;
-      } else if (__any_sync(0xffffffffu, m_new > m + RESCALE_LOG2)) {
-        const float alpha = fast_exp2(m - m_new);
+      if (rescale) {
 #pragma unroll
         for (int c = 0; c < HDIM / 16; ++c) {
           uint32_t o[16];
@@ -523,20 +537,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
           for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
           tmem_st_32x32b_x16(tO + lane_base + c * 16, o);
         }
-        tmem_wait_st();
-        l *= alpha;
-        m = m_new;
       }
-      float rs = 0.f;
-      const float neg = -m;
+      l = l * alpha + rs;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[16];
-        rs += diag ? exp_pack32<true>(sr + 32 * c, 32 * c, lim, scale_log2, neg, pk)
-                   : exp_pack32<false>(sr + 32 * c, 0, 0, scale_log2, neg, pk);
-        tmem_st_32x32b_x16(tP + lane_base + c * 16, pk);
-      }
-      l += rs;
+      for (int c = 0; c < 4; ++c) tmem_st_32x32b_x16(tP + lane_base + c * 16, pk[c]);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -582,21 +586,21 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
 constexpr int BWD_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 compute (two per TMEM lane quadrant)
 
 // One 32-query chunk of a key row: P^T = exp2(S^T*scale - lse), dS^T = P^T (dP^T - D) -> bf16 pairs.
-// nlse holds -lse.  MASK (diagonal tile only): queries q0+i < key are causal-masked.  The unmasked
+// lse: the query rows' log-sum-exp (log2 domain).  MASK (diagonal tile only): queries q0+i < key are causal-masked.  The unmasked
 // form runs two elements per FFMA2 / FMUL2.
 template <bool MASK>
-PD_DEVICE void bwd_chunk32(const uint32_t (&svr)[32], const uint32_t (&dpr)[32], const float* nlse, const float* Dd,
+PD_DEVICE void bwd_chunk32(const uint32_t (&svr)[32], const uint32_t (&dpr)[32], const float* lse_row, const float* Dd,
                            int q0, int key, float scale, uint32_t (&pk)[16], uint32_t (&dk)[16]) {
   const float* sv = reinterpret_cast<const float*>(svr);
   const float* dp = reinterpret_cast<const float*>(dpr);
-  const float4* L4 = reinterpret_cast<const float4*>(nlse);
+  const float4* L4 = reinterpret_cast<const float4*>(lse_row);
   const float4* D4 = reinterpret_cast<const float4*>(Dd);
   const float2 sc = make_float2(scale, scale), m1 = make_float2(-1.f, -1.f);
 #pragma unroll
   for (int i = 0; i < 32; i += 4) {
     const float4 lv = L4[i / 4], dv = D4[i / 4];
-    const float2 x0 = __ffma2_rn(make_float2(sv[i], sv[i + 1]), sc, make_float2(lv.x, lv.y));
-    const float2 x1 = __ffma2_rn(make_float2(sv[i + 2], sv[i + 3]), sc, make_float2(lv.z, lv.w));
+    const float2 x0 = __ffma2_rn(make_float2(sv[i], sv[i + 1]), sc, make_float2(-lv.x, -lv.y));
+    const float2 x1 = __ffma2_rn(make_float2(sv[i + 2], sv[i + 3]), sc, make_float2(-lv.z, -lv.w));
     float2 p0 = make_float2(fast_exp2(x0.x), fast_exp2(x0.y));
     float2 p1 = make_float2(fast_exp2(x1.x), fast_exp2(x1.y));
     if constexpr (MASK) {
@@ -627,16 +631,15 @@ struct BwdSmem {
   static constexpr int TOTAL = BAR + 256 + 1024;
 };
 
-PD_DEVICE void named_sync_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }  // the 8 compute warps
 
-__global__ void __launch_bounds__(BWD_THREADS, 1)
+__global__ void __maxnreg__(200)
     k_attn_bwd_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                   const __grid_constant__ CUtensorMap tm_dq,
                   const float* __restrict__ lse, const float* __restrict__ Dv, __nv_bfloat16* __restrict__ dqkv,
                   float* __restrict__ dq_acc, int S, int H, float scale_log2, float scale) {
   griddep_wait();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align_1k(smem_raw);
   uint8_t* sK = smem + BwdSmem::K;
   uint8_t* sV = smem + BwdSmem::V;
   uint8_t* sQ = smem + BwdSmem::Q;
@@ -644,7 +647,6 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint8_t* sdS = smem + BwdSmem::DS;
   float* sLD = reinterpret_cast<float*>(smem + BwdSmem::LD);
   float* sDQ = reinterpret_cast<float*>(smem + BwdSmem::DQ);
-  float* sLn = sLD;  // written once per tile by the compute warps (lse -> -lse)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BwdSmem::BAR);
   uint64_t* full_kv = bar + 0;
   uint64_t* full_qdo = bar + 1;                // [BWD_STAGES]
@@ -656,8 +658,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sdp_full + 4);
 
   const int n_t = S / TK;
-  const int kt = (int)blockIdx.x;  // key tile; tile 0 has the most query tiles and starts first
-  const int h = blockIdx.y, b = blockIdx.z;
+  const int kt = (int)blockIdx.z;  // key tile (slowest grid index): tile 0, the longest, is dispatched first
+  const int h = blockIdx.x, b = blockIdx.y;
   const int D = H * HDIM;
   const int row0 = b * S;
   const int N = n_t - kt;  // query tiles kt .. n_t-1
@@ -754,40 +756,35 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const int r = 32 * quad + lane_id();      // TMEM lane: key row (S^T, dP^T, dK, dV) / query row (dQ)
     const int key = kt * TK + r;
     const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
-    const int t = threadIdx.x - 64;           // 0..255 within the compute warps
-    // dQ rows of a query tile: TMEM -> staging smem (row r, 16-byte chunks in a per-thread rotated
-    // order against bank conflicts) -> one TMA reduce-add of the 128 x 64 fp32 box into dq_acc.
+    // dQ rows of a query tile: each compute warp moves its own 32 rows x 32 columns TMEM -> its
+    // 4 KB staging block (128B-swizzled, conflict-free) -> one TMA reduce-add of that 32 x 32 fp32
+    // box into dq_acc.  No barrier across warps: a warp only waits for its own previous reduce to
+    // have read the block.
+    uint8_t* dq_stage = reinterpret_cast<uint8_t*>(sDQ) + (warp - 2) * 4096;
     auto flush_dq = [&](int qt) {
-      // this warp's 32 dQ columns (half) of its 32 rows
       uint32_t v0[32];
       tmem_ld_32x32b_x32_nowait(tdQ + lane_base + half * 32, v0);
       tmem_wait_ld();
-      if (t == 0) bulk_wait_read0();  // the previous reduce has finished reading the staging
-      named_sync_compute();
-      // two [128][32] fp32 halves, 128B-swizzled (chunk c of row r at c ^ (r & 7)): conflict-free
-      uint8_t* st0 = reinterpret_cast<uint8_t*>(sDQ);
-      uint8_t* sth = st0 + half * 128 * 128;
+      if (lane_id() == 0) bulk_wait_read0();
+      __syncwarp();
+      const int rr = lane_id();
 #pragma unroll
       for (int c = 0; c < 8; ++c)
-        *reinterpret_cast<uint4*>(sth + sw128(r, c)) = make_uint4(v0[4 * c], v0[4 * c + 1], v0[4 * c + 2], v0[4 * c + 3]);
+        *reinterpret_cast<uint4*>(dq_stage + sw128(rr, c)) = make_uint4(v0[4 * c], v0[4 * c + 1], v0[4 * c + 2], v0[4 * c + 3]);
       fence_proxy_async_shared();
-      named_sync_compute();
-      if (t == 0) {
-        tma_reduce_add_2d(&tm_dq, st0, h * HDIM, row0 + qt * TQ);
-        tma_reduce_add_2d(&tm_dq, st0 + 128 * 128, h * HDIM + 32, row0 + qt * TQ);
+      __syncwarp();
+      if (lane_id() == 0) {
+        tma_reduce_add_2d(&tm_dq, dq_stage, h * HDIM + half * 32, row0 + qt * TQ + 32 * quad);
         bulk_commit();
       }
     };
     for (int n = 0; n < N; ++n) {
       const int qt = kt + n;
       const int par = n % BWD_STAGES;  // stage of this query tile's Q / dO / lse / D buffers
-      const float* sL = sLD + par * 256;  // -lse after the in-place negation below
+      const float* sL = sLD + par * 256;  // this query tile's lse (log2 domain), then D
       const float* sDd = sL + 128;
       mbar_wait(sdp_full, n & 1);  // implies the stage's TMA (incl. lse / D) has landed
       tc_fence_after();
-      // negate this tile's lse once in smem (thread t: entry t) so the exponent is one FFMA2
-      if (t < TQ) sLn[par * 256 + t] = -sLn[par * 256 + t];
-      named_sync_compute();
       const bool diag = n == 0;
       uint32_t pk[2][16], dk[2][16];
 #pragma unroll
@@ -828,7 +825,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     mbar_wait(dq_full, (N - 1) & 1);
     tc_fence_after();
     flush_dq(kt + N - 1);
-    if (t == 0) bulk_wait_all0();  // the last reduce-add has completed before the CTA exits
+    if (lane_id() == 0) bulk_wait_all0();  // this warp's last reduce-add has completed before the CTA exits
     // dK (scaled) and dV rows of this thread's key into the k / v slices of dqkv
     __nv_bfloat16* row = dqkv + ((int64_t)row0 + key) * 3 * D;
     {
@@ -901,7 +898,7 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int S, int H, cud
     launch_pdl(k_attn_fwd_tc, dim3(S / TQ, H, B), dim3(FWD_THREADS), FwdSmem::TOTAL, st, tm,
                static_cast<__nv_bfloat16*>(out), lse, S, H, scale_log2);
   else
-    launch_pdl(k_attn_fwd_tc2, dim3(S / TQ, H, B), dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm,
+    launch_pdl(k_attn_fwd_tc2, dim3(H, B, S / TQ), dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm,
                static_cast<__nv_bfloat16*>(out), lse, S, H, scale_log2);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "attention fwd: %s", cudaGetErrorString(e));
@@ -919,7 +916,7 @@ int attn_bwd_tc(const void* qkv, const void* dout, const float* lse, const float
     auto fn = encode_tiled();
     cuuint64_t dims[2] = {(cuuint64_t)H * HDIM, (cuuint64_t)B * S};
     cuuint64_t strides[1] = {(cuuint64_t)H * HDIM * 4};
-    cuuint32_t box[2] = {32, 128};
+    cuuint32_t box[2] = {32, 32};  // one compute warp's 32 rows x 32 fp32 columns
     cuuint32_t es[2] = {1, 1};
     if (fn(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq_acc, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
@@ -933,7 +930,7 @@ int attn_bwd_tc(const void* qkv, const void* dout, const float* lse, const float
     attr = true;
   }
   const float scale = 1.0f / sqrtf((float)HDIM);
-  launch_pdl(k_attn_bwd_tc, dim3(S / TK, H, B), dim3(BWD_THREADS), BwdSmem::TOTAL, st, 
+  launch_pdl(k_attn_bwd_tc, dim3(H, B, S / TK), dim3(BWD_THREADS), BwdSmem::TOTAL, st, 
       tq, tdo, tdq, lse, Dv, static_cast<__nv_bfloat16*>(dqkv), dq_acc, S, H, scale * 1.4426950408889634f, scale);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "attention bwd: %s", cudaGetErrorString(e));

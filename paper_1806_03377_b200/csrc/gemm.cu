@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   using C = TcCfg<CG, BN, B_MN, KIND>;
   constexpr int UM = TC_BM * CG;  // tile rows per unit (CTA or CTA pair)
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align_1k(smem_raw);
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);

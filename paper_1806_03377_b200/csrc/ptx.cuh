@@ -15,6 +15,14 @@ PD_DEVICE uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// First 1 KB-aligned byte of the dynamic shared-memory window (SW128 tiles need 1 KB alignment).
+// The result is smem_raw plus an integer offset, so the compiler still knows it points to shared
+// memory and emits LDS / STS for accesses through it; rounding the address as an integer
+// (uintptr_t) would turn every such access into a generic LD.E / ST.E.
+PD_DEVICE uint8_t* smem_align_1k(uint8_t* smem_raw) {
+  return smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+}
+
 PD_DEVICE uint32_t warp_id() { return threadIdx.x >> 5; }
 PD_DEVICE uint32_t lane_id() { return threadIdx.x & 31; }
 

@@ -70,3 +70,36 @@ def test_profile_plan_simulate_checkpoint(tmp_path):
     assert np.isfinite(lb).all() and lb[0] != la[0]
     w0 = np.load(ck / files[0])
     assert "W0" in w0 and w0["W0"].dtype == np.float32
+
+
+@pytest.mark.gpu
+def test_compare_regimes_on_device(tmp_path):
+    """The reference's five regimes (cli.py:211-261) executed on the runtime: every regime runs and
+    reports a measured throughput, single_machine is the 1.00x base, the artefact has the schema."""
+    env = dict(os.environ)
+    run = lambda *a: subprocess.run([sys.executable, "-m", "paper_1806_03377_b200", *a], cwd=REPO, env=env,  # noqa
+                                    capture_output=True, text=True, timeout=900)
+    model = "mlp:256:4:64:bf16"
+    r = run("profile", "--model", model, "--out", str(tmp_path / "profile.json"))
+    assert r.returncode == 0, r.stderr
+    r = run("compare", str(tmp_path / "profile.json"), "--model", model, "--machines", "4", "--minibatches", "16",
+            "--out-dir", str(tmp_path))
+    assert r.returncode == 0, r.stdout + r.stderr
+    doc = json.loads((tmp_path / "compare.json").read_text())
+    names = [x["regime"] for x in doc["regimes"]]
+    assert names == ["single_machine", "model_parallel", "data_parallel", "straight_pipeline", "full_plan"]
+    assert doc["regimes"][0]["speedup"] == 1.0 and doc["regimes"][2]["config"] == "4"
+    assert all(x["throughput"] > 0 and x["predicted_throughput"] > 0 for x in doc["regimes"])
+    assert doc["regimes"][1]["max_inflight"] == 1
+
+
+def test_compare_minibatches_whole_rounds():
+    from paper_1806_03377_b200.plans import Plan, Stage
+
+    p71 = Plan(stages=(Stage(1, 13, 7), Stage(14, 16, 1)), bottleneck_time=1.0, noam=2, machines_used=8)
+    assert cli._regime_minibatches(p71, 32) == 35
+    p8 = Plan(stages=(Stage(1, 16, 8),), bottleneck_time=1.0, noam=1, machines_used=8)
+    assert cli._regime_minibatches(p8, 32) == 32
+    with pytest.raises(SystemExit) as e:
+        cli.main(["compare", "x.json"])  # --model / --machines missing: usage error
+    assert e.value.code == cli.EXIT_USAGE
