@@ -584,6 +584,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
 //   Q / dO / lse / D stream through a 3-stage ring; S^T / dP^T of tile n+1 are issued once the
 //   compute warps hold tile n in registers (sdp_free).
 constexpr int BWD_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 compute (two per TMEM lane quadrant)
+PD_DEVICE void named_sync_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }  // the 8 compute warps
 
 // One 32-query chunk of a key row: P^T = exp2(S^T*scale - lse), dS^T = P^T (dP^T - D) -> bf16 pairs.
 // lse: the query rows' log-sum-exp (log2 domain).  MASK (diagonal tile only): queries q0+i < key are causal-masked.  The unmasked
@@ -632,7 +633,7 @@ struct BwdSmem {
 };
 
 
-__global__ void __maxnreg__(200)
+__global__ void __launch_bounds__(BWD_THREADS, 1)
     k_attn_bwd_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                   const __grid_constant__ CUtensorMap tm_dq,
                   const float* __restrict__ lse, const float* __restrict__ Dv, __nv_bfloat16* __restrict__ dqkv,
@@ -756,25 +757,26 @@ __global__ void __maxnreg__(200)
     const int r = 32 * quad + lane_id();      // TMEM lane: key row (S^T, dP^T, dK, dV) / query row (dQ)
     const int key = kt * TK + r;
     const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
-    // dQ rows of a query tile: each compute warp moves its own 32 rows x 32 columns TMEM -> its
-    // 4 KB staging block (128B-swizzled, conflict-free) -> one TMA reduce-add of that 32 x 32 fp32
-    // box into dq_acc.  No barrier across warps: a warp only waits for its own previous reduce to
-    // have read the block.
-    uint8_t* dq_stage = reinterpret_cast<uint8_t*>(sDQ) + (warp - 2) * 4096;
+    const int t = threadIdx.x - 64;           // 0..255 within the compute warps
+    // dQ rows of a query tile: TMEM -> staging smem (two [128][32] fp32 halves, 128B-swizzled,
+    // conflict-free) -> one TMA reduce-add per half of the 128 x 32 fp32 box into dq_acc.
     auto flush_dq = [&](int qt) {
+      // this warp's 32 dQ columns (half) of its 32 rows
       uint32_t v0[32];
       tmem_ld_32x32b_x32_nowait(tdQ + lane_base + half * 32, v0);
       tmem_wait_ld();
-      if (lane_id() == 0) bulk_wait_read0();
-      __syncwarp();
-      const int rr = lane_id();
+      if (t == 0) bulk_wait_read0();  // the previous reduce has finished reading the staging
+      named_sync_compute();
+      uint8_t* st0 = reinterpret_cast<uint8_t*>(sDQ);
+      uint8_t* sth = st0 + half * 128 * 128;
 #pragma unroll
       for (int c = 0; c < 8; ++c)
-        *reinterpret_cast<uint4*>(dq_stage + sw128(rr, c)) = make_uint4(v0[4 * c], v0[4 * c + 1], v0[4 * c + 2], v0[4 * c + 3]);
+        *reinterpret_cast<uint4*>(sth + sw128(r, c)) = make_uint4(v0[4 * c], v0[4 * c + 1], v0[4 * c + 2], v0[4 * c + 3]);
       fence_proxy_async_shared();
-      __syncwarp();
-      if (lane_id() == 0) {
-        tma_reduce_add_2d(&tm_dq, dq_stage, h * HDIM + half * 32, row0 + qt * TQ + 32 * quad);
+      named_sync_compute();
+      if (t == 0) {
+        tma_reduce_add_2d(&tm_dq, st0, h * HDIM, row0 + qt * TQ);
+        tma_reduce_add_2d(&tm_dq, st0 + 128 * 128, h * HDIM + 32, row0 + qt * TQ);
         bulk_commit();
       }
     };
@@ -825,7 +827,7 @@ __global__ void __maxnreg__(200)
     mbar_wait(dq_full, (N - 1) & 1);
     tc_fence_after();
     flush_dq(kt + N - 1);
-    if (lane_id() == 0) bulk_wait_all0();  // this warp's last reduce-add has completed before the CTA exits
+    if (t == 0) bulk_wait_all0();  // the last reduce-add has completed before the CTA exits
     // dK (scaled) and dV rows of this thread's key into the k / v slices of dqkv
     __nv_bfloat16* row = dqkv + ((int64_t)row0 + key) * 3 * D;
     {
@@ -916,7 +918,7 @@ int attn_bwd_tc(const void* qkv, const void* dout, const float* lse, const float
     auto fn = encode_tiled();
     cuuint64_t dims[2] = {(cuuint64_t)H * HDIM, (cuuint64_t)B * S};
     cuuint64_t strides[1] = {(cuuint64_t)H * HDIM * 4};
-    cuuint32_t box[2] = {32, 32};  // one compute warp's 32 rows x 32 fp32 columns
+    cuuint32_t box[2] = {32, 128};
     cuuint32_t es[2] = {1, 1};
     if (fn(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq_acc, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
