@@ -9,12 +9,14 @@ SimulationError, PD_ERR_CUDA -> NativeError).
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import POINTER, Structure, c_double, c_float, c_int, c_int32, c_int64, c_void_p
 from pathlib import Path
 
 from .errors import NativeError, SimulationError, ValidationError
 
-LIB_PATH = Path(__file__).resolve().parent / "libpd_b200.so"
+# PD_LIB: an alternative in-tree build of the same library (A/B measurements of compile-time variants)
+LIB_PATH = Path(os.environ.get("PD_LIB") or Path(__file__).resolve().parent / "libpd_b200.so")
 
 PD_F32, PD_BF16 = 0, 1
 EPI_STORE, EPI_LOSS, EPI_MASK, EPI_SGD, EPI_GRADF32, EPI_GELU, EPI_GELU_BWD, EPI_RESID = range(8)

@@ -129,10 +129,30 @@ PD_DEVICE float exp_pack64(const uint32_t (&sr)[64], int base, int lim, float sc
   }
 }
 
+// 2^x for two values on the FMA pipe (no MUFU): x = r + f with r = rint(x) (the 1.5*2^23 add puts
+// r in the low mantissa bits) and f in [-1/2, 1/2]; 2^f by a degree-3 minimax polynomial (max
+// relative error 7.5e-5, far below the bf16 rounding of P), 2^r by adding r << 23 to the exponent
+// field.  x is clamped at -126 so the exponent add cannot wrap (2^-126 ~ 0 after bf16 / the sum).
+PD_DEVICE float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 r = __fadd2_rn(x, magic);
+  const float2 ri = __fadd2_rn(r, make_float2(-12582912.f, -12582912.f));  // rint(x), exact
+  const float2 f = __ffma2_rn(ri, make_float2(-1.f, -1.f), x);                 // x - rint(x), exact
+  float2 p = __ffma2_rn(f, make_float2(0.05517134442925453f, 0.05517134442925453f),
+                        make_float2(0.24261033535003662f, 0.24261033535003662f));
+  p = __ffma2_rn(p, f, make_float2(0.6932609677314758f, 0.6932609677314758f));
+  p = __ffma2_rn(p, f, make_float2(0.9999281167984009f, 0.9999281167984009f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23)));
+}
+
 // p = exp2(s*scale + neg) for 32 scores sr[0..31] -> 16 packed bf16 pairs (pk[i] = keys 2i, 2i+1,
 // the column layout of a bf16 A operand in TMEM); returns the fp32 sum.  MASK: only columns
-// base+i <= lim are kept.
-template <bool MASK>
+// base+i <= lim are kept.  POLY8 of every 8 pairs are computed on the FMA pipe (exp2_poly2) instead
+// of the MUFU, whose 16 results / clock / SM bound the forward when every exp goes to it.
+template <bool MASK, int POLY8>
 PD_DEVICE float exp_pack32(const uint32_t* sr, int base, int lim, float scale, float neg, uint32_t (&pk)[16]) {
   const float2 sc = make_float2(scale, scale), ng = make_float2(neg, neg);
   float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;
@@ -140,8 +160,8 @@ PD_DEVICE float exp_pack32(const uint32_t* sr, int base, int lim, float scale, f
   for (int i = 0; i < 32; i += 4) {
     const float2 x0 = __ffma2_rn(make_float2(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])), sc, ng);
     const float2 x1 = __ffma2_rn(make_float2(__uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3])), sc, ng);
-    float2 p0 = make_float2(fast_exp2(x0.x), fast_exp2(x0.y));
-    float2 p1 = make_float2(fast_exp2(x1.x), fast_exp2(x1.y));
+    float2 p0 = ((i / 2) % 8) >= 8 - POLY8 ? exp2_poly2(x0) : make_float2(fast_exp2(x0.x), fast_exp2(x0.y));
+    float2 p1 = ((i / 2 + 1) % 8) >= 8 - POLY8 ? exp2_poly2(x1) : make_float2(fast_exp2(x1.x), fast_exp2(x1.y));
     if constexpr (MASK) {
       if (base + i > lim) p0.x = 0.f;
       if (base + i + 1 > lim) p0.y = 0.f;
@@ -361,6 +381,28 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
 // exp2 of tile j.  P_j goes to TMEM (tcgen05.st) and O += P_j V_j reads it as the A operand
 // straight from TMEM (the TS form), so P never touches shared memory.  K and V stream through a
 // two-stage ring.  Numerics are those of k_attn_fwd_tc (same max, exp2, lazy rescale, bf16 P).
+#if PD_ATTN_TRACE
+// Diagnostic build only (tools/build_variant.sh ... -DPD_ATTN_TRACE=1): %globaltimer stamps of the
+// forward's per-tile events for the first CTAs, read back with pd_attn_trace().
+constexpr int TR_CTAS = 2048, TR_EV = 64;
+__device__ unsigned long long g_attn_trace[TR_CTAS][TR_EV];
+PD_DEVICE void tr_stamp(int slot) {
+  const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (cta < TR_CTAS && slot < TR_EV) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_attn_trace[cta][slot] = t;
+    if (slot == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_attn_trace[cta][TR_EV - 1] = smid;
+    }
+  }
+}
+#define TR(slot) tr_stamp(slot)
+#else
+#define TR(slot) ((void)0)
+#endif
 constexpr int FWD2_STAGES = 2;
 struct Fwd2Smem {
   static constexpr int Q = 0;
@@ -370,10 +412,12 @@ struct Fwd2Smem {
   static constexpr int TOTAL = BAR + 256 + 1024;
 };
 
+template <int POLY8>
 __global__ void __launch_bounds__(FWD_THREADS, 2)
     k_attn_fwd_tc2(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ out,
                    float* __restrict__ lse, int S, int H, float scale_log2) {
   griddep_wait();
+  if (threadIdx.x == 64) TR(0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_align_1k(smem_raw);
   uint8_t* sQ = smem + Fwd2Smem::Q;
@@ -483,8 +527,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
     const int q = qt * TQ + r;
     const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
     float m = -INFINITY, l = 0.f;
+    if (threadIdx.x == 64) TR(1);
     for (int j = 0; j < n_kt; ++j) {
       mbar_wait(s_full, j & 1);
+      if (threadIdx.x == 64) TR(2 + 4 * j);
       tc_fence_after();
       uint32_t sr[128];
 #pragma unroll
@@ -518,9 +564,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
       uint32_t pk[4][16];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
-        rs += diag ? exp_pack32<true>(sr + 32 * c, 32 * c, lim, scale_log2, neg, pk[c])
-                   : exp_pack32<false>(sr + 32 * c, 0, 0, scale_log2, neg, pk[c]);
+        rs += diag ? exp_pack32<true, POLY8>(sr + 32 * c, 32 * c, lim, scale_log2, neg, pk[c])
+                   : exp_pack32<false, POLY8>(sr + 32 * c, 0, 0, scale_log2, neg, pk[c]);
+      if (threadIdx.x == 64) TR(3 + 4 * j);
       if (j > 0) mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} done: O final for j-1, P free
+      if (threadIdx.x == 64) TR(4 + 4 * j);
       tc_fence_after();
       if (rescale) {
 #pragma unroll
@@ -545,8 +593,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(p_ready);
+      if (threadIdx.x == 64) TR(5 + 4 * j);
     }
     mbar_wait(o_done, (n_kt - 1) & 1);
+    if (threadIdx.x == 64) TR(40);
     tc_fence_after();
     const float inv = 1.f / l;
     __nv_bfloat16* orow = out + ((int64_t)row0 + q) * D + h * HDIM;
@@ -559,6 +609,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 2)
       store32_bf16(orow, 0, 0, c * 32, o);
     }
     lse[((int64_t)b * H + h) * S + q] = m + log2f(l);
+    if (threadIdx.x == 64) TR(41);
   }
   tc_fence_before();
   __syncthreads();
@@ -619,11 +670,11 @@ PD_DEVICE void bwd_chunk32(const uint32_t (&svr)[32], const uint32_t (&dpr)[32],
     dk[i / 2 + 1] = pack_bf16x2(d1.x, d1.y);
   }
 }
-constexpr int BWD_STAGES = 3;  // Q / dO / lse / D ring: tile n+1's loads start while n-1's MMAs drain
+constexpr int BWD_STAGES = 2;  // Q / dO / lse / D ring (the K / V double buffer takes the third stage's smem)
 struct BwdSmem {
-  static constexpr int K = 0;
-  static constexpr int V = K + TILE_BYTES;
-  static constexpr int Q = V + TILE_BYTES;                      // [BWD_STAGES]
+  static constexpr int K = 0;                                   // [2] (this item's, the next item's)
+  static constexpr int V = K + 2 * TILE_BYTES;                  // [2]
+  static constexpr int Q = V + 2 * TILE_BYTES;                  // [BWD_STAGES]
   static constexpr int DO = Q + BWD_STAGES * TILE_BYTES;        // [BWD_STAGES]
   static constexpr int DS = DO + BWD_STAGES * TILE_BYTES;       // dS^T: two K-major atoms over queries
   static constexpr int LD = DS + 2 * TILE_BYTES;                // lse/D: [stage][2][128] floats
@@ -631,14 +682,48 @@ struct BwdSmem {
   static constexpr int BAR = DQ + 128 * 64 * 4;
   static constexpr int TOTAL = BAR + 256 + 1024;
 };
+static_assert(BwdSmem::TOTAL <= 227 * 1024, "attention bwd smem");
 
+// Work item of the persistent backward: one (key tile, head, sequence).  Items are numbered key tile
+// slowest, so item order is longest-first (key tile kt has n_t - kt query tiles); CTA c of P takes
+// items c, 2P-1-c, 2P+c, 4P-1-c, ... (a boustrophedon over the longest-first list), which balances
+// the per-CTA sums of query tiles to within one tile of the mean (8 x 1024 tokens, 16 heads: 32 vs 31.1).
+struct BwdItem {
+  int kt, h, b, N;
+};
+PD_DEVICE bool bwd_item(int r, int n_items, int H, int B, int n_t, BwdItem& it) {
+  const int P = (int)gridDim.x, c = (int)blockIdx.x;
+  const int idx = r * P + ((r & 1) ? P - 1 - c : c);
+  if (idx >= n_items) return false;
+  it.kt = idx / (H * B);
+  const int hb = idx - it.kt * (H * B);
+  it.h = hb % H;
+  it.b = hb / H;
+  it.N = n_t - it.kt;
+  return true;
+}
 
+// Persistent causal attention backward: one CTA per SM loops over its work items.  Per item the
+// K / V tiles are loaded once (double-buffered, so the next item's arrive during this one) and the
+// query tiles kt .. n_t-1 stream through the Q / dO / lse / D ring.  TMEM columns: S^T [0,128),
+// dP^T [128,256), dV [256,320), dK [320,384), dQ [384,448), P^T (bf16 pairs) [448,512).
+//   MMA warp:   S^T = K Q^T, dP^T = V dO^T (M = keys, N = queries, K = 64)
+//               dV += P^T dO (P^T from TMEM), dK += dS^T Q (M = keys, N = 64, K = queries)
+//               dQ  = dS K (M = queries, N = 64, K = keys; A = dS^T read MN-major)
+//   warps 2-9:  thread = TMEM lane, two warps per lane quadrant splitting the 128 query columns (and
+//               the 64 dQ / dK / dV columns): P^T = exp2(S^T*scale - lse) -> bf16 into TMEM, dS^T =
+//               P^T (dP^T - D) -> bf16 into shared memory, the previous tile's dQ out of TMEM into the
+//               fp32 dq_acc by TMA reduce-add, and at an item boundary the finished item's dK / dV.
+// S^T / dP^T of the next tile (also across an item boundary) are issued as soon as the compute warps
+// hold the current tile in registers (sdp_free), so the previous item's dQ flush and dK / dV
+// read-out run under the next item's first S^T / dP^T MMAs: there is no per-item prologue or tail.
 __global__ void __launch_bounds__(BWD_THREADS, 1)
     k_attn_bwd_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                   const __grid_constant__ CUtensorMap tm_dq,
                   const float* __restrict__ lse, const float* __restrict__ Dv, __nv_bfloat16* __restrict__ dqkv,
-                  float* __restrict__ dq_acc, int S, int H, float scale_log2, float scale) {
+                  float* __restrict__ dq_acc, int S, int H, int B, float scale_log2, float scale) {
   griddep_wait();
+  if (threadIdx.x == 64) TR(0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_align_1k(smem_raw);
   uint8_t* sK = smem + BwdSmem::K;
@@ -649,9 +734,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   float* sLD = reinterpret_cast<float*>(smem + BwdSmem::LD);
   float* sDQ = reinterpret_cast<float*>(smem + BwdSmem::DQ);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BwdSmem::BAR);
-  uint64_t* full_kv = bar + 0;
-  uint64_t* full_qdo = bar + 1;                // [BWD_STAGES]
-  uint64_t* empty_qdo = full_qdo + BWD_STAGES;  // [BWD_STAGES]
+  uint64_t* full_kv = bar + 0;                   // [2]
+  uint64_t* empty_kv = full_kv + 2;              // [2]
+  uint64_t* full_qdo = empty_kv + 2;             // [BWD_STAGES]
+  uint64_t* empty_qdo = full_qdo + BWD_STAGES;   // [BWD_STAGES]
   uint64_t* sdp_full = empty_qdo + BWD_STAGES;
   uint64_t* pds_ready = sdp_full + 1;
   uint64_t* dq_full = sdp_full + 2;
@@ -659,17 +745,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sdp_full + 4);
 
   const int n_t = S / TK;
-  const int kt = (int)blockIdx.z;  // key tile (slowest grid index): tile 0, the longest, is dispatched first
-  const int h = blockIdx.x, b = blockIdx.y;
+  const int n_items = n_t * H * B;
   const int D = H * HDIM;
-  const int row0 = b * S;
-  const int N = n_t - kt;  // query tiles kt .. n_t-1
   const int warp = warp_id();
 
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch_desc(&tm_qkv);
     tma_prefetch_desc(&tm_do);
-    mbar_init(full_kv, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&full_kv[i], 1); mbar_init(&empty_kv[i], 1); }
     for (int i = 0; i < BWD_STAGES; ++i) { mbar_init(&full_qdo[i], 1); mbar_init(&empty_qdo[i], 1); }
     mbar_init(sdp_full, 1);
     mbar_init(pds_ready, 8);
@@ -687,35 +770,43 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   const uint32_t tPt = tmem + 448;  // P^T as bf16 pairs (64 columns), the A operand of dV
 
   if (warp == 0) {
+    // ---------------- TMA producer: per item K / V (double-buffered), then the query tiles
     if (elect_one()) {
-      mbar_arrive_expect_tx(full_kv, 2 * TILE_BYTES);
-      tma_load_2d(sK, &tm_qkv, full_kv, D + h * HDIM, row0 + kt * TK);
-      tma_load_2d(sV, &tm_qkv, full_kv, 2 * D + h * HDIM, row0 + kt * TK);
-      for (int n = 0; n < N; ++n) {
-        const int st = n % BWD_STAGES, qt = kt + n;
-        mbar_wait(&empty_qdo[st], ((n / BWD_STAGES) & 1) ^ 1);
-        mbar_arrive_expect_tx(&full_qdo[st], 2 * TILE_BYTES + 2 * TQ * 4);
-        tma_load_2d(sQ + st * TILE_BYTES, &tm_qkv, &full_qdo[st], h * HDIM, row0 + qt * TQ);
-        tma_load_2d(sdO + st * TILE_BYTES, &tm_do, &full_qdo[st], h * HDIM, row0 + qt * TQ);
-        // this query tile's log-sum-exp and D rows ride along with Q / dO (stage buffers)
-        const int64_t lrow = ((int64_t)b * H + h) * S + qt * TQ;
-        bulk_load_1d(sLD + st * 256, lse + lrow, TQ * 4, &full_qdo[st]);
-        bulk_load_1d(sLD + st * 256 + 128, Dv + lrow, TQ * 4, &full_qdo[st]);
+      BwdItem it;
+      int g = 0, ic = 0;
+      for (int r = 0; r * (int)gridDim.x < n_items; ++r) {
+        if (!bwd_item(r, n_items, H, B, n_t, it)) continue;
+        const int kb = ic & 1, row0 = it.b * S;
+        mbar_wait(&empty_kv[kb], ((ic >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full_kv[kb], 2 * TILE_BYTES);
+        tma_load_2d(sK + kb * TILE_BYTES, &tm_qkv, &full_kv[kb], D + it.h * HDIM, row0 + it.kt * TK);
+        tma_load_2d(sV + kb * TILE_BYTES, &tm_qkv, &full_kv[kb], 2 * D + it.h * HDIM, row0 + it.kt * TK);
+        for (int n = 0; n < it.N; ++n, ++g) {
+          const int st = g % BWD_STAGES, qt = it.kt + n;
+          mbar_wait(&empty_qdo[st], ((g / BWD_STAGES) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full_qdo[st], 2 * TILE_BYTES + 2 * TQ * 4);
+          tma_load_2d(sQ + st * TILE_BYTES, &tm_qkv, &full_qdo[st], it.h * HDIM, row0 + qt * TQ);
+          tma_load_2d(sdO + st * TILE_BYTES, &tm_do, &full_qdo[st], it.h * HDIM, row0 + qt * TQ);
+          // this query tile's log-sum-exp and D rows ride along with Q / dO (stage buffers)
+          const int64_t lrow = ((int64_t)it.b * H + it.h) * S + qt * TQ;
+          bulk_load_1d(sLD + st * 256, lse + lrow, TQ * 4, &full_qdo[st]);
+          bulk_load_1d(sLD + st * 256 + 128, Dv + lrow, TQ * 4, &full_qdo[st]);
+        }
+        ++ic;
       }
     }
   } else if (warp == 1) {
+    // ---------------- MMA issuer
     if (elect_one()) {
       constexpr uint32_t idesc_sq = make_idesc_bf16(TK, TQ, false, false);      // S^T, dP^T
       constexpr uint32_t idesc_kv = make_idesc_bf16(TK, HDIM, false, true);     // dV, dK
       constexpr uint32_t idesc_q = make_idesc_bf16(TQ, HDIM, true, true);       // dQ (A = dS^T MN-major)
-      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), ds_addr = smem_u32(sdS);
-      // S^T / dP^T of tile n+1 are issued as soon as the compute warps have read tile n's (sdp_free),
-      // so they run under the compute warps' dQ flush and P / dS stores; dV / dK / dQ of tile n
-      // then run under the compute warps' exp / dS math of tile n+1.
-      auto issue_sdp = [&](int n) {
-        const int st = n % BWD_STAGES;
+      const uint32_t ds_addr = smem_u32(sdS);
+      auto issue_sdp = [&](int g, int kb) {
+        const int st = g % BWD_STAGES;
+        const uint32_t k_addr = smem_u32(sK + kb * TILE_BYTES), v_addr = smem_u32(sV + kb * TILE_BYTES);
         const uint32_t q_addr = smem_u32(sQ + st * TILE_BYTES), do_addr = smem_u32(sdO + st * TILE_BYTES);
-        mbar_wait(&full_qdo[st], (n / BWD_STAGES) & 1);
+        mbar_wait(&full_qdo[st], (g / BWD_STAGES) & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < HDIM / 16; ++k) {
@@ -726,42 +817,65 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         }
         umma_commit(sdp_full);
       };
-      mbar_wait(full_kv, 0);
-      issue_sdp(0);
-      for (int n = 0; n < N; ++n) {
-        const int st = n % BWD_STAGES;
-        const uint32_t q_addr = smem_u32(sQ + st * TILE_BYTES), do_addr = smem_u32(sdO + st * TILE_BYTES);
-        mbar_wait(sdp_free, n & 1);  // S^T / dP^T of n are in the compute warps' registers
-        if (n + 1 < N) issue_sdp(n + 1);
-        mbar_wait(pds_ready, n & 1);  // P^T / dS^T of n in smem, dQ of n-1 flushed out of TMEM
-        tc_fence_after();
+      BwdItem it, nx;
+      int r = 0;
+      auto fetch = [&](BwdItem& x) {  // next item of this CTA (false: none left)
+        for (; r * (int)gridDim.x < n_items; ++r)
+          if (bwd_item(r, n_items, H, B, n_t, x)) { ++r; return true; }
+        return false;
+      };
+      bool have = fetch(it);
+      int g = 0, ic = 0;
+      if (have) {
+        mbar_wait(&full_kv[0], 0);
+        issue_sdp(0, 0);
+      }
+      while (have) {
+        const int kb = ic & 1;
+        const bool more = fetch(nx);
+        const uint32_t k_addr = smem_u32(sK + kb * TILE_BYTES);
+        for (int n = 0; n < it.N; ++n, ++g) {
+          const int st = g % BWD_STAGES;
+          const uint32_t q_addr = smem_u32(sQ + st * TILE_BYTES), do_addr = smem_u32(sdO + st * TILE_BYTES);
+          mbar_wait(sdp_free, g & 1);  // S^T / dP^T of g are in the compute warps' registers
+          if (n + 1 < it.N) {
+            issue_sdp(g + 1, kb);
+          } else if (more) {  // the next item's first tile, on the other K / V buffer
+            mbar_wait(&full_kv[kb ^ 1], ((ic + 1) >> 1) & 1);
+            issue_sdp(g + 1, kb ^ 1);
+          }
+          mbar_wait(pds_ready, g & 1);  // P^T / dS^T of g in place, dQ of g-1 (and the last item's dK / dV) read
+          tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < TQ / 16; ++k) {
-          const uint32_t a_off = (k >> 2) * TILE_BYTES + (k & 3) * 32;  // K-major over queries
-          // dV += P^T dO with P^T in TMEM (8 columns = 16 bf16 queries per step)
-          umma_bf16_ts(tdV, tPt + k * 8, make_sw128_desc(do_addr + k * 2048, 8192, 1024), idesc_kv, (n | k) != 0);
-          umma_bf16(tdK, make_sw128_desc(ds_addr + a_off, 16, 1024), make_sw128_desc(q_addr + k * 2048, 8192, 1024),
-                    idesc_kv, (n | k) != 0);
+          for (int k = 0; k < TQ / 16; ++k) {
+            const uint32_t a_off = (k >> 2) * TILE_BYTES + (k & 3) * 32;  // K-major over queries
+            // dV += P^T dO with P^T in TMEM (8 columns = 16 bf16 queries per step)
+            umma_bf16_ts(tdV, tPt + k * 8, make_sw128_desc(do_addr + k * 2048, 8192, 1024), idesc_kv, (n | k) != 0);
+            umma_bf16(tdK, make_sw128_desc(ds_addr + a_off, 16, 1024), make_sw128_desc(q_addr + k * 2048, 8192, 1024),
+                      idesc_kv, (n | k) != 0);
+          }
+#pragma unroll
+          for (int k = 0; k < TK / 16; ++k)  // K = keys: dS^T rows (+2 KB per 16), query atoms 16 KB apart
+            umma_bf16(tdQ, make_sw128_desc(ds_addr + k * 2048, TILE_BYTES, 1024),
+                      make_sw128_desc(k_addr + k * 2048, 8192, 1024), idesc_q, k != 0);
+          umma_commit(dq_full);
+          umma_commit(&empty_qdo[st]);
         }
-#pragma unroll
-        for (int k = 0; k < TK / 16; ++k)  // K = keys: dS^T rows (+2 KB per 16), query atoms 16 KB apart
-          umma_bf16(tdQ, make_sw128_desc(ds_addr + k * 2048, TILE_BYTES, 1024),
-                    make_sw128_desc(k_addr + k * 2048, 8192, 1024), idesc_q, k != 0);
-        umma_commit(dq_full);
-        umma_commit(&empty_qdo[st]);
+        umma_commit(&empty_kv[kb]);
+        it = nx;
+        have = more;
+        ++ic;
       }
     }
   } else {
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;         // warps 2-5: query columns 0..63, warps 6-9: 64..127
     const int r = 32 * quad + lane_id();      // TMEM lane: key row (S^T, dP^T, dK, dV) / query row (dQ)
-    const int key = kt * TK + r;
     const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
     const int t = threadIdx.x - 64;           // 0..255 within the compute warps
     // dQ rows of a query tile: TMEM -> staging smem (two [128][32] fp32 halves, 128B-swizzled,
     // conflict-free) -> one TMA reduce-add per half of the 128 x 32 fp32 box into dq_acc.
-    auto flush_dq = [&](int qt) {
-      // this warp's 32 dQ columns (half) of its 32 rows
+    auto flush_dq = [&](int h, int trow) {
       uint32_t v0[32];
       tmem_ld_32x32b_x32_nowait(tdQ + lane_base + half * 32, v0);
       tmem_wait_ld();
@@ -775,71 +889,92 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       fence_proxy_async_shared();
       named_sync_compute();
       if (t == 0) {
-        tma_reduce_add_2d(&tm_dq, st0, h * HDIM, row0 + qt * TQ);
-        tma_reduce_add_2d(&tm_dq, st0 + 128 * 128, h * HDIM + 32, row0 + qt * TQ);
+        tma_reduce_add_2d(&tm_dq, st0, h * HDIM, trow);
+        tma_reduce_add_2d(&tm_dq, st0 + 128 * 128, h * HDIM + 32, trow);
         bulk_commit();
       }
     };
-    for (int n = 0; n < N; ++n) {
-      const int qt = kt + n;
-      const int par = n % BWD_STAGES;  // stage of this query tile's Q / dO / lse / D buffers
-      const float* sL = sLD + par * 256;  // this query tile's lse (log2 domain), then D
-      const float* sDd = sL + 128;
-      mbar_wait(sdp_full, n & 1);  // implies the stage's TMA (incl. lse / D) has landed
-      tc_fence_after();
-      const bool diag = n == 0;
-      uint32_t pk[2][16], dk[2][16];
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {  // this warp's two 32-query chunks
-        const int c = 2 * half + cc;
-        uint32_t svr[32], dpr[32];
-        tmem_ld_32x32b_x32_nowait(tS + lane_base + c * 32, svr);
-        tmem_ld_32x32b_x32_nowait(tP + lane_base + c * 32, dpr);
-        tmem_wait_ld();
-        if (diag) bwd_chunk32<true>(svr, dpr, sL + c * 32, sDd + c * 32, qt * TQ + c * 32, key, scale_log2, pk[cc], dk[cc]);
-        else bwd_chunk32<false>(svr, dpr, sL + c * 32, sDd + c * 32, 0, 0, scale_log2, pk[cc], dk[cc]);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane_id() == 0) mbar_arrive(sdp_free);  // the tensor core may overwrite S^T / dP^T now
-      if (n > 0) {  // dV / dK / dQ of n-1 are done: P / dS smem is free, flush dQ of n-1
-        mbar_wait(dq_full, (n - 1) & 1);
-        tc_fence_after();
-        flush_dq(qt - 1);
-      }
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c = 2 * half + cc;
-        const int atom = (c >> 1) * TILE_BYTES;
-        const int chunk0 = (c & 1) * 4;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          *reinterpret_cast<uint4*>(sdS + atom + sw128(r, chunk0 + u)) =
-              make_uint4(dk[cc][4 * u], dk[cc][4 * u + 1], dk[cc][4 * u + 2], dk[cc][4 * u + 3]);
-        tmem_st_32x32b_x16(tPt + lane_base + c * 16, pk[cc]);
-      }
-      tmem_wait_st();
-      fence_proxy_async_shared();
-      tc_fence_before();
-      __syncwarp();
-      if (lane_id() == 0) mbar_arrive(pds_ready);
-    }
-    mbar_wait(dq_full, (N - 1) & 1);
-    tc_fence_after();
-    flush_dq(kt + N - 1);
-    if (t == 0) bulk_wait_all0();  // the last reduce-add has completed before the CTA exits
-    // dK (scaled) and dV rows of this thread's key into the k / v slices of dqkv
-    __nv_bfloat16* row = dqkv + ((int64_t)row0 + key) * 3 * D;
-    {
+    // dK (scaled) and dV rows of this thread's key of a finished item into the k / v slices of dqkv
+    auto store_dkv = [&](const BwdItem& x) {
+      __nv_bfloat16* row = dqkv + ((int64_t)x.b * S + x.kt * TK + r) * 3 * D;
       const int c = half;  // this warp's 32 of the 64 head dims
       float v[32];
       tmem_ld_32x32b_x32(tdK + lane_base + c * 32, v);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] *= scale;
-      store32_bf16(row + D + h * HDIM, 0, 0, c * 32, v);
+      store32_bf16(row + D + x.h * HDIM, 0, 0, c * 32, v);
       tmem_ld_32x32b_x32(tdV + lane_base + c * 32, v);
-      store32_bf16(row + 2 * D + h * HDIM, 0, 0, c * 32, v);
+      store32_bf16(row + 2 * D + x.h * HDIM, 0, 0, c * 32, v);
+    };
+    BwdItem it, prev;
+    int pend_h = 0, pend_row = 0;  // the previous tile's dQ destination (head, token row)
+    int g = 0;
+    for (int rr = 0; rr * (int)gridDim.x < n_items; ++rr) {
+      if (!bwd_item(rr, n_items, H, B, n_t, it)) continue;
+      const int key = it.kt * TK + r;
+      for (int n = 0; n < it.N; ++n, ++g) {
+        const int qt = it.kt + n;
+        const int par = g % BWD_STAGES;  // stage of this query tile's Q / dO / lse / D buffers
+        const float* sL = sLD + par * 256;  // this query tile's lse (log2 domain), then D
+        const float* sDd = sL + 128;
+        mbar_wait(sdp_full, g & 1);  // implies the stage's TMA (incl. lse / D) has landed
+        if (threadIdx.x == 64 && g < 9) TR(1 + 4 * g);
+        tc_fence_after();
+        const bool diag = n == 0;
+        uint32_t pk[2][16], dk[2][16];
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {  // this warp's two 32-query chunks
+          const int c = 2 * half + cc;
+          uint32_t svr[32], dpr[32];
+          tmem_ld_32x32b_x32_nowait(tS + lane_base + c * 32, svr);
+          tmem_ld_32x32b_x32_nowait(tP + lane_base + c * 32, dpr);
+          tmem_wait_ld();
+          if (diag) bwd_chunk32<true>(svr, dpr, sL + c * 32, sDd + c * 32, qt * TQ + c * 32, key, scale_log2, pk[cc], dk[cc]);
+          else bwd_chunk32<false>(svr, dpr, sL + c * 32, sDd + c * 32, 0, 0, scale_log2, pk[cc], dk[cc]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(sdp_free);  // the tensor core may overwrite S^T / dP^T now
+        if (threadIdx.x == 64 && g < 9) TR(2 + 4 * g);
+        if (g > 0) {  // dV / dK / dQ of g-1 are done: P / dS smem is free, flush dQ of g-1
+          mbar_wait(dq_full, (g - 1) & 1);
+          if (threadIdx.x == 64 && g < 9) TR(3 + 4 * g);
+          tc_fence_after();
+          flush_dq(pend_h, pend_row);
+        }
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = 2 * half + cc;
+          const int atom = (c >> 1) * TILE_BYTES;
+          const int chunk0 = (c & 1) * 4;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<uint4*>(sdS + atom + sw128(r, chunk0 + u)) =
+                make_uint4(dk[cc][4 * u], dk[cc][4 * u + 1], dk[cc][4 * u + 2], dk[cc][4 * u + 3]);
+          tmem_st_32x32b_x16(tPt + lane_base + c * 16, pk[cc]);
+        }
+        // g-1 was the previous item's last tile: its dK / dV are final (dq_full above), read them
+        // out before pds_ready lets this item's first dV / dK MMAs overwrite the accumulators
+        if (diag && g > 0) store_dkv(prev);
+        tmem_wait_st();
+        fence_proxy_async_shared();
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(pds_ready);
+        if (threadIdx.x == 64 && g < 9) TR(4 + 4 * g);
+        pend_h = it.h;
+        pend_row = it.b * S + qt * TQ;
+      }
+      prev = it;
     }
+    if (g > 0) {
+      mbar_wait(dq_full, (g - 1) & 1);
+      tc_fence_after();
+      flush_dq(pend_h, pend_row);
+      store_dkv(prev);
+    }
+    if (t == 0) bulk_wait_all0();  // the last reduce-add has completed before the CTA exits
+    if (threadIdx.x == 64) TR(41);
   }
   tc_fence_before();
   __syncthreads();
@@ -883,25 +1018,34 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int S, int H, cud
   CUtensorMap tm;
   const int rc = map_rows(&tm, qkv, (int64_t)B * S, 3ll * H * HDIM);
   if (rc) return rc;
-  static int v1 = -1;  // PD_ATTN_FWD_V1=1: the round-1 kernel (P through shared memory), for A/B runs
+  static int v1 = -1, poly = -1;  // PD_ATTN_FWD_V1=1: the round-1 kernel; PD_ATTN_POLY: FMA-pipe exp2 pairs of 8
   if (v1 < 0) {
     const char* e = getenv("PD_ATTN_FWD_V1");
     v1 = e && atoi(e) ? 1 : 0;
+    const char* p = getenv("PD_ATTN_POLY");
+    poly = p ? atoi(p) : 3;
   }
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(k_attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem::TOTAL) != cudaSuccess ||
-        cudaFuncSetAttribute(k_attn_fwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Smem::TOTAL) != cudaSuccess)
+        cudaFuncSetAttribute(k_attn_fwd_tc2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Smem::TOTAL) != cudaSuccess ||
+        cudaFuncSetAttribute(k_attn_fwd_tc2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Smem::TOTAL) != cudaSuccess ||
+        cudaFuncSetAttribute(k_attn_fwd_tc2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Smem::TOTAL) != cudaSuccess ||
+        cudaFuncSetAttribute(k_attn_fwd_tc2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Smem::TOTAL) != cudaSuccess)
       return set_error(PD_ERR_CUDA, "attention fwd: shared memory attribute");
     attr = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)HDIM);
-  if (v1)
-    launch_pdl(k_attn_fwd_tc, dim3(S / TQ, H, B), dim3(FWD_THREADS), FwdSmem::TOTAL, st, tm,
-               static_cast<__nv_bfloat16*>(out), lse, S, H, scale_log2);
-  else
-    launch_pdl(k_attn_fwd_tc2, dim3(H, B, S / TQ), dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm,
-               static_cast<__nv_bfloat16*>(out), lse, S, H, scale_log2);
+  auto* __restrict__ o = static_cast<__nv_bfloat16*>(out);
+  if (v1) {
+    launch_pdl(k_attn_fwd_tc, dim3(S / TQ, H, B), dim3(FWD_THREADS), FwdSmem::TOTAL, st, tm, o, lse, S, H, scale_log2);
+  } else {
+    const dim3 grid(H, B, S / TQ);
+    if (poly == 0) launch_pdl(k_attn_fwd_tc2<0>, grid, dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm, o, lse, S, H, scale_log2);
+    else if (poly == 2) launch_pdl(k_attn_fwd_tc2<2>, grid, dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm, o, lse, S, H, scale_log2);
+    else if (poly == 4) launch_pdl(k_attn_fwd_tc2<4>, grid, dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm, o, lse, S, H, scale_log2);
+    else launch_pdl(k_attn_fwd_tc2<3>, grid, dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm, o, lse, S, H, scale_log2);
+  }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "attention fwd: %s", cudaGetErrorString(e));
 }
@@ -932,10 +1076,25 @@ int attn_bwd_tc(const void* qkv, const void* dout, const float* lse, const float
     attr = true;
   }
   const float scale = 1.0f / sqrtf((float)HDIM);
-  launch_pdl(k_attn_bwd_tc, dim3(H, B, S / TK), dim3(BWD_THREADS), BwdSmem::TOTAL, st, 
-      tq, tdo, tdq, lse, Dv, static_cast<__nv_bfloat16*>(dqkv), dq_acc, S, H, scale * 1.4426950408889634f, scale);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int items = (S / TK) * H * B;
+  launch_pdl(k_attn_bwd_tc, dim3(items < sms ? items : sms), dim3(BWD_THREADS), BwdSmem::TOTAL, st,
+      tq, tdo, tdq, lse, Dv, static_cast<__nv_bfloat16*>(dqkv), dq_acc, S, H, B, scale * 1.4426950408889634f, scale);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "attention bwd: %s", cudaGetErrorString(e));
 }
 
 }  // namespace pd
+
+#if PD_ATTN_TRACE
+extern "C" int pd_attn_trace(unsigned long long* host, int n) {
+  const size_t bytes = sizeof(unsigned long long) * (size_t)(n < pd::TR_CTAS ? n : pd::TR_CTAS) * pd::TR_EV;
+  return cudaMemcpyFromSymbol(host, pd::g_attn_trace, bytes) == cudaSuccess ? 0 : 1;
+}
+extern "C" int pd_attn_trace_clear() {
+  static unsigned long long zero[pd::TR_CTAS][pd::TR_EV];
+  return cudaMemcpyToSymbol(pd::g_attn_trace, zero, sizeof(zero)) == cudaSuccess ? 0 : 1;
+}
+#endif

@@ -57,8 +57,12 @@ PD_DEVICE void mbar_arrive(uint64_t* bar) {
 // The suspend-time hint lets the waiting warp sleep until the phase completes (or the hint
 // expires) instead of spinning: waiting producer / MMA warps then stop stealing issue slots from
 // the epilogue / softmax warps that share their SM sub-partition.
+#ifndef PD_MBAR_SUSPEND
+#define PD_MBAR_SUSPEND 1
+#endif
 PD_DEVICE bool mbar_try(uint32_t addr, uint32_t parity) {
   uint32_t ok;
+#if PD_MBAR_SUSPEND
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
@@ -66,6 +70,15 @@ PD_DEVICE bool mbar_try(uint32_t addr, uint32_t parity) {
       : "=r"(ok)
       : "r"(addr), "r"(parity), "r"(0x989680)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+#endif
   return ok != 0;
 }
 // Cold path of a wait that has not completed for 20 s: a protocol bug, not slowness.  Report the

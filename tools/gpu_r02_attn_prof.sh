@@ -2,7 +2,7 @@
 # ncu --set full of the attention kernels (one launch each) + the SGD raster-band sweep.
 set -u
 mkdir -p gpurun_out
-for g in 4 8 16 2; do PD_SGD_GROUP=$g python tools/gemm_bench.py | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('group $g', d['wgrad_sgd_ms'])"; done
+
 for k in k_attn_fwd_tc2 k_attn_bwd_tc; do
   timeout -s KILL 300 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
     -o gpurun_out/prof_$k -f python tools/attn_bench.py > gpurun_out/ncu_$k.log 2>&1; tail -1 gpurun_out/ncu_$k.log
