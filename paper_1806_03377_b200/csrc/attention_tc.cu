@@ -875,20 +875,24 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     const int t = threadIdx.x - 64;           // 0..255 within the compute warps
     // dQ rows of a query tile: TMEM -> staging smem (two [128][32] fp32 halves, 128B-swizzled,
     // conflict-free) -> one TMA reduce-add per half of the 128 x 32 fp32 box into dq_acc.
-    auto flush_dq = [&](int h, int trow) {
+    // dQ rows of a query tile: TMEM -> staging smem (two [128][32] fp32 halves, 128B-swizzled,
+    // conflict-free) -> one TMA reduce-add per half of the 128 x 32 fp32 box into dq_acc.  Staging
+    // and issue are split so the tile's dS^T / P^T stores share one proxy fence with the staging.
+    auto stage_dq = [&]() {
       uint32_t v0[32];
       tmem_ld_32x32b_x32_nowait(tdQ + lane_base + half * 32, v0);
       tmem_wait_ld();
       if (t == 0) bulk_wait_read0();  // the previous reduce has finished reading the staging
       named_sync_compute();
-      uint8_t* st0 = reinterpret_cast<uint8_t*>(sDQ);
-      uint8_t* sth = st0 + half * 128 * 128;
+      uint8_t* sth = reinterpret_cast<uint8_t*>(sDQ) + half * 128 * 128;
 #pragma unroll
       for (int c = 0; c < 8; ++c)
         *reinterpret_cast<uint4*>(sth + sw128(r, c)) = make_uint4(v0[4 * c], v0[4 * c + 1], v0[4 * c + 2], v0[4 * c + 3]);
-      fence_proxy_async_shared();
+    };
+    auto issue_dq = [&](int h, int trow) {  // after the staging stores + fence.proxy.async of every warp
       named_sync_compute();
       if (t == 0) {
+        uint8_t* st0 = reinterpret_cast<uint8_t*>(sDQ);
         tma_reduce_add_2d(&tm_dq, st0, h * HDIM, trow);
         tma_reduce_add_2d(&tm_dq, st0 + 128 * 128, h * HDIM + 32, trow);
         bulk_commit();
@@ -940,7 +944,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
           mbar_wait(dq_full, (g - 1) & 1);
           if (threadIdx.x == 64 && g < 9) TR(3 + 4 * g);
           tc_fence_after();
-          flush_dq(pend_h, pend_row);
+          stage_dq();
         }
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
@@ -958,6 +962,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
         if (diag && g > 0) store_dkv(prev);
         tmem_wait_st();
         fence_proxy_async_shared();
+        if (g > 0) issue_dq(pend_h, pend_row);
         tc_fence_before();
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(pds_ready);
@@ -970,7 +975,9 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     if (g > 0) {
       mbar_wait(dq_full, (g - 1) & 1);
       tc_fence_after();
-      flush_dq(pend_h, pend_row);
+      stage_dq();
+      fence_proxy_async_shared();
+      issue_dq(pend_h, pend_row);
       store_dkv(prev);
     }
     if (t == 0) bulk_wait_all0();  // the last reduce-add has completed before the CTA exits
