@@ -1030,7 +1030,7 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int S, int H, cud
     const char* e = getenv("PD_ATTN_FWD_V1");
     v1 = e && atoi(e) ? 1 : 0;
     const char* p = getenv("PD_ATTN_POLY");
-    poly = p ? atoi(p) : 3;
+    poly = p ? atoi(p) : 0;  // MUFU only: the FMA-pipe split measured no faster
   }
   static bool attr = false;
   if (!attr) {
@@ -1048,10 +1048,10 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int S, int H, cud
     launch_pdl(k_attn_fwd_tc, dim3(S / TQ, H, B), dim3(FWD_THREADS), FwdSmem::TOTAL, st, tm, o, lse, S, H, scale_log2);
   } else {
     const dim3 grid(H, B, S / TQ);
-    if (poly == 0) launch_pdl(k_attn_fwd_tc2<0>, grid, dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm, o, lse, S, H, scale_log2);
-    else if (poly == 2) launch_pdl(k_attn_fwd_tc2<2>, grid, dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm, o, lse, S, H, scale_log2);
+    if (poly == 2) launch_pdl(k_attn_fwd_tc2<2>, grid, dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm, o, lse, S, H, scale_log2);
+    else if (poly == 3) launch_pdl(k_attn_fwd_tc2<3>, grid, dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm, o, lse, S, H, scale_log2);
     else if (poly == 4) launch_pdl(k_attn_fwd_tc2<4>, grid, dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm, o, lse, S, H, scale_log2);
-    else launch_pdl(k_attn_fwd_tc2<3>, grid, dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm, o, lse, S, H, scale_log2);
+    else launch_pdl(k_attn_fwd_tc2<0>, grid, dim3(FWD_THREADS), Fwd2Smem::TOTAL, st, tm, o, lse, S, H, scale_log2);
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_error(PD_ERR_CUDA, "attention fwd: %s", cudaGetErrorString(e));

@@ -63,6 +63,7 @@ struct EpiArgs {
   float* bmaster;
   float* bring;
   int group;            // SGD rasterisation band height in tiles (set by the launcher; 0 = default 8)
+  int b_stream;         // set by the launcher: B operand loads carry an evict-first L2 policy
 };
 
 // GPT-2's tanh GELU and its derivative.

@@ -172,6 +172,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ---------------- TMA producer (every CTA loads its own halves)
     if (elect_one()) {
       const uint64_t keep = l2_policy_evict_last();
+      // a B operand far larger than L2's share (the MLP-8192 weights: 128 MB, read by the few
+      // co-resident M tiles of its column and never again) streams with evict-first, so it does not
+      // push the re-read A operand (dZ / X: every column tile reads it) out between waves
+      const uint64_t b_pol = ep.b_stream ? l2_policy_evict_first() : keep;
       int stage = 0;
       uint32_t phase = 0;
       for (int u = unit; u < work; u += units) {
@@ -188,20 +192,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
           const int k0 = kb * TC_BK;
-          auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
+          auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, uint64_t pol) {
             // operands are re-read by many tiles: keep them in L2 ahead of streamed epilogue data
-            if constexpr (CG == 2) tma_load_2d_2sm(dst, map, &full[stage], c0, c1, keep);
-            else tma_load_2d_hint(dst, map, &full[stage], c0, c1, keep);
+            if constexpr (CG == 2) tma_load_2d_2sm(dst, map, &full[stage], c0, c1, pol);
+            else tma_load_2d_hint(dst, map, &full[stage], c0, c1, pol);
           };
           if constexpr (SRC == SRC_CONV_FWD || SRC == SRC_CONV_DGRAD) {
             // 128 output pixels x 64 channels of tap `tap` (dgrad reads dY at the flipped offset)
             const int tap = k0 / cv.C, c0 = k0 - tap * cv.C;
             tma_load_im2col_4d(a_dst, &tmA, &full[stage], c0, aw, ah, an, (uint16_t)(tap % 3), (uint16_t)(tap / 3));
             if constexpr (SRC == SRC_CONV_DGRAD) {
-              load(b_dst, &tmB, c0, (8 - tap) * cv.brows + n0);  // Wt rows of the mirrored tap
+              load(b_dst, &tmB, c0, (8 - tap) * cv.brows + n0, keep);  // Wt rows of the mirrored tap
             } else {
 #pragma unroll
-              for (int i = 0; i < C::BNL / 64; ++i) load(b_dst + i * 8192, &tmB, n0 + 64 * i, k0);
+              for (int i = 0; i < C::BNL / 64; ++i) load(b_dst + i * 8192, &tmB, n0 + 64 * i, k0, keep);
             }
           } else if constexpr (SRC == SRC_CONV_WGRAD) {
             // A(m = tap*C + c, k = pixel): two 64-channel x 64-pixel im2col atoms (MN-major)
@@ -217,19 +221,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                  (uint16_t)(tap / 3));
             }
 #pragma unroll
-            for (int i = 0; i < C::BNL / 64; ++i) load(b_dst + i * 8192, &tmB, n0 + 64 * i, k0);
+            for (int i = 0; i < C::BNL / 64; ++i) load(b_dst + i * 8192, &tmB, n0 + 64 * i, k0, keep);
           } else {
             if constexpr (A_MN) {
 #pragma unroll
-              for (int i = 0; i < TC_BM / 64; ++i) load(a_dst + i * 8192, &tmA, m0 + 64 * i, k0);
+              for (int i = 0; i < TC_BM / 64; ++i) load(a_dst + i * 8192, &tmA, m0 + 64 * i, k0, keep);
             } else {
-              load(a_dst, &tmA, k0, m0);
+              load(a_dst, &tmA, k0, m0, keep);
             }
             if constexpr (B_MN) {
 #pragma unroll
-              for (int i = 0; i < C::BNL / 64; ++i) load(b_dst + i * 8192, &tmB, n0 + 64 * i, k0);
+              for (int i = 0; i < C::BNL / 64; ++i) load(b_dst + i * 8192, &tmB, n0 + 64 * i, k0, b_pol);
             } else {
-              load(b_dst, &tmB, k0, n0);
+              load(b_dst, &tmB, k0, n0, b_pol);
             }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -719,6 +723,17 @@ static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int
     if (rc) return rc;
   }
   EpiArgs epl = ep;
+  {
+    // B operand streamed with evict-first when it is far larger than its reuse window in L2
+    // (PD_B_STREAM=0/1 forces it off/on for A/B runs)
+    static int force = -2;
+    if (force == -2) {
+      const char* e = getenv("PD_B_STREAM");
+      force = e ? atoi(e) : -1;
+    }
+    const bool big = SRC == SRC_2D && !is_sgd(KIND) && (int64_t)N * K * 2 >= (64ll << 20);
+    epl.b_stream = force >= 0 ? force : (big ? 1 : 0);
+  }
   if constexpr (is_sgd(KIND)) {
     static int group = -1;  // PD_SGD_GROUP: tile rows per rasterisation band (A/B experiments)
     if (group < 0) {

@@ -32,8 +32,10 @@ def _ref_attn(qkv, B, S, H):
     return F.scaled_dot_product_attention(q, k, v, is_causal=True)
 
 
-@pytest.mark.parametrize("B,S,H", [(1, 128, 1), (2, 128, 2), (2, 384, 4), (1, 1024, 16)])
+@pytest.mark.parametrize("B,S,H", [(1, 128, 1), (2, 128, 2), (2, 384, 4), (1, 1024, 16), (8, 1024, 16), (2, 2048, 8)])
 def test_attention_fwd_bwd(B, S, H):
+    """Forward and the persistent backward vs torch SDPA; (8, 1024, 16) is the GPT-2 bench shape (1 024
+    backward items over the SMs, several per CTA), (1, 128, 1) a single item on one CTA."""
     d = 64 * H
     g = torch.Generator(device="cuda").manual_seed(0)
     qkv = torch.randn(B * S, 3 * d, device="cuda", generator=g).bfloat16()
@@ -55,6 +57,29 @@ def test_attention_fwd_bwd(B, S, H):
     torch.cuda.synchronize()
     for i in range(3):
         _close(dqkv[:, i * d:(i + 1) * d], x.grad[:, i * d:(i + 1) * d], rel=3e-2)
+
+
+def test_attention_fwd_poly_variant_matches():
+    """PD_ATTN_POLY=3 (3 of 8 exp2 pairs on the FMA pipe, degree-3 polynomial) stays within the
+    attention tolerance of torch SDPA; run in a child process (the variant is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import torch, paper_1806_03377_b200._native as nat\n"
+        "from tests.test_transformer_gpu import _ref_attn, _close\n"
+        "B,S,H=2,512,4; d=64*H\n"
+        "g=torch.Generator(device='cuda').manual_seed(3)\n"
+        "qkv=torch.randn(B*S,3*d,device='cuda',generator=g).bfloat16()\n"
+        "out=torch.empty(B*S,d,device='cuda',dtype=torch.bfloat16); lse=torch.empty(B,H,S,device='cuda')\n"
+        "nat.check(nat.lib().pd_attention_fwd(nat.ptr(qkv),nat.ptr(out),nat.ptr(lse),B,S,H,nat.stream_ptr()),'fwd')\n"
+        "torch.cuda.synchronize()\n"
+        "_close(out, _ref_attn(qkv,B,S,H).transpose(1,2).reshape(B*S,d))\n"
+        "print('ok')\n")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=repo, env=dict(os.environ, PD_ATTN_POLY="3"),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
 @pytest.mark.parametrize("T,D", [(64, 256), (1000, 1024), (8192, 1024)])
