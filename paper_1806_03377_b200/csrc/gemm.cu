@@ -731,7 +731,9 @@ static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int
       const char* e = getenv("PD_B_STREAM");
       force = e ? atoi(e) : -1;
     }
-    const bool big = SRC == SRC_2D && !is_sgd(KIND) && (int64_t)N * K * 2 >= (64ll << 20);
+    // measured on the MLP-8192 layer (tools/gpu_dram_ab.sh): forward (K-major W) DRAM reads 243 -> 194 MB
+    // and 180 -> 175 us; the dgrad (MN-major W) reads grew (310 -> 330 MB), so it keeps evict-last
+    const bool big = SRC == SRC_2D && !is_sgd(KIND) && !B_MN && (int64_t)N * K * 2 >= (64ll << 20);
     epl.b_stream = force >= 0 ? force : (big ? 1 : 0);
   }
   if constexpr (is_sgd(KIND)) {

@@ -66,8 +66,9 @@ def test_attention_fwd_poly_variant_matches():
     import subprocess
     import sys
     code = (
-        "import torch, paper_1806_03377_b200._native as nat\n"
-        "from tests.test_transformer_gpu import _ref_attn, _close\n"
+        "import sys, torch, paper_1806_03377_b200._native as nat\n"
+        "sys.path.insert(0, 'tests')\n"
+        "from test_transformer_gpu import _ref_attn, _close\n"
         "B,S,H=2,512,4; d=64*H\n"
         "g=torch.Generator(device='cuda').manual_seed(3)\n"
         "qkv=torch.randn(B*S,3*d,device='cuda',generator=g).bfloat16()\n"
