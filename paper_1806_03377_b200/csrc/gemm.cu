@@ -42,7 +42,10 @@ constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;  // warp0 TMA, warp1 MMA (+TM
 // VGG classifier at batch 32: the master read-modify-write is the whole kernel, four blocks in
 // flight per warp = a whole tile's master prefetched while its MMAs run).
 __host__ __device__ constexpr bool is_sgd(int kind) { return kind == EPI_SGD || kind == EPI_SGD_STREAM; }
-__host__ __device__ constexpr int sgd_bufs(int kind) { return kind == EPI_SGD_STREAM ? 4 : 1; }
+#ifndef PD_SGD_BUFS
+#define PD_SGD_BUFS 1
+#endif
+__host__ __device__ constexpr int sgd_bufs(int kind) { return kind == EPI_SGD_STREAM ? 4 : PD_SGD_BUFS; }
 constexpr int SGD_STREAM_MAX_K = 256;
 constexpr int TC_ACC_STRIDE = 256;  // TMEM columns between the two accumulator buffers
 
