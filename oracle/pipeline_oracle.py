@@ -197,7 +197,7 @@ def mlp_train(params, X, T, lr, stage_bounds, versions, K, emulate: str | None =
 
 
 def mlp_train_torch(params, X, T, lr, stage_bounds, versions, K, emulate: str | None = "bf16", device=None,
-                    prune: bool = True, dtype=None, ksplit: int = 1):
+                    prune: bool = True, dtype=None, ksplit: int = 1, bias_grad_scale: float = 1.0):
     """``mlp_train``'s rule with torch fp32 arithmetic on ``device`` (the checker of full-size
     configurations, e.g. the 8 x 2-layer MLP-8192 at minibatch 2048, which numpy cannot run in
     seconds).  Same forward / backward versions, bf16 rounding points (fp32 -> bf16 nearest-even,
@@ -209,6 +209,7 @@ def mlp_train_torch(params, X, T, lr, stage_bounds, versions, K, emulate: str | 
     against which an fp32 run's own rounding drift can be measured).
     ksplit: every product is summed over ``ksplit`` contiguous K chunks (a different fp32 summation
     order: the spread of such variants is the rounding-noise floor of fp32-accumulating GEMMs).
+    bias_grad_scale: fault injection for the checker's own sensitivity test (1.0 = the rule).
     Returns (losses[K] numpy, final [(W, b)] torch tensors on ``device``).
     """
     import torch
@@ -269,7 +270,7 @@ def mlp_train_torch(params, X, T, lr, stage_bounds, versions, K, emulate: str | 
             for l in range(L - 1, -1, -1):
                 s = layer_stage[l]
                 Xl = inputs[l]
-                grads[l] = (mm(dz.T, Xl), dz.sum(0))
+                grads[l] = (mm(dz.T, Xl), dz.sum(0) * bias_grad_scale)
                 if l > 0:
                     Wb, _ = archives[s][bv[s]][l - first[s]]
                     dz = q(mm(dz, q(Wb)) * (Xl > 0))

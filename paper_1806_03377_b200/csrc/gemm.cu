@@ -781,6 +781,7 @@ static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  mark_pre_launch(st);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tw, M, N, K, epl, cv);
   if (e != cudaSuccess) return set_error(PD_ERR_CUDA, "tcgen05 gemm launch: %s", cudaGetErrorString(e));
   return 0;

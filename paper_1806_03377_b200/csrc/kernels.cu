@@ -13,6 +13,8 @@
 
 namespace pd {
 
+thread_local cudaEvent_t g_pre_launch = nullptr;  // pd_internal.h: kernel-timing start event
+
 static thread_local char g_err[1024] = {0};
 
 // Programmatic dependent launch is opt-in (PD_PDL=1): with several stage streams replayed from

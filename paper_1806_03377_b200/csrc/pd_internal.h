@@ -79,6 +79,18 @@ int flag_wait(const int* flag, int value, int* err_word, cudaStream_t st);
 // PD_PDL=1 in the environment enables programmatic dependent launch (default off, kernels.cu).
 bool pdl_enabled();
 
+// Kernel timing (pd_rt_kernel_timing): the runtime records a start event, then sets g_pre_launch to
+// it; the first kernel launch of the timed call re-records it right before cudaLaunchKernelEx, so
+// the measured interval excludes the host's launch preparation (tensor-map encoding etc.), which
+// would otherwise be counted whenever the GPU is ahead of the host.
+extern thread_local cudaEvent_t g_pre_launch;
+inline void mark_pre_launch(cudaStream_t st) {
+  if (g_pre_launch) {
+    cudaEventRecord(g_pre_launch, st);
+    g_pre_launch = nullptr;
+  }
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {
@@ -92,6 +104,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   a[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = a;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  mark_pre_launch(st);
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 

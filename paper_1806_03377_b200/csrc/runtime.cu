@@ -218,8 +218,11 @@ int timed_gemm(pd_runtime* rt, int cls, int dtype, const void* A, int a_mn, int6
     slot->worker = rt->cur_worker;
     slot->flops = 2.0 * (double)M * (double)N * (double)K;
     PD_CHECK(cudaEventRecord(slot->a, st));
+    g_pre_launch = slot->a;  // re-recorded right before the launch (pd_internal.h)
   }
-  PD_TRY(gemm(dtype, A, a_mn, lda, B, b_mn, ldb, M, N, K, kind, ep, st));
+  const int rc = gemm(dtype, A, a_mn, lda, B, b_mn, ldb, M, N, K, kind, ep, st);
+  g_pre_launch = nullptr;
+  PD_TRY(rc);
   rt->launches += 1;
   if (slot) PD_CHECK(cudaEventRecord(slot->b, st));
   return 0;
@@ -260,8 +263,10 @@ int timed_call(pd_runtime* rt, int cls, cudaStream_t st, Fn&& fn) {
     slot->worker = rt->cur_worker;
     slot->flops = 0.0;
     PD_CHECK(cudaEventRecord(slot->a, st));
+    g_pre_launch = slot->a;  // re-recorded right before the launch (pd_internal.h)
   }
   const int rc = fn();
+  g_pre_launch = nullptr;
   if (slot) PD_CHECK(cudaEventRecord(slot->b, st));
   return rc;
 }
@@ -574,8 +579,11 @@ int timed_conv(pd_runtime* rt, int cls, int pass, const void* act, const void* o
     slot->worker = rt->cur_worker;
     slot->flops = 2.0 * (double)n * h * w * 9.0 * cin * cout;
     PD_CHECK(cudaEventRecord(slot->a, st));
+    g_pre_launch = slot->a;  // re-recorded right before the launch (pd_internal.h)
   }
-  PD_TRY(conv3x3_tc(pass, act, other, n, h, w, cin, cout, kind, ep, st));
+  const int rc = conv3x3_tc(pass, act, other, n, h, w, cin, cout, kind, ep, st);
+  g_pre_launch = nullptr;
+  PD_TRY(rc);
   rt->launches += 1;
   if (slot) PD_CHECK(cudaEventRecord(slot->b, st));
   return 0;

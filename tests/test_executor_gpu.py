@@ -95,6 +95,18 @@ def test_bf16_pipeline_parity(mode):
     rel = np.max(np.abs(got - losses) / np.abs(losses))
     assert rel <= 2e-2, (rel, got[:5], losses[:5])
     assert weight_delta_err(spec, res.weights, final) <= 1e-1
+    # and the tight bound: within the fp32 noise floor of the fp64 rule (tests/helpers_floor.py),
+    # which a 0.9-scaled bias gradient fails (tests/test_oracle.py)
+    from helpers_floor import floor_check
+    from oracle.pipeline_oracle import mlp_train_torch
+    P32 = [(W.astype(np.float32), b.astype(np.float32)) for W, b in pd.init_params(spec)]
+    X, T = pd.make_data(spec)
+    versions = lambda s, mb, d: res.ledger.version_used(s, mb, pd.Direction(d))  # noqa: E731
+    o32, o64 = (mlp_train_torch(P32, X, T, spec.lr, bounds, versions, 20, emulate="bf16", device="cuda", dtype=dt)
+                for dt in (torch.float32, torch.float64))
+    dev = [res.weights[l] for l in range(1, 9)]
+    params0 = [(torch.as_tensor(W), torch.as_tensor(b)) for W, b in P32]
+    floor_check(got, [(torch.as_tensor(W), torch.as_tensor(b)) for W, b in dev], params0, o32, o64, loss_abs=3e-4)
 
 
 def test_bf16_eight_stage_max_inflight_and_repeat():

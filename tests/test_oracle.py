@@ -66,3 +66,35 @@ def test_mlp_oracle_single_stage_is_plain_sgd():
         Ws = new[::-1]
     for (W, b), (W2, b2) in zip(final, Ws):
         assert np.allclose(W, W2, rtol=1e-12, atol=1e-14) and np.allclose(b, b2, rtol=1e-12, atol=1e-14)
+
+
+def test_noise_floor_check_catches_scaled_bias_gradient():
+    """The pipeline tests' noise-floor check (tests/helpers_floor.py) is sensitive: the fp32 rule
+    passes it, the same rule with every bias gradient scaled by 0.9 (a wrong-but-correlated update,
+    VERDICT r01 weak #2) fails it by a wide margin.  CPU torch, 4-stage 8-layer MLP-64, 16 minibatches."""
+    import torch
+
+    from helpers_floor import floor_check
+    from oracle.pipeline_oracle import mlp_train_torch
+
+    import paper_1806_03377_b200 as pd
+
+    spec = pd.mlp(64, 8, batch=32, dtype="bf16", lr=5e-3, n_blocks=4, seed=0)
+    P = pd.init_params(spec)
+    X, T = pd.make_data(spec)
+    bounds = [(2 * s + 1, 2 * s + 2) for s in range(4)]
+    stages = tuple(pd.Stage(a, b, 1) for a, b in bounds)
+    plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=4, machines_used=4)
+    ledger = pd.compile_program(pd.build_schedule(plan, 16), "weight_stashing").ledger
+    versions = lambda s, mb, d: ledger.version_used(s, mb, pd.Direction(d))  # noqa: E731
+    run = lambda dt, **kw: mlp_train_torch(P, X, T, spec.lr, bounds, versions, 16, emulate="bf16",  # noqa: E731
+                                           device="cpu", dtype=dt, **kw)
+    o64, o32 = run(torch.float64), run(torch.float32)
+    params0 = [(torch.as_tensor(W), torch.as_tensor(b)) for W, b in P]
+    floor_check(o32[0], o32[1], params0, o32, o64, loss_abs=3e-4)  # the rule itself passes
+    bad = run(torch.float32, bias_grad_scale=0.9)
+    with pytest.raises(AssertionError):
+        floor_check(bad[0], bad[1], params0, o32, o64, loss_abs=3e-4)
+    from helpers_floor import delta_err
+    worst = max(delta_err(b_bad, b64, b0) for (_, b_bad), (_, b64), (_, b0) in zip(bad[1], o64[1], params0))
+    assert worst > 0.05, worst  # ~10 %, five times the absolute allowance
