@@ -207,8 +207,9 @@ def dtype_code(torch_dtype) -> int:
 
 def gemm(A, a_mn: bool, B, b_mn: bool, M: int, N: int, K: int, *, kind: int = EPI_STORE, out=None, ldo=None,
          bias=None, relu=False, mask=None, ldm=None, target=None, ldt=None, scale=1.0, loss=None, master=None,
-         ldw=None, lr=0.0, stream=None) -> None:
-    """C[M,N] = sum_k A(m,k) B(n,k) + fused epilogue, on torch tensors (row-major, contiguous rows)."""
+         ldw=None, lr=0.0, aux=None, stream=None) -> None:
+    """C[M,N] = sum_k A(m,k) B(n,k) + fused epilogue, on torch tensors (row-major, contiguous rows).
+    aux: EPI_GELU's pre-activation output (ld = ldo)."""
     lda = A.stride(0)
     ldb = B.stride(0)
     ep = Epilogue(kind=kind, out=ptr(out), ldo=ldo if ldo is not None else (out.stride(0) if out is not None else 0),
@@ -216,7 +217,8 @@ def gemm(A, a_mn: bool, B, b_mn: bool, M: int, N: int, K: int, *, kind: int = EP
                   ldm=ldm if ldm is not None else (mask.stride(0) if mask is not None else 0),
                   target=ptr(target), ldt=ldt if ldt is not None else (target.stride(0) if target is not None else 0),
                   scale=scale, loss=ptr(loss), master=ptr(master),
-                  ldw=ldw if ldw is not None else (master.stride(0) if master is not None else 0), lr=lr)
+                  ldw=ldw if ldw is not None else (master.stride(0) if master is not None else 0), lr=lr,
+                  aux=ptr(aux))
     check(lib().pd_gemm(dtype_code(A.dtype), ptr(A), int(a_mn), lda, ptr(B), int(b_mn), ldb, M, N, K,
                         ctypes.byref(ep), stream_ptr(stream)), "pd_gemm")
 

@@ -49,6 +49,20 @@ def main():
                                                   lr=0.0)),
                           timeit(lambda: torch.matmul(dY.t(), X))),
         }
+        # the epilogues the pipeline actually runs (GELU fc1 stores pre-activation + output; proj / fc2
+        # add the residual; the fc2 dgrad applies GELU'); compared with the plain-store rows above
+        Z = torch.empty(T, N, device="cuda", dtype=bf)
+        R = torch.randn(T, N, device="cuda").to(bf)
+        if name == "fc1":
+            epi = timeit(lambda: nat.gemm(X, False, W, False, T, N, K, kind=nat.EPI_GELU, out=Y, aux=Z, bias=bias))
+            print(json.dumps({"gemm": name, "pass": "fwd+gelu", "ms": round(epi, 4), "tflops": round(fl / epi / 1e9, 1)}))
+        if name in ("proj", "fc2"):
+            epi = timeit(lambda: nat.gemm(X, False, W, False, T, N, K, kind=nat.EPI_RESID, out=Y, mask=R, bias=bias))
+            print(json.dumps({"gemm": name, "pass": "fwd+resid", "ms": round(epi, 4), "tflops": round(fl / epi / 1e9, 1)}))
+        if name == "fc2":
+            Zf = torch.randn(T, K, device="cuda").to(bf)
+            epi = timeit(lambda: nat.gemm(dY, False, W, True, T, K, N, kind=nat.EPI_GELU_BWD, out=dX, mask=Zf))
+            print(json.dumps({"gemm": name, "pass": "dgrad+gelu'", "ms": round(epi, 4), "tflops": round(fl / epi / 1e9, 1)}))
         for pas, (a, b) in rows.items():
             total["ours"] += a
             total["torch"] += b
