@@ -169,7 +169,13 @@ __device__ __forceinline__ void unpack_bf16x2(uint32_t u, float& a, float& b) {
 // Chunked tcgen05 epilogue with one-chunk-ahead prefetch of the per-element global input
 // (fp32 master for SGD, bf16 mask for dgrad, fp32 target for the loss), so the HBM latency
 // of chunk c+1 overlaps the math/stores of chunk c.
+// STORE / GELU also prefetch the next chunk's 32 bias values (loaded at use they put a global-load
+// latency on every chunk's critical path: ncu showed the FC1 GELU epilogue stalled on long
+// scoreboard at the bias add, tensor pipe 41 %).  RESID / LOSS keep the load at use: with their
+// prefetched residual / target the extra 2 x 32 registers spill.
 template <int KIND> struct Aux { };
+template <> struct Aux<EPI_STORE> { float4 b[8]; };
+template <> struct Aux<EPI_GELU> { float4 b[8]; };
 template <> struct Aux<EPI_SGD> { float4 m[8]; };
 template <> struct Aux<EPI_MASK> { uint4 m[4]; };
 template <> struct Aux<EPI_LOSS> { float4 t[8]; };
@@ -191,6 +197,12 @@ __device__ __forceinline__ void aux_load(const EpiArgs& ep, int64_t r, int64_t c
     const float4* t4 = reinterpret_cast<const float4*>(ep.target + r * ep.ldt + c0);
 #pragma unroll
     for (int i = 0; i < 8; ++i) a.t[i] = t4[i];
+  } else if constexpr (KIND == EPI_STORE || KIND == EPI_GELU) {
+    if (ep.bias) {
+      const float4* b4 = reinterpret_cast<const float4*>(ep.bias + c0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a.b[i] = __ldg(b4 + i);
+    }
   }
 }
 
@@ -209,10 +221,9 @@ __device__ __forceinline__ float apply_chunk(const EpiArgs& ep, int64_t r, int64
   float lsum = 0.f;
   if constexpr (KIND == EPI_STORE) {
     if (ep.bias) {
-      const float4* b4 = reinterpret_cast<const float4*>(ep.bias + c0);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        float4 b = __ldg(b4 + i);
+        const float4 b = a.b[i];
         v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
       }
     }
@@ -246,10 +257,9 @@ __device__ __forceinline__ float apply_chunk(const EpiArgs& ep, int64_t r, int64
     store32_bf16(ep.out, ep.ldo, r, c0, v);
   } else if constexpr (KIND == EPI_GELU) {
     if (ep.bias) {
-      const float4* b4 = reinterpret_cast<const float4*>(ep.bias + c0);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        float4 b = __ldg(b4 + i);
+        const float4 b = a.b[i];
         v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
       }
     }
