@@ -62,7 +62,7 @@ struct EpiArgs {
   int nrb;
   float* bmaster;
   float* bring;
-  int group;            // SGD rasterisation band height in tiles (set by the launcher; 0 = default 8)
+  int group;            // SGD rasterisation band height in tiles (set by the launcher; 0 = default 16)
   int b_stream;         // set by the launcher: B operand loads carry an evict-first L2 policy
 };
 
