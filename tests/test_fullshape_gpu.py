@@ -253,7 +253,9 @@ def test_cfg3_vgg16_7_1_full_shape_parity():
     K = 42  # whole rounds of 7 and the steady window (2*2*7 + 2 + 7 = 37)
     plan = pd.Plan(stages=(pd.Stage(1, 13, 7), pd.Stage(14, 16, 1)), bottleneck_time=1.0, noam=2, machines_used=8)
     cfg = pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=K)
-    spec = pd.vgg16(batch=32, lr=1e-4, n_blocks=2, seed=0)
+    # lr 1e-5: at 1e-4 the 42-minibatch run is chaotic enough that the fp32 oracle drifts 0.9 % in loss
+    # and 45 % in the weight deltas from fp64, leaving the floor check a 5 % margin (tools/fullshape_sweep.py)
+    spec = pd.vgg16(batch=32, lr=1e-5, n_blocks=2, seed=0)
     ex = pd.Executor(cfg, model=spec)
     try:
         params0, X, y = _snapshot(ex)
