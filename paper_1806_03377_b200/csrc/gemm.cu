@@ -800,16 +800,22 @@ static void pick_cfg(int M, int N, bool b_mn, int* cg, int* bn) {
   long best = -1;
   *cg = 1;
   *bn = 256;
-  (void)b_mn;
   for (int c = 1; c <= 2; ++c) {
     if (g_force_cg && c != g_force_cg) continue;
     if (c == 2 && M <= TC_BM) continue;  // a single 128-row tile gains nothing from a pair
     for (int b : {256, 224, 192, 128}) {
       // waves x (tile width + ~24 columns of fixed per-tile cost: prologue, operand re-reads);
-      // a pair is ~2.5 % faster per tile than two single CTAs (halved B traffic per SM)
+      // a pair is ~2.5 % faster per tile than two single CTAs (halved B traffic per SM).  An MN-major
+      // B is staged in whole 64-column swizzle atoms, so 224 / 192-wide pair tiles load as much as a
+      // 256-wide one, and narrow tiles re-read the A operand once per extra column tile: measured on
+      // the MLP-8192 dgrad (2048 x 8192, whole bench step on one box) 256 / 224 / 128-wide tiles gave
+      // 193.5k / 190.9k / 188.7k samples/s.  So MN-major B tiles are 256 or 128 wide, with a larger
+      // fixed cost.
+      if (b_mn && (b == 224 || b == 192)) continue;
+      const int fixed = b_mn ? 64 : 24;
       const long units = (long)((M + TC_BM * c - 1) / (TC_BM * c)) * ((N + b - 1) / b);
       const long slots = sms / c;
-      const long cost = ((units + slots - 1) / slots) * (b + 24) * (c == 2 ? 2 : 1) * 1000 / (c == 2 ? 2050 : 1000);
+      const long cost = ((units + slots - 1) / slots) * (b + fixed) * (c == 2 ? 2 : 1) * 1000 / (c == 2 ? 2050 : 1000);
       if (best < 0 || cost < best) { best = cost; *cg = c; *bn = b; }
     }
   }
@@ -817,6 +823,18 @@ static void pick_cfg(int M, int N, bool b_mn, int* cg, int* bn) {
 
 // The tile configuration of one problem (also reported by pd_gemm_pick for the tests).
 static void choose_cfg(int M, int N, bool a_mn, bool b_mn, int kind, int* cg, int* bn) {
+  if (!a_mn && b_mn && kind == EPI_MASK) {
+    static int force = -1;  // PD_DGRAD_BN=256|224|192|128: tile width of the MN-major-B dgrad (A/B runs)
+    if (force < 0) {
+      const char* e = getenv("PD_DGRAD_BN");
+      force = e ? atoi(e) : 0;
+    }
+    if (force == 256 || force == 224 || force == 192 || force == 128) {
+      *cg = M > TC_BM ? 2 : 1;
+      *bn = force;
+      return;
+    }
+  }
   if (!a_mn && b_mn && kind == EPI_STORE && N <= 128) {
     // narrow outputs (the im2col'ed first convolution, c_out = 64): a 256-wide tile would be 3/4 padding
     *cg = 1;

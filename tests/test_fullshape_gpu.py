@@ -3,7 +3,7 @@
 1. The exact tcgen05 instantiations the cfg2 bench step launches, at the bench's layer shapes,
    against a plain PyTorch fp32 reference (TF32 off):
      wgrad+SGD  k_gemm_tc<2,256,MN,MN,EPI_SGD>    8192 x 8192 x 2048
-     dgrad      k_gemm_tc<2,224,K,MN,EPI_MASK>    2048 x 8192 x 8192
+     dgrad      k_gemm_tc<2,256,K,MN,EPI_MASK>    2048 x 8192 x 8192
      forward    k_gemm_tc<2,224,K,K,EPI_STORE>    2048 x 8192 x 8192
    pd_gemm_pick pins that these shapes reach those instantiations.
 2. Whole pipelines at full size against the oracle's rule run on the same GPU in torch fp32
@@ -59,7 +59,7 @@ def _ops(M, N, K, a_mn, b_mn, seed):
 
 def test_bench_instantiations_are_pinned():
     assert nat.gemm_pick(8192, 8192, 2048, True, True, nat.EPI_SGD) == (2, 256)
-    assert nat.gemm_pick(2048, 8192, 8192, False, True, nat.EPI_MASK) == (2, 224)
+    assert nat.gemm_pick(2048, 8192, 8192, False, True, nat.EPI_MASK) == (2, 256)
     assert nat.gemm_pick(2048, 8192, 8192, False, False, nat.EPI_STORE) == (2, 224)
     assert nat.gemm_pick(2048, 8192, 8192, False, False, nat.EPI_LOSS) == (2, 224)
 
@@ -124,15 +124,39 @@ def test_bn224_partial_atom_dgrad_and_forward():
         torch.testing.assert_close(out.float(), expect, atol=1e-3 * ref.abs().max().item(), rtol=4e-3)
 
 
-def test_bn224_forced_mn_major_partial_atom():
-    """N = 224 exactly with K-major A / MN-major B: one pair tile of 224 columns, 112 B rows per CTA."""
-    M, N, K = 256, 224, 512
-    a, b, ref = _ops(M, N, K, False, True, 61)
-    mask = torch.ones(M, N, device="cuda").to(torch.bfloat16)
-    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    nat.gemm(a, False, b, True, M, N, K, kind=nat.EPI_MASK, out=out, mask=mask)
-    torch.cuda.synchronize()
-    torch.testing.assert_close(out.float(), ref, atol=1e-3 * ref.abs().max().item(), rtol=4e-3)
+def _forced_dgrad_bn(bn, M, N, K):
+    """Run an MN-major-B dgrad with the tile width forced by PD_DGRAD_BN (read once per process, so
+    in a child); the picker costs MN-major tiles at their whole-atom width and never picks 224 / 192."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, torch, paper_1806_03377_b200._native as nat\n"
+        "sys.path.insert(0, 'tests')\n"
+        "from test_fullshape_gpu import _ops\n"
+        f"M, N, K = {M}, {N}, {K}\n"
+        f"assert nat.gemm_pick(M, N, K, False, True, nat.EPI_MASK)[1] == {bn}\n"
+        "a, b, ref = _ops(M, N, K, False, True, 61)\n"
+        "mask = torch.randn(M, N, device='cuda').to(torch.bfloat16)\n"
+        "out = torch.empty(M, N, device='cuda', dtype=torch.bfloat16)\n"
+        "nat.gemm(a, False, b, True, M, N, K, kind=nat.EPI_MASK, out=out, mask=mask)\n"
+        "torch.cuda.synchronize()\n"
+        "expect = ref * (mask.float() > 0)\n"
+        "torch.testing.assert_close(out.float(), expect, atol=1e-3 * ref.abs().max().item(), rtol=4e-3)\n"
+        "print('ok')\n")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=repo, env=dict(os.environ, PD_DGRAD_BN=str(bn)),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("bn", [224, 192])
+def test_forced_mn_major_partial_atom(bn):
+    """224 / 192-wide pair tiles with an MN-major B (112 / 96 B rows per CTA: a whole plus a partial
+    64-wide swizzle atom, the MMA reading only the first rows), on N = 224 exactly and on a partial
+    last column tile (2048 x 8000)."""
+    _forced_dgrad_bn(bn, 256, 224, 512)
+    _forced_dgrad_bn(bn, 2048, 8000, 1024)
 
 
 # ------------------------------------------------------------------ 2. full-size pipelines
