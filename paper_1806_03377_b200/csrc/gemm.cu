@@ -823,6 +823,18 @@ static void pick_cfg(int M, int N, bool b_mn, int* cg, int* bn) {
 
 // The tile configuration of one problem (also reported by pd_gemm_pick for the tests).
 static void choose_cfg(int M, int N, bool a_mn, bool b_mn, int kind, int* cg, int* bn) {
+  if (!a_mn && !b_mn && (kind == EPI_STORE || kind == EPI_LOSS)) {
+    static int force = -1;  // PD_FWD_BN=256|224|192|128: tile width of the K-major forward (A/B runs)
+    if (force < 0) {
+      const char* e = getenv("PD_FWD_BN");
+      force = e ? atoi(e) : 0;
+    }
+    if (force == 256 || force == 224 || force == 192 || force == 128) {
+      *cg = M > TC_BM ? 2 : 1;
+      *bn = force;
+      return;
+    }
+  }
   if (!a_mn && b_mn && kind == EPI_MASK) {
     static int force = -1;  // PD_DGRAD_BN=256|224|192|128: tile width of the MN-major-B dgrad (A/B runs)
     if (force < 0) {
