@@ -236,6 +236,17 @@ PD_DEVICE void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* map, uint64_t*
       : "memory");
 }
 
+// 2-CTA im2col load: data lands in this CTA's smem, the byte count goes to the leader CTA's barrier.
+PD_DEVICE void tma_load_im2col_4d_2sm(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c, int w, int h,
+                                      int n, uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow),
+      "h"(oh)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <uint32_t kCols, int CG = 1>
 PD_DEVICE void tmem_alloc(uint32_t* dst_smem) {  // whole warp (one warp in each CTA of a pair)
