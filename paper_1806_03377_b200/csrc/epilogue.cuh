@@ -64,6 +64,7 @@ struct EpiArgs {
   float* bring;
   int group;            // SGD rasterisation band height in tiles (set by the launcher; 0 = default 16)
   int b_stream;         // set by the launcher: B operand loads carry an evict-first L2 policy
+  int tma_out;          // set by the launcher: GRADF32 stores its fp32 blocks with TMA (map in tmW)
 };
 
 // GPT-2's tanh GELU and its derivative.  tanh on the SFU (tanh.approx.f32, max relative error

@@ -53,6 +53,9 @@ constexpr int TC_ACC_STRIDE = 256;  // TMEM columns between the two accumulator 
 // 32x32 accumulator block through shared memory so global traffic is row-contiguous per warp.
 __host__ __device__ constexpr bool transposed_epilogue(int kind) { return is_sgd(kind) || kind == EPI_GRADF32; }
 constexpr int TC_STG_FLOATS = 32 * 33;  // per epilogue warp, padded against bank conflicts
+// GRADF32 per-warp staging: the padded transpose block, or (plain fp32 output) a 1 KB-aligned 4 KB
+// 128B-swizzled block for a TMA store
+constexpr int TC_STG_WARP_BYTES = 5120;
 
 // CG = CTA group: 1 -> one SM computes a 128 x BN tile; 2 -> a CTA pair (cluster of 2) computes
 // 256 x BN with tcgen05 cta_group::2: each CTA stages its 128 rows of A and BN/2 rows of B, the
@@ -71,7 +74,7 @@ struct TcCfg {
   // / 4: the smem is worth more as operand stages, 6 / 5 / 4 / 3); short K wants four (see is_sgd);
   // GRADF32: per warp a padded 32x33 transpose block.
   static constexpr int STG_BYTES = is_sgd(KIND) ? TC_EPI_WARPS * sgd_bufs(KIND) * 4096
-                                 : (KIND == EPI_GRADF32 ? TC_EPI_WARPS * TC_STG_FLOATS * 4 : 0);
+                                 : (KIND == EPI_GRADF32 ? TC_EPI_WARPS * TC_STG_WARP_BYTES : 0);
   static constexpr int PIPE_BUDGET = 227 * 1024 - 2048 - STG_BYTES;  // all of the 227 KB opt-in smem
   static constexpr int STAGES = PIPE_BUDGET / STAGE_BYTES > 8 ? 8 : PIPE_BUDGET / STAGE_BYTES;
   static constexpr int TMEM_COLS = 512;
@@ -403,7 +406,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr int NC = BN / 32;
     const int c_begin = half ? (NC + 1) / 2 : 0;
     const int c_end = half ? NC : (NC + 1) / 2;
-    float* stg = reinterpret_cast<float*>(epi_smem) + (warp - 2) * TC_STG_FLOATS;
+    float* stg = reinterpret_cast<float*>(epi_smem + (warp - 2) * (is_sgd(KIND) ? TC_STG_FLOATS * 4 : TC_STG_WARP_BYTES));
     const int lane = lane_id();
     const uint64_t stream = l2_policy_evict_first();  // master / ring are touched once per GEMM
     int acc = 0;
@@ -415,6 +418,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int64_t row0 = m0 + 32 * q;
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
+      if constexpr (KIND == EPI_GRADF32) {
+        if (ep.tma_out) {
+          // plain fp32 output (the GPT-2 head's logits, replicated-stage gradients): each lane's row
+          // of a 32x32 block -> swizzled smem -> one asynchronous TMA store per block (the output map
+          // clips rows / columns past M / N), instead of 32 row stores per block from the transpose
+          uint8_t* blk = reinterpret_cast<uint8_t*>(stg);
+#pragma unroll 1
+          for (int c = c_begin; c < c_end; ++c) {
+            float v[32];
+            tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * TC_ACC_STRIDE + c * 32, v);
+            const int64_t col0 = n0 + c * 32;
+            if (ep.bias && col0 < N) {
+              const float* bp = ep.bias + col0;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += col0 + j < N ? __ldg(bp + j) : 0.f;
+            }
+            if (lane == 0) bulk_wait_read0();  // the previous block's store has read the buffer
+            __syncwarp();
+            float4* row = reinterpret_cast<float4*>(blk + lane * 128);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) row[j ^ (lane & 7)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            fence_proxy_async_shared();
+            __syncwarp();
+            if (lane == 0 && col0 < N && row0 < M) {
+              tma_store_2d_hint(&tmW, blk, (int)col0, (int)row0, stream);
+              bulk_commit();
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 2) mbar_arrive_cluster_relaxed(&tmem_empty[acc], 0); else mbar_arrive(&tmem_empty[acc]);
+          }
+          acc ^= 1;
+          if (acc == 0) acc_phase ^= 1;
+          continue;
+        }
+      }
       // Two 32-column chunks per step: 64 independent 128-byte master loads in flight per warp
       // (the epilogue is HBM-latency bound, it has to keep up with the next tile's MMAs).
 #pragma unroll 1
@@ -480,6 +521,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if constexpr (KIND == EPI_GRADF32)
+      if (lane == 0) bulk_wait_all0();  // TMA-store path: the last blocks' stores completed
   } else {
     // ---------------- epilogue warps: TMEM -> registers -> fused epilogue -> HBM
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
@@ -732,7 +775,23 @@ static int launch_tc(const void* A, int64_t lda, const void* B, int64_t ldb, int
     rc = make_map(&tw, ep.master, (uint64_t)N, (uint64_t)M, ep.ldw, 32, 32, true);
     if (rc) return rc;
   }
+  // plain fp32 output (no split-K, no red.add): asynchronous TMA stores of 32 x 32 blocks
+  bool tma_out = false;
+  if (KIND == EPI_GRADF32 && !ep.accumulate && cv.splits == 1 && !(ep.ldo % 4) &&
+      !(reinterpret_cast<uintptr_t>(ep.out) % 16)) {
+    static int off = -1;  // PD_F32_TMA_STORE=0: the row-store path (A/B runs)
+    if (off < 0) {
+      const char* e = getenv("PD_F32_TMA_STORE");
+      off = e && atoi(e) == 0 ? 1 : 0;
+    }
+    if (!off) {
+      rc = make_map(&tw, ep.out, (uint64_t)N, (uint64_t)M, ep.ldo, 32, 32, true);
+      if (rc) return rc;
+      tma_out = true;
+    }
+  }
   EpiArgs epl = ep;
+  epl.tma_out = tma_out ? 1 : 0;
   {
     // B operand streamed with evict-first when it is far larger than its reuse window in L2
     // (PD_B_STREAM=0/1 forces it off/on for A/B runs)
