@@ -534,15 +534,22 @@ def run_ours(args, rank, world):
     h2d = (X_host.numel() * X_host.element_size() if hosts_first else 0) + \
           (T_host.numel() * T_host.element_size() if hosts_last else 0)
     d2h = loss_host.numel() * 4 if hosts_last else 0
+
+    def e2e_step():
+        ex.load_inputs(X_host if hosts_first else None, T_host if hosts_last else None, stream=stream)
+        ex.step(stream=stream)
+        if hosts_last:
+            loss_host.copy_(ex.loss_tensor(), non_blocking=True)
+
+    # one untimed e2e step first: the serial roofline pass above dropped the CUDA graph, and its
+    # re-capture belongs in warm-up, not in the timed region
+    e2e_step()
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.e2e_steps):
-        ex.load_inputs(X_host if hosts_first else None, T_host if hosts_last else None, stream=stream)
-        ex.step(stream=stream)
-        if hosts_last:
-            loss_host.copy_(ex.loss_tensor(), non_blocking=True)
+        e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)

@@ -510,12 +510,20 @@ class Executor:
         """Copy host (pinned) input / target blocks into the resident data buffers (e2e path)."""
         torch = _torch()
         s = stream or torch.cuda.current_stream(self.device)
+        # Replicas of a stage hosted here hold the same resident blocks: one host->device copy,
+        # then device-to-device copies to the other replicas' buffers.
         with torch.cuda.stream(s):
+            first = {}
             for b in self.bufs.values():
-                if b.stage == 0 and X_host is not None:
-                    b.tensors["act_in"].copy_(X_host, non_blocking=True)
-                if b.stage == self.cfg.plan.num_stages - 1 and T_host is not None:
-                    b.tensors["target"].copy_(T_host, non_blocking=True)
+                for want, src, key in ((0, X_host, "act_in"), (self.cfg.plan.num_stages - 1, T_host, "target")):
+                    if b.stage != want or src is None:
+                        continue
+                    dst = b.tensors[key]
+                    if key in first and first[key].device == dst.device:
+                        dst.copy_(first[key], non_blocking=True)
+                    else:
+                        dst.copy_(src, non_blocking=True)
+                        first.setdefault(key, dst)
 
     def hosts_stage(self, s: int) -> bool:
         return any(b.stage == s for b in self.bufs.values())

@@ -249,6 +249,35 @@ def test_replicated_graph_replay_multi_step_parity():
         ex.close()
 
 
+def test_load_inputs_fills_every_replica():
+    """Executor.load_inputs (the e2e path) copies the host blocks once and fans them out to the
+    other replicas of the stage on the device: every stage-0 replica's inputs and the last stage's
+    targets equal the host tensors, and a step on them gives the same losses as the resident data."""
+    stages = (pd.Stage(1, 2, 2), pd.Stage(3, 4, 1))
+    plan = pd.Plan(stages=stages, bottleneck_time=1.0, noam=pd.noam_for(3, 2), machines_used=3)
+    cfg = pd.SimConfig(plan=plan, mode="weight_stashing", num_minibatches=8)
+    spec = pd.mlp(256, 4, batch=128, dtype="bf16", lr=2e-3, n_blocks=4, seed=4)
+    ex = pd.Executor(cfg, model=spec)
+    try:
+        b0 = [b for b in ex.bufs.values() if b.stage == 0]
+        last = [b for b in ex.bufs.values() if b.stage == 1][0]
+        X_host = b0[0].tensors["act_in"].cpu().pin_memory()
+        T_host = last.tensors["target"].cpu().pin_memory()
+        for b in b0:
+            b.tensors["act_in"].zero_()
+        last.tensors["target"].zero_()
+        ex.load_inputs(X_host, T_host)
+        torch.cuda.synchronize()
+        assert len(b0) == 2
+        for b in b0:
+            assert torch.equal(b.tensors["act_in"].cpu(), X_host)
+        assert torch.equal(last.tensors["target"].cpu(), T_host)
+        ex.step(trace=True)
+        assert np.all(np.isfinite(ex.result().losses[:8]))
+    finally:
+        ex.close()
+
+
 def test_device_ledger_matches_golden_and_counts_no_peer_bytes():
     """The ledger returned by run() is rebuilt from the version tags the device passes read
     (pd_rt_set_records) and equals the reference simulator's golden ledger; in one process no
