@@ -29,9 +29,13 @@ def _wt_to_oihw(wt, cin, cout):
 
 
 SHAPES = [(2, 8, 8, 64, 128), (1, 7, 7, 64, 64), (2, 14, 14, 128, 64), (2, 16, 16, 256, 256), (1, 28, 28, 64, 512)]
+# wide and ragged images: 128-pixel tiles straddling image rows and images (W 112, 120, 224, 250),
+# an odd tile count (a CTA pair's padding tile), a partial last tile
+ROW_SHAPES = [(1, 5, 112, 64, 64), (2, 3, 224, 64, 128), (1, 4, 120, 128, 64), (1, 3, 250, 64, 256),
+              (2, 6, 56, 64, 64)]
 
 
-@pytest.mark.parametrize("n,h,w,cin,cout", SHAPES)
+@pytest.mark.parametrize("n,h,w,cin,cout", SHAPES + ROW_SHAPES)
 def test_conv_fwd(n, h, w, cin, cout):
     g = torch.Generator(device="cuda").manual_seed(1)
     x = torch.randn(n, h, w, cin, device="cuda", generator=g).bfloat16()
@@ -44,7 +48,7 @@ def test_conv_fwd(n, h, w, cin, cout):
     _close(y, ref.permute(0, 2, 3, 1))
 
 
-@pytest.mark.parametrize("n,h,w,cin,cout", SHAPES)
+@pytest.mark.parametrize("n,h,w,cin,cout", SHAPES + ROW_SHAPES)
 def test_conv_dgrad(n, h, w, cin, cout):
     g = torch.Generator(device="cuda").manual_seed(2)
     dy = torch.randn(n, h, w, cout, device="cuda", generator=g).bfloat16()
