@@ -990,9 +990,37 @@ int splitk_plan(int M, int N, int K, int* splits, int* kb_per) {
   const int bn = conv_bn(N);
   const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + bn - 1) / bn);
   const int num_kb = (K + TC_BK - 1) / TC_BK;
-  int s = (2 * num_sms() + tiles - 1) / tiles;  // about two waves of work units
   const int cap = num_kb / 4 > 1 ? num_kb / 4 : 1;  // at least 4 k-blocks per split
-  s = s < 1 ? 1 : (s > cap ? cap : s);
+  const int sms = num_sms();
+  static int old = -1;  // PD_SPLITK_OLD=1: the round-1 rule (about two waves of units), for A/B runs
+  if (old < 0) {
+    const char* e = getenv("PD_SPLITK_OLD");
+    old = e && atoi(e) == 1 ? 1 : 0;
+  }
+  int s;
+  if (old) {
+    s = (2 * sms + tiles - 1) / tiles;
+    s = s < 1 ? 1 : (s > cap ? cap : s);
+  } else {
+    // wave-quantisation aware: minimise (waves of (tile, split) units) x (k-blocks per unit) x
+    // the k-block time (128 x bn x 64 MACs at ~10 TFLOP/s per SM), plus each split's fp32 partial
+    // (M x N x 4 B written, then read by the reduce, at ~6 TB/s).  E.g. 4608 x 512 x 6272 (VGG
+    // 14x14, 72 tiles): 2 splits = 1 wave x 49 k-blocks, where the two-wave rule's 5 splits give
+    // 3 waves x 20 k-blocks and 2.5x the partial traffic
+    s = 1;
+    double best = -1.0;
+    const double kb_ns = 128.0 * bn * TC_BK * 2.0 / 1.0e4;
+    const double part_ns = 8.0 * (double)M * (double)N / 6000.0;
+    const int lim = cap < 4 * sms ? cap : 4 * sms;
+    for (int c = 1; c <= lim; ++c) {
+      const int per_c = (num_kb + c - 1) / c;
+      const int used = (num_kb + per_c - 1) / per_c;
+      if (used != c) continue;  // c splits would leave an empty one
+      const long waves = ((long)tiles * c + sms - 1) / sms;
+      const double cost = (double)waves * per_c * kb_ns + c * part_ns;
+      if (best < 0.0 || cost < best) { best = cost; s = c; }
+    }
+  }
   const int per = (num_kb + s - 1) / s;
   *kb_per = per;
   *splits = (num_kb + per - 1) / per;  // no empty split
