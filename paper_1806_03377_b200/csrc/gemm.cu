@@ -986,6 +986,29 @@ static int dispatch_kind(int kind, const void* A, int64_t lda, const void* B, in
 // (zero-filled halo = padding), so no im2col matrix is ever materialised in HBM.
 static int conv_bn(int N) { return N >= 256 ? 256 : (N >= 128 ? 128 : 64); }
 
+// Split count minimising (waves of (tile, split) units) x (k-blocks per unit) x the k-block time
+// (128 x bn x 64 MACs per SM at ~10 TFLOP/s), plus each split's fp32 partial (M x N x 4 B written,
+// then read by the reduce, at ~6 TB/s); cg = 2 counts CTA-pair tiles of 256 rows on sms / 2 pairs.
+// E.g. 4608 x 512 x 6272 (VGG 14x14, 72 tiles): 2 splits = 1 wave x 49 k-blocks, where a
+// two-wave rule's 5 splits give 3 waves x 20 k-blocks and 2.5x the partial traffic.
+static int wave_splits(int M, int N, int num_kb, int cg, int max_s) {
+  const int bn = conv_bn(N);
+  const int tiles = ((M + TC_BM * cg - 1) / (TC_BM * cg)) * ((N + bn - 1) / bn);
+  const int slots = num_sms() / cg;
+  const double kb_ns = 128.0 * bn * TC_BK * 2.0 / 1.0e4;
+  const double part_ns = 8.0 * (double)M * (double)N / 6000.0;
+  int s = 1;
+  double best = -1.0;
+  for (int c = 1; c <= max_s; ++c) {
+    const int per_c = (num_kb + c - 1) / c;
+    if ((num_kb + per_c - 1) / per_c != c) continue;  // c splits would leave an empty one
+    const long waves = ((long)tiles * c + slots - 1) / slots;
+    const double cost = (double)waves * per_c * kb_ns + c * part_ns;
+    if (best < 0.0 || cost < best) { best = cost; s = c; }
+  }
+  return s;
+}
+
 int splitk_plan(int M, int N, int K, int* splits, int* kb_per) {
   const int bn = conv_bn(N);
   const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + bn - 1) / bn);
@@ -1002,24 +1025,7 @@ int splitk_plan(int M, int N, int K, int* splits, int* kb_per) {
     s = (2 * sms + tiles - 1) / tiles;
     s = s < 1 ? 1 : (s > cap ? cap : s);
   } else {
-    // wave-quantisation aware: minimise (waves of (tile, split) units) x (k-blocks per unit) x
-    // the k-block time (128 x bn x 64 MACs at ~10 TFLOP/s per SM), plus each split's fp32 partial
-    // (M x N x 4 B written, then read by the reduce, at ~6 TB/s).  E.g. 4608 x 512 x 6272 (VGG
-    // 14x14, 72 tiles): 2 splits = 1 wave x 49 k-blocks, where the two-wave rule's 5 splits give
-    // 3 waves x 20 k-blocks and 2.5x the partial traffic
-    s = 1;
-    double best = -1.0;
-    const double kb_ns = 128.0 * bn * TC_BK * 2.0 / 1.0e4;
-    const double part_ns = 8.0 * (double)M * (double)N / 6000.0;
-    const int lim = cap < 4 * sms ? cap : 4 * sms;
-    for (int c = 1; c <= lim; ++c) {
-      const int per_c = (num_kb + c - 1) / c;
-      const int used = (num_kb + per_c - 1) / per_c;
-      if (used != c) continue;  // c splits would leave an empty one
-      const long waves = ((long)tiles * c + sms - 1) / sms;
-      const double cost = (double)waves * per_c * kb_ns + c * part_ns;
-      if (best < 0.0 || cost < best) { best = cost; s = c; }
-    }
+    s = wave_splits(M, N, num_kb, 1, cap < 4 * sms ? cap : 4 * sms);
   }
   const int per = (num_kb + s - 1) / s;
   *kb_per = per;
@@ -1065,13 +1071,21 @@ static int conv_launch(int pass, const void* act, const void* other, int n, int 
   cv.split_stride = ep.accumulate ? 0 : (int64_t)M * ep.ldo;  // accumulate: every split adds into one buffer
   if (pass == PD_CONV_WGRAD) {
     cv.C = cin;
-    static int wpair = -1;  // PD_CONV_WGRAD_CG=2: CTA pairs for the split-K weight gradient (A/B runs)
+    // CTA pairs (each CTA stages half of the dY tile).  Accumulating into one gradient (the
+    // runtime's path: splits red.add), they use their own split plan capped at the single-CTA
+    // count; with per-split partials (pd_conv3x3 callers size and reduce pd_splitk_plan's count)
+    // they keep that count.  VGG-16 step: 7 986-8 006 -> 8 051-8 071 images/s with the single-CTA
+    // plan's splits.  PD_CONV_WGRAD_CG=1: single CTAs.
+    static int wpair = -1;
     if (wpair < 0) {
       const char* e = getenv("PD_CONV_WGRAD_CG");
-      wpair = e && atoi(e) == 2 ? 1 : 0;
+      wpair = e && atoi(e) == 1 ? 0 : 1;
     }
     if (wpair && M > TC_BM) {
-      splitk_plan(M, cout, pix, &cv.splits, &cv.kb_per);
+      const int num_kb = (pix + TC_BK - 1) / TC_BK;
+      const int s = ep.accumulate ? wave_splits(M, cout, num_kb, 2, cv.splits) : cv.splits;
+      cv.kb_per = (num_kb + s - 1) / s;
+      cv.splits = (num_kb + cv.kb_per - 1) / cv.kb_per;
       return launch_tc<2, BN, true, true, EPI_GRADF32, SRC_CONV_WGRAD>(act, cin, other, cout, M, cout, pix, ep, st, cv);
     }
     return launch_tc<1, BN, true, true, EPI_GRADF32, SRC_CONV_WGRAD>(act, cin, other, cout, M, cout, pix, ep, st, cv);
